@@ -1,0 +1,456 @@
+// C ABI of libcqp_b200.so (include/cqp_b200.h): handle management, uploads, result download.
+// Mirrors the reference's Solver lifecycle (/root/reference/proj/src/solver.cpp:180-218).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "cqp_internal.h"
+
+namespace cqp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what;
+  return CQP_ERR_CUDA;
+}
+
+namespace {
+
+template <typename T>
+int dev_alloc(T** p, size_t count) {
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1)));
+  return CQP_OK;
+}
+
+size_t result_bytes(int n, int m, int cap) {
+  return sizeof(DevResultHead) + sizeof(int) * 4 * (size_t)cap + sizeof(double) * 2 * (size_t)cap +
+         sizeof(double) * ((size_t)n + 2 * (size_t)m);
+}
+
+int ensure_result_capacity(cqp_handle* h, int cap) {
+  if (cap <= h->res_cap) return CQP_OK;
+  if (h->dres) cudaFree(h->dres);
+  if (h->hres) cudaFreeHost(h->hres);
+  h->dres = h->hres = nullptr;
+  h->res_cap = cap;
+  h->res_bytes = result_bytes(h->n, h->m, cap);
+  CQP_CUDA(cudaMalloc(&h->dres, h->res_bytes));
+  CQP_CUDA(cudaMallocHost(&h->hres, h->res_bytes));
+  return CQP_OK;
+}
+
+// solver.cpp:29-34
+int check_settings(const cqp_settings& s) {
+  if (s.check_interval < 1) {
+    set_error("check_interval must be >= 1");
+    return CQP_ERR_SETTINGS;
+  }
+  if (s.max_iters < s.check_interval) {
+    set_error("max_iters must be >= check_interval");
+    return CQP_ERR_SETTINGS;
+  }
+  return CQP_OK;
+}
+
+// Upload a column-major host matrix as a row-major, even-padded device matrix.
+int upload_transposed(cqp_handle* h, const double* host, int rows, int cols, double* dst, int ld,
+                      double* scratch) {
+  CQP_CUDA(cudaMemcpyAsync(scratch, host, sizeof(double) * (size_t)rows * cols,
+                           cudaMemcpyHostToDevice, h->stream));
+  return launch_transpose_pad(h->stream, scratch, rows, cols, dst, ld);
+}
+
+}  // namespace
+
+// Allocates everything whose size depends only on (n, m, L) and fills the fields shared by both
+// creation paths.  Device buffers for the ladder are allocated here and filled by the caller.
+int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    set_error("no CUDA device available: libcqp_b200 has no CPU fallback");
+    return CQP_ERR_CUDA;
+  }
+  if (device < 0) CQP_CUDA(cudaGetDevice(&device));
+  CQP_CUDA(cudaSetDevice(device));
+  cqp_handle* h = new cqp_handle();
+  *out = h;
+  h->n = n; h->m = m; h->D = n + 2 * m; h->L = L;
+  h->npad = pad2(n); h->mpad = pad2(m); h->Dpad = pad2(h->D);
+  h->s = s;
+  h->device = device;
+  cudaDeviceProp prop;
+  CQP_CUDA(cudaGetDeviceProperties(&prop, device));
+  h->num_sms = prop.multiProcessorCount;
+  int coop = 0;
+  CQP_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) {
+    set_error("device does not support cooperative launch");
+    return CQP_ERR_CUDA;
+  }
+  CQP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CQP_CUDA(cudaEventCreate(&h->ev0));
+  CQP_CUDA(cudaEventCreate(&h->ev1));
+  const size_t D = h->D, nm = (size_t)n + m;
+  int rc;
+  if ((rc = dev_alloc(&h->W, (size_t)L * D * h->Dpad))) return rc;
+  if ((rc = dev_alloc(&h->Dk, (size_t)L * nm * h->npad))) return rc;
+  if ((rc = dev_alloc(&h->H, (size_t)n * h->npad))) return rc;
+  if ((rc = dev_alloc(&h->Gr, (size_t)m * h->npad))) return rc;
+  if ((rc = dev_alloc(&h->Gt, (size_t)n * h->mpad))) return rc;
+  if ((rc = dev_alloc(&h->Gs, (size_t)m * h->npad))) return rc;
+  if ((rc = dev_alloc(&h->E, (size_t)n))) return rc;
+  if ((rc = dev_alloc(&h->F, (size_t)m))) return rc;
+  if ((rc = dev_alloc(&h->dgrid, (size_t)L))) return rc;
+  if ((rc = dev_alloc(&h->dlog_grid, (size_t)L))) return rc;
+  if ((rc = dev_alloc(&h->g, nm + m))) return rc;
+  h->c = h->g + n;
+  h->d = h->c + m;
+  if ((rc = dev_alloc(&h->vbuf, 2 * (size_t)h->Dpad))) return rc;
+  if ((rc = dev_alloc(&h->state, 2))) return rc;
+  if ((rc = dev_alloc(&h->barrier, 1))) return rc;
+  if ((rc = dev_alloc(&h->partial, 8 * (size_t)(h->num_sms + 1)))) return rc;
+  if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
+  if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
+  CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->hstage), sizeof(double) * (nm + m)));
+  if ((rc = ensure_result_capacity(h, s.max_iters / s.check_interval + 2))) return rc;
+  if ((rc = configure_launch(h))) return rc;
+  return CQP_OK;
+}
+
+// grid values + their log10 (host libm, so the table equals what the reference recomputes at
+// every selection, layers.cpp:43), E, F.
+int upload_small(cqp_handle* h, const double* grid, const double* E, const double* F) {
+  h->grid.assign(grid, grid + h->L);
+  h->E_host.assign(E, E + h->n);
+  h->F_host.assign(F, F + h->m);
+  std::vector<double> lg(h->L);
+  for (int k = 0; k < h->L; ++k) lg[k] = std::log10(grid[k]);
+  CQP_CUDA(cudaMemcpyAsync(h->dgrid, grid, sizeof(double) * h->L, cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->dlog_grid, lg.data(), sizeof(double) * h->L, cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->E, E, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->F, F, sizeof(double) * h->m, cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));  // lg is a local
+  return CQP_OK;
+}
+
+int upload_vectors(cqp_handle* h, const double* g, const double* c, const double* d) {
+  const int n = h->n, m = h->m;
+  std::memcpy(h->hstage, g, sizeof(double) * n);
+  std::memcpy(h->hstage + n, c, sizeof(double) * m);
+  std::memcpy(h->hstage + n + m, d, sizeof(double) * m);
+  h->c_host.assign(c, c + m);
+  h->d_host.assign(d, d + m);
+  CQP_CUDA(cudaMemcpyAsync(h->g, h->hstage, sizeof(double) * ((size_t)n + 2 * (size_t)m),
+                           cudaMemcpyHostToDevice, h->stream));
+  return CQP_OK;
+}
+
+int cold_start(cqp_handle* h) {
+  CQP_CUDA(cudaMemsetAsync(h->vbuf, 0, sizeof(double) * 2 * (size_t)h->Dpad, h->stream));
+  return launch_set_state(h, h->initial_index, 0);
+}
+
+}  // namespace cqp
+
+using namespace cqp;
+
+extern "C" {
+
+void cqp_default_settings(cqp_settings* s) {
+  // solver.hpp:43-53, layers.hpp:100-104
+  s->eps_prim = 1e-6;
+  s->eps_dual = 1e-6;
+  s->check_interval = 25;
+  s->max_iters = 4000;
+  s->sigma = 1e-6;
+  s->grid_points = 13;
+  s->rho_switch_threshold = 5.0;
+  s->adaptive_rho = 1;
+  s->eq_enabled = 1;
+  s->eq_max_passes = 10;
+  s->eq_tol = 1e-3;
+}
+
+const char* cqp_last_error(void) { return g_last_error.c_str(); }
+
+int cqp_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) return 0;
+  return count;
+}
+
+int cqp_create_from_layers(cqp_handle** out, int n, int m, int L, const double* const* W,
+                           const double* const* Dk, const double* const* GDk,
+                           const double* grid_values, int initial_index, const double* H,
+                           const double* g, const double* G, const double* c, const double* d,
+                           const double* Gs, const double* E, const double* F, double cost_scale,
+                           const cqp_settings* settings, int device) {
+  if (!out) return CQP_ERR_ARGUMENT;
+  *out = nullptr;
+  if (n < 1 || m < 1 || L < 2 || initial_index < 0 || initial_index >= L) {
+    set_error("cqp_create_from_layers: bad dimensions");
+    return CQP_ERR_DIMENSION;
+  }
+  cqp_settings s;
+  if (settings) s = *settings; else cqp_default_settings(&s);
+  int rc = check_settings(s);
+  if (rc) return rc;
+  cqp_handle* h = nullptr;
+  rc = handle_alloc(&h, n, m, L, s, device);
+  if (rc) { cqp_destroy(h); return rc; }
+  h->initial_index = initial_index;
+  h->cost_scale = cost_scale;
+  const size_t D = h->D, nm = (size_t)n + m;
+  double* scratch = nullptr;
+  if ((rc = dev_alloc(&scratch, D * D))) { cqp_destroy(h); return rc; }
+  auto fail = [&](int code) { cudaFree(scratch); cqp_destroy(h); return code; };
+  for (int k = 0; k < L; ++k) {
+    if ((rc = upload_transposed(h, W[k], (int)D, (int)D, h->W + (size_t)k * D * h->Dpad, h->Dpad, scratch))) return fail(rc);
+    double* dg = h->Dk + (size_t)k * nm * h->npad;
+    if ((rc = upload_transposed(h, Dk[k], n, n, dg, h->npad, scratch))) return fail(rc);
+    if ((rc = upload_transposed(h, GDk[k], m, n, dg + (size_t)n * h->npad, h->npad, scratch))) return fail(rc);
+  }
+  if ((rc = upload_transposed(h, H, n, n, h->H, h->npad, scratch))) return fail(rc);
+  if ((rc = upload_transposed(h, G, m, n, h->Gr, h->npad, scratch))) return fail(rc);
+  if ((rc = upload_transposed(h, Gs, m, n, h->Gs, h->npad, scratch))) return fail(rc);
+  {
+    // G' (n x m) in the kernel's row-major padded layout
+    std::vector<double> Gt_host((size_t)n * m);
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < n; ++i) Gt_host[i + (size_t)j * n] = G[j + (size_t)i * m];
+    if ((rc = upload_transposed(h, Gt_host.data(), n, m, h->Gt, h->mpad, scratch))) return fail(rc);
+    CQP_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  // per-row penalties (layers.cpp:210-215): equality rows (scaled c == d) get eq_scale = 1e3
+  {
+    std::vector<double> rho((size_t)L * m);
+    for (int k = 0; k < L; ++k)
+      for (int i = 0; i < m; ++i) {
+        const bool eq = (F[i] * c[i]) == (F[i] * d[i]);
+        rho[(size_t)k * m + i] = (eq ? 1e3 : 1.0) * grid_values[k];
+      }
+    CQP_CUDA(cudaMemcpy(h->rho_vec, rho.data(), sizeof(double) * rho.size(), cudaMemcpyHostToDevice));
+  }
+  if ((rc = upload_small(h, grid_values, E, F))) return fail(rc);
+  if ((rc = upload_vectors(h, g, c, d))) return fail(rc);
+  if ((rc = cold_start(h))) return fail(rc);
+  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  cudaFree(scratch);
+  *out = h;
+  return CQP_OK;
+}
+
+void cqp_destroy(cqp_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->W); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
+  cudaFree(h->Gs); cudaFree(h->E); cudaFree(h->F); cudaFree(h->dgrid); cudaFree(h->dlog_grid);
+  cudaFree(h->g); cudaFree(h->vbuf); cudaFree(h->state); cudaFree(h->barrier);
+  cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp); cudaFree(h->dres);
+  if (h->hres) cudaFreeHost(h->hres);
+  if (h->hstage) cudaFreeHost(h->hstage);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int cqp_update_vectors(cqp_handle* h, const double* g, const double* c, const double* d) {
+  if (!h || !g || !c || !d) { set_error("update_vectors: null argument"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  return upload_vectors(h, g, c, d);
+}
+
+int cqp_cold_start(cqp_handle* h) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  CQP_CUDA(cudaSetDevice(h->device));
+  return cold_start(h);
+}
+
+int cqp_warm_start(cqp_handle* h, const double* y, const double* lambda, int layer_index) {
+  if (!h || !y || !lambda) { set_error("warm_start: null argument"); return CQP_ERR_ARGUMENT; }
+  if (layer_index >= h->L) { set_error("warm_start: layer index out of range"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  const int n = h->n, m = h->m;
+  CQP_CUDA(cudaStreamSynchronize(h->stream));  // hstage may still feed an update_vectors copy
+  double* hs = h->hstage;
+  double* ds = h->dtmp;
+  std::memcpy(hs, y, sizeof(double) * n);
+  std::memcpy(hs + n, lambda, sizeof(double) * m);
+  CQP_CUDA(cudaMemcpyAsync(ds, hs, sizeof(double) * ((size_t)n + m), cudaMemcpyHostToDevice, h->stream));
+  int rc = launch_warm_start(h, ds, ds + n, layer_index < 0 ? h->initial_index : layer_index);
+  if (rc) return rc;
+  CQP_CUDA(cudaStreamSynchronize(h->stream));  // hstage is reused by update_vectors
+  return CQP_OK;
+}
+
+int cqp_refresh_z(cqp_handle* h) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  CQP_CUDA(cudaSetDevice(h->device));
+  int st[2];
+  CQP_CUDA(cudaMemcpyAsync(st, h->state, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  return launch_refresh_z(h, st[1]);
+}
+
+static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = ensure_result_capacity(h, total / h->s.check_interval + 2);
+  if (rc) return rc;
+  CQP_CUDA(cudaEventRecord(h->ev0, h->stream));
+  if ((rc = launch_run(h, early_exit, total, refresh))) return rc;
+  CQP_CUDA(cudaEventRecord(h->ev1, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->hres, h->dres, h->res_bytes, cudaMemcpyDeviceToHost, h->stream));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  const unsigned char* base = static_cast<const unsigned char*>(h->hres);
+  const DevResultHead* head = reinterpret_cast<const DevResultHead*>(base);
+  size_t off = sizeof(DevResultHead);
+  const int cap = h->res_cap;
+  const int* trace = reinterpret_cast<const int*>(base + off); off += sizeof(int) * 2 * (size_t)cap;
+  const int* hist_i = reinterpret_cast<const int*>(base + off); off += sizeof(int) * 2 * (size_t)cap;
+  const double* hist_r = reinterpret_cast<const double*>(base + off); off += sizeof(double) * 2 * (size_t)cap;
+  const double* y = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->n;
+  const double* z = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  const double* lam = reinterpret_cast<const double*>(base + off);
+  if (out) {
+    out->status = head->status;
+    out->iterations = head->iterations;
+    out->r_prim = head->r_prim;
+    out->r_dual = head->r_dual;
+    if (out->y) std::memcpy(out->y, y, sizeof(double) * h->n);
+    if (out->z) std::memcpy(out->z, z, sizeof(double) * h->m);
+    if (out->lambda) std::memcpy(out->lambda, lam, sizeof(double) * h->m);
+    out->rho_trace_len = head->n_trace;
+    out->history_len = head->n_hist;
+    if (out->rho_trace) {
+      const int cnt = std::min(std::min(head->n_trace, out->rho_trace_cap), cap);
+      for (int i = 0; i < cnt; ++i) out->rho_trace[i] = {trace[2 * i], trace[2 * i + 1]};
+    }
+    if (out->history) {
+      const int cnt = std::min(std::min(head->n_hist, out->history_cap), cap);
+      for (int i = 0; i < cnt; ++i)
+        out->history[i] = {hist_i[2 * i], hist_r[2 * i], hist_r[2 * i + 1], hist_i[2 * i + 1]};
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    out->kernel_us = 1e3 * (double)ms;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return CQP_OK;
+}
+
+int cqp_solve(cqp_handle* h, cqp_result* out) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  CQP_CUDA(cudaSetDevice(h->device));
+  return run_and_fetch(h, true, h->s.max_iters, false, out);
+}
+
+int cqp_fixed_iters(cqp_handle* h, int k, cqp_result* out) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  if (k < 1) { set_error("fixed_iters: k must be >= 1"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  return run_and_fetch(h, false, k, false, out);
+}
+
+int cqp_mpc_step(cqp_handle* h, const double* g, const double* c, const double* d, int k,
+                 cqp_result* out) {
+  if (!h || !g || !c || !d) { set_error("mpc_step: null argument"); return CQP_ERR_ARGUMENT; }
+  if (k < 1) { set_error("mpc_step: k must be >= 1"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  int rc = upload_vectors(h, g, c, d);
+  if (rc) return rc;
+  return run_and_fetch(h, false, k, true, out);
+}
+
+int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  CQP_CUDA(cudaSetDevice(h->device));
+  int st[2];
+  CQP_CUDA(cudaMemcpyAsync(st, h->state, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  if (layer_index) *layer_index = st[0];
+  if (v) {
+    CQP_CUDA(cudaMemcpyAsync(v, h->vbuf + (size_t)st[1] * h->Dpad, sizeof(double) * h->D,
+                             cudaMemcpyDeviceToHost, h->stream));
+    CQP_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return CQP_OK;
+}
+
+int cqp_get_layer(cqp_handle* h, int k, double* W, double* Dk, double* GDk, double* b,
+                  double* rho_vec) {
+  if (!h || k < 0 || k >= h->L) { set_error("get_layer: bad index"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  const int n = h->n, m = h->m, D = h->D;
+  const size_t nm = (size_t)n + m;
+  double* scratch = nullptr;
+  int rc = dev_alloc(&scratch, (size_t)D * D);
+  if (rc) return rc;
+  auto done = [&](int code) { cudaStreamSynchronize(h->stream); cudaFree(scratch); return code; };
+  if (W) {
+    if ((rc = launch_untranspose(h->stream, h->W + (size_t)k * D * h->Dpad, D, D, h->Dpad, scratch))) return done(rc);
+    if (cudaMemcpyAsync(W, scratch, sizeof(double) * (size_t)D * D, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+    cudaStreamSynchronize(h->stream);
+  }
+  const double* dg = h->Dk + (size_t)k * nm * h->npad;
+  if (Dk) {
+    if ((rc = launch_untranspose(h->stream, dg, n, n, h->npad, scratch))) return done(rc);
+    if (cudaMemcpyAsync(Dk, scratch, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+    cudaStreamSynchronize(h->stream);
+  }
+  if (GDk) {
+    if ((rc = launch_untranspose(h->stream, dg + (size_t)n * h->npad, m, n, h->npad, scratch))) return done(rc);
+    if (cudaMemcpyAsync(GDk, scratch, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+    cudaStreamSynchronize(h->stream);
+  }
+  if (b) {
+    if ((rc = launch_bias(h, k, scratch))) return done(rc);
+    if (cudaMemcpyAsync(b, scratch, sizeof(double) * (size_t)D, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+    cudaStreamSynchronize(h->stream);
+  }
+  if (rho_vec) {
+    if (cudaMemcpyAsync(rho_vec, h->rho_vec + (size_t)k * m, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+  }
+  return done(CQP_OK);
+}
+
+int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, double* grid,
+                    int* initial_index, double* c_tilde, double* d_tilde) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  const int n = h->n, m = h->m;
+  if (E) std::memcpy(E, h->E_host.data(), sizeof(double) * n);
+  if (F) std::memcpy(F, h->F_host.data(), sizeof(double) * m);
+  if (cost_scale) *cost_scale = h->cost_scale;
+  if (grid) std::memcpy(grid, h->grid.data(), sizeof(double) * h->L);
+  if (initial_index) *initial_index = h->initial_index;
+  for (int i = 0; i < h->D; ++i) {
+    const bool zrow = i >= n && i < n + m;
+    if (c_tilde) c_tilde[i] = zrow ? h->F_host[i - n] * h->c_host[i - n] : -INFINITY;
+    if (d_tilde) d_tilde[i] = zrow ? h->F_host[i - n] * h->d_host[i - n] : INFINITY;
+  }
+  return CQP_OK;
+}
+
+int cqp_dims(const cqp_handle* h, int* n, int* m, int* L) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  if (n) *n = h->n;
+  if (m) *m = h->m;
+  if (L) *L = h->L;
+  return CQP_OK;
+}
+
+int cqp_launch_info(const cqp_handle* h, int* ctas, int* rows_per_cta, int* tier, int* smem_bytes) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  if (ctas) *ctas = h->G;
+  if (rows_per_cta) *rows_per_cta = h->R;
+  if (tier) *tier = h->w_smem ? 0 : 1;
+  if (smem_bytes) *smem_bytes = h->smem_bytes;
+  return CQP_OK;
+}
+
+}  // extern "C"

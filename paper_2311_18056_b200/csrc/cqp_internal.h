@@ -1,0 +1,136 @@
+// Internal declarations shared by the translation units of libcqp_b200.so.
+// Public surface: include/cqp_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "cqp_b200.h"
+
+namespace cqp {
+
+constexpr int kMaxSmemBytes = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100)
+constexpr int kThreads = 512;          // threads per CTA of the persistent solve kernel
+constexpr int kWarps = kThreads / 32;
+
+inline int pad2(int x) { return (x + 1) & ~1; }
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define CQP_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t e__ = (call);                                 \
+    if (e__ != cudaSuccess) return ::cqp::cuda_fail(e__, #call); \
+  } while (0)
+
+// Header of the device result buffer; followed by the record arrays and y, z, lambda.
+struct DevResultHead {
+  int status;
+  int iterations;
+  int n_trace;
+  int n_hist;
+  double r_prim;
+  double r_dual;
+  int final_layer;
+  int final_buf;
+};
+
+// Everything the persistent kernel needs (device pointers; row-major padded matrices).
+struct RunParams {
+  int n, m, D;
+  int npad, mpad, Dpad;  // even-padded leading dimensions
+  int L;
+  int R;        // rows of W owned by one CTA
+  int G;        // CTAs
+  int w_smem;   // 1: W slice resident in shared memory; 0: streamed from global (L2/HBM)
+  const double* W;    // [L][D][Dpad] row-major
+  const double* Dk;   // [L][n+m][npad]  rows 0..n: D_k, rows n..n+m: G D_k (bias operator)
+  const double* H;    // [n][npad]   unscaled
+  const double* Gr;   // [m][npad]   unscaled G, row-major
+  const double* Gt;   // [n][mpad]   unscaled G', row-major
+  const double* Gs;   // [m][npad]   scaled G, row-major (refresh_z)
+  const double* E;    // n
+  const double* F;    // m
+  double cost_scale;
+  const double* grid;      // L
+  const double* log_grid;  // L  (log10 of the grid values, computed on the host)
+  const double* g;   // n unscaled
+  const double* c;   // m unscaled
+  const double* d;   // m unscaled
+  double* vbuf;      // [2][Dpad] iterate, double buffered
+  int* state;        // [0] layer index, [1] current buffer
+  unsigned* barrier;  // grid barrier counter (zeroed before launch)
+  double* partial;    // [G][8] per-CTA partial maxima
+  double eps_prim, eps_dual, threshold;
+  int check_interval, adaptive, early_exit, total_iters;
+  int do_refresh;     // run Solver::refresh_z before the first iteration
+  int cap;            // capacity of the record arrays
+  DevResultHead* head;
+  int* trace;         // [cap][2]
+  int* hist_i;        // [cap][2]  (iteration, grid index)
+  double* hist_r;     // [cap][2]  (r_prim, r_dual)
+  double* out_y;      // n
+  double* out_z;      // m
+  double* out_lam;    // m
+};
+
+}  // namespace cqp
+
+struct cqp_handle {
+  int n = 0, m = 0, D = 0, L = 0;
+  int npad = 0, mpad = 0, Dpad = 0;
+  cqp_settings s{};
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int initial_index = 0;
+  double cost_scale = 1.0;
+  std::vector<double> grid, E_host, F_host;
+  // device memory
+  double *W = nullptr, *Dk = nullptr;  // Dk: [L][n+m][npad] = [D_k; G D_k]
+  double *H = nullptr, *Gr = nullptr, *Gt = nullptr, *Gs = nullptr;
+  double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;
+  double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
+  double* vbuf = nullptr;
+  int* state = nullptr;
+  unsigned* barrier = nullptr;
+  double* partial = nullptr;
+  double* rho_vec = nullptr;  // [L][m]
+  double* dtmp = nullptr;     // Dpad scratch (warm start staging)
+  // result buffer (device) and its pinned host mirror
+  void* dres = nullptr;
+  void* hres = nullptr;
+  size_t res_bytes = 0;
+  int res_cap = 0;
+  // pinned staging for update_vectors: [g; c; d]
+  double* hstage = nullptr;
+  std::vector<double> c_host, d_host;  // current unscaled bounds (for cqp_get_scaling)
+  // launch configuration
+  int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
+};
+
+namespace cqp {
+
+// cqp_single.cu
+int configure_launch(cqp_handle* h);
+int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh);
+int launch_refresh_z(cqp_handle* h, int buf);
+int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index);
+int launch_set_state(cqp_handle* h, int layer, int buf);
+int launch_transpose_pad(cudaStream_t st, const double* src_colmajor, int rows, int cols,
+                         double* dst_rowmajor, int ld);
+int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, int cols, int ld,
+                       double* dst_colmajor);
+int launch_bias(cqp_handle* h, int k, double* b_out);  // b_out: device, D doubles
+
+// cqp_setup.cu : offline stage on the device (layers.cpp:189-228)
+int device_precompute(cqp_handle* h, const double* H, const double* g, const double* G,
+                      const double* c, const double* d);
+
+}  // namespace cqp

@@ -1,0 +1,626 @@
+// Single-QP solve path: one persistent cooperative sm_100a kernel per solve()/fixed_iters().
+//
+// Replaces the reference's run_loop (/root/reference/proj/src/solver.cpp:43-105) and the
+// helpers it calls (iterate :109-117, residuals :119-124, rho_nominal :126-134,
+// select_layer :136-142 + nearest_grid_index layers.cpp:38-50), plus the per-MPC-step
+// vector update (layers.cpp:177-187) and z refresh (solver.cpp:197-200).
+//
+// Design:
+//   * W_k (D x D, D = n + 2m) is stored row-major; CTA b owns rows [b*R, b*R + R) and keeps
+//     that slice resident in shared memory (tier 0) or streams it from L2/HBM (tier 1).
+//   * One iteration = every CTA reads the full iterate v (D doubles) from L2, forms its R dot
+//     products (each thread owns a fixed set of column pairs, 16-byte LDS/LDG, FP64 FMA),
+//     reduces them with a shuffle butterfly + one shared-memory pass in a FIXED order
+//     (bit-reproducible run to run), adds the bias, clamps, publishes its rows, and crosses
+//     one hand-rolled grid barrier (red.release / ld.acquire on one L2 word).
+//   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
+//     problem (H y, G' lambda, G y spread over the CTAs, six max-norms exchanged through L2),
+//     and every CTA takes the identical rho decision; a switch reloads the W slice and
+//     recomputes the bias rows b = -[D_k; G D_k] g_s for the rows it owns.
+//   * Nothing is launched per iteration; the host sees one launch and one result download.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "cqp_internal.h"
+
+namespace cqp {
+namespace {
+
+__device__ __forceinline__ double nanmax(double best, double a) {
+  // max that keeps NaN once seen (the oracle's inf_norm propagates NaN the same way)
+  return (a > best || a != a) ? a : best;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks) {
+  __syncthreads();
+  epoch += nblocks;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    unsigned seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+    } while (seen < epoch);
+  }
+  __syncthreads();
+}
+
+template <int RB>
+struct Log2;
+template <> struct Log2<4> { static constexpr int v = 2; };
+template <> struct Log2<8> { static constexpr int v = 3; };
+template <> struct Log2<16> { static constexpr int v = 4; };
+
+// Reduce RB per-lane partial sums across the warp with RB + (5 - log2 RB) - 1 shuffles of a
+// double instead of 5*RB.  Afterwards every lane holds the warp total of row
+// (lane >> (5 - log2 RB)).
+template <int RB>
+__device__ __forceinline__ double warp_butterfly(double (&acc)[RB], int lane) {
+  int width = 16;
+#pragma unroll
+  for (int half = RB / 2; half >= 1; half >>= 1) {
+    const bool upper = (lane & width) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? acc[i] : acc[i + half];
+      const double keep = upper ? acc[i + half] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, width);
+    }
+    width >>= 1;
+  }
+#pragma unroll
+  for (; width >= 1; width >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], width);
+  return acc[0];
+}
+
+// out (threads 0..nvalid-1) = M[r, :] . x for r < nvalid <= RB.  M row-major with even leading
+// dimension ld (shared or global memory), x in shared memory, ncols_pad even, pad entries zero.
+// Contains two __syncthreads(); must be called by the whole CTA.
+template <int RB>
+__device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, int ld, int nvalid,
+                                                 const double* __restrict__ x, int ncols_pad,
+                                                 double* sred) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+  const int nc2 = ncols_pad >> 1;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  constexpr int CH = RB < 8 ? RB : 8;  // rows loaded per batch (keeps RB = 16 out of spills)
+  for (int c2 = t; c2 < nc2; c2 += kThreads) {
+    const double2 xv = x2[c2];
+#pragma unroll
+    for (int r0 = 0; r0 < RB; r0 += CH) {
+      double2 w[CH];
+#pragma unroll
+      for (int r = 0; r < CH; ++r) {
+        w[r] = (r0 + r < nvalid) ? reinterpret_cast<const double2*>(M + (size_t)(r0 + r) * ld)[c2]
+                                 : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int r = 0; r < CH; ++r) {
+        acc[r0 + r] = fma(w[r].x, xv.x, acc[r0 + r]);
+        acc[r0 + r] = fma(w[r].y, xv.y, acc[r0 + r]);
+      }
+    }
+  }
+  constexpr int shift = 5 - Log2<RB>::v;
+  const double total = warp_butterfly<RB>(acc, lane);
+  if ((lane & ((1 << shift) - 1)) == 0) sred[warp * RB + (lane >> shift)] = total;
+  __syncthreads();
+  double s = 0.0;
+  if (t < RB) {
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += sred[w * RB + t];
+  }
+  __syncthreads();
+  return s;
+}
+
+struct Smem {
+  double* sW;    // R * Dpad   (tier 0 only)
+  double* xs;    // Dpad       current iterate (cache space)
+  double* uy;    // npad       unscaled y   (also scratch for g_s)
+  double* uz;    // mpad       unscaled z
+  double* ul;    // mpad       unscaled lambda
+  double* sred;  // kWarps * 16
+  double* sb;    // Rp  bias rows
+  double* slo;   // Rp
+  double* shi;   // Rp
+  double* sval;  // 128 scratch
+};
+
+__host__ __device__ inline size_t smem_doubles(int R, int Dpad, int npad, int mpad, int w_smem) {
+  const int Rp = (R + 1) & ~1;
+  return (size_t)(w_smem ? (size_t)R * Dpad : 0) + Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
+         3 * (size_t)Rp + 128;
+}
+
+__device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
+  Smem s;
+  double* base = reinterpret_cast<double*>(raw);
+  const int Rp = (p.R + 1) & ~1;
+  s.sW = base;
+  s.xs = base + (p.w_smem ? (size_t)p.R * p.Dpad : 0);
+  s.uy = s.xs + p.Dpad;
+  s.uz = s.uy + p.npad;
+  s.ul = s.uz + p.mpad;
+  s.sred = s.ul + p.mpad;
+  s.sb = s.sred + kWarps * 16;
+  s.slo = s.sb + Rp;
+  s.shi = s.slo + Rp;
+  s.sval = s.shi + Rp;
+  return s;
+}
+
+// Makes layer k current for this CTA: W slice -> shared memory (tier 0), bias rows for the
+// rows it owns: b = -[D_k; G D_k] g_s, 0 on the lambda rows (layers.cpp:168-175).
+// Uses s.uy as scratch for g_s = cost_scale * E o g (layers.cpp:181).
+template <int RB>
+__device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows) {
+  const int t = threadIdx.x;
+  if (p.w_smem) {
+    const double2* src =
+        reinterpret_cast<const double2*>(p.W + ((size_t)k * p.D + row0) * p.Dpad);
+    double2* dst = reinterpret_cast<double2*>(s.sW);
+    const int count = nrows * (p.Dpad >> 1);
+    for (int i = t; i < count; i += kThreads) dst[i] = __ldg(src + i);
+  }
+  for (int i = t; i < p.npad; i += kThreads)
+    s.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * p.g[i]) : 0.0;
+  __syncthreads();
+  const int nm = p.n + p.m;
+  const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
+  for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
+    const int first = row0 + rb0;
+    int nv = min(RB, nrows - rb0);
+    int nv_dot = max(0, min(nv, nm - first));  // rows that have a D/GD row
+    double sum = 0.0;
+    if (first < nm) sum = block_rows_dot<RB>(DG + (size_t)first * p.npad, p.npad, nv_dot, s.uy, p.npad, s.sred);
+    if (t < nv) s.sb[rb0 + t] = (t < nv_dot) ? -sum : 0.0;
+  }
+  __syncthreads();
+}
+
+// Residual pass on the unscaled problem (solver.cpp:67-70,119-134; epilogue :90-95 when
+// `final`).  On return every thread of every CTA holds the same seven norms in out[]:
+//   0 ||Gy - z||  1 ||Hy + g + G'lam||  2 ||Hy||  3 ||G'lam||  4 ||Gy||  5 ||z||  6 ||g||
+template <int RB>
+__device__ void residual_pass(const RunParams& p, const Smem& s, int cur, bool final,
+                              unsigned& epoch, double (&out)[7]) {
+  const int t = threadIdx.x;
+  const int n = p.n, m = p.m;
+  const double* v = p.vbuf + (size_t)cur * p.Dpad;
+  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < p.D) ? __ldcg(v + i) : 0.0;
+  __syncthreads();
+  // unscale (layers.hpp:57-59)
+  for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? p.E[i] * s.xs[i] : 0.0;
+  for (int i = t; i < p.mpad; i += kThreads) {
+    double z = 0.0, l = 0.0;
+    if (i < m) {
+      z = s.xs[n + i] / p.F[i];
+      if (final) {  // solver.cpp:94  z = clamp(z, p.c, p.d) in original units
+        const double lo = p.c[i], hi = p.d[i];
+        z = z < lo ? lo : z;
+        z = z > hi ? hi : z;
+      }
+      l = (p.F[i] * s.xs[n + m + i]) / p.cost_scale;
+    }
+    s.uz[i] = z;
+    s.ul[i] = l;
+  }
+  __syncthreads();
+
+  double mx[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int G = p.G;
+  // rows of H and G' owned by this CTA
+  {
+    const int per = (n + G - 1) / G;
+    const int h0 = blockIdx.x * per;
+    const int nh = max(0, min(per, n - h0));
+    for (int rb0 = 0; rb0 < nh; rb0 += RB) {
+      const int nv = min(RB, nh - rb0);
+      const int row = h0 + rb0;
+      const double hy = block_rows_dot<RB>(p.H + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
+      const double gtl = block_rows_dot<RB>(p.Gt + (size_t)row * p.mpad, p.mpad, nv, s.ul, p.mpad, s.sred);
+      if (t < nv) {
+        const double gi = p.g[row + t];
+        const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
+        mx[6] = nanmax(mx[6], fabs(gi));
+        mx[1] = nanmax(mx[1], fabs(dual));
+        mx[2] = nanmax(mx[2], fabs(hy));
+        mx[3] = nanmax(mx[3], fabs(gtl));
+      }
+    }
+  }
+  // rows of G owned by this CTA
+  {
+    const int per = (m + G - 1) / G;
+    const int g0 = blockIdx.x * per;
+    const int ng = max(0, min(per, m - g0));
+    for (int rb0 = 0; rb0 < ng; rb0 += RB) {
+      const int nv = min(RB, ng - rb0);
+      const int row = g0 + rb0;
+      const double gy = block_rows_dot<RB>(p.Gr + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
+      if (t < nv) {
+        const double z = s.uz[row + t];
+        mx[0] = nanmax(mx[0], fabs(gy - z));
+        mx[4] = nanmax(mx[4], fabs(gy));
+        mx[5] = nanmax(mx[5], fabs(z));
+      }
+    }
+  }
+  // combine the RB threads that hold values, publish, exchange
+  if (t < RB) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s.sval[t * 7 + k] = mx[k];
+  }
+  __syncthreads();
+  if (t < 7) {
+    double best = 0.0;
+    for (int r = 0; r < RB; ++r) best = nanmax(best, s.sval[r * 7 + t]);
+    __stcg(p.partial + (size_t)blockIdx.x * 8 + t, best);
+  }
+  grid_barrier(p.barrier, epoch, G);
+  if (t < 7) {
+    double best = 0.0;
+    for (int b = 0; b < G; ++b) best = nanmax(best, __ldcg(p.partial + (size_t)b * 8 + t));
+    s.sval[t] = best;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 7; ++k) out[k] = s.sval[k];
+  __syncthreads();
+}
+
+// layers.cpp:38-50 with log10(grid) tabulated on the host.
+__device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L, double rho) {
+  const double target = log10(rho);
+  int best = 0;
+  double best_dist = INFINITY;
+  for (int k = 0; k < L; ++k) {
+    const double dist = fabs(log_grid[k] - target);
+    if (dist < best_dist - 1e-15) {
+      best = k;
+      best_dist = dist;
+    }
+  }
+  return best;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Smem s = carve(smem_raw, p);
+  const int t = threadIdx.x;
+  const int n = p.n, m = p.m, D = p.D;
+  const int row0 = blockIdx.x * p.R;
+  const int nrows = max(0, min(p.R, D - row0));
+  unsigned epoch = 0;
+
+  int layer = p.state[0];
+  int cur = p.state[1];
+
+  // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
+  // (layers.cpp:182-186, 223-226)
+  for (int r = t; r < nrows; r += kThreads) {
+    const int row = row0 + r;
+    double lo = -INFINITY, hi = INFINITY;
+    if (row >= n && row < n + m) {
+      lo = p.F[row - n] * p.c[row - n];
+      hi = p.F[row - n] * p.d[row - n];
+    }
+    s.slo[r] = lo;
+    s.shi[r] = hi;
+  }
+
+  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place
+  if (p.do_refresh) {
+    double* v = p.vbuf + (size_t)cur * p.Dpad;
+    for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? __ldcg(v + i) : 0.0;
+    __syncthreads();
+    const int per = (m + p.G - 1) / p.G;
+    const int g0 = blockIdx.x * per;
+    const int ng = max(0, min(per, m - g0));
+    for (int rb0 = 0; rb0 < ng; rb0 += RB) {
+      const int nv = min(RB, ng - rb0);
+      const int row = g0 + rb0;
+      const double zs = block_rows_dot<RB>(p.Gs + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
+      if (t < nv) __stcg(v + n + row + t, zs);
+    }
+    grid_barrier(p.barrier, epoch, p.G);
+  }
+
+  load_layer<RB>(p, s, layer, row0, nrows);
+
+  int n_trace = 0, n_hist = 0;
+  if (blockIdx.x == 0 && t == 0) {
+    p.trace[0] = 0;
+    p.trace[1] = layer;
+  }
+  n_trace = 1;
+
+  bool converged = false;
+  int iters_done = 0;
+  const double* Wg = p.W;  // tier 1 base
+  for (int i = 1; i <= p.total_iters; ++i) {
+    // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
+    const double* v = p.vbuf + (size_t)cur * p.Dpad;
+    double* vn = p.vbuf + (size_t)(cur ^ 1) * p.Dpad;
+    for (int c = t; c < p.Dpad; c += kThreads) s.xs[c] = (c < D) ? __ldcg(v + c) : 0.0;
+    __syncthreads();
+    const double* Wrows = p.w_smem ? s.sW : (Wg + ((size_t)layer * D + row0) * p.Dpad);
+    for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
+      const int nv = min(RB, nrows - rb0);
+      const double dot = block_rows_dot<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, s.xs, p.Dpad, s.sred);
+      if (t < nv) {
+        double x = dot + s.sb[rb0 + t];
+        const double lo = s.slo[rb0 + t], hi = s.shi[rb0 + t];
+        x = x < lo ? lo : x;
+        x = x > hi ? hi : x;
+        __stcg(vn + row0 + rb0 + t, x);
+      }
+    }
+    cur ^= 1;
+    grid_barrier(p.barrier, epoch, p.G);
+    iters_done = i;
+    if (i % p.check_interval != 0) continue;
+
+    // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
+    double nr[7];
+    residual_pass<RB>(p, s, cur, false, epoch, nr);
+    const double r_prim = nr[0], r_dual = nr[1];
+    if (blockIdx.x == 0 && t == 0 && n_hist < p.cap) {
+      p.hist_i[2 * n_hist] = i;
+      p.hist_i[2 * n_hist + 1] = layer;
+      p.hist_r[2 * n_hist] = r_prim;
+      p.hist_r[2 * n_hist + 1] = r_dual;
+    }
+    ++n_hist;
+    if (p.adaptive) {
+      const double rho_cur = p.grid[layer];
+      double rho_nom = rho_cur;
+      if (!(r_prim == 0.0 || r_dual == 0.0)) {
+        const double g_norm = nr[6];
+        double num = nr[2] < nr[3] ? nr[3] : nr[2];           // std::max({hy, gtl, ||g||, 1e-4})
+        num = num < g_norm ? g_norm : num;
+        num = num < 1e-4 ? 1e-4 : num;
+        double den = nr[4] < nr[5] ? nr[5] : nr[4];           // std::max({gy, ||z||, 1e-4})
+        den = den < 1e-4 ? 1e-4 : den;
+        rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+      }
+      const int cand_near = nearest_grid_index(p.log_grid, p.L, rho_nom);
+      const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
+      const double ratio = a < b ? b : a;
+      const int cand = ratio >= p.threshold ? cand_near : layer;
+      if (cand != layer) {
+        layer = cand;
+        if (blockIdx.x == 0 && t == 0 && n_trace < p.cap) {
+          p.trace[2 * n_trace] = i;
+          p.trace[2 * n_trace + 1] = cand;
+        }
+        ++n_trace;
+        load_layer<RB>(p, s, layer, row0, nrows);
+      }
+    }
+    if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
+      converged = true;
+      break;
+    }
+  }
+
+  // ---- epilogue (solver.cpp:90-99) ----
+  double nr[7];
+  residual_pass<RB>(p, s, cur, true, epoch, nr);
+  if (blockIdx.x == 0) {
+    for (int i = t; i < n; i += kThreads) p.out_y[i] = s.uy[i];
+    for (int i = t; i < m; i += kThreads) {
+      p.out_z[i] = s.uz[i];
+      p.out_lam[i] = s.ul[i];
+    }
+    if (t == 0) {
+      DevResultHead h;
+      h.r_prim = nr[0];
+      h.r_dual = nr[1];
+      h.iterations = iters_done;
+      h.status = (converged || (nr[0] <= p.eps_prim && nr[1] <= p.eps_dual)) ? CQP_SOLVED
+                                                                             : CQP_MAX_ITERS;
+      h.n_trace = n_trace;
+      h.n_hist = n_hist;
+      h.final_layer = layer;
+      h.final_buf = cur;
+      *p.head = h;
+      p.state[0] = layer;
+      p.state[1] = cur;
+    }
+  }
+}
+
+// ---- small helper kernels ---------------------------------------------------------------
+
+__global__ void transpose_pad_kernel(const double* __restrict__ src, int rows, int cols,
+                                     double* __restrict__ dst, int ld) {
+  // src column-major rows x cols -> dst row-major rows x ld (pad columns zeroed)
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx: column block, by: row block
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + threadIdx.x, c = bx + j;
+    tile[j][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)c * rows + r] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < rows && c < ld) dst[(size_t)r * ld + c] = tile[threadIdx.x][j];
+  }
+}
+
+__global__ void untranspose_kernel(const double* __restrict__ src, int rows, int cols, int ld,
+                                   double* __restrict__ dst) {
+  // src row-major rows x ld -> dst column-major rows x cols
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + j, c = bx + threadIdx.x;
+    tile[j][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + threadIdx.x, c = bx + j;
+    if (r < rows && c < cols) dst[(size_t)c * rows + r] = tile[threadIdx.x][j];
+  }
+}
+
+// out[row] = alpha * M[row, :] . x(scaled on the fly) ; one warp per row.
+// mode 0: x given; mode 1: x_i = cost_scale * E_i * g_i (g_s, for the bias read-back)
+__global__ void rows_dot_kernel(const double* __restrict__ M, int rows, int cols, int ld,
+                                const double* __restrict__ x, const double* __restrict__ E,
+                                double cost_scale, int mode, double alpha,
+                                double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  double acc = 0.0;
+  for (int c = lane; c < cols; c += 32) {
+    const double xv = mode ? cost_scale * (E[c] * x[c]) : x[c];
+    acc = fma(M[(size_t)warp * ld + c], xv, acc);
+  }
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+  if (lane == 0) out[warp] = alpha * acc;
+}
+
+// warm_start (solver.cpp:144-156): y_s = y / E, lambda_s = cost_scale * (lambda / F); z_s is
+// filled by the refresh kernel afterwards.
+__global__ void warm_scale_kernel(const double* __restrict__ y, const double* __restrict__ lam,
+                                  const double* __restrict__ E, const double* __restrict__ F,
+                                  double cost_scale, int n, int m, double* __restrict__ v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = y[i] / E[i];
+  if (i < m) v[n + m + i] = cost_scale * (lam[i] / F[i]);
+}
+
+__global__ void set_state_kernel(int* state, int layer, int buf) {
+  state[0] = layer;
+  state[1] = buf;
+}
+
+template <int RB>
+int launch_run_rb(cqp_handle* h, RunParams& p) {
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                h->smem_bytes));
+  void* args[] = {&p};
+  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB>, dim3(h->G), dim3(kThreads),
+                                       args, (size_t)h->smem_bytes, h->stream));
+  return CQP_OK;
+}
+
+}  // namespace
+
+int configure_launch(cqp_handle* h) {
+  const int D = h->D;
+  int G = h->num_sms;
+  int R = (D + G - 1) / G;
+  if (R < 1) R = 1;
+  G = (D + R - 1) / R;
+  h->R = R;
+  h->G = G;
+  h->rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
+  size_t need = smem_doubles(R, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
+  h->w_smem = need <= (size_t)kMaxSmemBytes ? 1 : 0;
+  if (const char* force = std::getenv("CQP_FORCE_TIER")) {  // test hook: "1" streams W from L2/HBM
+    if (force[0] == '1') h->w_smem = 0;
+  }
+  if (!h->w_smem) need = smem_doubles(R, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
+  if (need > (size_t)kMaxSmemBytes) {
+    set_error("problem too large for the persistent kernel's shared-memory vectors");
+    return CQP_ERR_CAPACITY;
+  }
+  h->smem_bytes = (int)need;
+  return CQP_OK;
+}
+
+int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh) {
+  RunParams p{};
+  p.n = h->n; p.m = h->m; p.D = h->D;
+  p.npad = h->npad; p.mpad = h->mpad; p.Dpad = h->Dpad;
+  p.L = h->L; p.R = h->R; p.G = h->G; p.w_smem = h->w_smem;
+  p.W = h->W; p.Dk = h->Dk; p.H = h->H; p.Gr = h->Gr; p.Gt = h->Gt; p.Gs = h->Gs;
+  p.E = h->E; p.F = h->F; p.cost_scale = h->cost_scale;
+  p.grid = h->dgrid; p.log_grid = h->dlog_grid;
+  p.g = h->g; p.c = h->c; p.d = h->d;
+  p.vbuf = h->vbuf; p.state = h->state; p.barrier = h->barrier; p.partial = h->partial;
+  p.eps_prim = h->s.eps_prim; p.eps_dual = h->s.eps_dual; p.threshold = h->s.rho_switch_threshold;
+  p.check_interval = h->s.check_interval; p.adaptive = h->s.adaptive_rho;
+  p.early_exit = early_exit ? 1 : 0; p.total_iters = total_iters; p.do_refresh = do_refresh ? 1 : 0;
+  p.cap = h->res_cap;
+  unsigned char* base = static_cast<unsigned char*>(h->dres);
+  p.head = reinterpret_cast<DevResultHead*>(base);
+  size_t off = sizeof(DevResultHead);
+  p.trace = reinterpret_cast<int*>(base + off); off += sizeof(int) * 2 * (size_t)h->res_cap;
+  p.hist_i = reinterpret_cast<int*>(base + off); off += sizeof(int) * 2 * (size_t)h->res_cap;
+  p.hist_r = reinterpret_cast<double*>(base + off); off += sizeof(double) * 2 * (size_t)h->res_cap;
+  p.out_y = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->n;
+  p.out_z = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  p.out_lam = reinterpret_cast<double*>(base + off);
+  CQP_CUDA(cudaMemsetAsync(h->barrier, 0, sizeof(unsigned), h->stream));
+  switch (h->rb) {
+    case 4: return launch_run_rb<4>(h, p);
+    case 8: return launch_run_rb<8>(h, p);
+    default: return launch_run_rb<16>(h, p);
+  }
+}
+
+int launch_refresh_z(cqp_handle* h, int buf) {
+  double* v = h->vbuf + (size_t)buf * h->Dpad;
+  const int threads = 256, rows_per_block = threads / 32;
+  rows_dot_kernel<<<(h->m + rows_per_block - 1) / rows_per_block, threads, 0, h->stream>>>(
+      h->Gs, h->m, h->n, h->npad, v, nullptr, 1.0, 0, 1.0, v + h->n);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index) {
+  CQP_CUDA(cudaMemsetAsync(h->vbuf, 0, sizeof(double) * 2 * (size_t)h->Dpad, h->stream));
+  const int cnt = h->n > h->m ? h->n : h->m;
+  warm_scale_kernel<<<(cnt + 255) / 256, 256, 0, h->stream>>>(dy, dlam, h->E, h->F, h->cost_scale,
+                                                             h->n, h->m, h->vbuf);
+  CQP_CUDA(cudaGetLastError());
+  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer_index, 0);
+  CQP_CUDA(cudaGetLastError());
+  return launch_refresh_z(h, 0);
+}
+
+int launch_set_state(cqp_handle* h, int layer, int buf) {
+  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer, buf);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+int launch_transpose_pad(cudaStream_t st, const double* src, int rows, int cols, double* dst,
+                         int ld) {
+  dim3 grid((ld + 31) / 32, (rows + 31) / 32), block(32, 8);
+  transpose_pad_kernel<<<grid, block, 0, st>>>(src, rows, cols, dst, ld);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+int launch_untranspose(cudaStream_t st, const double* src, int rows, int cols, int ld,
+                       double* dst) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  untranspose_kernel<<<grid, block, 0, st>>>(src, rows, cols, ld, dst);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+int launch_bias(cqp_handle* h, int k, double* b_out) {
+  const int nm = h->n + h->m;
+  CQP_CUDA(cudaMemsetAsync(b_out, 0, sizeof(double) * (size_t)h->D, h->stream));
+  const int threads = 256, rows_per_block = threads / 32;
+  rows_dot_kernel<<<(nm + rows_per_block - 1) / rows_per_block, threads, 0, h->stream>>>(
+      h->Dk + (size_t)k * nm * h->npad, nm, h->n, h->npad, h->g, h->E, h->cost_scale, 1, -1.0,
+      b_out);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+}  // namespace cqp

@@ -1,0 +1,272 @@
+"""Host-side mirror of the reference's `clampqp::Solver` over the C ABI (include/cqp_b200.h).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/clampqp/solver.hpp:107-135 and the Python module the reference
+ships (python/bindings.cpp:101-112), so tests read like the reference's own.  All compute runs
+in libcqp_b200.so on the GPU; this file only marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import CqpResidualSample, CqpResult, CqpRhoSwitch, CqpSettings, c_double_p
+
+SOLVED, MAX_ITERS, INVALID = 0, 1, 2  # SolveStatus, problem.hpp:51
+
+
+class ProblemError(RuntimeError):
+    """problem.hpp:73-92."""
+    CODES = {1: "DimensionMismatch", 2: "NonSymmetricH", 3: "NonPositiveDefiniteH",
+             4: "InvertedBounds", 5: "NonFiniteEntry"}
+
+    def __init__(self, code: int, msg: str):
+        self.code = self.CODES.get(code, str(code))
+        super().__init__(f"{self.code}: {msg}")
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc: int) -> None:
+    """Map cqp_status onto the reference's exception types."""
+    if rc == 0:
+        return
+    msg = _lib.last_error()
+    if 1 <= rc <= 5:
+        raise ProblemError(rc, msg)
+    if rc in (6, 8):
+        raise ValueError(msg)              # std::invalid_argument
+    if rc == 7:
+        raise RuntimeError(msg)            # std::runtime_error (factorisation)
+    if rc == 10:
+        raise MemoryError(msg)
+    raise CudaError(msg)
+
+
+@dataclass
+class SolverSettings:
+    """solver.hpp:43-53 (identical defaults)."""
+    eps_prim: float = 1e-6
+    eps_dual: float = 1e-6
+    check_interval: int = 25
+    max_iters: int = 4000
+    sigma: float = 1e-6
+    grid_points: int = 13
+    rho_switch_threshold: float = 5.0
+    adaptive_rho: bool = True
+    eq_enabled: bool = True
+    eq_max_passes: int = 10
+    eq_tol: float = 1e-3
+
+    def _c(self) -> CqpSettings:
+        return CqpSettings(self.eps_prim, self.eps_dual, self.check_interval, self.max_iters,
+                           self.sigma, self.grid_points, self.rho_switch_threshold,
+                           int(self.adaptive_rho), int(self.eq_enabled), self.eq_max_passes,
+                           self.eq_tol)
+
+
+@dataclass
+class Solution:
+    """problem.hpp:62-71."""
+    y: np.ndarray
+    z: np.ndarray
+    lam: np.ndarray
+    status: int = INVALID
+    iterations: int = 0
+    r_prim: float = 0.0
+    r_dual: float = 0.0
+    rho_trace: List[Tuple[int, int]] = field(default_factory=list)
+
+
+@dataclass
+class SolveReport:
+    """solver.hpp:63-67 (+ the kernel-only CUDA-event time)."""
+    solution: Solution
+    wall_ms: float = 0.0
+    residual_history: List[Tuple[int, float, float, int]] = field(default_factory=list)
+    kernel_us: float = 0.0
+
+
+def _vec(a, size: Optional[int] = None, name: str = "vector") -> np.ndarray:
+    v = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    if size is not None and v.size != size:
+        raise ValueError(f"{name}: dimension mismatch")
+    return v
+
+
+def _mat(a) -> np.ndarray:
+    return np.asfortranarray(np.atleast_2d(np.asarray(a, dtype=np.float64)))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(c_double_p)
+
+
+class Solver:
+    """GPU `clampqp::Solver`: build once, then solve / update_vectors + refresh_z + fixed_iters."""
+
+    def __init__(self, H, g, G, c, d, settings: Optional[SolverSettings] = None,
+                 device: int = -1, layers: Optional[dict] = None):
+        """Solver(QProblem, SolverSettings) (solver.cpp:180-186).
+
+        `layers`: optional precomputed LayerCache fields (W, D, GD lists, grid, initial_index,
+        Gs, E, F, cost_scale) -> cqp_create_from_layers; otherwise the offline stage runs on
+        the device (cqp_create)."""
+        self._L = _lib.load()
+        self._h = C.c_void_p()
+        self.settings = settings or SolverSettings()
+        H, G = _mat(H), _mat(G)
+        g, c, d = _vec(g), _vec(c), _vec(d)
+        n, m = H.shape[0], G.shape[0]
+        if (n < 1 or m < 1 or H.shape[1] != n or g.size != n or G.shape[1] != n or c.size != m
+                or d.size != m):
+            raise ProblemError(1, "inconsistent problem dimensions")
+        self.n, self.m = n, m
+        cs = self.settings._c()
+        if layers is None:
+            rc = self._L.cqp_create(C.byref(self._h), n, m, _p(H), _p(g), _p(G), _p(c), _p(d),
+                                    C.byref(cs), device)
+        else:
+            Lk = len(layers["W"])
+            keep = []
+
+            def ptr_array(mats):
+                arr = (c_double_p * Lk)()
+                for k, a in enumerate(mats):
+                    a = _mat(a)
+                    keep.append(a)
+                    arr[k] = _p(a)
+                return arr
+
+            Wp, Dp, GDp = ptr_array(layers["W"]), ptr_array(layers["D"]), ptr_array(layers["GD"])
+            grid = _vec(layers["grid"], Lk)
+            Gs, E, F = _mat(layers["Gs"]), _vec(layers["E"], n), _vec(layers["F"], m)
+            rc = self._L.cqp_create_from_layers(
+                C.byref(self._h), n, m, Lk, Wp, Dp, GDp, _p(grid), int(layers["initial_index"]),
+                _p(H), _p(g), _p(G), _p(c), _p(d), _p(Gs), _p(E), _p(F),
+                C.c_double(float(layers["cost_scale"])), C.byref(cs), device)
+        if rc:
+            self._h = C.c_void_p()
+            _raise(rc)
+        Lc = C.c_int()
+        self._L.cqp_dims(self._h, None, None, C.byref(Lc))
+        self.L = Lc.value
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), C.c_void_p()
+        if h:
+            self._L.cqp_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- solver.hpp:111-121 ----
+    def cold_start(self) -> None:
+        _raise(self._L.cqp_cold_start(self._h))
+
+    def warm_start(self, prev: Solution) -> None:
+        y, lam = _vec(prev.y), _vec(prev.lam)
+        if y.size != self.n or lam.size != self.m:
+            raise ValueError("warm_start: dimension mismatch")
+        last = prev.rho_trace[-1][1] if prev.rho_trace else -1
+        _raise(self._L.cqp_warm_start(self._h, _p(y), _p(lam), last))
+
+    def refresh_z(self) -> None:
+        _raise(self._L.cqp_refresh_z(self._h))
+
+    def update_vectors(self, g, c, d) -> None:
+        g = _vec(g, self.n, "update_vectors")
+        c = _vec(c, self.m, "update_vectors")
+        d = _vec(d, self.m, "update_vectors")
+        _raise(self._L.cqp_update_vectors(self._h, _p(g), _p(c), _p(d)))
+
+    def _result(self, cap: int):
+        y, z, lam = np.empty(self.n), np.empty(self.m), np.empty(self.m)
+        trace = (CqpRhoSwitch * cap)()
+        hist = (CqpResidualSample * cap)()
+        res = CqpResult(_p(y), _p(z), _p(lam), trace, cap, 0, hist, cap, 0, INVALID, 0, 0.0, 0.0,
+                        0.0, 0.0)
+        return res, (y, z, lam, trace, hist)
+
+    @staticmethod
+    def _report(res: CqpResult, bufs) -> SolveReport:
+        y, z, lam, trace, hist = bufs
+        nt = min(res.rho_trace_len, res.rho_trace_cap)
+        nh = min(res.history_len, res.history_cap)
+        sol = Solution(y, z, lam, res.status, res.iterations, res.r_prim, res.r_dual,
+                       [(trace[i].iteration, trace[i].grid_index) for i in range(nt)])
+        return SolveReport(sol, res.wall_ms,
+                           [(hist[i].iteration, hist[i].r_prim, hist[i].r_dual, hist[i].grid_index)
+                            for i in range(nh)], res.kernel_us)
+
+    def solve(self) -> SolveReport:
+        s = self.settings
+        res, bufs = self._result(s.max_iters // s.check_interval + 2)
+        _raise(self._L.cqp_solve(self._h, C.byref(res)))
+        return self._report(res, bufs)
+
+    def fixed_iters(self, k: int) -> SolveReport:
+        if k < 1:
+            raise ValueError("fixed_iters: k must be >= 1")
+        res, bufs = self._result(k // self.settings.check_interval + 2)
+        _raise(self._L.cqp_fixed_iters(self._h, int(k), C.byref(res)))
+        return self._report(res, bufs)
+
+    def mpc_step(self, g, c, d, k: int) -> SolveReport:
+        """update_vectors + refresh_z + fixed_iters(k) as one upload + one launch
+        (the per-step protocol of bench.cpp:157-167)."""
+        if k < 1:
+            raise ValueError("mpc_step: k must be >= 1")
+        g = _vec(g, self.n, "mpc_step")
+        c = _vec(c, self.m, "mpc_step")
+        d = _vec(d, self.m, "mpc_step")
+        res, bufs = self._result(k // self.settings.check_interval + 2)
+        _raise(self._L.cqp_mpc_step(self._h, _p(g), _p(c), _p(d), int(k), C.byref(res)))
+        return self._report(res, bufs)
+
+    # ---- accessors, solver.hpp:123-127 ----
+    @property
+    def state(self) -> np.ndarray:
+        v = np.empty(self.n + 2 * self.m)
+        _raise(self._L.cqp_get_state(self._h, _p(v), None))
+        return v
+
+    @property
+    def layer_index(self) -> int:
+        idx = C.c_int()
+        _raise(self._L.cqp_get_state(self._h, None, C.byref(idx)))
+        return idx.value
+
+    def layer(self, k: int) -> dict:
+        """cache().layers[k]: W, D, GD, b (for the current g), rho_vec."""
+        n, m = self.n, self.m
+        dim = n + 2 * m
+        W = np.empty((dim, dim), order="F"); D = np.empty((n, n), order="F")
+        GD = np.empty((m, n), order="F"); b = np.empty(dim); rho = np.empty(m)
+        _raise(self._L.cqp_get_layer(self._h, k, _p(W), _p(D), _p(GD), _p(b), _p(rho)))
+        return {"W": W, "D": D, "GD": GD, "b": b, "rho_vec": rho}
+
+    def scaling(self) -> dict:
+        """cache().scaling, grid and clamp bounds."""
+        n, m = self.n, self.m
+        E, F, grid = np.empty(n), np.empty(m), np.empty(self.L)
+        lo, hi = np.empty(n + 2 * m), np.empty(n + 2 * m)
+        cs, idx = C.c_double(), C.c_int()
+        _raise(self._L.cqp_get_scaling(self._h, _p(E), _p(F), C.byref(cs), _p(grid), C.byref(idx),
+                                       _p(lo), _p(hi)))
+        return {"E": E, "F": F, "cost_scale": cs.value, "grid": grid, "initial_index": idx.value,
+                "c_tilde": lo, "d_tilde": hi}
+
+    def launch_info(self) -> dict:
+        a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _raise(self._L.cqp_launch_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return {"ctas": a.value, "rows_per_cta": b.value, "tier": c.value, "smem_bytes": d.value}

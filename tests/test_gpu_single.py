@@ -1,0 +1,351 @@
+"""GPU parity tests of the single-QP path, through the C ABI (libcqp_b200.so) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): identical iteration counts and rho-switch sequence in FP64;
+primal and dual solutions within 1e-6 relative.  Residual samples are compared to 1e-7
+relative (they are sums of O(n) FP64 terms in a different order).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REL_SOL = 1e-6     # north_star tolerance on y and lambda
+REL_RES = 1e-6     # residual samples (different summation order, amplified near convergence)
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2311_18056_b200 import solver as S
+    from paper_2311_18056_b200 import _lib
+    if _lib.load().cqp_device_count() < 1:
+        pytest.fail("no CUDA device: the solve path has no CPU fallback")
+    return S
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2311_18056_b200 import problems
+    return problems
+
+
+def oracle_layers(cache):
+    return {"W": [cache.W(k) for k in range(cache.L)], "D": [cache.D(k) for k in range(cache.L)],
+            "GD": [cache.GD(k) for k in range(cache.L)], "grid": cache.grid,
+            "initial_index": cache.initial_index, "Gs": cache.Gs, "E": cache.E, "F": cache.F,
+            "cost_scale": cache.cost_scale}
+
+
+def settings_pair(O, S, **kw):
+    return O.SolverSettings(**kw), S.SolverSettings(**kw)
+
+
+def rel_err(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(1.0, np.abs(np.asarray(b)).max()))
+
+
+def assert_report_parity(rg, ro, sol_tol=REL_SOL):
+    sg, so = rg.solution, ro.solution
+    assert sg.iterations == so.iterations
+    assert sg.status == so.status
+    assert sg.rho_trace == so.rho_trace
+    assert [(h[0], h[3]) for h in rg.residual_history] == [(h[0], h[3]) for h in ro.residual_history]
+    for hg, ho in zip(rg.residual_history, ro.residual_history):
+        assert abs(hg[1] - ho[1]) <= REL_RES * max(abs(ho[1]), 1e-9) + 1e-12
+        assert abs(hg[2] - ho[2]) <= REL_RES * max(abs(ho[2]), 1e-9) + 1e-12
+    assert rel_err(sg.y, so.y) <= sol_tol
+    assert rel_err(sg.lam, so.lam) <= sol_tol
+    assert rel_err(sg.z, so.z) <= sol_tol
+
+
+def make_pair(O, S, p, so=None, sg=None, from_layers=True):
+    """(gpu solver, oracle solver) on the same problem; with from_layers the GPU gets the
+    oracle's ladder so the ONLY difference is the online loop."""
+    so = so or O.SolverSettings()
+    sg = sg or S.SolverSettings()
+    osolver = O.Solver(O.QProblem(p.H, p.g, p.G, p.c, p.d), so, variant="ref")
+    layers = oracle_layers(osolver.cache) if from_layers else None
+    gsolver = S.Solver(p.H, p.g, p.G, p.c, p.d, sg, layers=layers)
+    return gsolver, osolver
+
+
+# ---- known answers of the reference, on the GPU path --------------------------------------------
+def test_1d_hand_worked_iterate(G, oracle):
+    # tests/test_solver.cpp:58-72 / SPEC.md:212: sigma = 0, rho = 1: one iterate from 0 = [2/3, .5, 0]
+    O = oracle
+    D = O.build_kkt_inverse([[2.0]], [[1.0]], 0.0, [1.0])
+    W, GD, b = O.build_layer([[2.0]], [[1.0]], [-2.0], 0.0, [1.0], D)
+    layers = {"W": [W, W], "D": [D, D], "GD": [GD, GD], "grid": [1.0, 10.0], "initial_index": 0,
+              "Gs": [[1.0]], "E": [1.0], "F": [1.0], "cost_scale": 1.0}
+    s = G.Solver([[2.0]], [-2.0], [[1.0]], [0.0], [0.5], G.SolverSettings(adaptive_rho=False),
+                 layers=layers)
+    got = s.layer(0)
+    expected = np.array([[-1 / 3, 2 / 3, -1 / 3], [2 / 3, -1 / 3, 2 / 3], [1.0, -1.0, 1.0]])
+    assert np.abs(got["W"] - expected).max() < 1e-15          # tests/test_layers.cpp:191-207
+    assert np.abs(got["b"] - np.array([2 / 3, 2 / 3, 0.0])).max() < 1e-15
+    s.fixed_iters(1)
+    v = s.state
+    assert v[0] == pytest.approx(2.0 / 3.0, rel=1e-14)
+    assert v[1] == 0.5
+    assert v[2] == 0.0
+
+
+def test_three_1d_kkt_solves(G):
+    # tests/test_solver.cpp:175-209
+    st = G.SolverSettings(eps_prim=1e-8, eps_dual=1e-8, max_iters=20000)
+    sol = G.Solver([[2.0]], [-2.0], [[1.0]], [0.0], [0.5], st).solve().solution
+    assert sol.status == G.SOLVED
+    assert sol.y[0] == pytest.approx(0.5, rel=1e-6) and sol.lam[0] == pytest.approx(1.0, rel=1e-6)
+    sol = G.Solver([[1.0]], [0.0], [[1.0]], [1.0], [1.0], st).solve().solution
+    assert sol.status == G.SOLVED
+    assert sol.y[0] == pytest.approx(1.0, rel=1e-6) and sol.lam[0] == pytest.approx(-1.0, rel=1e-6)
+    sol = G.Solver([[2.0]], [-2.0], [[1.0]], [-10.0], [10.0], st).solve().solution
+    assert sol.status == G.SOLVED
+    assert sol.y[0] == pytest.approx(1.0, rel=1e-6) and abs(sol.lam[0]) < 1e-6
+
+
+def test_1d_solves_match_oracle_exactly_in_counts(G, oracle):
+    for (H, g, c, d) in [(2.0, -2.0, 0.0, 0.5), (1.0, 0.0, 1.0, 1.0), (2.0, -2.0, -10.0, 10.0)]:
+        kw = dict(eps_prim=1e-8, eps_dual=1e-8, max_iters=20000)
+        so, sg = settings_pair(oracle, G, **kw)
+        p = oracle.QProblem([[H]], [g], [[1.0]], [c], [d])
+        gs, os_ = make_pair(oracle, G, p, so, sg, from_layers=False)
+        assert_report_parity(gs.solve(), os_.solve())
+
+
+# ---- parity on the reference's random dense QP family (equality rows -> rho switches) -----------
+@pytest.mark.parametrize("n,seeds", [(8, range(4)), (20, range(4)), (50, range(3)), (200, range(2))])
+def test_dense_qp_parity_with_oracle_ladder(G, oracle, n, seeds):
+    for seed in seeds:
+        p = oracle.gen_random_dense_qp(n, seed)
+        gs, os_ = make_pair(oracle, G, p, from_layers=True)
+        assert_report_parity(gs.solve(), os_.solve())
+
+
+@pytest.mark.parametrize("n,seeds", [(12, range(3)), (50, range(2)), (200, range(1))])
+def test_dense_qp_parity_with_device_offline_stage(G, oracle, n, seeds):
+    for seed in seeds:
+        p = oracle.gen_random_dense_qp(n, seed)
+        gs, os_ = make_pair(oracle, G, p, from_layers=False)
+        # offline stage: every W / D / GD against the oracle (tests/test_layers.cpp:265-274);
+        # the two stiffest grid points are ill-conditioned (see test_oracle_known_answers.py)
+        sc = gs.scaling()
+        assert np.array_equal(sc["E"], os_.cache.E) and np.array_equal(sc["F"], os_.cache.F)
+        assert sc["cost_scale"] == os_.cache.cost_scale
+        assert sc["initial_index"] == os_.cache.initial_index
+        assert np.array_equal(sc["grid"], os_.cache.grid)
+        assert np.array_equal(sc["c_tilde"], os_.cache.c_tilde)
+        for k in range(gs.L):
+            lay = gs.layer(k)
+            tol = 1e-10 if os_.cache.grid[k] <= 1.0 else 1e-7
+            assert np.abs(lay["W"] - os_.cache.W(k)).max() <= tol * max(1.0, np.abs(os_.cache.W(k)).max())
+            assert np.abs(lay["D"] - os_.cache.D(k)).max() <= tol * max(1.0, np.abs(os_.cache.D(k)).max())
+            assert np.array_equal(lay["rho_vec"], os_.cache.rho_vec(k))
+            assert np.abs(lay["b"] - os_.cache.b(k)).max() <= tol * max(1.0, np.abs(os_.cache.b(k)).max())
+        assert_report_parity(gs.solve(), os_.solve())
+
+
+# ---- the BASELINE.json MPC configs ---------------------------------------------------------------
+@pytest.mark.parametrize("nu,hard,unstable", [(10, 1.0, False), (10, 10.0, False), (10, 10.0, True),
+                                             (30, 1.0, False), (30, 10.0, False), (50, 10.0, False)])
+def test_random_mpc_parity(G, oracle, P, nu, hard, unstable):
+    wl = P.config2(nu, seed=0, unstable=unstable)
+    base = wl.base_problem()
+    gs, os_ = make_pair(oracle, G, base, from_layers=True)
+    q = wl.problem_at(wl.x0(hard))
+    for s in (gs, os_):
+        s.update_vectors(q.g, q.c, q.d)
+        s.cold_start()
+    rg, ro = gs.solve(), os_.solve()
+    assert ro.solution.status == oracle.SOLVED
+    assert_report_parity(rg, ro)
+    # size-independent property: the returned point satisfies the KKT residual bound itself
+    y, z, lam = rg.solution.y, rg.solution.z, rg.solution.lam
+    assert np.abs(q.G @ y - z).max() <= 1e-6 and np.abs(q.H @ y + q.g + q.G.T @ lam).max() <= 1e-6
+    assert np.all(z >= q.c) and np.all(z <= q.d)
+
+
+def test_mpc_device_offline_stage_counts(G, oracle, P):
+    wl = P.config2(30, seed=1)
+    base = wl.base_problem()
+    gs, os_ = make_pair(oracle, G, base, from_layers=False)
+    q = wl.problem_at(wl.x0(10.0))
+    for s in (gs, os_):
+        s.update_vectors(q.g, q.c, q.d)
+        s.cold_start()
+    assert_report_parity(gs.solve(), os_.solve())
+
+
+# ---- structural tests of the reference ----------------------------------------------------------
+def test_fixed_iters_composes_and_history(G, oracle):
+    # tests/test_solver.cpp:211-233, 378-388
+    p = oracle.gen_random_dense_qp(8, 6)
+    kw = dict(adaptive_rho=False, eq_enabled=False)
+    so, sg = settings_pair(oracle, G, **kw)
+    gs, os_ = make_pair(oracle, G, p, so, sg)
+    cache = os_.cache
+    k0 = cache.initial_index
+    W, b = cache.W(k0), cache.b(k0)
+    one = gs.fixed_iters(1)
+    v1 = oracle.iterate(np.zeros(16), W, b, cache.c_tilde, cache.d_tilde)
+    assert rel_err(one.solution.y, v1[:8]) <= 1e-13 and one.solution.iterations == 1
+    gs.cold_start()
+    many = gs.fixed_iters(25)
+    assert many.solution.iterations == 25 and len(many.residual_history) == 1
+    # k calls of fixed_iters(1) == one call of fixed_iters(k), bit for bit (persistent iterate)
+    gs.cold_start()
+    for _ in range(25):
+        gs.fixed_iters(1)
+    v_steps = gs.state
+    gs.cold_start()
+    gs.fixed_iters(25)
+    assert np.array_equal(gs.state, v_steps)
+    p13 = oracle.gen_random_dense_qp(8, 13)
+    gs2, _ = make_pair(oracle, G, p13, oracle.SolverSettings(adaptive_rho=False),
+                       G.SolverSettings(adaptive_rho=False))
+    rep = gs2.fixed_iters(100)
+    assert [h[0] for h in rep.residual_history] == [25, 50, 75, 100]
+
+
+def test_rho_trace_structure_and_persistent_index(G, oracle):
+    # tests/test_solver.cpp:390-401 + semantics 2/6 of SURVEY.md section 8(a)
+    p = oracle.gen_random_dense_qp(16, 14)
+    gs, os_ = make_pair(oracle, G, p)
+    rg, ro = gs.solve(), os_.solve()
+    tr = rg.solution.rho_trace
+    assert tr[0] == (0, os_.cache.initial_index)
+    for i in range(1, len(tr)):
+        assert tr[i][0] % 25 == 0 and tr[i][1] != tr[i - 1][1]
+    assert gs.layer_index == os_.layer_index == tr[-1][1]
+    # a second solve() continues from the persistent state (solver.cpp:202-205)
+    assert_report_parity(gs.solve(), os_.solve())
+
+
+def test_identical_solves_bit_for_bit(G, oracle):
+    # tests/test_solver.cpp:318-334
+    p = oracle.gen_random_dense_qp(20, 11)
+    a, _ = make_pair(oracle, G, p)
+    b, _ = make_pair(oracle, G, p)
+    ra, rb = a.solve(), b.solve()
+    assert np.array_equal(ra.solution.y, rb.solution.y)
+    assert np.array_equal(ra.solution.z, rb.solution.z)
+    assert np.array_equal(ra.solution.lam, rb.solution.lam)
+    assert ra.solution.iterations == rb.solution.iterations
+    assert ra.residual_history == rb.residual_history
+    a.cold_start()
+    rc = a.solve()
+    assert np.array_equal(ra.solution.y, rc.solution.y) and ra.residual_history == rc.residual_history
+
+
+def test_warm_start_mapping(G, oracle):
+    # tests/test_solver.cpp:139-173
+    p = oracle.gen_random_dense_qp(8, 4)
+    gs, os_ = make_pair(oracle, G, p, oracle.SolverSettings(grid_points=7), G.SolverSettings(grid_points=7))
+    rng = oracle.Rng(5)
+    prev_o = oracle.Solution(y=rng.normal_vector(8), lam=rng.normal_vector(4), z=np.full(4, 123.0),
+                             rho_trace=[(0, 2), (50, 4)])
+    prev_g = G.Solution(prev_o.y, prev_o.z, prev_o.lam, rho_trace=prev_o.rho_trace)
+    gs.warm_start(prev_g)
+    os_.warm_start(prev_o)
+    assert gs.layer_index == 4 == os_.layer_index
+    assert rel_err(gs.state, os_.state) <= 1e-14
+    with pytest.raises(ValueError):
+        gs.warm_start(G.Solution(np.zeros(3), np.zeros(4), np.zeros(4)))
+    gs.warm_start(G.Solution(np.zeros(8), np.zeros(4), np.zeros(4), rho_trace=[(0, 2)]))
+    assert np.all(gs.state == 0.0) and gs.layer_index == 2
+
+
+def test_validation_and_argument_errors(G):
+    # tests/test_problem.cpp validate codes; tests/test_solver.cpp:362-376
+    with pytest.raises(G.ProblemError) as e:
+        G.Solver([[1.0, 0.5], [0.0, 1.0]], [0.0, 0.0], [[1.0, 0.0]], [0.0], [1.0])
+    assert e.value.code == "NonSymmetricH"
+    with pytest.raises(G.ProblemError) as e:
+        G.Solver([[-1.0]], [0.0], [[1.0]], [0.0], [1.0])
+    assert e.value.code == "NonPositiveDefiniteH"
+    with pytest.raises(G.ProblemError) as e:
+        G.Solver([[1.0]], [0.0], [[1.0]], [1.0], [0.0])
+    assert e.value.code == "InvertedBounds"
+    with pytest.raises(G.ProblemError) as e:
+        G.Solver([[1.0]], [float("nan")], [[1.0]], [0.0], [1.0])
+    assert e.value.code == "NonFiniteEntry"
+    with pytest.raises(G.ProblemError) as e:
+        G.Solver([[1.0]], [0.0, 1.0], [[1.0]], [0.0], [1.0])
+    assert e.value.code == "DimensionMismatch"
+    with pytest.raises(ValueError):
+        G.Solver([[1.0]], [0.0], [[1.0]], [0.0], [1.0], G.SolverSettings(check_interval=0))
+    with pytest.raises(ValueError):
+        G.Solver([[1.0]], [0.0], [[1.0]], [0.0], [1.0], G.SolverSettings(max_iters=10))
+    with pytest.raises(ValueError):
+        G.Solver([[1.0]], [0.0], [[1.0]], [0.0], [1.0], G.SolverSettings(grid_points=1))
+    s = G.Solver([[1.0]], [0.0], [[1.0]], [0.0], [1.0])
+    with pytest.raises(ValueError):
+        s.fixed_iters(0)
+    with pytest.raises(ValueError):
+        s.update_vectors([0.0, 1.0], [0.0], [1.0])
+
+
+def test_infinite_bounds_pass_through(G, oracle):
+    # +-inf bounds survive scaling and the clamp
+    p = oracle.gen_random_dense_qp(12, 3)
+    p.c[7] = -np.inf
+    p.d[8] = np.inf
+    p.c[9], p.d[9] = -np.inf, np.inf
+    gs, os_ = make_pair(oracle, G, p)
+    assert_report_parity(gs.solve(), os_.solve())
+
+
+def test_max_iters_status(G, oracle):
+    p = oracle.gen_random_dense_qp(50, 1)
+    kw = dict(eps_prim=1e-13, eps_dual=1e-13, max_iters=100)
+    so, sg = settings_pair(oracle, G, **kw)
+    gs, os_ = make_pair(oracle, G, p, so, sg)
+    rg, ro = gs.solve(), os_.solve()
+    assert rg.solution.status == G.MAX_ITERS == ro.solution.status
+    assert rg.solution.iterations == 100 and len(rg.residual_history) == 4
+    assert rg.solution.rho_trace == ro.solution.rho_trace
+
+
+# ---- MPC step protocol (bench.cpp:157-185): update_vectors + refresh_z + fixed_iters(k) ---------
+@pytest.mark.parametrize("k", [1, 2, 15])
+def test_closed_loop_protocol_matches_oracle(G, oracle, P, k):
+    wl = P.config1(seed=3)
+    base = wl.base_problem()
+    gs, os_ = make_pair(oracle, G, base)
+    gs2, _ = make_pair(oracle, G, base)
+    x = wl.x0(1.0)
+    A, B, K = wl.sys.A, wl.sys.B, wl.tmpl.K
+    nu = wl.sys.nu
+    for step in range(25):
+        q = wl.problem_at(x)
+        os_.update_vectors(q.g, q.c, q.d); os_.refresh_z(); ro = os_.fixed_iters(k)
+        gs.update_vectors(q.g, q.c, q.d); gs.refresh_z(); rg = gs.fixed_iters(k)
+        rf = gs2.mpc_step(q.g, q.c, q.d, k)          # fused single-launch step
+        assert rg.solution.iterations == k == ro.solution.iterations
+        assert rel_err(rg.solution.y, ro.solution.y) <= 1e-9
+        assert rel_err(rg.solution.lam, ro.solution.lam) <= 1e-9
+        assert abs(rg.solution.r_prim - ro.solution.r_prim) <= 1e-9 * max(1.0, ro.solution.r_prim)
+        assert abs(rg.solution.r_dual - ro.solution.r_dual) <= 1e-9 * max(1.0, ro.solution.r_dual)
+        assert np.array_equal(rf.solution.y, rg.solution.y)      # fused == 3 calls, bit for bit
+        assert np.array_equal(rf.solution.lam, rg.solution.lam)
+        assert rf.solution.r_prim == rg.solution.r_prim
+        u = np.clip(-K @ x + ro.solution.y[:nu], -1.0, 1.0)
+        x = A @ x + B @ u
+
+
+# ---- tiers ---------------------------------------------------------------------------------------
+def test_streaming_tier_equals_resident_tier(G, oracle, P, monkeypatch):
+    wl = P.config2(14, seed=2)
+    base = wl.base_problem()
+    q = wl.problem_at(wl.x0(10.0))
+    reports = []
+    for tier in ("0", "1"):
+        monkeypatch.setenv("CQP_FORCE_TIER", tier)
+        s, os_ = make_pair(oracle, G, base)
+        assert s.launch_info()["tier"] == int(tier)
+        s.update_vectors(q.g, q.c, q.d); s.cold_start()
+        reports.append(s.solve())
+    monkeypatch.delenv("CQP_FORCE_TIER")
+    a, b = reports
+    assert np.array_equal(a.solution.y, b.solution.y) and a.residual_history == b.residual_history
+    os_.update_vectors(q.g, q.c, q.d); os_.cold_start()
+    assert_report_parity(a, os_.solve())
