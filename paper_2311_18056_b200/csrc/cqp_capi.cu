@@ -109,7 +109,7 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->g, nm + m))) return rc;
   h->c = h->g + n;
   h->d = h->c + m;
-  if ((rc = dev_alloc(&h->vbuf, 2 * (size_t)h->Dpad))) return rc;
+  if ((rc = dev_alloc(&h->vq, 4 * (size_t)h->Dpad))) return rc;
   if ((rc = dev_alloc(&h->state, 2))) return rc;
   if ((rc = dev_alloc(&h->barrier, 1))) return rc;
   if ((rc = dev_alloc(&h->partial, 8 * (size_t)(h->num_sms + 1)))) return rc;
@@ -150,8 +150,10 @@ int upload_vectors(cqp_handle* h, const double* g, const double* c, const double
 }
 
 int cold_start(cqp_handle* h) {
-  CQP_CUDA(cudaMemsetAsync(h->vbuf, 0, sizeof(double) * 2 * (size_t)h->Dpad, h->stream));
-  return launch_set_state(h, h->initial_index, 0);
+  // ring invariant between launches: slot 0 = iterate (zero), slots 1..3 = sentinel (all ones)
+  CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemsetAsync(h->vq + h->Dpad, 0xFF, sizeof(double) * 3 * (size_t)h->Dpad, h->stream));
+  return launch_set_state(h, h->initial_index);
 }
 
 }  // namespace cqp
@@ -250,7 +252,7 @@ void cqp_destroy(cqp_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->W); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
   cudaFree(h->Gs); cudaFree(h->E); cudaFree(h->F); cudaFree(h->dgrid); cudaFree(h->dlog_grid);
-  cudaFree(h->g); cudaFree(h->vbuf); cudaFree(h->state); cudaFree(h->barrier);
+  cudaFree(h->g); cudaFree(h->vq); cudaFree(h->state); cudaFree(h->barrier);
   cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp); cudaFree(h->dres);
   if (h->hres) cudaFreeHost(h->hres);
   if (h->hstage) cudaFreeHost(h->hstage);
@@ -292,10 +294,7 @@ int cqp_warm_start(cqp_handle* h, const double* y, const double* lambda, int lay
 int cqp_refresh_z(cqp_handle* h) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
-  int st[2];
-  CQP_CUDA(cudaMemcpyAsync(st, h->state, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
-  CQP_CUDA(cudaStreamSynchronize(h->stream));
-  return launch_refresh_z(h, st[1]);
+  return launch_refresh_z(h);
 }
 
 static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out) {
@@ -370,12 +369,12 @@ int cqp_mpc_step(cqp_handle* h, const double* g, const double* c, const double* 
 int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
-  int st[2];
+  int st[1];
   CQP_CUDA(cudaMemcpyAsync(st, h->state, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
   CQP_CUDA(cudaStreamSynchronize(h->stream));
   if (layer_index) *layer_index = st[0];
   if (v) {
-    CQP_CUDA(cudaMemcpyAsync(v, h->vbuf + (size_t)st[1] * h->Dpad, sizeof(double) * h->D,
+    CQP_CUDA(cudaMemcpyAsync(v, h->vq, sizeof(double) * h->D,
                              cudaMemcpyDeviceToHost, h->stream));
     CQP_CUDA(cudaStreamSynchronize(h->stream));
   }

