@@ -170,6 +170,10 @@ CQP_API int cqp_get_scaling(cqp_handle *h, double *E, double *F, double *cost_sc
 
 CQP_API int cqp_dims(const cqp_handle *h, int *n, int *m, int *L);
 
+/* Diagnostics: the 64-int host-mapped watchdog record of the persistent kernel (word 0 != 0
+ * after a watchdog trap: 1 = where, 2 = iteration, 3 = CTA, 4 = thread). */
+CQP_API int cqp_debug_words(const cqp_handle *h, int *out64);
+
 /* How the persistent kernel was configured: CTAs, rows of W per CTA, tier (0: W slice
  * resident in shared memory, 1: streamed from L2/HBM), dynamic shared memory bytes. */
 CQP_API int cqp_launch_info(const cqp_handle *h, int *ctas, int *rows_per_cta, int *tier,

@@ -53,7 +53,8 @@ EXPORTS = [
     "cqp_default_settings", "cqp_last_error", "cqp_device_count", "cqp_create",
     "cqp_create_from_layers", "cqp_destroy", "cqp_update_vectors", "cqp_cold_start",
     "cqp_warm_start", "cqp_refresh_z", "cqp_solve", "cqp_fixed_iters", "cqp_mpc_step",
-    "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_launch_info",
+    "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
+    "cqp_launch_info",
     "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve",
 ]
 
@@ -99,6 +100,7 @@ def load() -> C.CDLL:
     L.cqp_get_scaling.argtypes = [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p,
                                   c_int_p, c_double_p, c_double_p]
     L.cqp_dims.argtypes = [C.c_void_p, c_int_p, c_int_p, c_int_p]
+    L.cqp_debug_words.argtypes = [C.c_void_p, c_int_p]
     L.cqp_launch_info.argtypes = [C.c_void_p, c_int_p, c_int_p, c_int_p, c_int_p]
     L.cqp_batch_create.argtypes = [C.POINTER(C.c_void_p), C.c_void_p, C.c_int]
     L.cqp_batch_destroy.argtypes = [C.c_void_p]

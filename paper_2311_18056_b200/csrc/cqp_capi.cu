@@ -116,6 +116,9 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
   if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
   CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->hstage), sizeof(double) * (nm + m)));
+  CQP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->dbg_host), sizeof(int) * 64, cudaHostAllocMapped));
+  std::memset(h->dbg_host, 0, sizeof(int) * 64);
+  CQP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dbg_dev), h->dbg_host, 0));
   if ((rc = ensure_result_capacity(h, s.max_iters / s.check_interval + 2))) return rc;
   if ((rc = configure_launch(h))) return rc;
   return CQP_OK;
@@ -256,6 +259,7 @@ void cqp_destroy(cqp_handle* h) {
   cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp); cudaFree(h->dres);
   if (h->hres) cudaFreeHost(h->hres);
   if (h->hstage) cudaFreeHost(h->hstage);
+  if (h->dbg_host) cudaFreeHost(h->dbg_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -294,7 +298,9 @@ int cqp_warm_start(cqp_handle* h, const double* y, const double* lambda, int lay
 int cqp_refresh_z(cqp_handle* h) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
-  return launch_refresh_z(h);
+  // Same device code as the fused step's prologue (run kernel, zero iterations), so that
+  // update_vectors + refresh_z + fixed_iters(k) and cqp_mpc_step agree bit for bit.
+  return launch_run(h, false, 0, true);
 }
 
 static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out) {
@@ -305,7 +311,17 @@ static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh
   if ((rc = launch_run(h, early_exit, total, refresh))) return rc;
   CQP_CUDA(cudaEventRecord(h->ev1, h->stream));
   CQP_CUDA(cudaMemcpyAsync(h->hres, h->dres, h->res_bytes, cudaMemcpyDeviceToHost, h->stream));
-  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  {
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+      const int* d = h->dbg_host;
+      set_error(std::string("solve kernel failed: ") + cudaGetErrorString(e) +
+                (d && d[0] ? " (watchdog: where=" + std::to_string(d[1]) + " iter=" + std::to_string(d[2]) +
+                                 " cta=" + std::to_string(d[3]) + " thread=" + std::to_string(d[4]) + ")"
+                           : std::string()));
+      return CQP_ERR_CUDA;
+    }
+  }
   const unsigned char* base = static_cast<const unsigned char*>(h->hres);
   const DevResultHead* head = reinterpret_cast<const DevResultHead*>(base);
   size_t off = sizeof(DevResultHead);
@@ -432,6 +448,12 @@ int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, dou
     if (c_tilde) c_tilde[i] = zrow ? h->F_host[i - n] * h->c_host[i - n] : -INFINITY;
     if (d_tilde) d_tilde[i] = zrow ? h->F_host[i - n] * h->d_host[i - n] : INFINITY;
   }
+  return CQP_OK;
+}
+
+int cqp_debug_words(const cqp_handle* h, int* out64) {
+  if (!h || !out64) return CQP_ERR_ARGUMENT;
+  for (int i = 0; i < 64; ++i) out64[i] = ((volatile int*)h->dbg_host)[i];
   return CQP_OK;
 }
 

@@ -16,7 +16,9 @@ namespace cqp {
 constexpr int kMaxSmemBytes = 232448;  // 227 KB opt-in dynamic shared memory per CTA (sm_100)
 constexpr int kComputeThreads = 512;   // 16 compute warps of the persistent solve kernel
 constexpr int kComputeWarps = kComputeThreads / 32;
-constexpr int kThreads = kComputeThreads + 32;  // + 1 publisher warp
+constexpr int kLoaderWarps = 3;         // the only warps that poll L2 for the iterate
+constexpr int kLoaderThreads = kLoaderWarps * 32;
+constexpr int kThreads = kComputeThreads + 32 + kLoaderThreads;  // + 1 publisher warp + loaders
 constexpr int kWarps = kThreads / 32;
 
 inline int pad2(int x) { return (x + 1) & ~1; }
@@ -71,6 +73,7 @@ struct RunParams {
   double eps_prim, eps_dual, threshold;
   int check_interval, adaptive, early_exit, total_iters;
   int do_refresh;     // run Solver::refresh_z before the first iteration
+  int fence_mode;     // 0: fence after re-arm (default); 1: none; 2: release-store publish
   int cap;            // capacity of the record arrays
   DevResultHead* head;
   int* trace;         // [cap][2]
@@ -113,6 +116,8 @@ struct cqp_handle {
   // pinned staging for update_vectors: [g; c; d]
   double* hstage = nullptr;
   std::vector<double> c_host, d_host;  // current unscaled bounds (for cqp_get_scaling)
+  int* dbg_host = nullptr;  // host-mapped watchdog record (16 ints)
+  int* dbg_dev = nullptr;
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
 };

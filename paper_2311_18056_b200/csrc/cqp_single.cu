@@ -14,12 +14,16 @@
 //     produces), so the data word is its own "ready" flag (8-byte accesses are single-copy
 //     atomic).  Each compute thread owns a fixed set of column pairs, polls exactly the x
 //     entries it needs into registers and starts its FMAs as soon as they land.
-//   * 16 compute warps form the R dot products (16-byte LDS/LDG, FP64 FMA), reduce them with a
-//     shuffle butterfly and hand per-warp partials to a 17th "publisher" warp through a named
-//     barrier (bar.arrive / bar.sync): compute warps never block inside the CTA.  The
-//     publisher sums the partials in a FIXED order (bit-reproducible run to run), adds the
-//     bias, clamps, stores the rows to q[i&3], re-arms its rows of q[(i+2)&3] with the
-//     sentinel and fences -- all off the compute warps' critical path.
+//   * Warp roles inside a CTA (no CTA-wide barrier in the iteration loop):
+//       - 16 compute warps form the R dot products (x from shared memory, 16-byte LDS/LDG of
+//         W, FP64 FMA), reduce them with a shuffle butterfly and hand per-warp partials to
+//       - 1 publisher warp, which sums the partials in a FIXED order (bit-reproducible run to
+//         run), adds the bias, clamps, stores the rows to q[i&3], wakes the loaders, re-arms
+//         its rows of q[(i+2)&3] with the sentinel and fences (off the critical path);
+//       - 4 loader warps, the only threads that poll L2: they fetch v_i into a double-buffered
+//         shared-memory copy (all loads in flight, re-polling only the entries still armed).
+//     Hand-offs use parity-split mbarriers (full[2], xready[2], go), so a role can run at most
+//     one phase ahead and arrivals of different iterations never mix.
 //   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
 //     problem (H y, G' lambda, G y spread over the CTAs, seven max-norms exchanged through L2
 //     behind one grid barrier), and every CTA takes the identical rho decision; a switch
@@ -42,39 +46,110 @@ __device__ __forceinline__ double nanmax(double best, double a) {
   return (a > best || a != a) ? a : best;
 }
 
+// Watchdog: a spin that lasts longer than ~2 s records where it was stuck in host-mapped memory
+// and traps, so a protocol bug or a lost CTA becomes a CUDA error instead of a hung GPU.
+__device__ int* g_dbg = nullptr;  // set per launch (host-mapped, 16 ints)
+constexpr long long kSpinLimitCycles = 4000000000ll;
+
+__device__ __noinline__ void watchdog_fire(int where, int iter) {
+  int* d = g_dbg;
+  if (d && atomicCAS(d, 0, 1) == 0) {
+    d[1] = where;
+    d[2] = iter;
+    d[3] = (int)blockIdx.x;
+    d[4] = (int)threadIdx.x;
+    __threadfence_system();
+  }
+  __trap();
+}
+
+__device__ __forceinline__ void progress(int role, int value) {
+#ifdef CQP_DEBUG_PROGRESS
+  int* d = g_dbg;
+  if (d && blockIdx.x < 12) {
+    *((volatile int*)(d + 16 + blockIdx.x * 4 + role)) = value;
+  }
+#endif
+}
+
 __device__ __forceinline__ bool is_sentinel(double x) {
   return (unsigned long long)__double_as_longlong(x) == kSentinel;
-}
-
-// 16-byte relaxed load at GPU scope (L2), spinning until neither half is the sentinel.
-__device__ __forceinline__ double2 poll_pair(const double* p) {
-  double2 v;
-  do {
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(p)
-                 : "memory");
-  } while (is_sentinel(v.x) || is_sentinel(v.y));
-  return v;
-}
-
-__device__ __forceinline__ double poll_one(const double* p) {
-  double v;
-  do {
-    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  } while (is_sentinel(v));
-  return v;
 }
 
 __device__ __forceinline__ void publish(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ void publish_release(double* p, double v) {
+  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
-__device__ __forceinline__ void bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, int where, int iter) {
+  unsigned ok;
+  long long t0 = 0;
+  unsigned spins = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && (++spins & 0xFF) == 0) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(where, iter);
+    }
+  } while (!ok);
+}
+
+__device__ __forceinline__ double2 load_pair(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// Loader warps: fetch the whole iterate (nc2 column pairs) from ring slot `q` into shared memory
+// `xs`.  All loads of a batch are in flight together; only entries still holding the sentinel are
+// re-polled.  `lt` is the thread's index among the kLoaderThreads loader threads.
+__device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int nc2, int lt, int iter) {
+  constexpr int U = 8;
+  double2* xs2 = reinterpret_cast<double2*>(xs);
+  for (int base = lt; base < nc2; base += kLoaderThreads * U) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c2 = base + u * kLoaderThreads;
+      if (c2 < nc2) v[u] = load_pair(q + 2 * c2);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c2 = base + u * kLoaderThreads;
+      if (c2 < nc2) {
+        long long t0 = 0;
+        unsigned spins = 0;
+        while (is_sentinel(v[u].x) || is_sentinel(v[u].y)) {
+          v[u] = load_pair(q + 2 * c2);
+          if ((++spins & 0x3FF) == 0) {
+            if (t0 == 0) t0 = clock64();
+            else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(100 + c2, iter);
+          }
+        }
+        xs2[c2] = v[u];
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks) {
@@ -82,9 +157,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch,
   epoch += nblocks;
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
-    unsigned seen;
+    unsigned seen, spins = 0;
+    long long t0 = 0;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+      if ((++spins & 0x3FF) == 0) {
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(5, (int)epoch);
+      }
     } while (seen < epoch);
   }
   __syncthreads();
@@ -122,7 +202,7 @@ __device__ __forceinline__ double warp_butterfly(double (&acc)[RB], int lane) {
 template <int RB>
 __device__ __forceinline__ void fma_rows(const double* __restrict__ M, int ld, int nvalid, int c2,
                                          const double2 xv, double (&acc)[RB]) {
-  constexpr int CH = RB < 8 ? RB : 8;  // rows loaded per batch (keeps RB = 16 out of spills)
+  constexpr int CH = RB == 16 ? 4 : RB;  // rows loaded per batch (register pressure at RB = 16)
 #pragma unroll
   for (int r0 = 0; r0 < RB; r0 += CH) {
     double2 w[CH];
@@ -169,7 +249,7 @@ __device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, i
 
 struct Smem {
   double* sW;    // R * Dpad   (tier 0 only)
-  double* xs;    // Dpad       current iterate (cache space), check passes only
+  double* xs;    // 2 * Dpad   iterate (cache space), double buffered by iteration parity
   double* uy;    // npad       unscaled y   (also scratch for g_s)
   double* uz;    // mpad       unscaled z
   double* ul;    // mpad       unscaled lambda
@@ -179,6 +259,7 @@ struct Smem {
   double* slo;   // Rp
   double* shi;   // Rp
   double* sval;  // 128 scratch
+  unsigned long long* bars;  // full[2], xready[2], go
 };
 
 __host__ __device__ inline int round_up(int x, int q) { return (x + q - 1) / q * q; }
@@ -187,8 +268,8 @@ __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad
                                                int w_smem) {
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
-  return (size_t)(w_smem ? (size_t)R * Dpad : 0) + Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
-         2 * (size_t)kComputeWarps * Rcap + 3 * (size_t)Rp + 128;
+  return (size_t)(w_smem ? (size_t)R * Dpad : 0) + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad +
+         kWarps * 16 + 2 * (size_t)kComputeWarps * Rcap + 3 * (size_t)Rp + 128 + 8;
 }
 
 template <int RB>
@@ -199,7 +280,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   const int Rcap = round_up(p.R, RB);
   s.sW = base;
   s.xs = base + (p.w_smem ? (size_t)p.R * p.Dpad : 0);
-  s.uy = s.xs + p.Dpad;
+  s.uy = s.xs + 2 * p.Dpad;
   s.uz = s.uy + p.npad;
   s.ul = s.uz + p.mpad;
   s.sred = s.ul + p.mpad;
@@ -208,6 +289,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
+  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128);
   return s;
 }
 
@@ -243,30 +325,27 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
 }
 
 // Residual pass on the unscaled problem (solver.cpp:67-70,119-134; epilogue :90-95 when
-// `final`).  `slot` is the ring slot holding the iterate.  On return every thread of every CTA
-// holds the same seven norms in out[]:
+// `final`).  `xs` is the shared-memory copy of the iterate (filled by the loader warps).  On
+// return every thread of every CTA holds the same seven norms in out[]:
 //   0 ||Gy - z||  1 ||Hy + g + G'lam||  2 ||Hy||  3 ||G'lam||  4 ||Gy||  5 ||z||  6 ||g||
 template <int RB>
-__device__ void residual_pass(const RunParams& p, const Smem& s, int slot, bool final,
+__device__ void residual_pass(const RunParams& p, const Smem& s, const double* xs, bool final,
                               unsigned& epoch, double (&out)[7]) {
   const int t = threadIdx.x;
   const int n = p.n, m = p.m;
-  const double* v = p.vq + (size_t)slot * p.Dpad;
-  __syncthreads();
-  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < p.D) ? poll_one(v + i) : 0.0;
   __syncthreads();
   // unscale (layers.hpp:57-59)
-  for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? p.E[i] * s.xs[i] : 0.0;
+  for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? p.E[i] * xs[i] : 0.0;
   for (int i = t; i < p.mpad; i += kThreads) {
     double z = 0.0, l = 0.0;
     if (i < m) {
-      z = s.xs[n + i] / p.F[i];
+      z = xs[n + i] / p.F[i];
       if (final) {  // solver.cpp:94  z = clamp(z, p.c, p.d) in original units
         const double lo = p.c[i], hi = p.d[i];
         z = z < lo ? lo : z;
         z = z > hi ? hi : z;
       }
-      l = (p.F[i] * s.xs[n + m + i]) / p.cost_scale;
+      l = (p.F[i] * xs[n + m + i]) / p.cost_scale;
     }
     s.uz[i] = z;
     s.ul[i] = l;
@@ -324,10 +403,28 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, int slot, bool 
     __stcg(p.partial + (size_t)blockIdx.x * 8 + t, best);
   }
   grid_barrier(p.barrier, epoch, G);
-  if (t < 7) {
-    double best = 0.0;
-    for (int b = 0; b < G; ++b) best = nanmax(best, __ldcg(p.partial + (size_t)b * 8 + t));
-    s.sval[t] = best;
+  // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
+  // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant)
+  {
+    double mine[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) mine[k] = (t < G) ? __ldcg(p.partial + (size_t)t * 8 + k) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) mine[k] = nanmax(mine[k], __shfl_xor_sync(0xffffffffu, mine[k], w));
+    }
+    const int lane_ = t & 31, warp_ = t >> 5;
+    if (lane_ == 0) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) s.sred[warp_ * 8 + k] = mine[k];
+    }
+    __syncthreads();
+    if (t < 7) {
+      double best = 0.0;
+      for (int w = 0; w < kWarps; ++w) best = nanmax(best, s.sred[w * 8 + t]);
+      s.sval[t] = best;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -355,7 +452,20 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const bool publisher = warp == kComputeWarps;  // the 17th warp
+  // warp roles: [0,16) compute, 16 publisher, [17,21) loaders
+  const bool compute = warp < kComputeWarps;
+  const bool publisher = warp == kComputeWarps;
+  const int lt = t - (kComputeThreads + 32);  // loader thread index (>= 0 for loader warps)
+  unsigned long long* full = s.bars;        // [2] compute -> publisher: partials of iteration i
+  unsigned long long* xready = s.bars + 2;  // [2] loaders -> compute: v_i is in xs[i&1]
+  unsigned long long* go = s.bars + 4;      //     publisher -> loaders: v_i rows published
+  if (t == 0) {
+    mbar_init(&full[0], kComputeWarps);
+    mbar_init(&full[1], kComputeWarps);
+    mbar_init(&xready[0], kLoaderWarps);
+    mbar_init(&xready[1], kLoaderWarps);
+    mbar_init(go, 1);
+  }
   const int n = p.n, m = p.m, D = p.D;
   const int row0 = blockIdx.x * p.R;
   const int nrows = max(0, min(p.R, D - row0));
@@ -397,6 +507,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
   load_layer<RB>(p, s, layer, row0, nrows);
 
+  // v_0 -> xs[0] (slot 0 holds the iterate between launches; refresh_z above is complete)
+  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
+  __syncthreads();
+
   int n_trace = 1, n_hist = 0;
   if (blockIdx.x == 0 && t == 0) {
     p.trace[0] = 0;
@@ -409,25 +523,32 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   constexpr int shift = 5 - Log2<RB>::v;
   for (int i = 1; i <= p.total_iters; ++i) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
-    const double* qin = p.vq + (size_t)((i - 1) & 3) * p.Dpad;
-    double* part = s.spart + (size_t)(i & 1) * kComputeWarps * Rcap;
-    if (!publisher) {
+    const int b = i & 1;
+    const int par = ((i - 1) >> 1) & 1;  // phase parity of the k-th use of a [2]-split barrier
+    double* part = s.spart + (size_t)b * kComputeWarps * Rcap;
+    if (compute) {
+      if (lane == 0 && warp == 0) progress(0, i * 10 + 1);
+      if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, 1, i);
+      if (lane == 0 && warp == 0) progress(0, i * 10 + 2);  // v_{i-1} landed in xs[(i-1)&1]
+      const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
       const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
       for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
         const int nv = min(RB, nrows - rb0);
         double acc[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-        for (int c2 = t; c2 < nc2; c2 += kComputeThreads) {
-          const double2 xv = poll_pair(qin + 2 * c2);
-          fma_rows<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, c2, xv, acc);
-        }
+        for (int c2 = t; c2 < nc2; c2 += kComputeThreads)
+          fma_rows<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, c2, x2[c2], acc);
         const double total = warp_butterfly<RB>(acc, lane);
         if ((lane & ((1 << shift) - 1)) == 0) part[warp * Rcap + rb0 + (lane >> shift)] = total;
       }
-      bar_arrive(1, kThreads);
-    } else {
-      bar_sync(1, kThreads);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
+      if (lane == 0 && warp == 0) progress(0, i * 10 + 3);
+    } else if (publisher) {
+      if (lane == 0) progress(1, i * 10 + 1);
+      mbar_wait(&full[b], par, 2, i);
+      if (lane == 0) progress(1, i * 10 + 2);
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
       for (int r = lane; r < nrows; r += 32) {
@@ -439,24 +560,36 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         x = x < lo ? lo : x;
         x = x > hi ? hi : x;
         if (x != x) x = __longlong_as_double(0x7FF8000000000000ll);  // never publish the sentinel
-        publish(qout + row0 + r, x);
+        if (p.fence_mode == 2) publish_release(qout + row0 + r, x);
+        else publish(qout + row0 + r, x);
       }
       if (owns_pad && lane == 0) publish(qout + D, 0.0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(go);
       // re-arm this CTA's rows of the slot that will carry v_{i+2}; every reader of its old
       // content (v_{i-2}) finished before any v_{i-1} row was published, and all of v_{i-1} has
-      // been consumed by this CTA's compute warps.  The fence orders the re-arm before the next
-      // iteration's publish (off the compute warps' critical path).
+      // been consumed by this CTA.  The fence orders the re-arm before the next iteration's
+      // publish (off the compute warps' critical path).
       const double sentinel = __longlong_as_double((long long)kSentinel);
       for (int r = lane; r < nrows; r += 32) publish(qclr + row0 + r, sentinel);
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
-      __threadfence();
+      if (p.fence_mode == 0) __threadfence();
+      if (lane == 0) progress(1, i * 10 + 3);
+    } else {
+      if (lt == 0) progress(2, i * 10 + 1);
+      mbar_wait(go, (i - 1) & 1, 3, i);
+      if (lt == 0) progress(2, i * 10 + 2);
+      fetch_iterate(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, i);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xready[b]);
+      if (lt == 0) progress(2, i * 10 + 3);
     }
     iters_done = i;
     if (i % p.check_interval != 0) continue;
 
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     double nr[7];
-    residual_pass<RB>(p, s, i & 3, false, epoch, nr);
+    residual_pass<RB>(p, s, s.xs + (size_t)(i & 1) * p.Dpad, false, epoch, nr);
     const double r_prim = nr[0], r_dual = nr[1];
     if (blockIdx.x == 0 && t == 0 && n_hist < p.cap) {
       p.hist_i[2 * n_hist] = i;
@@ -498,8 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   }
 
   // ---- epilogue (solver.cpp:90-99) ----
+  if (t == 0) progress(3, iters_done * 10 + 9);
   double nr[7];
-  residual_pass<RB>(p, s, iters_done & 3, true, epoch, nr);
+  const double* xfinal = s.xs + (size_t)(iters_done & 1) * p.Dpad;
+  residual_pass<RB>(p, s, xfinal, true, epoch, nr);
   // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
   // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
   {
@@ -507,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     const int count = nrows + (owns_pad ? 1 : 0);
     for (int r = t; r < count; r += kThreads) {
       const int row = row0 + r;
-      p.vq[row] = (row < D) ? s.xs[row] : 0.0;
+      p.vq[row] = (row < D) ? xfinal[row] : 0.0;
       p.vq[(size_t)p.Dpad + row] = sentinel;
       p.vq[2 * (size_t)p.Dpad + row] = sentinel;
       p.vq[3 * (size_t)p.Dpad + row] = sentinel;
@@ -658,7 +793,10 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.out_y = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->n;
   p.out_z = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->m;
   p.out_lam = reinterpret_cast<double*>(base + off);
+  p.fence_mode = 0;
+  if (const char* fm = std::getenv("CQP_FENCE_MODE")) p.fence_mode = std::atoi(fm);  // experiment knob
   CQP_CUDA(cudaMemsetAsync(h->barrier, 0, sizeof(unsigned), h->stream));
+  CQP_CUDA(cudaMemcpyToSymbolAsync(g_dbg, &h->dbg_dev, sizeof(int*), 0, cudaMemcpyHostToDevice, h->stream));
   switch (h->rb) {
     case 4: return launch_run_rb<4>(h, p);
     case 8: return launch_run_rb<8>(h, p);
