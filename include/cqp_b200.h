@@ -196,6 +196,12 @@ CQP_API int cqp_batch_solve(cqp_batch *b, int B, const double *g_cols, const dou
                             int *final_index, double *r_prim, double *r_dual, int *n_switches,
                             double *device_ms);
 
+/* CUDA-event times of the last cqp_batch_solve: compute_ms = from "inputs resident in HBM" to
+ * "results ready in HBM"; total_ms additionally covers the host->device and device->host
+ * copies; gemm_launches = DMMA GEMM kernels launched. */
+CQP_API int cqp_batch_last_timing(const cqp_batch *b, double *compute_ms, double *total_ms,
+                                  long long *gemm_launches);
+
 #ifdef __cplusplus
 }
 #endif

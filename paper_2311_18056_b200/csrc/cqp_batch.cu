@@ -1,28 +1,698 @@
-// Batched path (placeholder until the DMMA kernel lands in this round): see DESIGN.md section 4.
+// Batched solve path: B QPs that share (H, G) -- hence the whole W ladder -- and differ in
+// (g, c, d): MPC instances at different x0.  Semantically B independent cold-start `solve()`
+// calls (/root/reference/proj/src/solver.cpp:158-166 -> run_loop :43-105), one per column.
+//
+// Design:
+//   * The iterates are the columns of S (D x B, each column contiguous); one batch iteration is
+//     the dense contraction  S <- clamp(W_k S + Bias_k, lo, hi)  evaluated with FP64 tensor
+//     cores (mma.sync m8n8k4 f64 = DMMA.8x8x4, the only FP64 tensor shape sm_100a has; tcgen05
+//     has no f64 kind).  128x128x16 CTA tiles, 8 warps of 64x32, operands staged in shared
+//     memory by a 4-stage cp.async pipeline in a 16-byte-chunk XOR swizzle (conflict-free 8-byte
+//     fragment loads), bias + clamp fused into the epilogue.
+//   * Every QP adapts rho on its own (parity demands it), so columns are bucketed by ladder
+//     index: a slot map lists, per 128-column tile, which columns it holds and which W_k it
+//     multiplies (a grouped GEMM).  Tiles gather their columns through the map, so re-bucketing
+//     never moves S.
+//   * Every check_interval iterations: unscale, three more DMMA GEMMs (H Y, G' Lambda, G Y) on
+//     the active columns, a per-column reduction/decision kernel (residuals, rho rule, early
+//     exit, finalisation of converged columns), re-bucketing and the bias GEMM
+//     Bias = -[D_k; G D_k] G_s.  Converged columns leave the slot map, so they stop costing work.
+//   * No host round trip inside a round; the host only polls a pinned "active columns" word with
+//     a lag of two rounds to know when to stop enqueuing.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "cqp_internal.h"
+
+namespace cqp {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_SMEM = STAGES * (BM + BN) * BK * (int)sizeof(double) + BN * (int)sizeof(int);
+
+struct TileDesc {
+  int slot0;    // first slot of this 128-column tile
+  int a_index;  // which A matrix (ladder index) the tile multiplies
+};
+
+struct GemmParams {
+  const double* A;   // [a_index][M_pad][lda] row-major, K contiguous, zero padded
+  size_t a_stride;   // doubles between consecutive A matrices (0: one shared A)
+  int lda;
+  int M;             // valid output rows
+  int m_tiles;
+  int k_tiles;
+  const double* Bm;  // [col][ldb], K contiguous
+  int ldb;
+  const int* cols;   // slot -> column, or -1 for a padding slot
+  const TileDesc* tiles;
+  const int* n_tiles;  // device scalar
+  double* C;         // [col][ldc]
+  int ldc;
+  double alpha;
+  int mode;          // 0: C = alpha A B ; 1: C = clamp(A B + bias, lo, hi) (one ADMM layer)
+  const double* bias;  // [col][ld_bias], rows < nm
+  int ld_bias;
+  int nm;              // n + m
+  int n;
+  const double* lo;    // [col][ld_lohi], rows n..nm-1
+  const double* hi;
+  int ld_lohi;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// element (row r, k index e) of a [rows][16] tile in the 16-byte-chunk XOR swizzle
+__device__ __forceinline__ int swz(int r, int e) { return r * BK + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1)); }
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) dmma_gemm_kernel(const GemmParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  double* Bs = As + STAGES * BM * BK;
+  int* cols_s = reinterpret_cast<int*>(Bs + STAGES * BN * BK);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int warp_m = warp & 1, warp_n = warp >> 1;  // 2 x 4 warps, warp tile 64 x 32
+  const int total = (*p.n_tiles) * p.m_tiles;
+
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int nt = tile / p.m_tiles, mt = tile - nt * p.m_tiles;
+    const TileDesc td = p.tiles[nt];
+    const int m0 = mt * BM;
+    const double* A = p.A + (size_t)td.a_index * p.a_stride + (size_t)m0 * p.lda;
+    __syncthreads();  // previous tile's readers of cols_s / smem are done
+    if (tid < BN) cols_s[tid] = p.cols[td.slot0 + tid];
+    __syncthreads();
+
+    auto issue = [&](int kt, int stage) {
+      const int k0 = kt * BK;
+      double* as = As + stage * BM * BK;
+      double* bs = Bs + stage * BN * BK;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int chunk = tid + GEMM_THREADS * i;
+        const int r = chunk >> 3, c = chunk & 7;
+        const int dst = r * BK + ((c ^ (r & 7)) << 1);
+        cp_async16(as + dst, A + (size_t)r * p.lda + k0 + c * 2, 16);
+        const int col = cols_s[r];
+        const double* src = p.Bm + (size_t)(col < 0 ? 0 : col) * p.ldb + k0 + c * 2;
+        cp_async16(bs + dst, src, col < 0 ? 0 : 16);
+      }
+    };
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < p.k_tiles) issue(s, s);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < p.k_tiles; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      const int next = kt + STAGES - 1;
+      if (next < p.k_tiles) issue(next, next % STAGES);
+      cp_async_commit();
+      const double* as = As + (kt % STAGES) * BM * BK + (warp_m * 64) * BK;
+      const double* bs = Bs + (kt % STAGES) * BN * BK + (warp_n * 32) * BK;
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int e = ks * 4 + t4;
+        const int off = (((e >> 1) ^ g) << 1) | (e & 1);  // rows are 8-aligned + g, so r & 7 == g
+        double a[8], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) a[mi] = as[(mi * 8 + g) * BK + off];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = bs[(ni * 8 + g) * BK + off];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+      }
+    }
+    cp_async_wait<0>();
+
+    // epilogue: C fragment (row = g, cols 2*t4, 2*t4+1) of each 8x8 sub-tile
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = cols_s[warp_n * 32 + ni * 8 + 2 * t4 + j];
+        if (col < 0) continue;
+        double* crow = p.C + (size_t)col * p.ldc;
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) {
+          const int row = m0 + warp_m * 64 + mi * 8 + g;
+          if (row >= p.M) continue;
+          double v = p.alpha * acc[mi][ni][j];
+          if (p.mode == 1 && row < p.nm) {
+            v += p.bias[(size_t)col * p.ld_bias + row];
+            if (row >= p.n) {
+              const double lo = p.lo[(size_t)col * p.ld_lohi + row - p.n];
+              const double hi = p.hi[(size_t)col * p.ld_lohi + row - p.n];
+              v = v < lo ? lo : v;
+              v = v > hi ? hi : v;
+            }
+          }
+          crow[row] = v;
+        }
+      }
+    }
+  }
+}
+
+// dst[a][r][c] (rows_pad x ld_dst, zero padded) <- src[a][r][c] (rows x ld_src, first `cols`)
+__global__ void repad_kernel(const double* __restrict__ src, int rows, int cols, int ld_src,
+                             size_t src_stride, double* __restrict__ dst, int rows_pad, int ld_dst,
+                             size_t dst_stride, int count) {
+  const size_t per = (size_t)rows_pad * ld_dst;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= per * count) return;
+  const int a = (int)(idx / per);
+  const size_t rem = idx - (size_t)a * per;
+  const int r = (int)(rem / ld_dst), c = (int)(rem % ld_dst);
+  dst[(size_t)a * dst_stride + rem] =
+      (r < rows && c < cols) ? src[(size_t)a * src_stride + (size_t)r * ld_src + c] : 0.0;
+}
+
+struct BatchDev {
+  int n, m, D, B;
+  int ld_s;    // leading dimension of S columns (D padded to BK)
+  int ld_n;    // n padded to BK
+  int ld_m;    // m padded to BK
+  int ld_nm;   // n + m padded to even
+  const double* E;
+  const double* F;
+  double cost_scale;
+  const double* grid;
+  const double* log_grid;
+  int L;
+  // per-column inputs
+  const double* g;   // [B][n] unscaled
+  const double* c;   // [B][m]
+  const double* d;   // [B][m]
+  double* gs;        // [B][ld_n] scaled g
+  double* lo;        // [B][ld_m] scaled bounds
+  double* hi;
+  // unscaled iterate + products
+  double* uy;        // [B][ld_n]
+  double* ul;        // [B][ld_m]
+  double* uz;        // [B][ld_m]
+  double* hy;        // [B][ld_n]
+  double* gtl;       // [B][ld_n]
+  double* gy;        // [B][ld_m]
+  // per-column state
+  int* layer;
+  int* active;
+  int* iters;
+  int* status;
+  int* nsw;
+  double* rp;
+  double* rd;
+  // outputs
+  double* out_y;     // [B][n]
+  double* out_z;     // [B][m]
+  double* out_l;     // [B][m]
+  // slot map
+  int* cols;         // [slot_cap]
+  TileDesc* tiles;   // [tile_cap]
+  int* n_tiles;
+  int* n_active;
+  // settings
+  double eps_prim, eps_dual, threshold;
+  int adaptive, max_iters;
+};
+
+// gs = cost_scale * E o g ; lo = F o c ; hi = F o d   (layers.cpp:181-183), per column
+__global__ void batch_prepare_kernel(BatchDev b, int initial_index) {
+  const int col = blockIdx.x;
+  for (int i = threadIdx.x; i < b.ld_n; i += blockDim.x)
+    b.gs[(size_t)col * b.ld_n + i] = (i < b.n) ? b.cost_scale * (b.E[i] * b.g[(size_t)col * b.n + i]) : 0.0;
+  for (int i = threadIdx.x; i < b.ld_m; i += blockDim.x) {
+    const bool in = i < b.m;
+    b.lo[(size_t)col * b.ld_m + i] = in ? b.F[i] * b.c[(size_t)col * b.m + i] : 0.0;
+    b.hi[(size_t)col * b.ld_m + i] = in ? b.F[i] * b.d[(size_t)col * b.m + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    b.layer[col] = initial_index;
+    b.active[col] = 1;
+    b.iters[col] = 0;
+    b.status[col] = CQP_INVALID;
+    b.nsw[col] = 0;
+    b.rp[col] = 0.0;
+    b.rd[col] = 0.0;
+  }
+}
+
+// unscale the active columns (layers.hpp:57-59): y = E o y_s, z = z_s / F, lambda = F o l_s / cs
+__global__ void batch_unscale_kernel(BatchDev b, const double* __restrict__ S) {
+  const int col = blockIdx.x;
+  if (!b.active[col]) return;
+  const double* v = S + (size_t)col * b.ld_s;
+  for (int i = threadIdx.x; i < b.ld_n; i += blockDim.x)
+    b.uy[(size_t)col * b.ld_n + i] = (i < b.n) ? b.E[i] * v[i] : 0.0;
+  for (int i = threadIdx.x; i < b.ld_m; i += blockDim.x) {
+    double z = 0.0, l = 0.0;
+    if (i < b.m) {
+      z = v[b.n + i] / b.F[i];
+      l = (b.F[i] * v[b.n + b.m + i]) / b.cost_scale;
+    }
+    b.uz[(size_t)col * b.ld_m + i] = z;
+    b.ul[(size_t)col * b.ld_m + i] = l;
+  }
+}
+
+__device__ __forceinline__ double nanmax(double best, double a) { return (a > best || a != a) ? a : best; }
+__device__ __forceinline__ double warp_nanmax(double v) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, w));
+  return v;
+}
+
+// One warp per column: residuals (solver.cpp:119-124), rho rule (:126-142), early exit (:84-87)
+// and, for columns that stop, the epilogue (:90-99).  `it` = iterations done so far;
+// `check` = 0 for the trailing partial round (no check happens at i % check_interval != 0).
+__global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exit) {
+  const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= b.B || !b.active[col]) return;
+  const int n = b.n, m = b.m;
+  const double* hy = b.hy + (size_t)col * b.ld_n;
+  const double* gtl = b.gtl + (size_t)col * b.ld_n;
+  const double* gy = b.gy + (size_t)col * b.ld_m;
+  const double* uz = b.uz + (size_t)col * b.ld_m;
+  const double* g = b.g + (size_t)col * n;
+  const double* c = b.c + (size_t)col * m;
+  const double* d = b.d + (size_t)col * m;
+  double r_dual = 0.0, n_hy = 0.0, n_gtl = 0.0, n_g = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double a = hy[i], bb = gtl[i], gi = g[i];
+    r_dual = nanmax(r_dual, fabs((a + gi) + bb));
+    n_hy = nanmax(n_hy, fabs(a));
+    n_gtl = nanmax(n_gtl, fabs(bb));
+    n_g = nanmax(n_g, fabs(gi));
+  }
+  double r_prim = 0.0, r_prim_final = 0.0, n_gy = 0.0, n_z = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const double a = gy[i], z = uz[i];
+    double zc = z < c[i] ? c[i] : z;  // solver.cpp:94 clamp in original units
+    zc = zc > d[i] ? d[i] : zc;
+    r_prim = nanmax(r_prim, fabs(a - z));
+    r_prim_final = nanmax(r_prim_final, fabs(a - zc));
+    n_gy = nanmax(n_gy, fabs(a));
+    n_z = nanmax(n_z, fabs(z));
+  }
+  r_dual = warp_nanmax(r_dual); n_hy = warp_nanmax(n_hy); n_gtl = warp_nanmax(n_gtl);
+  n_g = warp_nanmax(n_g); r_prim = warp_nanmax(r_prim); r_prim_final = warp_nanmax(r_prim_final);
+  n_gy = warp_nanmax(n_gy); n_z = warp_nanmax(n_z);
+
+  int layer = b.layer[col];
+  bool converged = false;
+  if (check) {
+    if (b.adaptive) {
+      const double rho_cur = b.grid[layer];
+      double rho_nom = rho_cur;
+      if (!(r_prim == 0.0 || r_dual == 0.0)) {
+        double num = n_hy < n_gtl ? n_gtl : n_hy;
+        num = num < n_g ? n_g : num;
+        num = num < 1e-4 ? 1e-4 : num;
+        double den = n_gy < n_z ? n_z : n_gy;
+        den = den < 1e-4 ? 1e-4 : den;
+        rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+      }
+      const double target = log10(rho_nom);
+      int best = 0;
+      double best_dist = INFINITY;
+      for (int k = 0; k < b.L; ++k) {
+        const double dist = fabs(b.log_grid[k] - target);
+        if (dist < best_dist - 1e-15) { best = k; best_dist = dist; }
+      }
+      const double ra = rho_nom / rho_cur, rb = rho_cur / rho_nom;
+      const double ratio = ra < rb ? rb : ra;
+      const int cand = ratio >= b.threshold ? best : layer;
+      if (cand != layer) {
+        layer = cand;
+        if (lane == 0) { b.layer[col] = cand; b.nsw[col] += 1; }
+      }
+    }
+    converged = early_exit && r_prim <= b.eps_prim && r_dual <= b.eps_dual;
+  }
+  if (converged || it >= b.max_iters) {
+    const double* uy = b.uy + (size_t)col * b.ld_n;
+    const double* ul = b.ul + (size_t)col * b.ld_m;
+    for (int i = lane; i < n; i += 32) b.out_y[(size_t)col * n + i] = uy[i];
+    for (int i = lane; i < m; i += 32) {
+      double zc = uz[i] < c[i] ? c[i] : uz[i];
+      zc = zc > d[i] ? d[i] : zc;
+      b.out_z[(size_t)col * m + i] = zc;
+      b.out_l[(size_t)col * m + i] = ul[i];
+    }
+    if (lane == 0) {
+      b.status[col] = (converged || (r_prim_final <= b.eps_prim && r_dual <= b.eps_dual)) ? CQP_SOLVED : CQP_MAX_ITERS;
+      b.iters[col] = it;
+      b.rp[col] = r_prim_final;
+      b.rd[col] = r_dual;
+      b.active[col] = 0;
+    }
+  }
+}
+
+// Rebuild the slot map: active columns bucketed by ladder index, every bucket padded to a
+// multiple of BN with -1 slots, one TileDesc per 128 slots.  Single CTA, deterministic (stable
+// in the column index).
+__global__ void batch_regroup_kernel(BatchDev b) {
+  __shared__ int warp_sums[32];
+  __shared__ int base_s, slot_base_s, total_active_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (tid == 0) { slot_base_s = 0; total_active_s = 0; }
+  __syncthreads();
+  int n_tiles = 0;
+  for (int k = 0; k < b.L; ++k) {
+    if (tid == 0) base_s = 0;
+    __syncthreads();
+    for (int start = 0; start < b.B; start += blockDim.x) {
+      const int col = start + tid;
+      const int flag = (col < b.B && b.active[col] && b.layer[col] == k) ? 1 : 0;
+      const unsigned ballot = __ballot_sync(0xffffffffu, flag);
+      const int in_warp = __popc(ballot & ((1u << lane) - 1));
+      if (lane == 0) warp_sums[warp] = __popc(ballot);
+      __syncthreads();
+      int warp_off = 0, chunk_total = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const int s = warp_sums[w];
+        if (w < warp) warp_off += s;
+        chunk_total += s;
+      }
+      if (flag) b.cols[slot_base_s + base_s + warp_off + in_warp] = col;
+      __syncthreads();
+      if (tid == 0) base_s += chunk_total;
+      __syncthreads();
+    }
+    const int count = base_s;
+    const int padded = (count + BN - 1) / BN * BN;
+    for (int i = count + tid; i < padded; i += blockDim.x) b.cols[slot_base_s + i] = -1;
+    for (int t = tid; t < padded / BN; t += blockDim.x) {
+      b.tiles[n_tiles + t].slot0 = slot_base_s + t * BN;
+      b.tiles[n_tiles + t].a_index = k;
+    }
+    n_tiles += padded / BN;
+    __syncthreads();
+    if (tid == 0) { slot_base_s += padded; total_active_s += count; }
+    __syncthreads();
+  }
+  if (tid == 0) { *b.n_tiles = n_tiles; *b.n_active = total_active_s; }
+}
+
+}  // namespace
+}  // namespace cqp
 
 using namespace cqp;
 
-extern "C" {
+struct cqp_batch {
+  cqp_handle* h = nullptr;
+  int capacity = 0;
+  int n = 0, m = 0, D = 0, L = 0;
+  int ld_s = 0, ld_n = 0, ld_m = 0, ld_nm = 0;
+  int Dm_pad = 0, nm_mpad = 0, n_mpad = 0, m_mpad = 0;
+  int grid_ctas = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;
+  float last_total_ms = 0.f, last_compute_ms = 0.f;
+  long long last_launches = 0;
+  std::vector<cudaEvent_t> round_events;
+  // shared matrices re-padded for the GEMM tiles
+  double *Wb = nullptr, *DGb = nullptr, *Hb = nullptr, *Gb = nullptr, *Gtb = nullptr;
+  // per-column buffers
+  double *S0 = nullptr, *S1 = nullptr, *bias = nullptr;
+  double *g = nullptr, *c = nullptr, *d = nullptr, *gs = nullptr, *lo = nullptr, *hi = nullptr;
+  double *uy = nullptr, *ul = nullptr, *uz = nullptr, *hy = nullptr, *gtl = nullptr, *gy = nullptr;
+  int *layer = nullptr, *active = nullptr, *iters = nullptr, *status = nullptr, *nsw = nullptr;
+  double *rp = nullptr, *rd = nullptr, *out_y = nullptr, *out_z = nullptr, *out_l = nullptr;
+  int* cols = nullptr;
+  TileDesc* tiles = nullptr;
+  int *n_tiles = nullptr, *n_active = nullptr;
+  int* h_active = nullptr;  // pinned, one word per round
+  int h_active_cap = 0;
+};
 
-int cqp_batch_create(cqp_batch** out, cqp_handle* shared, int capacity) {
-  (void)shared; (void)capacity;
-  if (out) *out = nullptr;
-  set_error("batched path not built yet");
-  return CQP_ERR_CAPACITY;
+namespace {
+
+template <typename T>
+int balloc(T** p, size_t count) {
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1)));
+  CQP_CUDA(cudaMemset(*p, 0, sizeof(T) * (count ? count : 1)));
+  return CQP_OK;
 }
 
-void cqp_batch_destroy(cqp_batch* b) { (void)b; }
+int round_up_i(int x, int q) { return (x + q - 1) / q * q; }
+
+int launch_gemm(cqp_batch* b, const GemmParams& p) {
+  b->last_launches += 1;
+  dmma_gemm_kernel<<<b->grid_ctas, GEMM_THREADS, GEMM_SMEM, b->stream>>>(p);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+int repad(cqp_batch* b, const double* src, int rows, int cols, int ld_src, size_t src_stride,
+          double* dst, int rows_pad, int ld_dst, size_t dst_stride, int count) {
+  const size_t total = (size_t)rows_pad * ld_dst * count;
+  repad_kernel<<<(unsigned)((total + 255) / 256), 256, 0, b->stream>>>(src, rows, cols, ld_src, src_stride,
+                                                                      dst, rows_pad, ld_dst, dst_stride, count);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
+  if (!out || !h || capacity < 1) { set_error("batch_create: bad argument"); return CQP_ERR_ARGUMENT; }
+  *out = nullptr;
+  CQP_CUDA(cudaSetDevice(h->device));
+  cqp_batch* b = new cqp_batch();
+  b->h = h; b->capacity = capacity;
+  b->n = h->n; b->m = h->m; b->D = h->D; b->L = h->L;
+  const int n = b->n, m = b->m, D = b->D, L = b->L, nm = n + m;
+  b->ld_s = round_up_i(D, BK); b->ld_n = round_up_i(n, BK); b->ld_m = round_up_i(m, BK);
+  b->ld_nm = round_up_i(nm, 2);
+  b->Dm_pad = round_up_i(D, BM); b->nm_mpad = round_up_i(nm, BM);
+  b->n_mpad = round_up_i(n, BM); b->m_mpad = round_up_i(m, BM);
+  b->grid_ctas = h->num_sms;
+  auto fail = [&](int rc) { cqp_batch_destroy(b); return rc; };
+  if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CQP_ERR_CUDA);
+  cudaEventCreate(&b->ev0); cudaEventCreate(&b->ev1);
+  cudaEventCreate(&b->evc0); cudaEventCreate(&b->evc1);
+  if (cudaFuncSetAttribute(dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) != cudaSuccess)
+    return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dmma_gemm_kernel)"));
+  int rc;
+  const size_t cap = (size_t)capacity;
+  const size_t slot_cap = cap + (size_t)L * BN, tile_cap = slot_cap / BN + L;
+#define BA(ptr, count) if ((rc = balloc(&b->ptr, (count)))) return fail(rc)
+  BA(Wb, (size_t)L * b->Dm_pad * b->ld_s);
+  BA(DGb, (size_t)L * b->nm_mpad * b->ld_n);
+  BA(Hb, (size_t)b->n_mpad * b->ld_n);
+  BA(Gb, (size_t)b->m_mpad * b->ld_n);
+  BA(Gtb, (size_t)b->n_mpad * b->ld_m);
+  BA(S0, cap * b->ld_s); BA(S1, cap * b->ld_s); BA(bias, cap * b->ld_nm);
+  BA(g, cap * n); BA(c, cap * m); BA(d, cap * m);
+  BA(gs, cap * b->ld_n); BA(lo, cap * b->ld_m); BA(hi, cap * b->ld_m);
+  BA(uy, cap * b->ld_n); BA(ul, cap * b->ld_m); BA(uz, cap * b->ld_m);
+  BA(hy, cap * b->ld_n); BA(gtl, cap * b->ld_n); BA(gy, cap * b->ld_m);
+  BA(layer, cap); BA(active, cap); BA(iters, cap); BA(status, cap); BA(nsw, cap);
+  BA(rp, cap); BA(rd, cap); BA(out_y, cap * n); BA(out_z, cap * m); BA(out_l, cap * m);
+  BA(cols, slot_cap); BA(tiles, tile_cap); BA(n_tiles, 1); BA(n_active, 1);
+#undef BA
+  // shared matrices: handle layouts (row-major, even ld) -> tile-padded copies
+  if ((rc = repad(b, h->W, D, D, h->Dpad, (size_t)D * h->Dpad, b->Wb, b->Dm_pad, b->ld_s,
+                  (size_t)b->Dm_pad * b->ld_s, L))) return fail(rc);
+  if ((rc = repad(b, h->Dk, nm, n, h->npad, (size_t)nm * h->npad, b->DGb, b->nm_mpad, b->ld_n,
+                  (size_t)b->nm_mpad * b->ld_n, L))) return fail(rc);
+  if ((rc = repad(b, h->H, n, n, h->npad, 0, b->Hb, b->n_mpad, b->ld_n, 0, 1))) return fail(rc);
+  if ((rc = repad(b, h->Gr, m, n, h->npad, 0, b->Gb, b->m_mpad, b->ld_n, 0, 1))) return fail(rc);
+  if ((rc = repad(b, h->Gt, n, m, h->mpad, 0, b->Gtb, b->n_mpad, b->ld_m, 0, 1))) return fail(rc);
+  if (cudaStreamSynchronize(b->stream) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "batch_create sync"));
+  *out = b;
+  return CQP_OK;
+}
+
+void cqp_batch_destroy(cqp_batch* b) {
+  if (!b) return;
+  if (b->h) cudaSetDevice(b->h->device);
+  if (b->stream) cudaStreamSynchronize(b->stream);
+  void* ptrs[] = {b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+                  b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
+                  b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
+                  b->tiles, b->n_tiles, b->n_active};
+  for (void* p : ptrs) cudaFree(p);
+  if (b->h_active) cudaFreeHost(b->h_active);
+  for (cudaEvent_t e : b->round_events) cudaEventDestroy(e);
+  if (b->ev0) cudaEventDestroy(b->ev0);
+  if (b->ev1) cudaEventDestroy(b->ev1);
+  if (b->evc0) cudaEventDestroy(b->evc0);
+  if (b->evc1) cudaEventDestroy(b->evc1);
+  if (b->stream) cudaStreamDestroy(b->stream);
+  delete b;
+}
 
 int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_cols,
                     const double* d_cols, double* y_cols, double* z_cols, double* lambda_cols,
                     int* status, int* iterations, int* final_index, double* r_prim,
                     double* r_dual, int* n_switches, double* device_ms) {
-  (void)b; (void)B; (void)g_cols; (void)c_cols; (void)d_cols; (void)y_cols; (void)z_cols;
-  (void)lambda_cols; (void)status; (void)iterations; (void)final_index; (void)r_prim;
-  (void)r_dual; (void)n_switches; (void)device_ms;
-  set_error("batched path not built yet");
-  return CQP_ERR_CAPACITY;
+  if (!b || !g_cols || !c_cols || !d_cols) { set_error("batch_solve: null argument"); return CQP_ERR_ARGUMENT; }
+  if (B < 1 || B > b->capacity) { set_error("batch_solve: B exceeds the batch capacity"); return CQP_ERR_CAPACITY; }
+  cqp_handle* h = b->h;
+  CQP_CUDA(cudaSetDevice(h->device));
+  const int n = b->n, m = b->m, nm = n + m;
+  const cqp_settings& s = h->s;
+  const int interval = s.check_interval;
+  const int full_rounds = s.max_iters / interval, rem = s.max_iters % interval;
+  const int rounds = full_rounds + (rem ? 1 : 0);
+  if (b->h_active_cap < rounds + 1) {
+    if (b->h_active) cudaFreeHost(b->h_active);
+    CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&b->h_active), sizeof(int) * (rounds + 1)));
+    b->h_active_cap = rounds + 1;
+  }
+  while ((int)b->round_events.size() < rounds + 1) {
+    cudaEvent_t e;
+    CQP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    b->round_events.push_back(e);
+  }
+  cudaStream_t st = b->stream;
+  CQP_CUDA(cudaEventRecord(b->ev0, st));
+  CQP_CUDA(cudaMemcpyAsync(b->g, g_cols, sizeof(double) * (size_t)n * B, cudaMemcpyHostToDevice, st));
+  CQP_CUDA(cudaMemcpyAsync(b->c, c_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));
+  CQP_CUDA(cudaMemcpyAsync(b->d, d_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));
+  CQP_CUDA(cudaMemsetAsync(b->S0, 0, sizeof(double) * (size_t)B * b->ld_s, st));  // cold start: v = 0
+  CQP_CUDA(cudaMemsetAsync(b->S1, 0, sizeof(double) * (size_t)B * b->ld_s, st));
+
+  BatchDev bd{};
+  bd.n = n; bd.m = m; bd.D = b->D; bd.B = B;
+  bd.ld_s = b->ld_s; bd.ld_n = b->ld_n; bd.ld_m = b->ld_m; bd.ld_nm = b->ld_nm;
+  bd.E = h->E; bd.F = h->F; bd.cost_scale = h->cost_scale;
+  bd.grid = h->dgrid; bd.log_grid = h->dlog_grid; bd.L = b->L;
+  bd.g = b->g; bd.c = b->c; bd.d = b->d; bd.gs = b->gs; bd.lo = b->lo; bd.hi = b->hi;
+  bd.uy = b->uy; bd.ul = b->ul; bd.uz = b->uz; bd.hy = b->hy; bd.gtl = b->gtl; bd.gy = b->gy;
+  bd.layer = b->layer; bd.active = b->active; bd.iters = b->iters; bd.status = b->status;
+  bd.nsw = b->nsw; bd.rp = b->rp; bd.rd = b->rd;
+  bd.out_y = b->out_y; bd.out_z = b->out_z; bd.out_l = b->out_l;
+  bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
+  bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
+  bd.adaptive = s.adaptive_rho; bd.max_iters = s.max_iters;
+
+  CQP_CUDA(cudaEventRecord(b->evc0, st));  // inputs are resident from here on
+  b->last_launches = 0;
+  batch_prepare_kernel<<<B, 128, 0, st>>>(bd, h->initial_index);
+  CQP_CUDA(cudaGetLastError());
+
+  GemmParams base{};
+  base.cols = b->cols; base.tiles = b->tiles; base.n_tiles = b->n_tiles;
+  base.alpha = 1.0;
+  auto gemm_bias = [&]() {  // Bias = -[D_k; G D_k] g_s  (layers.cpp:168-175), per bucket
+    GemmParams p = base;
+    p.A = b->DGb; p.a_stride = (size_t)b->nm_mpad * b->ld_n; p.lda = b->ld_n; p.M = nm;
+    p.m_tiles = b->nm_mpad / BM; p.k_tiles = b->ld_n / BK;
+    p.Bm = b->gs; p.ldb = b->ld_n; p.C = b->bias; p.ldc = b->ld_nm; p.alpha = -1.0; p.mode = 0;
+    return launch_gemm(b, p);
+  };
+  auto gemm_iter = [&](const double* Sin, double* Sout) {  // one ADMM layer for every active column
+    GemmParams p = base;
+    p.A = b->Wb; p.a_stride = (size_t)b->Dm_pad * b->ld_s; p.lda = b->ld_s; p.M = b->D;
+    p.m_tiles = b->Dm_pad / BM; p.k_tiles = b->ld_s / BK;
+    p.Bm = Sin; p.ldb = b->ld_s; p.C = Sout; p.ldc = b->ld_s; p.mode = 1;
+    p.bias = b->bias; p.ld_bias = b->ld_nm; p.nm = nm; p.n = n;
+    p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
+    return launch_gemm(b, p);
+  };
+  auto gemm_plain = [&](const double* A, int M, int m_pad, int lda, const double* Bm, int ldb, double* C, int ldc) {
+    GemmParams p = base;
+    p.A = A; p.a_stride = 0; p.lda = lda; p.M = M; p.m_tiles = m_pad / BM; p.k_tiles = lda / BK;
+    p.Bm = Bm; p.ldb = ldb; p.C = C; p.ldc = ldc; p.mode = 0;
+    return launch_gemm(b, p);
+  };
+
+  int rc;
+  batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
+  CQP_CUDA(cudaGetLastError());
+  if ((rc = gemm_bias())) return rc;
+
+  double* Sa = b->S0;
+  double* Sb = b->S1;
+  int it = 0;
+  for (int r = 0; r < rounds; ++r) {
+    if (r >= 2) {  // stay at most two rounds ahead of the device; stop once every column is done
+      CQP_CUDA(cudaEventSynchronize(b->round_events[r - 2]));
+      if (b->h_active[r - 2] == 0) break;
+    }
+    const int steps = (r < full_rounds) ? interval : rem;
+    for (int k = 0; k < steps; ++k) {
+      if ((rc = gemm_iter(Sa, Sb))) return rc;
+      std::swap(Sa, Sb);
+    }
+    it += steps;
+    // NOTE: columns that stopped earlier keep their (stale) value in whichever buffer they were
+    // last written to; they are never read again (results were captured when they stopped).
+    batch_unscale_kernel<<<B, 128, 0, st>>>(bd, Sa);
+    CQP_CUDA(cudaGetLastError());
+    if ((rc = gemm_plain(b->Hb, n, b->n_mpad, b->ld_n, b->uy, b->ld_n, b->hy, b->ld_n))) return rc;
+    if ((rc = gemm_plain(b->Gtb, n, b->n_mpad, b->ld_m, b->ul, b->ld_m, b->gtl, b->ld_n))) return rc;
+    if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m))) return rc;
+    batch_decide_kernel<<<(B + 7) / 8, 256, 0, st>>>(bd, it, r < full_rounds ? 1 : 0, 1);
+    CQP_CUDA(cudaGetLastError());
+    batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
+    CQP_CUDA(cudaGetLastError());
+    CQP_CUDA(cudaMemcpyAsync(&b->h_active[r], b->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CQP_CUDA(cudaEventRecord(b->round_events[r], st));
+    if (r + 1 < rounds && (rc = gemm_bias())) return rc;
+  }
+  CQP_CUDA(cudaEventRecord(b->evc1, st));
+  // results
+  if (y_cols) CQP_CUDA(cudaMemcpyAsync(y_cols, b->out_y, sizeof(double) * (size_t)n * B, cudaMemcpyDeviceToHost, st));
+  if (z_cols) CQP_CUDA(cudaMemcpyAsync(z_cols, b->out_z, sizeof(double) * (size_t)m * B, cudaMemcpyDeviceToHost, st));
+  if (lambda_cols) CQP_CUDA(cudaMemcpyAsync(lambda_cols, b->out_l, sizeof(double) * (size_t)m * B, cudaMemcpyDeviceToHost, st));
+  if (status) CQP_CUDA(cudaMemcpyAsync(status, b->status, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (iterations) CQP_CUDA(cudaMemcpyAsync(iterations, b->iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (final_index) CQP_CUDA(cudaMemcpyAsync(final_index, b->layer, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (r_prim) CQP_CUDA(cudaMemcpyAsync(r_prim, b->rp, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  if (r_dual) CQP_CUDA(cudaMemcpyAsync(r_dual, b->rd, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  if (n_switches) CQP_CUDA(cudaMemcpyAsync(n_switches, b->nsw, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  CQP_CUDA(cudaEventRecord(b->ev1, st));
+  CQP_CUDA(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&b->last_total_ms, b->ev0, b->ev1);
+  cudaEventElapsedTime(&b->last_compute_ms, b->evc0, b->evc1);
+  if (device_ms) *device_ms = b->last_total_ms;
+  return CQP_OK;
+}
+
+int cqp_batch_last_timing(const cqp_batch* b, double* compute_ms, double* total_ms, long long* gemm_launches) {
+  if (!b) return CQP_ERR_ARGUMENT;
+  if (compute_ms) *compute_ms = b->last_compute_ms;
+  if (total_ms) *total_ms = b->last_total_ms;
+  if (gemm_launches) *gemm_launches = b->last_launches;
+  return CQP_OK;
 }
 
 }  // extern "C"

@@ -270,3 +270,51 @@ class Solver:
         a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         _raise(self._L.cqp_launch_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
         return {"ctas": a.value, "rows_per_cta": b.value, "tier": c.value, "smem_bytes": d.value}
+
+
+class BatchSolver:
+    """Many QPs sharing (H, G) -- MPC instances that differ in x0, i.e. in (g, c, d) -- solved
+    together from a cold start: column j of the result equals what `Solver.solve()` returns
+    after `update_vectors(g[:, j], c[:, j], d[:, j]); cold_start()` (solver.cpp:158-166)."""
+
+    def __init__(self, solver: Solver, capacity: int):
+        self._L = solver._L
+        self._solver = solver          # keeps the shared ladder alive
+        self._b = C.c_void_p()
+        self.capacity = int(capacity)
+        _raise(self._L.cqp_batch_create(C.byref(self._b), solver._h, self.capacity))
+        self.n, self.m = solver.n, solver.m
+
+    def close(self) -> None:
+        b, self._b = getattr(self, "_b", None), C.c_void_p()
+        if b:
+            self._L.cqp_batch_destroy(b)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve(self, g_cols, c_cols, d_cols) -> dict:
+        g = np.asfortranarray(np.asarray(g_cols, dtype=np.float64))
+        c = np.asfortranarray(np.asarray(c_cols, dtype=np.float64))
+        d = np.asfortranarray(np.asarray(d_cols, dtype=np.float64))
+        if g.ndim != 2 or g.shape[0] != self.n or c.shape != (self.m, g.shape[1]) or d.shape != c.shape:
+            raise ValueError("batch solve: dimension mismatch")
+        B = g.shape[1]
+        y = np.empty((self.n, B), order="F"); z = np.empty((self.m, B), order="F")
+        lam = np.empty((self.m, B), order="F")
+        status = np.empty(B, dtype=np.int32); iters = np.empty(B, dtype=np.int32)
+        final = np.empty(B, dtype=np.int32); nsw = np.empty(B, dtype=np.int32)
+        rp = np.empty(B); rd = np.empty(B)
+        ms = C.c_double()
+        ip = lambda a: a.ctypes.data_as(_lib.c_int_p)  # noqa: E731
+        _raise(self._L.cqp_batch_solve(self._b, B, _p(g), _p(c), _p(d), _p(y), _p(z), _p(lam),
+                                       ip(status), ip(iters), ip(final), _p(rp), _p(rd), ip(nsw),
+                                       C.byref(ms)))
+        comp, tot, launches = C.c_double(), C.c_double(), C.c_longlong()
+        self._L.cqp_batch_last_timing(self._b, C.byref(comp), C.byref(tot), C.byref(launches))
+        return {"y": y, "z": z, "lam": lam, "status": status, "iterations": iters,
+                "final_index": final, "n_switches": nsw, "r_prim": rp, "r_dual": rd,
+                "device_ms": ms.value, "compute_ms": comp.value, "gemm_launches": launches.value}

@@ -1,0 +1,91 @@
+"""GPU parity tests of the batched path (FP64 DMMA grouped GEMM) vs the CPU oracle, column by
+column: identical iteration counts, final ladder index and switch counts; y, lambda within 1e-6."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2311_18056_b200 import solver as S
+    from paper_2311_18056_b200 import _lib
+    if _lib.load().cqp_device_count() < 1:
+        pytest.fail("no CUDA device: the solve path has no CPU fallback")
+    return S
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2311_18056_b200 import problems
+    return problems
+
+
+def rel_err(a, b):
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+def oracle_columns(O, base, g, c, d):
+    s = O.Solver(O.QProblem(base.H, base.g, base.G, base.c, base.d), variant="v3")
+    out = []
+    for j in range(g.shape[1]):
+        s.update_vectors(g[:, j], c[:, j], d[:, j])
+        s.cold_start()
+        out.append(s.solve().solution)
+    return s, out
+
+
+@pytest.mark.parametrize("nu,B,unstable", [(10, 200, False), (10, 131, True), (4, 1, False), (20, 300, False)])
+def test_batch_matches_per_column_oracle(G, oracle, P, nu, B, unstable):
+    wl = P.config2(nu, seed=5, unstable=unstable)
+    base = wl.base_problem()
+    g, c, d, _ = P.batch_instances(wl, B, lo=0.3, hi=10.0)
+    cpu, ref = oracle_columns(oracle, base, g, c, d)
+    layers = {"W": [cpu.cache.W(k) for k in range(cpu.cache.L)], "D": [cpu.cache.D(k) for k in range(cpu.cache.L)],
+              "GD": [cpu.cache.GD(k) for k in range(cpu.cache.L)], "grid": cpu.cache.grid,
+              "initial_index": cpu.cache.initial_index, "Gs": cpu.cache.Gs, "E": cpu.cache.E,
+              "F": cpu.cache.F, "cost_scale": cpu.cache.cost_scale}
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=layers)
+    batch = G.BatchSolver(single, capacity=B)
+    out = batch.solve(g, c, d)
+    iters_ref = np.array([s.iterations for s in ref])
+    assert np.array_equal(out["iterations"], iters_ref)
+    assert np.array_equal(out["status"], np.array([s.status for s in ref]))
+    assert np.array_equal(out["final_index"], np.array([s.rho_trace[-1][1] for s in ref]))
+    assert np.array_equal(out["n_switches"], np.array([len(s.rho_trace) - 1 for s in ref]))
+    assert len(set(iters_ref.tolist())) > 1 or B == 1      # the batch really is heterogeneous
+    for j, s in enumerate(ref):
+        assert rel_err(out["y"][:, j], s.y) <= 1e-6
+        assert rel_err(out["lam"][:, j], s.lam) <= 1e-6
+        assert rel_err(out["z"][:, j], s.z) <= 1e-6
+        assert abs(out["r_prim"][j] - s.r_prim) <= 2e-3 * s.r_prim + 1e-9
+        assert abs(out["r_dual"][j] - s.r_dual) <= 2e-3 * s.r_dual + 1e-9
+        assert np.all(out["z"][:, j] >= c[:, j]) and np.all(out["z"][:, j] <= d[:, j])
+    # second call on the same batch object (buffers are reused) and the single-QP kernel agree
+    out2 = batch.solve(g, c, d)
+    assert np.array_equal(out2["iterations"], out["iterations"]) and np.array_equal(out2["y"], out["y"])
+    single.update_vectors(g[:, 0], c[:, 0], d[:, 0]); single.cold_start()
+    r = single.solve()
+    assert r.solution.iterations == out["iterations"][0]
+    assert rel_err(out["y"][:, 0], r.solution.y) <= 1e-9
+
+
+def test_batch_max_iters_and_capacity(G, oracle, P):
+    wl = P.config2(4, seed=1)
+    base = wl.base_problem()
+    g, c, d, _ = P.batch_instances(wl, 40, lo=5.0, hi=10.0)
+    st = G.SolverSettings(eps_prim=1e-13, eps_dual=1e-13, max_iters=60)   # 2 checks + 10 trailing iterations
+    so = oracle.SolverSettings(eps_prim=1e-13, eps_dual=1e-13, max_iters=60)
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d, st)
+    batch = G.BatchSolver(single, capacity=64)
+    out = batch.solve(g, c, d)
+    cpu = oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), so)
+    for j in range(40):
+        cpu.update_vectors(g[:, j], c[:, j], d[:, j]); cpu.cold_start()
+        s = cpu.solve().solution
+        assert out["iterations"][j] == 60 == s.iterations
+        assert out["status"][j] == s.status == G.MAX_ITERS
+        assert out["n_switches"][j] == len(s.rho_trace) - 1
+        assert rel_err(out["y"][:, j], s.y) <= 1e-6
+    with pytest.raises(MemoryError):
+        batch.solve(np.zeros((base.n, 65)), np.zeros((base.m, 65)), np.ones((base.m, 65)))
