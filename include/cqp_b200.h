@@ -198,9 +198,15 @@ CQP_API int cqp_batch_solve(cqp_batch *b, int B, const double *g_cols, const dou
 
 /* CUDA-event times of the last cqp_batch_solve: compute_ms = from "inputs resident in HBM" to
  * "results ready in HBM"; total_ms additionally covers the host->device and device->host
- * copies; gemm_launches = DMMA GEMM kernels launched. */
+ * copies; launches = kernels launched by the solve. */
 CQP_API int cqp_batch_last_timing(const cqp_batch *b, double *compute_ms, double *total_ms,
-                                  long long *gemm_launches);
+                                  long long *launches);
+
+/* Iteration-GEMM profile of the last cqp_batch_solve: gemm_ms = CUDA-event time spent in the
+ * iteration GEMM launches, gemm_flops = the algorithmic flops they carried (2 D^2 per active
+ * column per iteration), rounds = check rounds executed. */
+CQP_API int cqp_batch_last_profile(const cqp_batch *b, double *gemm_ms, double *gemm_flops,
+                                   int *rounds);
 
 #ifdef __cplusplus
 }

@@ -442,7 +442,9 @@ struct cqp_batch {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;
   float last_total_ms = 0.f, last_compute_ms = 0.f;
   long long last_launches = 0;
-  std::vector<cudaEvent_t> round_events;
+  std::vector<cudaEvent_t> round_events, it0, it1;  // it0/it1: around each round's iteration GEMMs
+  double last_gemm_ms = 0.0, last_gemm_flops = 0.0;
+  int last_rounds = 0;
   // shared matrices re-padded for the GEMM tiles
   double *Wb = nullptr, *DGb = nullptr, *Hb = nullptr, *Gb = nullptr, *Gtb = nullptr;
   // per-column buffers
@@ -550,6 +552,8 @@ void cqp_batch_destroy(cqp_batch* b) {
   for (void* p : ptrs) cudaFree(p);
   if (b->h_active) cudaFreeHost(b->h_active);
   for (cudaEvent_t e : b->round_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : b->it0) cudaEventDestroy(e);
+  for (cudaEvent_t e : b->it1) cudaEventDestroy(e);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
   if (b->evc0) cudaEventDestroy(b->evc0);
@@ -577,9 +581,13 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     b->h_active_cap = rounds + 1;
   }
   while ((int)b->round_events.size() < rounds + 1) {
-    cudaEvent_t e;
+    cudaEvent_t e, e0, e1;
     CQP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CQP_CUDA(cudaEventCreate(&e0));
+    CQP_CUDA(cudaEventCreate(&e1));
     b->round_events.push_back(e);
+    b->it0.push_back(e0);
+    b->it1.push_back(e1);
   }
   cudaStream_t st = b->stream;
   CQP_CUDA(cudaEventRecord(b->ev0, st));
@@ -637,26 +645,31 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   int rc;
   batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
   CQP_CUDA(cudaGetLastError());
+  b->last_launches += 2;  // prepare, regroup
   if ((rc = gemm_bias())) return rc;
 
   double* Sa = b->S0;
   double* Sb = b->S1;
-  int it = 0;
+  int it = 0, rounds_done = 0;
   for (int r = 0; r < rounds; ++r) {
     if (r >= 2) {  // stay at most two rounds ahead of the device; stop once every column is done
       CQP_CUDA(cudaEventSynchronize(b->round_events[r - 2]));
       if (b->h_active[r - 2] == 0) break;
     }
     const int steps = (r < full_rounds) ? interval : rem;
+    CQP_CUDA(cudaEventRecord(b->it0[r], st));
     for (int k = 0; k < steps; ++k) {
       if ((rc = gemm_iter(Sa, Sb))) return rc;
       std::swap(Sa, Sb);
     }
+    CQP_CUDA(cudaEventRecord(b->it1[r], st));
+    rounds_done = r + 1;
     it += steps;
     // NOTE: columns that stopped earlier keep their (stale) value in whichever buffer they were
     // last written to; they are never read again (results were captured when they stopped).
     batch_unscale_kernel<<<B, 128, 0, st>>>(bd, Sa);
     CQP_CUDA(cudaGetLastError());
+    b->last_launches += 3;  // unscale, decide, regroup
     if ((rc = gemm_plain(b->Hb, n, b->n_mpad, b->ld_n, b->uy, b->ld_n, b->hy, b->ld_n))) return rc;
     if ((rc = gemm_plain(b->Gtb, n, b->n_mpad, b->ld_m, b->ul, b->ld_m, b->gtl, b->ld_n))) return rc;
     if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m))) return rc;
@@ -681,17 +694,38 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   if (n_switches) CQP_CUDA(cudaMemcpyAsync(n_switches, b->nsw, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
   CQP_CUDA(cudaEventRecord(b->ev1, st));
   CQP_CUDA(cudaStreamSynchronize(st));
+  // iteration-GEMM profile of this solve: time of every round's GEMM launches and the
+  // algorithmic flops they carried (2 D^2 per active column per iteration)
+  b->last_gemm_ms = 0.0;
+  b->last_gemm_flops = 0.0;
+  b->last_rounds = rounds_done;
+  for (int r = 0; r < rounds_done; ++r) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, b->it0[r], b->it1[r]);
+    const int steps = (r < full_rounds) ? interval : rem;
+    const double active = (r == 0) ? (double)B : (double)b->h_active[r - 1];
+    b->last_gemm_ms += ms;
+    b->last_gemm_flops += 2.0 * (double)b->D * (double)b->D * active * steps;
+  }
   cudaEventElapsedTime(&b->last_total_ms, b->ev0, b->ev1);
   cudaEventElapsedTime(&b->last_compute_ms, b->evc0, b->evc1);
   if (device_ms) *device_ms = b->last_total_ms;
   return CQP_OK;
 }
 
-int cqp_batch_last_timing(const cqp_batch* b, double* compute_ms, double* total_ms, long long* gemm_launches) {
+int cqp_batch_last_timing(const cqp_batch* b, double* compute_ms, double* total_ms, long long* launches) {
   if (!b) return CQP_ERR_ARGUMENT;
   if (compute_ms) *compute_ms = b->last_compute_ms;
   if (total_ms) *total_ms = b->last_total_ms;
-  if (gemm_launches) *gemm_launches = b->last_launches;
+  if (launches) *launches = b->last_launches;
+  return CQP_OK;
+}
+
+int cqp_batch_last_profile(const cqp_batch* b, double* gemm_ms, double* gemm_flops, int* rounds) {
+  if (!b) return CQP_ERR_ARGUMENT;
+  if (gemm_ms) *gemm_ms = b->last_gemm_ms;
+  if (gemm_flops) *gemm_flops = b->last_gemm_flops;
+  if (rounds) *rounds = b->last_rounds;
   return CQP_OK;
 }
 

@@ -315,6 +315,9 @@ class BatchSolver:
                                        C.byref(ms)))
         comp, tot, launches = C.c_double(), C.c_double(), C.c_longlong()
         self._L.cqp_batch_last_timing(self._b, C.byref(comp), C.byref(tot), C.byref(launches))
+        gms, gfl, rounds = C.c_double(), C.c_double(), C.c_int()
+        self._L.cqp_batch_last_profile(self._b, C.byref(gms), C.byref(gfl), C.byref(rounds))
         return {"y": y, "z": z, "lam": lam, "status": status, "iterations": iters,
                 "final_index": final, "n_switches": nsw, "r_prim": rp, "r_dual": rd,
-                "device_ms": ms.value, "compute_ms": comp.value, "gemm_launches": launches.value}
+                "device_ms": ms.value, "compute_ms": comp.value, "launches": launches.value,
+                "gemm_ms": gms.value, "gemm_flops": gfl.value, "rounds": rounds.value}
