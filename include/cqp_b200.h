@@ -208,6 +208,10 @@ CQP_API int cqp_batch_last_timing(const cqp_batch *b, double *compute_ms, double
 CQP_API int cqp_batch_last_profile(const cqp_batch *b, double *gemm_ms, double *gemm_flops,
                                    int *rounds);
 
+/* Per check round of the last solve (up to `cap` rounds): active columns during the round and
+ * the CUDA-event time of its iteration GEMM launches. */
+CQP_API int cqp_batch_round_profile(const cqp_batch *b, int cap, int *active, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

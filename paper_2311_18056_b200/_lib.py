@@ -55,7 +55,7 @@ EXPORTS = [
     "cqp_warm_start", "cqp_refresh_z", "cqp_solve", "cqp_fixed_iters", "cqp_mpc_step",
     "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
     "cqp_launch_info",
-    "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve", "cqp_batch_last_timing", "cqp_batch_last_profile",
+    "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve", "cqp_batch_last_timing", "cqp_batch_last_profile", "cqp_batch_round_profile",
 ]
 
 _lib = None
@@ -109,6 +109,7 @@ def load() -> C.CDLL:
         c_int_p, c_int_p, c_int_p, c_double_p, c_double_p, c_int_p, c_double_p]
     L.cqp_batch_last_timing.argtypes = [C.c_void_p, c_double_p, c_double_p, C.POINTER(C.c_longlong)]
     L.cqp_batch_last_profile.argtypes = [C.c_void_p, c_double_p, c_double_p, c_int_p]
+    L.cqp_batch_round_profile.argtypes = [C.c_void_p, C.c_int, c_int_p, c_double_p]
     _lib = L
     return L
 

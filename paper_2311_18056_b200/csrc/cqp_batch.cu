@@ -21,6 +21,8 @@
 //     a lag of two rounds to know when to stop enqueuing.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -29,12 +31,11 @@
 namespace cqp {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
-constexpr int GEMM_THREADS = 256;
-constexpr int GEMM_SMEM = STAGES * (BM + BN) * BK * (int)sizeof(double) + BN * (int)sizeof(int);
+constexpr int BK = 16, STAGES = 4;
+constexpr int SLOT_TILE = 128;  // slot-map granularity: buckets are padded to 128 slots
 
 struct TileDesc {
-  int slot0;    // first slot of this 128-column tile
+  int slot0;    // first slot of this 128-slot tile
   int a_index;  // which A matrix (ladder index) the tile multiplies
 };
 
@@ -43,7 +44,7 @@ struct GemmParams {
   size_t a_stride;   // doubles between consecutive A matrices (0: one shared A)
   int lda;
   int M;             // valid output rows
-  int m_tiles;
+  int M_pad;         // padded rows of A (multiple of 128)
   int k_tiles;
   const double* Bm;  // [col][ldb], K contiguous
   int ldb;
@@ -80,10 +81,21 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-// element (row r, k index e) of a [rows][16] tile in the 16-byte-chunk XOR swizzle
-__device__ __forceinline__ int swz(int r, int e) { return r * BK + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1)); }
+template <int BM, int BN>
+constexpr int gemm_smem_bytes() {
+  return STAGES * (BM + BN) * BK * (int)sizeof(double) + BN * (int)sizeof(int);
+}
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) dmma_gemm_kernel(const GemmParams p) {
+// C[col][row] = epilogue(A[a_index] (BM x K) . B(cols) (K x BN)) for every (slot tile, sub-tile,
+// m-tile) work item; persistent CTAs stride over the items.  WM x WN warps, warp tile
+// (BM/WM) x (BN/WN) made of 8x8 DMMA tiles.  Operand tiles are [rows][16] doubles whose
+// 16-byte chunks are XOR-swizzled with (row & 7): the 8-byte fragment loads of a warp (8 rows x
+// 4 consecutive k) then hit 32 distinct banks per half-warp.
+template <int BM, int BN, int WM, int WN, int MINB>
+__global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const GemmParams p) {
+  constexpr int T = WM * WN * 32;
+  constexpr int TM = BM / WM, TN = BN / WN, MI = TM / 8, NI = TN / 8;
+  constexpr int SUB = SLOT_TILE / BN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
   double* Bs = As + STAGES * BM * BK;
@@ -91,16 +103,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dmma_gemm_kernel(const GemmPa
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int warp_m = warp & 1, warp_n = warp >> 1;  // 2 x 4 warps, warp tile 64 x 32
-  const int total = (*p.n_tiles) * p.m_tiles;
+  const int warp_m = warp % WM, warp_n = warp / WM;
+  const int m_tiles = p.M_pad / BM;
+  const int total = (*p.n_tiles) * SUB * m_tiles;
 
-  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    const int nt = tile / p.m_tiles, mt = tile - nt * p.m_tiles;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int ns = item / m_tiles, mt = item - ns * m_tiles;
+    const int nt = ns / SUB, sub = ns - nt * SUB;
     const TileDesc td = p.tiles[nt];
+    const int slot0 = td.slot0 + sub * BN;
+    if (p.cols[slot0] < 0) continue;  // padding slots sit at the end of a bucket: empty sub-tile
     const int m0 = mt * BM;
+    if (m0 >= p.M) continue;
     const double* A = p.A + (size_t)td.a_index * p.a_stride + (size_t)m0 * p.lda;
-    __syncthreads();  // previous tile's readers of cols_s / smem are done
-    if (tid < BN) cols_s[tid] = p.cols[td.slot0 + tid];
+    __syncthreads();  // previous item's readers of cols_s / smem are done
+    if (tid < BN) cols_s[tid] = p.cols[slot0 + tid];
     __syncthreads();
 
     auto issue = [&](int kt, int stage) {
@@ -108,22 +125,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dmma_gemm_kernel(const GemmPa
       double* as = As + stage * BM * BK;
       double* bs = Bs + stage * BN * BK;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int chunk = tid + GEMM_THREADS * i;
-        const int r = chunk >> 3, c = chunk & 7;
-        const int dst = r * BK + ((c ^ (r & 7)) << 1);
-        cp_async16(as + dst, A + (size_t)r * p.lda + k0 + c * 2, 16);
+      for (int ch = tid; ch < BM * 8; ch += T) {
+        const int r = ch >> 3, c = ch & 7;
+        cp_async16(as + r * BK + ((c ^ (r & 7)) << 1), A + (size_t)r * p.lda + k0 + c * 2, 16);
+      }
+#pragma unroll
+      for (int ch = tid; ch < BN * 8; ch += T) {
+        const int r = ch >> 3, c = ch & 7;
         const int col = cols_s[r];
         const double* src = p.Bm + (size_t)(col < 0 ? 0 : col) * p.ldb + k0 + c * 2;
-        cp_async16(bs + dst, src, col < 0 ? 0 : 16);
+        cp_async16(bs + r * BK + ((c ^ (r & 7)) << 1), src, col < 0 ? 0 : 16);
       }
     };
 
-    double acc[8][4][2];
+    double acc[MI][NI][2];
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -136,36 +155,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) dmma_gemm_kernel(const GemmPa
       const int next = kt + STAGES - 1;
       if (next < p.k_tiles) issue(next, next % STAGES);
       cp_async_commit();
-      const double* as = As + (kt % STAGES) * BM * BK + (warp_m * 64) * BK;
-      const double* bs = Bs + (kt % STAGES) * BN * BK + (warp_n * 32) * BK;
+      const double* as = As + (kt % STAGES) * BM * BK + (warp_m * TM) * BK;
+      const double* bs = Bs + (kt % STAGES) * BN * BK + (warp_n * TN) * BK;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         const int e = ks * 4 + t4;
         const int off = (((e >> 1) ^ g) << 1) | (e & 1);  // rows are 8-aligned + g, so r & 7 == g
-        double a[8], b[4];
+        double a[MI], b[NI];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) a[mi] = as[(mi * 8 + g) * BK + off];
+        for (int mi = 0; mi < MI; ++mi) a[mi] = as[(mi * 8 + g) * BK + off];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) b[ni] = bs[(ni * 8 + g) * BK + off];
+        for (int ni = 0; ni < NI; ++ni) b[ni] = bs[(ni * 8 + g) * BK + off];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
     }
     cp_async_wait<0>();
 
     // epilogue: C fragment (row = g, cols 2*t4, 2*t4+1) of each 8x8 sub-tile
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
+    for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int col = cols_s[warp_n * 32 + ni * 8 + 2 * t4 + j];
+        const int col = cols_s[warp_n * TN + ni * 8 + 2 * t4 + j];
         if (col < 0) continue;
         double* crow = p.C + (size_t)col * p.ldc;
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-          const int row = m0 + warp_m * 64 + mi * 8 + g;
+        for (int mi = 0; mi < MI; ++mi) {
+          const int row = m0 + warp_m * TM + mi * 8 + g;
           if (row >= p.M) continue;
           double v = p.alpha * acc[mi][ni][j];
           if (p.mode == 1 && row < p.nm) {
@@ -381,7 +400,7 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
 }
 
 // Rebuild the slot map: active columns bucketed by ladder index, every bucket padded to a
-// multiple of BN with -1 slots, one TileDesc per 128 slots.  Single CTA, deterministic (stable
+// multiple of 128 with -1 slots, one TileDesc per 128 slots.  Single CTA, deterministic (stable
 // in the column index).
 __global__ void batch_regroup_kernel(BatchDev b) {
   __shared__ int warp_sums[32];
@@ -412,13 +431,13 @@ __global__ void batch_regroup_kernel(BatchDev b) {
       __syncthreads();
     }
     const int count = base_s;
-    const int padded = (count + BN - 1) / BN * BN;
+    const int padded = (count + SLOT_TILE - 1) / SLOT_TILE * SLOT_TILE;
     for (int i = count + tid; i < padded; i += blockDim.x) b.cols[slot_base_s + i] = -1;
-    for (int t = tid; t < padded / BN; t += blockDim.x) {
-      b.tiles[n_tiles + t].slot0 = slot_base_s + t * BN;
+    for (int t = tid; t < padded / SLOT_TILE; t += blockDim.x) {
+      b.tiles[n_tiles + t].slot0 = slot_base_s + t * SLOT_TILE;
       b.tiles[n_tiles + t].a_index = k;
     }
-    n_tiles += padded / BN;
+    n_tiles += padded / SLOT_TILE;
     __syncthreads();
     if (tid == 0) { slot_base_s += padded; total_active_s += count; }
     __syncthreads();
@@ -437,7 +456,12 @@ struct cqp_batch {
   int n = 0, m = 0, D = 0, L = 0;
   int ld_s = 0, ld_n = 0, ld_m = 0, ld_nm = 0;
   int Dm_pad = 0, nm_mpad = 0, n_mpad = 0, m_mpad = 0;
-  int grid_ctas = 0;
+  int grid_ctas[4] = {0, 0, 0, 0};  // persistent grid per tile configuration
+  // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/):
+  // 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size (less wave quantisation, 12
+  // warps/SM), 64x32 wins below ~3400 columns, 32x32 for the last few dozen columns.
+  int thr_big = 1 << 30, thr_mid = 3400, thr_small = 96;
+  int force_cfg = -1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;
   float last_total_ms = 0.f, last_compute_ms = 0.f;
@@ -445,6 +469,8 @@ struct cqp_batch {
   std::vector<cudaEvent_t> round_events, it0, it1;  // it0/it1: around each round's iteration GEMMs
   double last_gemm_ms = 0.0, last_gemm_flops = 0.0;
   int last_rounds = 0;
+  std::vector<float> round_ms;
+  std::vector<int> round_active;
   // shared matrices re-padded for the GEMM tiles
   double *Wb = nullptr, *DGb = nullptr, *Hb = nullptr, *Gb = nullptr, *Gtb = nullptr;
   // per-column buffers
@@ -471,9 +497,34 @@ int balloc(T** p, size_t count) {
 
 int round_up_i(int x, int q) { return (x + q - 1) / q * q; }
 
-int launch_gemm(cqp_batch* b, const GemmParams& p) {
+// Tile configurations: 0: 128x128 (8 warps), 1: 64x64 (4 warps), 2: 64x32 (4 warps),
+// 3: 32x32 (4 warps).  Smaller tiles keep the SMs busy when few columns are still active.
+using GemmKernel = void (*)(const GemmParams);
+struct GemmConfig {
+  GemmKernel fn;
+  int threads;
+  int smem;
+};
+const GemmConfig kConfigs[4] = {
+    {dmma_gemm_kernel<128, 128, 2, 4, 1>, 256, gemm_smem_bytes<128, 128>()},
+    {dmma_gemm_kernel<64, 64, 2, 2, 3>, 128, gemm_smem_bytes<64, 64>()},
+    {dmma_gemm_kernel<64, 32, 2, 2, 4>, 128, gemm_smem_bytes<64, 32>()},
+    {dmma_gemm_kernel<32, 32, 2, 2, 6>, 128, gemm_smem_bytes<32, 32>()},
+};
+
+// Tile shape for a round with (at most) `active` columns still iterating.
+int pick_config(const cqp_batch* b, int active) {
+  if (b->force_cfg >= 0) return b->force_cfg;
+  if (active >= b->thr_big) return 0;
+  if (active >= b->thr_mid) return 1;
+  if (active >= b->thr_small) return 2;
+  return 3;
+}
+
+int launch_gemm(cqp_batch* b, const GemmParams& p, int cfg) {
   b->last_launches += 1;
-  dmma_gemm_kernel<<<b->grid_ctas, GEMM_THREADS, GEMM_SMEM, b->stream>>>(p);
+  const GemmConfig& c = kConfigs[cfg];
+  c.fn<<<b->grid_ctas[cfg], c.threads, c.smem, b->stream>>>(p);
   CQP_CUDA(cudaGetLastError());
   return CQP_OK;
 }
@@ -501,18 +552,26 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   const int n = b->n, m = b->m, D = b->D, L = b->L, nm = n + m;
   b->ld_s = round_up_i(D, BK); b->ld_n = round_up_i(n, BK); b->ld_m = round_up_i(m, BK);
   b->ld_nm = round_up_i(nm, 2);
-  b->Dm_pad = round_up_i(D, BM); b->nm_mpad = round_up_i(nm, BM);
-  b->n_mpad = round_up_i(n, BM); b->m_mpad = round_up_i(m, BM);
-  b->grid_ctas = h->num_sms;
+  b->Dm_pad = round_up_i(D, 128); b->nm_mpad = round_up_i(nm, 128);
+  b->n_mpad = round_up_i(n, 128); b->m_mpad = round_up_i(m, 128);
   auto fail = [&](int rc) { cqp_batch_destroy(b); return rc; };
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CQP_ERR_CUDA);
   cudaEventCreate(&b->ev0); cudaEventCreate(&b->ev1);
   cudaEventCreate(&b->evc0); cudaEventCreate(&b->evc1);
-  if (cudaFuncSetAttribute(dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) != cudaSuccess)
-    return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dmma_gemm_kernel)"));
+  for (int cfg = 0; cfg < 4; ++cfg) {
+    const GemmConfig& gc = kConfigs[cfg];
+    if (cudaFuncSetAttribute(gc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gc.smem) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dmma_gemm_kernel)"));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gc.fn, gc.threads, gc.smem) != cudaSuccess || occ < 1)
+      return fail(cuda_fail(cudaGetLastError(), "occupancy(dmma_gemm_kernel)"));
+    b->grid_ctas[cfg] = occ * h->num_sms;
+  }
+  if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
+  if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
   int rc;
   const size_t cap = (size_t)capacity;
-  const size_t slot_cap = cap + (size_t)L * BN, tile_cap = slot_cap / BN + L;
+  const size_t slot_cap = cap + (size_t)L * SLOT_TILE, tile_cap = slot_cap / SLOT_TILE + L;
 #define BA(ptr, count) if ((rc = balloc(&b->ptr, (count)))) return fail(rc)
   BA(Wb, (size_t)L * b->Dm_pad * b->ld_s);
   BA(DGb, (size_t)L * b->nm_mpad * b->ld_n);
@@ -619,34 +678,34 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   GemmParams base{};
   base.cols = b->cols; base.tiles = b->tiles; base.n_tiles = b->n_tiles;
   base.alpha = 1.0;
-  auto gemm_bias = [&]() {  // Bias = -[D_k; G D_k] g_s  (layers.cpp:168-175), per bucket
+  auto gemm_bias = [&](int cfg) {  // Bias = -[D_k; G D_k] g_s  (layers.cpp:168-175), per bucket
     GemmParams p = base;
     p.A = b->DGb; p.a_stride = (size_t)b->nm_mpad * b->ld_n; p.lda = b->ld_n; p.M = nm;
-    p.m_tiles = b->nm_mpad / BM; p.k_tiles = b->ld_n / BK;
+    p.M_pad = b->nm_mpad; p.k_tiles = b->ld_n / BK;
     p.Bm = b->gs; p.ldb = b->ld_n; p.C = b->bias; p.ldc = b->ld_nm; p.alpha = -1.0; p.mode = 0;
-    return launch_gemm(b, p);
+    return launch_gemm(b, p, cfg);
   };
-  auto gemm_iter = [&](const double* Sin, double* Sout) {  // one ADMM layer for every active column
+  auto gemm_iter = [&](const double* Sin, double* Sout, int cfg) {  // one ADMM layer for every active column
     GemmParams p = base;
     p.A = b->Wb; p.a_stride = (size_t)b->Dm_pad * b->ld_s; p.lda = b->ld_s; p.M = b->D;
-    p.m_tiles = b->Dm_pad / BM; p.k_tiles = b->ld_s / BK;
+    p.M_pad = b->Dm_pad; p.k_tiles = b->ld_s / BK;
     p.Bm = Sin; p.ldb = b->ld_s; p.C = Sout; p.ldc = b->ld_s; p.mode = 1;
     p.bias = b->bias; p.ld_bias = b->ld_nm; p.nm = nm; p.n = n;
     p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
-    return launch_gemm(b, p);
+    return launch_gemm(b, p, cfg);
   };
-  auto gemm_plain = [&](const double* A, int M, int m_pad, int lda, const double* Bm, int ldb, double* C, int ldc) {
+  auto gemm_plain = [&](const double* A, int M, int m_pad, int lda, const double* Bm, int ldb, double* C, int ldc, int cfg) {
     GemmParams p = base;
-    p.A = A; p.a_stride = 0; p.lda = lda; p.M = M; p.m_tiles = m_pad / BM; p.k_tiles = lda / BK;
+    p.A = A; p.a_stride = 0; p.lda = lda; p.M = M; p.M_pad = m_pad; p.k_tiles = lda / BK;
     p.Bm = Bm; p.ldb = ldb; p.C = C; p.ldc = ldc; p.mode = 0;
-    return launch_gemm(b, p);
+    return launch_gemm(b, p, cfg);
   };
 
   int rc;
   batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
   CQP_CUDA(cudaGetLastError());
   b->last_launches += 2;  // prepare, regroup
-  if ((rc = gemm_bias())) return rc;
+  if ((rc = gemm_bias(pick_config(b, B)))) return rc;
 
   double* Sa = b->S0;
   double* Sb = b->S1;
@@ -657,9 +716,11 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
       if (b->h_active[r - 2] == 0) break;
     }
     const int steps = (r < full_rounds) ? interval : rem;
+    // the host knows the active count with a lag of two rounds; it only decreases
+    const int cfg = pick_config(b, r >= 2 ? b->h_active[r - 2] : B);
     CQP_CUDA(cudaEventRecord(b->it0[r], st));
     for (int k = 0; k < steps; ++k) {
-      if ((rc = gemm_iter(Sa, Sb))) return rc;
+      if ((rc = gemm_iter(Sa, Sb, cfg))) return rc;
       std::swap(Sa, Sb);
     }
     CQP_CUDA(cudaEventRecord(b->it1[r], st));
@@ -670,16 +731,16 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     batch_unscale_kernel<<<B, 128, 0, st>>>(bd, Sa);
     CQP_CUDA(cudaGetLastError());
     b->last_launches += 3;  // unscale, decide, regroup
-    if ((rc = gemm_plain(b->Hb, n, b->n_mpad, b->ld_n, b->uy, b->ld_n, b->hy, b->ld_n))) return rc;
-    if ((rc = gemm_plain(b->Gtb, n, b->n_mpad, b->ld_m, b->ul, b->ld_m, b->gtl, b->ld_n))) return rc;
-    if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m))) return rc;
+    if ((rc = gemm_plain(b->Hb, n, b->n_mpad, b->ld_n, b->uy, b->ld_n, b->hy, b->ld_n, cfg))) return rc;
+    if ((rc = gemm_plain(b->Gtb, n, b->n_mpad, b->ld_m, b->ul, b->ld_m, b->gtl, b->ld_n, cfg))) return rc;
+    if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m, cfg))) return rc;
     batch_decide_kernel<<<(B + 7) / 8, 256, 0, st>>>(bd, it, r < full_rounds ? 1 : 0, 1);
     CQP_CUDA(cudaGetLastError());
     batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
     CQP_CUDA(cudaGetLastError());
     CQP_CUDA(cudaMemcpyAsync(&b->h_active[r], b->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CQP_CUDA(cudaEventRecord(b->round_events[r], st));
-    if (r + 1 < rounds && (rc = gemm_bias())) return rc;
+    if (r + 1 < rounds && (rc = gemm_bias(cfg))) return rc;
   }
   CQP_CUDA(cudaEventRecord(b->evc1, st));
   // results
@@ -699,11 +760,15 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   b->last_gemm_ms = 0.0;
   b->last_gemm_flops = 0.0;
   b->last_rounds = rounds_done;
+  b->round_ms.assign(rounds_done, 0.f);
+  b->round_active.assign(rounds_done, 0);
   for (int r = 0; r < rounds_done; ++r) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, b->it0[r], b->it1[r]);
     const int steps = (r < full_rounds) ? interval : rem;
     const double active = (r == 0) ? (double)B : (double)b->h_active[r - 1];
+    b->round_ms[r] = ms;
+    b->round_active[r] = (int)active;
     b->last_gemm_ms += ms;
     b->last_gemm_flops += 2.0 * (double)b->D * (double)b->D * active * steps;
   }
@@ -718,6 +783,16 @@ int cqp_batch_last_timing(const cqp_batch* b, double* compute_ms, double* total_
   if (compute_ms) *compute_ms = b->last_compute_ms;
   if (total_ms) *total_ms = b->last_total_ms;
   if (launches) *launches = b->last_launches;
+  return CQP_OK;
+}
+
+int cqp_batch_round_profile(const cqp_batch* b, int cap, int* active, double* ms) {
+  if (!b) return CQP_ERR_ARGUMENT;
+  const int cnt = std::min(cap, (int)b->round_ms.size());
+  for (int r = 0; r < cnt; ++r) {
+    if (active) active[r] = b->round_active[r];
+    if (ms) ms[r] = b->round_ms[r];
+  }
   return CQP_OK;
 }
 

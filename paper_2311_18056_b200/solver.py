@@ -317,7 +317,10 @@ class BatchSolver:
         self._L.cqp_batch_last_timing(self._b, C.byref(comp), C.byref(tot), C.byref(launches))
         gms, gfl, rounds = C.c_double(), C.c_double(), C.c_int()
         self._L.cqp_batch_last_profile(self._b, C.byref(gms), C.byref(gfl), C.byref(rounds))
-        return {"y": y, "z": z, "lam": lam, "status": status, "iterations": iters,
+        ract = np.zeros(max(rounds.value, 1), dtype=np.int32); rms = np.zeros(max(rounds.value, 1))
+        self._L.cqp_batch_round_profile(self._b, rounds.value, ip(ract), _p(rms))
+        return {"round_active": ract, "round_ms": rms,
+                "y": y, "z": z, "lam": lam, "status": status, "iterations": iters,
                 "final_index": final, "n_switches": nsw, "r_prim": rp, "r_dual": rd,
                 "device_ms": ms.value, "compute_ms": comp.value, "launches": launches.value,
                 "gemm_ms": gms.value, "gemm_flops": gfl.value, "rounds": rounds.value}

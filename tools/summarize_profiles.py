@@ -1,0 +1,88 @@
+"""Turns the ncu outputs under gpurun_out/ into the committed summaries under profiles/.
+
+  gpurun_out/launches_batch.csv, launches_single.csv : `ncu --metrics gpu__time_duration.sum` launch lists
+  gpurun_out/prof_dmma.ncu-rep, prof_single.ncu-rep  : `ncu --set full` captures of the two hot kernels
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "profiles")
+SRC = os.path.join(ROOT, "gpurun_out")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+
+def launch_summary(name):
+    path = os.path.join(SRC, name)
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = None
+    for i, r in enumerate(rows):
+        if "Kernel Name" in r:
+            hdr, rows = r, rows[i + 1:]
+            break
+    ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    tot, cnt = collections.OrderedDict(), collections.Counter()
+    for r in rows:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
+        k = r[ki].split("(")[0].replace("void ", "")
+        tot[k] = tot.get(k, 0.0) + float(r[vi].replace(",", ""))
+        cnt[k] += 1
+    total = sum(tot.values())
+    return [{"kernel": k, "launches": cnt[k], "total_us": v / 1e3, "avg_us": v / 1e3 / cnt[k], "share": v / total}
+            for k, v in sorted(tot.items(), key=lambda kv: -kv[1])]
+
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg", "smsp__cycles_active.avg"]
+
+
+def full_summary(rep):
+    path = os.path.join(SRC, rep)
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        out.append({"kernel": d.get("Kernel Name"), **{k: f"{d[k]} {u[k]}".strip() for k in KEYS if k in d}})
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    summary = {}
+    for name in ("launches_batch.csv", "launches_single.csv"):
+        if os.path.exists(os.path.join(SRC, name)):
+            summary[name] = launch_summary(name)[:12]
+    for rep in ("prof_dmma.ncu-rep", "prof_single.ncu-rep"):
+        if os.path.exists(os.path.join(SRC, rep)):
+            summary[rep] = full_summary(rep)
+    json.dump(summary, open(os.path.join(OUT, f"{TAG}_ncu_summary.json"), "w"), indent=1)
+    # per-launch DRAM traffic of the dominant batched kernel, for bench.py's roofline.traffic
+    if "prof_dmma.ncu-rep" in summary and summary["prof_dmma.ncu-rep"]:
+        def to_bytes(s):
+            v, unit = s.split()[0].replace(",", ""), s.split()[1] if len(s.split()) > 1 else "byte"
+            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            return float(v) * mult
+        recs = summary["prof_dmma.ncu-rep"]
+        traffic = sum(to_bytes(r["dram__bytes_read.sum"]) + to_bytes(r["dram__bytes_write.sum"]) for r in recs) / len(recs)
+        json.dump({"dram_bytes_per_launch": traffic, "captures": len(recs), "source": f"{TAG}_ncu_summary.json"},
+                  open(os.path.join(OUT, "dmma_gemm_traffic.json"), "w"), indent=1)
+    print(json.dumps(summary, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main()
