@@ -174,8 +174,10 @@ CQP_API int cqp_dims(const cqp_handle *h, int *n, int *m, int *L);
  * after a watchdog trap: 1 = where, 2 = iteration, 3 = CTA, 4 = thread). */
 CQP_API int cqp_debug_words(const cqp_handle *h, int *out64);
 
-/* How the persistent kernel was configured: CTAs, rows of W per CTA, tier (0: W slice
- * resident in shared memory, 1: streamed from L2/HBM), dynamic shared memory bytes. */
+/* How the persistent kernel was configured: CTAs, rows of W per CTA, tier (0: all-SM grid, W
+ * slice resident in shared memory; 1: all-SM grid, W streamed from L2/HBM; 2: one thread-block
+ * cluster, W resident, iterate exchanged through distributed shared memory), dynamic shared
+ * memory bytes. */
 CQP_API int cqp_launch_info(const cqp_handle *h, int *ctas, int *rows_per_cta, int *tier,
                             int *smem_bytes);
 

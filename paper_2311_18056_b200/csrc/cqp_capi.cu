@@ -111,7 +111,8 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   h->d = h->c + m;
   if ((rc = dev_alloc(&h->vq, 4 * (size_t)h->Dpad))) return rc;
   if ((rc = dev_alloc(&h->state, 2))) return rc;
-  if ((rc = dev_alloc(&h->barrier, 1))) return rc;
+  if ((rc = dev_alloc(&h->barrier, 2))) return rc;
+  CQP_CUDA(cudaMemset(h->barrier, 0, 2 * sizeof(unsigned)));
   if ((rc = dev_alloc(&h->partial, 8 * (size_t)(h->num_sms + 1)))) return rc;
   if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
   if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
@@ -303,8 +304,8 @@ int cqp_refresh_z(cqp_handle* h) {
   return launch_run(h, false, 0, true);
 }
 
-static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out) {
-  const auto t0 = std::chrono::steady_clock::now();
+static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out,
+                         std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now()) {
   int rc = ensure_result_capacity(h, total / h->s.check_interval + 2);
   if (rc) return rc;
   CQP_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -377,9 +378,10 @@ int cqp_mpc_step(cqp_handle* h, const double* g, const double* c, const double* 
   if (!h || !g || !c || !d) { set_error("mpc_step: null argument"); return CQP_ERR_ARGUMENT; }
   if (k < 1) { set_error("mpc_step: k must be >= 1"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  const auto t0 = std::chrono::steady_clock::now();  // wall_ms of a fused step includes the upload
   int rc = upload_vectors(h, g, c, d);
   if (rc) return rc;
-  return run_and_fetch(h, false, k, true, out);
+  return run_and_fetch(h, false, k, true, out, t0);
 }
 
 int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
@@ -469,7 +471,7 @@ int cqp_launch_info(const cqp_handle* h, int* ctas, int* rows_per_cta, int* tier
   if (!h) return CQP_ERR_ARGUMENT;
   if (ctas) *ctas = h->G;
   if (rows_per_cta) *rows_per_cta = h->R;
-  if (tier) *tier = h->w_smem ? 0 : 1;
+  if (tier) *tier = h->cluster ? 2 : (h->w_smem ? 0 : 1);
   if (smem_bytes) *smem_bytes = h->smem_bytes;
   return CQP_OK;
 }

@@ -68,7 +68,9 @@ struct RunParams {
   const double* d;   // m unscaled
   double* vq;        // [4][Dpad] iterate ring; between launches slot 0 = iterate, 1..3 = sentinel
   int* state;        // [0] layer index
-  unsigned* barrier;  // grid barrier counter (zeroed before launch)
+  unsigned* barrier;       // grid barrier counter of this launch (zero on entry)
+  unsigned* barrier_next;  // counter of the next launch, zeroed by this one
+  int* dbg;                // host-mapped watchdog record
   double* partial;    // [G][8] per-CTA partial maxima
   double eps_prim, eps_dual, threshold;
   int check_interval, adaptive, early_exit, total_iters;
@@ -104,7 +106,8 @@ struct cqp_handle {
   double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
   double* vq = nullptr;  // [4][Dpad] iterate ring (see RunParams::vq)
   int* state = nullptr;
-  unsigned* barrier = nullptr;
+  unsigned* barrier = nullptr;  // [2] ping-pong grid-barrier counters
+  int launch_parity = 0;
   double* partial = nullptr;
   double* rho_vec = nullptr;  // [L][m]
   double* dtmp = nullptr;     // Dpad scratch (warm start staging)
@@ -120,6 +123,7 @@ struct cqp_handle {
   int* dbg_dev = nullptr;
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
+  int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)
 };
 
 namespace cqp {

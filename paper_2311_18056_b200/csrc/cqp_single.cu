@@ -48,11 +48,9 @@ __device__ __forceinline__ double nanmax(double best, double a) {
 
 // Watchdog: a spin that lasts longer than ~2 s records where it was stuck in host-mapped memory
 // and traps, so a protocol bug or a lost CTA becomes a CUDA error instead of a hung GPU.
-__device__ int* g_dbg = nullptr;  // set per launch (host-mapped, 16 ints)
 constexpr long long kSpinLimitCycles = 4000000000ll;
 
-__device__ __noinline__ void watchdog_fire(int where, int iter) {
-  int* d = g_dbg;
+__device__ __noinline__ void watchdog_fire(int* d, int where, int iter) {
   if (d && atomicCAS(d, 0, 1) == 0) {
     d[1] = where;
     d[2] = iter;
@@ -63,9 +61,8 @@ __device__ __noinline__ void watchdog_fire(int where, int iter) {
   __trap();
 }
 
-__device__ __forceinline__ void progress(int role, int value) {
+__device__ __forceinline__ void progress(int* d, int role, int value) {
 #ifdef CQP_DEBUG_PROGRESS
-  int* d = g_dbg;
   if (d && blockIdx.x < 12) {
     *((volatile int*)(d + 16 + blockIdx.x * 4 + role)) = value;
   }
@@ -94,7 +91,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, int where, int iter) {
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
   unsigned ok;
   long long t0 = 0;
   unsigned spins = 0;
@@ -106,7 +103,41 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, i
         : "memory");
     if (!ok && (++spins & 0xFF) == 0) {
       if (t0 == 0) t0 = clock64();
-      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(where, iter);
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
+    }
+  } while (!ok);
+}
+
+// ---- thread-block-cluster helpers (small problems: the whole W ladder slice set fits the shared
+// memory of one cluster, and the iterate is exchanged through distributed shared memory) ----
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned map_to_cta(unsigned local_smem_addr, unsigned cta_rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(cta_rank));
+  return r;
+}
+__device__ __forceinline__ void st_remote(unsigned cluster_addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cluster_addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
+  unsigned ok;
+  long long t0 = 0;
+  unsigned spins = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && (++spins & 0xFF) == 0) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
     }
   } while (!ok);
 }
@@ -123,7 +154,7 @@ __device__ __forceinline__ double2 load_pair(const double* p) {
 // Loader warps: fetch the whole iterate (nc2 column pairs) from ring slot `q` into shared memory
 // `xs`.  All loads of a batch are in flight together; only entries still holding the sentinel are
 // re-polled.  `lt` is the thread's index among the kLoaderThreads loader threads.
-__device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int nc2, int lt, int iter) {
+__device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int nc2, int lt, int* dbg, int iter) {
   constexpr int U = 8;
   double2* xs2 = reinterpret_cast<double2*>(xs);
   for (int base = lt; base < nc2; base += kLoaderThreads * U) {
@@ -143,7 +174,7 @@ __device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int n
           v[u] = load_pair(q + 2 * c2);
           if ((++spins & 0x3FF) == 0) {
             if (t0 == 0) t0 = clock64();
-            else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(100 + c2, iter);
+            else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 100 + c2, iter);
           }
         }
         xs2[c2] = v[u];
@@ -152,7 +183,7 @@ __device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int n
   }
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks) {
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks, int* dbg) {
   __syncthreads();
   epoch += nblocks;
   if (threadIdx.x == 0) {
@@ -163,7 +194,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch,
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
       if ((++spins & 0x3FF) == 0) {
         if (t0 == 0) t0 = clock64();
-        else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(5, (int)epoch);
+        else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 5, (int)epoch);
       }
     } while (seen < epoch);
   }
@@ -258,7 +289,7 @@ struct Smem {
   double* sb;    // Rp  bias rows
   double* slo;   // Rp
   double* shi;   // Rp
-  double* sval;  // 128 scratch
+  double* sval;  // 128 + Rp scratch (cluster mode stages the CTA's rows of v here)
   unsigned long long* bars;  // full[2], xready[2], go
 };
 
@@ -269,7 +300,7 @@ __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
   return (size_t)(w_smem ? (size_t)R * Dpad : 0) + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad +
-         kWarps * 16 + 2 * (size_t)kComputeWarps * Rcap + 3 * (size_t)Rp + 128 + 8;
+         kWarps * 16 + 2 * (size_t)kComputeWarps * Rcap + 4 * (size_t)Rp + 128 + 8;
 }
 
 template <int RB>
@@ -289,7 +320,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
-  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128);
+  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128 + Rp);
   return s;
 }
 
@@ -402,7 +433,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     for (int r = 0; r < RB; ++r) best = nanmax(best, s.sval[r * 7 + t]);
     __stcg(p.partial + (size_t)blockIdx.x * 8 + t, best);
   }
-  grid_barrier(p.barrier, epoch, G);
+  grid_barrier(p.barrier, epoch, G, p.dbg);
   // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
   // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant)
   {
@@ -447,7 +478,12 @@ __device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L,
   return best;
 }
 
-template <int RB>
+// CL = false: all-SM grid, iterate exchanged through the L2 ring (cooperative launch).
+// CL = true : ONE thread-block cluster of p.G CTAs; every CTA keeps a full copy of the iterate
+//             in shared memory and the publisher warp writes its rows straight into every peer's
+//             copy (st.shared::cluster) followed by a remote mbarrier arrive: no L2 round trip,
+//             no polling.  Used when the W slices of one ladder level fit the cluster's SMEM.
+template <int RB, bool CL>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
@@ -462,9 +498,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if (t == 0) {
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
-    mbar_init(&xready[0], kLoaderWarps);
-    mbar_init(&xready[1], kLoaderWarps);
+    mbar_init(&xready[0], CL ? p.G : kLoaderWarps);
+    mbar_init(&xready[1], CL ? p.G : kLoaderWarps);
     mbar_init(go, 1);
+  }
+  if (CL) {
+    __syncthreads();
+    cluster_sync_all();  // every peer's barriers exist before anyone arrives on them remotely
   }
   const int n = p.n, m = p.m, D = p.D;
   const int row0 = blockIdx.x * p.R;
@@ -474,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   unsigned epoch = 0;
 
   int layer = p.state[0];
+  if (blockIdx.x == 0 && t == 0) *p.barrier_next = 0u;  // counter of the NEXT launch (ping-pong)
 
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
   // (layers.cpp:182-186, 223-226)
@@ -502,13 +543,16 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       const double zs = block_rows_dot<RB>(p.Gs + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
       if (t < nv) __stcg(v + n + row + t, zs);
     }
-    grid_barrier(p.barrier, epoch, p.G);
+    grid_barrier(p.barrier, epoch, p.G, p.dbg);
   }
 
   load_layer<RB>(p, s, layer, row0, nrows);
 
   // v_0 -> xs[0] (slot 0 holds the iterate between launches; refresh_z above is complete)
-  for (int i = t; i < p.Dpad; i += kThreads) s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
+  for (int i = t; i < p.Dpad; i += kThreads) {
+    s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
+    s.xs[p.Dpad + i] = 0.0;
+  }
   __syncthreads();
 
   int n_trace = 1, n_hist = 0;
@@ -527,9 +571,12 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     const int par = ((i - 1) >> 1) & 1;  // phase parity of the k-th use of a [2]-split barrier
     double* part = s.spart + (size_t)b * kComputeWarps * Rcap;
     if (compute) {
-      if (lane == 0 && warp == 0) progress(0, i * 10 + 1);
-      if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, 1, i);
-      if (lane == 0 && warp == 0) progress(0, i * 10 + 2);  // v_{i-1} landed in xs[(i-1)&1]
+      if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 1);
+      if (i > 1) {
+        if (CL) mbar_wait_cluster(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
+        else mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
+      }
+      if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 2);  // v_{i-1} landed in xs[(i-1)&1]
       const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
       const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
       for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
@@ -544,11 +591,32 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
-      if (lane == 0 && warp == 0) progress(0, i * 10 + 3);
+      if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
     } else if (publisher) {
-      if (lane == 0) progress(1, i * 10 + 1);
-      mbar_wait(&full[b], par, 2, i);
-      if (lane == 0) progress(1, i * 10 + 2);
+      if (lane == 0) progress(p.dbg, 1, i * 10 + 1);
+      mbar_wait(&full[b], par, p.dbg, 2, i);
+      if (lane == 0) progress(p.dbg, 1, i * 10 + 2);
+      if (CL) {
+        // rows of v_i -> s.sval (local), then lane j delivers them to peer j's copy xs[b] and
+        // arrives on peer j's xready[b] (release at cluster scope orders the stores before it)
+        for (int r = lane; r < nrows; r += 32) {
+          double x = 0.0;
+#pragma unroll
+          for (int w = 0; w < kComputeWarps; ++w) x += part[w * Rcap + r];
+          x += s.sb[r];
+          const double lo = s.slo[r], hi = s.shi[r];
+          x = x < lo ? lo : x;
+          x = x > hi ? hi : x;
+          s.sval[r] = x;
+        }
+        __syncwarp();
+        if (lane < p.G) {
+          const unsigned xdst = map_to_cta(smem_u32(s.xs + (size_t)b * p.Dpad + row0), (unsigned)lane);
+          for (int r = 0; r < nrows; ++r) st_remote(xdst + 8u * (unsigned)r, s.sval[r]);
+          mbar_arrive_remote(map_to_cta(smem_u32(&xready[b]), (unsigned)lane));
+        }
+        __syncwarp();
+      } else {
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
       for (int r = lane; r < nrows; r += 32) {
@@ -574,15 +642,16 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       for (int r = lane; r < nrows; r += 32) publish(qclr + row0 + r, sentinel);
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
       if (p.fence_mode == 0) __threadfence();
-      if (lane == 0) progress(1, i * 10 + 3);
-    } else {
-      if (lt == 0) progress(2, i * 10 + 1);
-      mbar_wait(go, (i - 1) & 1, 3, i);
-      if (lt == 0) progress(2, i * 10 + 2);
-      fetch_iterate(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, i);
+      if (lane == 0) progress(p.dbg, 1, i * 10 + 3);
+      }
+    } else if (!CL) {
+      if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
+      mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
+      if (lt == 0) progress(p.dbg, 2, i * 10 + 2);
+      fetch_iterate(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, p.dbg, i);
       __syncwarp();
       if (lane == 0) mbar_arrive(&xready[b]);
-      if (lt == 0) progress(2, i * 10 + 3);
+      if (lt == 0) progress(p.dbg, 2, i * 10 + 3);
     }
     iters_done = i;
     if (i % p.check_interval != 0) continue;
@@ -631,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   }
 
   // ---- epilogue (solver.cpp:90-99) ----
-  if (t == 0) progress(3, iters_done * 10 + 9);
+  if (t == 0) progress(p.dbg, 3, iters_done * 10 + 9);
   double nr[7];
   const double* xfinal = s.xs + (size_t)(iters_done & 1) * p.Dpad;
   residual_pass<RB>(p, s, xfinal, true, epoch, nr);
@@ -668,6 +737,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       *p.head = h;
       p.state[0] = layer;
     }
+  }
+  if (CL) {
+    __syncthreads();
+    cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
   }
 }
 
@@ -737,18 +810,76 @@ __global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
 
 template <int RB>
 int launch_run_rb(cqp_handle* h, RunParams& p) {
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (h->cluster) {
+    auto fn = run_kernel<RB, true>;
+    CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    if (h->G > 8) CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)h->smem_bytes;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)h->G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CQP_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
+    return CQP_OK;
+  }
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->smem_bytes));
   void* args[] = {&p};
-  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB>, dim3(h->G), dim3(kThreads),
+  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, false>, dim3(h->G), dim3(kThreads),
                                        args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
+}
+
+// Can a single cluster of `C` CTAs hold one ladder level (and does the device schedule it)?
+template <int RB>
+bool cluster_fits(int C, int smem_bytes) {
+  auto fn = run_kernel<RB, true>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return false;
+  if (C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) { cudaGetLastError(); return false; }
+  return clusters >= 1;
 }
 
 }  // namespace
 
 int configure_launch(cqp_handle* h) {
   const int D = h->D;
+  h->cluster = 0;
+  // Small problems: one thread-block cluster (16 CTAs, else 8) keeps W_k in its shared memory and
+  // exchanges the iterate through DSMEM.  CQP_FORCE_GRID=1 (test hook) disables this mode.
+  const char* force_grid = std::getenv("CQP_FORCE_GRID");
+  const char* force_tier = std::getenv("CQP_FORCE_TIER");
+  if (D >= 64 && !(force_grid && force_grid[0] == '1') && !(force_tier && force_tier[0] == '1')) {
+    for (int C : {16, 8}) {
+      const int R = (D + C - 1) / C;
+      const int rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
+      const size_t need = smem_doubles(R, rb, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
+      if (need > (size_t)kMaxSmemBytes) continue;
+      const bool ok = rb == 4 ? cluster_fits<4>(C, (int)need) : (rb == 8 ? cluster_fits<8>(C, (int)need) : cluster_fits<16>(C, (int)need));
+      if (!ok) continue;
+      h->cluster = 1; h->R = R; h->G = C; h->rb = rb; h->w_smem = 1; h->smem_bytes = (int)need;
+      return CQP_OK;
+    }
+  }
   int G = h->num_sms;
   int R = (D + G - 1) / G;
   if (R < 1) R = 1;
@@ -758,9 +889,7 @@ int configure_launch(cqp_handle* h) {
   h->rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
   size_t need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
   h->w_smem = need <= (size_t)kMaxSmemBytes ? 1 : 0;
-  if (const char* force = std::getenv("CQP_FORCE_TIER")) {  // test hook: "1" streams W from L2/HBM
-    if (force[0] == '1') h->w_smem = 0;
-  }
+  if (force_tier && force_tier[0] == '1') h->w_smem = 0;  // test hook: stream W from L2/HBM
   if (!h->w_smem) need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
   if (need > (size_t)kMaxSmemBytes) {
     set_error("problem too large for the persistent kernel's shared-memory vectors");
@@ -779,7 +908,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.E = h->E; p.F = h->F; p.cost_scale = h->cost_scale;
   p.grid = h->dgrid; p.log_grid = h->dlog_grid;
   p.g = h->g; p.c = h->c; p.d = h->d;
-  p.vq = h->vq; p.state = h->state; p.barrier = h->barrier; p.partial = h->partial;
+  p.vq = h->vq; p.state = h->state; p.partial = h->partial;
   p.eps_prim = h->s.eps_prim; p.eps_dual = h->s.eps_dual; p.threshold = h->s.rho_switch_threshold;
   p.check_interval = h->s.check_interval; p.adaptive = h->s.adaptive_rho;
   p.early_exit = early_exit ? 1 : 0; p.total_iters = total_iters; p.do_refresh = do_refresh ? 1 : 0;
@@ -795,8 +924,14 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.out_lam = reinterpret_cast<double*>(base + off);
   p.fence_mode = 0;
   if (const char* fm = std::getenv("CQP_FENCE_MODE")) p.fence_mode = std::atoi(fm);  // experiment knob
-  CQP_CUDA(cudaMemsetAsync(h->barrier, 0, sizeof(unsigned), h->stream));
-  CQP_CUDA(cudaMemcpyToSymbolAsync(g_dbg, &h->dbg_dev, sizeof(int*), 0, cudaMemcpyHostToDevice, h->stream));
+  // grid-barrier counters ping-pong between launches: this launch counts on barrier[parity]
+  // (zeroed by the previous launch, or at allocation) and zeroes the other one.
+  p.barrier = h->barrier + (h->launch_parity & 1);
+  p.barrier_next = h->barrier + ((h->launch_parity + 1) & 1);
+  h->launch_parity ^= 1;
+  p.dbg = h->dbg_dev;
+  // few iterations: copying the W slice into shared memory costs as much as streaming it once
+  if (total_iters < 4 && !h->cluster) p.w_smem = 0;
   switch (h->rb) {
     case 4: return launch_run_rb<4>(h, p);
     case 8: return launch_run_rb<8>(h, p);

@@ -190,16 +190,21 @@ class Solver:
         _raise(self._L.cqp_update_vectors(self._h, _p(g), _p(c), _p(d)))
 
     def _result(self, cap: int):
-        y, z, lam = np.empty(self.n), np.empty(self.m), np.empty(self.m)
-        trace = (CqpRhoSwitch * cap)()
-        hist = (CqpResidualSample * cap)()
-        res = CqpResult(_p(y), _p(z), _p(lam), trace, cap, 0, hist, cap, 0, INVALID, 0, 0.0, 0.0,
-                        0.0, 0.0)
-        return res, (y, z, lam, trace, hist)
+        # result buffers are cached per capacity (the MPC step path calls this at kHz rates)
+        cache = self.__dict__.setdefault("_res_cache", {})
+        if cap not in cache:
+            y, z, lam = np.empty(self.n), np.empty(self.m), np.empty(self.m)
+            trace = (CqpRhoSwitch * cap)()
+            hist = (CqpResidualSample * cap)()
+            res = CqpResult(_p(y), _p(z), _p(lam), trace, cap, 0, hist, cap, 0, INVALID, 0, 0.0, 0.0,
+                            0.0, 0.0)
+            cache[cap] = (res, (y, z, lam, trace, hist))
+        return cache[cap]
 
     @staticmethod
     def _report(res: CqpResult, bufs) -> SolveReport:
         y, z, lam, trace, hist = bufs
+        y, z, lam = y.copy(), z.copy(), lam.copy()
         nt = min(res.rho_trace_len, res.rho_trace_cap)
         nh = min(res.history_len, res.history_cap)
         sol = Solution(y, z, lam, res.status, res.iterations, res.r_prim, res.r_dual,

@@ -339,19 +339,34 @@ def test_closed_loop_protocol_matches_oracle(G, oracle, P, k):
 
 
 # ---- tiers ---------------------------------------------------------------------------------------
-def test_streaming_tier_equals_resident_tier(G, oracle, P, monkeypatch):
+def test_all_kernel_modes_agree_bit_for_bit(G, oracle, P, monkeypatch):
+    """tier 0 (all-SM grid, W in shared memory), tier 1 (W streamed from L2/HBM) and tier 2 (one
+    thread-block cluster, DSMEM exchange) run the same arithmetic in the same order."""
     wl = P.config2(14, seed=2)
     base = wl.base_problem()
     q = wl.problem_at(wl.x0(10.0))
     reports = []
-    for tier in ("0", "1"):
-        monkeypatch.setenv("CQP_FORCE_TIER", tier)
+    for env, tier in (({"CQP_FORCE_GRID": "1", "CQP_FORCE_TIER": "0"}, 0),
+                      ({"CQP_FORCE_GRID": "1", "CQP_FORCE_TIER": "1"}, 1), ({}, 2)):
+        monkeypatch.delenv("CQP_FORCE_GRID", raising=False)
+        monkeypatch.delenv("CQP_FORCE_TIER", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         s, os_ = make_pair(oracle, G, base)
-        assert s.launch_info()["tier"] == int(tier)
+        assert s.launch_info()["tier"] == tier
         s.update_vectors(q.g, q.c, q.d); s.cold_start()
         reports.append(s.solve())
-    monkeypatch.delenv("CQP_FORCE_TIER")
-    a, b = reports
+        s.cold_start()
+        s.fixed_iters(3)                       # few iterations: the W slice is streamed, same bits
+        v3 = s.state
+        s.cold_start()
+        for _ in range(3):
+            s.fixed_iters(1)
+        assert np.array_equal(s.state, v3)
+    monkeypatch.delenv("CQP_FORCE_GRID", raising=False)
+    monkeypatch.delenv("CQP_FORCE_TIER", raising=False)
+    a, b, c = reports
     assert np.array_equal(a.solution.y, b.solution.y) and a.residual_history == b.residual_history
+    assert np.array_equal(a.solution.y, c.solution.y) and a.residual_history == c.residual_history
     os_.update_vectors(q.g, q.c, q.d); os_.cold_start()
     assert_report_parity(a, os_.solve())
