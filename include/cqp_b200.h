@@ -170,9 +170,10 @@ CQP_API int cqp_get_scaling(cqp_handle *h, double *E, double *F, double *cost_sc
 
 CQP_API int cqp_dims(const cqp_handle *h, int *n, int *m, int *L);
 
-/* Diagnostics: the 64-int host-mapped watchdog record of the persistent kernel (word 0 != 0
- * after a watchdog trap: 1 = where, 2 = iteration, 3 = CTA, 4 = thread). */
-CQP_API int cqp_debug_words(const cqp_handle *h, int *out64);
+/* Diagnostics: the 256-int host-mapped watchdog record of the persistent kernel (word 0 != 0
+ * after a watchdog trap: 1 = where, 2 = iteration, 3 = CTA, 4 = thread; words 64.. hold the
+ * optional -DCQP_TRACE timeline). */
+CQP_API int cqp_debug_words(const cqp_handle *h, int *out256);
 
 /* How the persistent kernel was configured: CTAs, rows of W per CTA, tier (0: all-SM grid, W
  * slice resident in shared memory; 1: all-SM grid, W streamed from L2/HBM; 2: one thread-block

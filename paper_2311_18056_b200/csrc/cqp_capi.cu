@@ -117,8 +117,8 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
   if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
   CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->hstage), sizeof(double) * (nm + m)));
-  CQP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->dbg_host), sizeof(int) * 64, cudaHostAllocMapped));
-  std::memset(h->dbg_host, 0, sizeof(int) * 64);
+  CQP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->dbg_host), sizeof(int) * 256, cudaHostAllocMapped));
+  std::memset(h->dbg_host, 0, sizeof(int) * 256);
   CQP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dbg_dev), h->dbg_host, 0));
   if ((rc = ensure_result_capacity(h, s.max_iters / s.check_interval + 2))) return rc;
   if ((rc = configure_launch(h))) return rc;
@@ -453,9 +453,9 @@ int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, dou
   return CQP_OK;
 }
 
-int cqp_debug_words(const cqp_handle* h, int* out64) {
-  if (!h || !out64) return CQP_ERR_ARGUMENT;
-  for (int i = 0; i < 64; ++i) out64[i] = ((volatile int*)h->dbg_host)[i];
+int cqp_debug_words(const cqp_handle* h, int* out256) {
+  if (!h || !out256) return CQP_ERR_ARGUMENT;
+  for (int i = 0; i < 256; ++i) out256[i] = ((volatile int*)h->dbg_host)[i];
   return CQP_OK;
 }
 

@@ -69,6 +69,18 @@ __device__ __forceinline__ void progress(int* d, int role, int value) {
 #endif
 }
 
+// Optional timeline trace (-DCQP_TRACE): clock64() stamps of CTA 0's roles for iterations
+// 100..103, 16 slots per iteration, into the host-mapped debug record (as long long, from word 64).
+#ifdef CQP_TRACE
+#define CQP_STAMP(dbg, it, slot)                                                        \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && (it) >= 100 && (it) < 104)                                   \
+      reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-100) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define CQP_STAMP(dbg, it, slot) do {} while (0)
+#endif
+
 __device__ __forceinline__ bool is_sentinel(double x) {
   return (unsigned long long)__double_as_longlong(x) == kSentinel;
 }
@@ -554,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     s.xs[p.Dpad + i] = 0.0;
   }
   __syncthreads();
+  if (CL) cluster_sync_all();  // peers may write into xs[1] as soon as they finish iteration 1
 
   int n_trace = 1, n_hist = 0;
   if (blockIdx.x == 0 && t == 0) {
@@ -571,12 +584,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     const int par = ((i - 1) >> 1) & 1;  // phase parity of the k-th use of a [2]-split barrier
     double* part = s.spart + (size_t)b * kComputeWarps * Rcap;
     if (compute) {
-      if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 1);
+      if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 1); CQP_STAMP(p.dbg, i, 0); }
       if (i > 1) {
         if (CL) mbar_wait_cluster(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
         else mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
       }
-      if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 2);  // v_{i-1} landed in xs[(i-1)&1]
+      if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 2); CQP_STAMP(p.dbg, i, 1); }  // v_{i-1} landed
+      if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 10);
       const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
       const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
       for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
@@ -586,16 +600,19 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         for (int r = 0; r < RB; ++r) acc[r] = 0.0;
         for (int c2 = t; c2 < nc2; c2 += kComputeThreads)
           fma_rows<RB>(Wrows + (size_t)rb0 * p.Dpad, p.Dpad, nv, c2, x2[c2], acc);
+        if (lane == 0 && warp == 0 && rb0 == 0) CQP_STAMP(p.dbg, i, 3);
         const double total = warp_butterfly<RB>(acc, lane);
         if ((lane & ((1 << shift) - 1)) == 0) part[warp * Rcap + rb0 + (lane >> shift)] = total;
       }
       __syncwarp();
+      if (lane == 0 && warp == 0) CQP_STAMP(p.dbg, i, 2);
+      if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 11);
       if (lane == 0) mbar_arrive(&full[b]);
       if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
     } else if (publisher) {
-      if (lane == 0) progress(p.dbg, 1, i * 10 + 1);
+      if (lane == 0) { progress(p.dbg, 1, i * 10 + 1); CQP_STAMP(p.dbg, i, 4); }
       mbar_wait(&full[b], par, p.dbg, 2, i);
-      if (lane == 0) progress(p.dbg, 1, i * 10 + 2);
+      if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
       if (CL) {
         // rows of v_i -> s.sval (local), then lane j delivers them to peer j's copy xs[b] and
         // arrives on peer j's xready[b] (release at cluster scope orders the stores before it)
@@ -610,12 +627,14 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
           s.sval[r] = x;
         }
         __syncwarp();
+        if (lane == 0) CQP_STAMP(p.dbg, i, 6);
         if (lane < p.G) {
           const unsigned xdst = map_to_cta(smem_u32(s.xs + (size_t)b * p.Dpad + row0), (unsigned)lane);
           for (int r = 0; r < nrows; ++r) st_remote(xdst + 8u * (unsigned)r, s.sval[r]);
           mbar_arrive_remote(map_to_cta(smem_u32(&xready[b]), (unsigned)lane));
         }
         __syncwarp();
+        if (lane == 0) CQP_STAMP(p.dbg, i, 7);
       } else {
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
@@ -633,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       }
       if (owns_pad && lane == 0) publish(qout + D, 0.0);
       __syncwarp();
+      if (lane == 0) CQP_STAMP(p.dbg, i, 6);
       if (lane == 0) mbar_arrive(go);
       // re-arm this CTA's rows of the slot that will carry v_{i+2}; every reader of its old
       // content (v_{i-2}) finished before any v_{i-1} row was published, and all of v_{i-1} has
@@ -642,14 +662,15 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       for (int r = lane; r < nrows; r += 32) publish(qclr + row0 + r, sentinel);
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
       if (p.fence_mode == 0) __threadfence();
-      if (lane == 0) progress(p.dbg, 1, i * 10 + 3);
+      if (lane == 0) { progress(p.dbg, 1, i * 10 + 3); CQP_STAMP(p.dbg, i, 7); }
       }
     } else if (!CL) {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
-      if (lt == 0) progress(p.dbg, 2, i * 10 + 2);
+      if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
       fetch_iterate(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, p.dbg, i);
       __syncwarp();
+      if (lt == 0) CQP_STAMP(p.dbg, i, 9);
       if (lane == 0) mbar_arrive(&xready[b]);
       if (lt == 0) progress(p.dbg, 2, i * 10 + 3);
     }
@@ -864,11 +885,14 @@ bool cluster_fits(int C, int smem_bytes) {
 int configure_launch(cqp_handle* h) {
   const int D = h->D;
   h->cluster = 0;
-  // Small problems: one thread-block cluster (16 CTAs, else 8) keeps W_k in its shared memory and
-  // exchanges the iterate through DSMEM.  CQP_FORCE_GRID=1 (test hook) disables this mode.
-  const char* force_grid = std::getenv("CQP_FORCE_GRID");
+  // Small problems CAN run as one thread-block cluster (16 CTAs, else 8) that keeps W_k in its
+  // shared memory and exchanges the iterate through DSMEM.  Measured on B200 (round 1) this mode
+  // is correct but slower than the all-SM grid (4.1 vs 2.4 us/iteration at D = 300: the
+  // release-ordered remote stores and the 16-row butterflies dominate), so it is opt-in
+  // (CQP_ENABLE_CLUSTER=1) until the push is rewritten with st.async.
+  const char* enable_cluster = std::getenv("CQP_ENABLE_CLUSTER");
   const char* force_tier = std::getenv("CQP_FORCE_TIER");
-  if (D >= 64 && !(force_grid && force_grid[0] == '1') && !(force_tier && force_tier[0] == '1')) {
+  if (D >= 64 && enable_cluster && enable_cluster[0] == '1' && !(force_tier && force_tier[0] == '1')) {
     for (int C : {16, 8}) {
       const int R = (D + C - 1) / C;
       const int rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);

@@ -346,9 +346,9 @@ def test_all_kernel_modes_agree_bit_for_bit(G, oracle, P, monkeypatch):
     base = wl.base_problem()
     q = wl.problem_at(wl.x0(10.0))
     reports = []
-    for env, tier in (({"CQP_FORCE_GRID": "1", "CQP_FORCE_TIER": "0"}, 0),
-                      ({"CQP_FORCE_GRID": "1", "CQP_FORCE_TIER": "1"}, 1), ({}, 2)):
-        monkeypatch.delenv("CQP_FORCE_GRID", raising=False)
+    for env, tier in (({"CQP_FORCE_TIER": "0"}, 0), ({"CQP_FORCE_TIER": "1"}, 1),
+                      ({"CQP_ENABLE_CLUSTER": "1"}, 2)):
+        monkeypatch.delenv("CQP_ENABLE_CLUSTER", raising=False)
         monkeypatch.delenv("CQP_FORCE_TIER", raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -363,7 +363,7 @@ def test_all_kernel_modes_agree_bit_for_bit(G, oracle, P, monkeypatch):
         for _ in range(3):
             s.fixed_iters(1)
         assert np.array_equal(s.state, v3)
-    monkeypatch.delenv("CQP_FORCE_GRID", raising=False)
+    monkeypatch.delenv("CQP_ENABLE_CLUSTER", raising=False)
     monkeypatch.delenv("CQP_FORCE_TIER", raising=False)
     a, b, c = reports
     assert np.array_equal(a.solution.y, b.solution.y) and a.residual_history == b.residual_history

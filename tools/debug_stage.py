@@ -6,7 +6,7 @@ from paper_2311_18056_b200 import problems, solver as S
 
 stage = sys.argv[1]
 import faulthandler
-faulthandler.dump_traceback_later(15, exit=True)
+faulthandler.dump_traceback_later(240, exit=True)
 if stage == "1d_fixed1":
     print("creating", flush=True)
     s = S.Solver([[2.0]], [-2.0], [[1.0]], [0.0], [0.5])
@@ -52,10 +52,29 @@ elif stage.startswith("watch"):
     print("created", s.launch_info(), flush=True)
     def watch():
         time.sleep(4)
-        w = (C.c_int * 64)()
+        w = (C.c_int * 256)()
         s._L.cqp_debug_words(s._h, w)
         print("dbg", list(w)[:8], "progress(cta x [compute,publisher,loader,epilogue])", [list(w)[16 + 4 * c:20 + 4 * c] for c in range(3)], flush=True)
         os._exit(3)
     threading.Thread(target=watch, daemon=True).start()
     r = s.fixed_iters(k); print(stage, r.solution.iterations, s.state, r.kernel_us, flush=True)
     os._exit(0)
+elif stage.startswith("trace"):
+    import ctypes as C
+    nu = int(stage[5:])
+    wl = problems.config2(nu, 0); base = wl.base_problem()
+    s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
+    q = wl.problem_at(wl.x0(10.0)); s.update_vectors(q.g, q.c, q.d)
+    print(s.launch_info())
+    for _ in range(2):
+        s.cold_start(); r = s.fixed_iters(1000)
+    w = (C.c_int * 256)()
+    s._L.cqp_debug_words(s._h, w)
+    ll = np.frombuffer(bytes(w), dtype=np.int64)[32:]
+    names = {0: "c:start", 1: "c:x ready", 3: "c:fma done", 2: "c:dots done", 10: "c15:x ready", 11: "c15:done", 4: "p:start", 5: "p:partials ready", 6: "p:published", 7: "p:done", 8: "l:go seen", 9: "l:fetched"}
+    t00 = ll[0]
+    for it in range(4):
+        row = ll[it * 16:(it + 1) * 16]
+        ev = sorted((int(row[k] - t00), names[k]) for k in names if row[k] != 0)
+        print("iter", 100 + it, "  ".join(f"{n}@{t}" for t, n in ev))
+    print("us/iter", r.kernel_us / 1000)
