@@ -540,6 +540,62 @@ int repad(cqp_batch* b, const double* src, int rows, int cols, int ld_src, size_
 
 }  // namespace
 
+namespace cqp {
+
+// Dense C = alpha * A * B on the DMMA kernel for the offline stage (cqp_setup.cu):
+//   A: [M_pad128][lda] row-major (K contiguous, zero padded, lda % 16 == 0)
+//   B: N columns of [ldb] (K contiguous, zero padded), C: N columns of [ldc].
+struct DenseGemm {
+  int* cols = nullptr;
+  TileDesc* tiles = nullptr;
+  int* n_tiles = nullptr;
+  int N = 0;
+  int grid = 0;
+};
+
+int dense_gemm_create(DenseGemm** out, int N, int num_sms) {
+  DenseGemm* g = new DenseGemm();
+  *out = g;
+  g->N = N;
+  const int slots = (N + SLOT_TILE - 1) / SLOT_TILE * SLOT_TILE, tiles = slots / SLOT_TILE;
+  std::vector<int> cols(slots, -1);
+  for (int i = 0; i < N; ++i) cols[i] = i;
+  std::vector<TileDesc> td(tiles);
+  for (int t = 0; t < tiles; ++t) td[t] = {t * SLOT_TILE, 0};
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->cols), sizeof(int) * slots));
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->tiles), sizeof(TileDesc) * tiles));
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->n_tiles), sizeof(int)));
+  CQP_CUDA(cudaMemcpy(g->cols, cols.data(), sizeof(int) * slots, cudaMemcpyHostToDevice));
+  CQP_CUDA(cudaMemcpy(g->tiles, td.data(), sizeof(TileDesc) * tiles, cudaMemcpyHostToDevice));
+  CQP_CUDA(cudaMemcpy(g->n_tiles, &tiles, sizeof(int), cudaMemcpyHostToDevice));
+  const GemmConfig& gc = kConfigs[1];
+  CQP_CUDA(cudaFuncSetAttribute(gc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gc.smem));
+  int occ = 0;
+  CQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gc.fn, gc.threads, gc.smem));
+  g->grid = (occ < 1 ? 1 : occ) * num_sms;
+  return CQP_OK;
+}
+
+void dense_gemm_destroy(DenseGemm* g) {
+  if (!g) return;
+  cudaFree(g->cols); cudaFree(g->tiles); cudaFree(g->n_tiles);
+  delete g;
+}
+
+int dense_gemm_run(const DenseGemm* g, cudaStream_t st, const double* A, int lda, int M, int M_pad,
+                   const double* B, int ldb, double* C, int ldc, double alpha) {
+  GemmParams p{};
+  p.A = A; p.a_stride = 0; p.lda = lda; p.M = M; p.M_pad = M_pad; p.k_tiles = lda / BK;
+  p.Bm = B; p.ldb = ldb; p.cols = g->cols; p.tiles = g->tiles; p.n_tiles = g->n_tiles;
+  p.C = C; p.ldc = ldc; p.alpha = alpha; p.mode = 0;
+  const GemmConfig& gc = kConfigs[1];  // 64 x 64 tiles
+  gc.fn<<<g->grid, gc.threads, gc.smem, st>>>(p);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
+}
+
+}  // namespace cqp
+
 extern "C" {
 
 int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {

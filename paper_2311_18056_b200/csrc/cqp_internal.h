@@ -135,13 +135,16 @@ int launch_refresh_z(cqp_handle* h);
 int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index);
 int launch_set_state(cqp_handle* h, int layer);
 int launch_transpose_pad(cudaStream_t st, const double* src_colmajor, int rows, int cols,
-                         double* dst_rowmajor, int ld);
+                         double* dst_rowmajor, int ld, int src_ld = 0);
 int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, int cols, int ld,
                        double* dst_colmajor);
 int launch_bias(cqp_handle* h, int k, double* b_out);  // b_out: device, D doubles
 
-// cqp_setup.cu : offline stage on the device (layers.cpp:189-228)
-int device_precompute(cqp_handle* h, const double* H, const double* g, const double* G,
-                      const double* c, const double* d);
+// cqp_batch.cu : dense DMMA GEMM with an identity slot map, used by the offline stage
+struct DenseGemm;
+int dense_gemm_create(DenseGemm** out, int N, int num_sms);
+void dense_gemm_destroy(DenseGemm* g);
+int dense_gemm_run(const DenseGemm* g, cudaStream_t st, const double* A, int lda, int M, int M_pad,
+                   const double* B, int ldb, double* C, int ldc, double alpha);
 
 }  // namespace cqp

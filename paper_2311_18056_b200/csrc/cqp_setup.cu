@@ -2,14 +2,21 @@
 // (/root/reference/proj/src/solver.cpp:180-186, src/problem.cpp:121-164,
 //  src/layers.cpp:22-36 grid, :82-120 Ruiz, :122-131 D, :133-166 W, :189-228 precompute_all).
 //
-// This is setup work, off the hot path: the O(L n^3) dense algebra goes through cuSOLVER
-// (potrf/potri) and cuBLAS (dgemm); the Ruiz equilibration (O(passes * n(n+m)) elementwise
-// work on H and G) runs on the host exactly in the reference's operation order so that E, F
-// and cost_scale are bit-identical to a host implementation.  The result is the same device
-// layout cqp_create_from_layers produces: W_k row-major padded, [D_k; G D_k] row-major padded.
-#include <cublas_v2.h>
-#include <cusolverDn.h>
-
+// Setup work, off the hot path, but still hand-written CUDA with no library dependency (an
+// earlier cuSOLVER/cuBLAS version pulled 1.7 GB of shared objects into every process, minutes
+// of cold-load time on a fresh box):
+//   * D = (H + sigma I + G' rho G)^-1 by a right-looking Cholesky (one scale + one rank-1
+//     update kernel per column) followed by forward and backward substitution on the identity
+//     (layers.cpp:126-130 does LLT + solve(I)); a non-positive pivot is reported like
+//     Eigen::LLT's NumericalIssue (-> ProblemError::NonPositiveDefiniteH / std::runtime_error);
+//   * the five dense products of build_layer (layers.cpp:140-155) on the FP64 tensor-core GEMM
+//     of cqp_batch.cu;
+//   * the Ruiz equilibration (O(passes * n(n+m)) elementwise work on H and G) on the host,
+//     exactly in the reference's operation order, so E, F and cost_scale are bit-identical to a
+//     host implementation.
+// The result is the same device layout cqp_create_from_layers produces: W_k row-major padded,
+// [D_k; G D_k] row-major padded.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -25,58 +32,119 @@ int cold_start(cqp_handle* h);
 
 namespace {
 
-#define CQP_BLAS(call)                                                    \
-  do {                                                                    \
-    cublasStatus_t st__ = (call);                                         \
-    if (st__ != CUBLAS_STATUS_SUCCESS) {                                  \
-      set_error(std::string("cuBLAS error ") + std::to_string((int)st__) + " in " #call); \
-      return cleanup(CQP_ERR_CUDA);                                              \
-    }                                                                     \
-  } while (0)
-#define CQP_SOLVER(call)                                                  \
-  do {                                                                    \
-    cusolverStatus_t st__ = (call);                                       \
-    if (st__ != CUSOLVER_STATUS_SUCCESS) {                                \
-      set_error(std::string("cuSOLVER error ") + std::to_string((int)st__) + " in " #call); \
-      return cleanup(CQP_ERR_CUDA);                                              \
-    }                                                                     \
-  } while (0)
+// All offline-stage matrices are column-major with a padded leading dimension (multiple of 16)
+// so that they can feed the DMMA GEMM directly (K contiguous, zero padded).
 
-// rG = diag(rho) G   (m x n column-major)
+// rG = diag(rho) G   (m x n, leading dimension ld)
 __global__ void scale_rows_kernel(const double* __restrict__ G, const double* __restrict__ rho,
-                                  int m, int n, double* __restrict__ out) {
+                                  int m, int n, int ld, double* __restrict__ out) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < (size_t)m * n) out[idx] = rho[idx % m] * G[idx];
+  if (idx >= (size_t)m * n) return;
+  const int i = (int)(idx % m), j = (int)(idx / m);
+  out[i + (size_t)j * ld] = rho[i] * G[i + (size_t)j * ld];
 }
 
-// kkt = H + sigma I + M ;  T = sigma I - M   (n x n column-major)
+// kkt = H + sigma I + M ;  T = sigma I - M   (n x n, leading dimension ld)
 __global__ void kkt_and_t_kernel(const double* __restrict__ H, const double* __restrict__ M,
-                                 double sigma, int n, double* __restrict__ kkt,
+                                 double sigma, int n, int ld, double* __restrict__ kkt,
                                  double* __restrict__ T) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n * n) return;
   const int i = (int)(idx % n), j = (int)(idx / n);
+  const size_t at = i + (size_t)j * ld;
   const double s = (i == j) ? sigma : 0.0;
-  kkt[idx] = (H[idx] + s) + M[idx];
-  T[idx] = s - M[idx];
+  kkt[at] = (H[at] + s) + M[at];
+  T[at] = s - M[at];
 }
 
-// potri leaves the inverse in the lower triangle: mirror it.
-__global__ void mirror_lower_kernel(double* __restrict__ A, int n) {
+// ---- Cholesky + inverse (LLT, then solve(I)) -------------------------------------------------
+// Column j of the factor: l_jj = sqrt(a_jj), a_ij /= l_jj.  A non-positive pivot is recorded
+// (first one wins) and replaced by 1 so that the remaining kernels stay finite.
+__global__ void chol_scale_kernel(double* __restrict__ A, int ld, int n, int j, int* fail) {
+  __shared__ double l;
+  if (threadIdx.x == 0) {
+    double a = A[j + (size_t)j * ld];
+    if (!(a > 0.0)) {
+      atomicCAS(fail, 0, j + 1);
+      a = 1.0;
+    }
+    l = sqrt(a);
+    A[j + (size_t)j * ld] = l;
+  }
+  __syncthreads();
+  for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + (size_t)j * ld] /= l;
+}
+
+// Trailing update of the lower triangle: a_ic -= l_ij l_cj for i >= c > j.
+__global__ void chol_update_kernel(double* __restrict__ A, int ld, int n, int j) {
+  if (blockIdx.y > blockIdx.x) return;  // tile strictly above the diagonal
+  const int i = j + 1 + blockIdx.x * 32 + threadIdx.x;
+  const int c0 = j + 1 + blockIdx.y * 32;
+  if (i >= n) return;
+  const double li = A[i + (size_t)j * ld];
+  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
+    const int c = c0 + cc;
+    if (c < n && c <= i) A[i + (size_t)c * ld] -= li * A[c + (size_t)j * ld];
+  }
+}
+
+// row k of Y /= l_kk   (columns [0, ncols))
+__global__ void tri_scale_row_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
+                                     int k, int ncols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncols) Y[k + (size_t)c * ld] /= L[k + (size_t)k * ld];
+}
+
+// forward substitution step k (L Y = I): y_ic -= l_ik y_kc for i > k, c <= k
+__global__ void fwd_update_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
+                                  int n, int k) {
+  const int i = k + 1 + blockIdx.x * 32 + threadIdx.x;
+  const int c0 = blockIdx.y * 32;
+  if (i >= n) return;
+  const double lik = L[i + (size_t)k * ld];
+  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
+    const int c = c0 + cc;
+    if (c <= k) Y[i + (size_t)c * ld] -= lik * Y[k + (size_t)c * ld];
+  }
+}
+
+// backward substitution step k (L' X = Y, in place): y_ic -= l_ki x_kc for i < k, all c
+__global__ void bwd_update_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
+                                  int n, int k) {
+  const int i = blockIdx.x * 32 + threadIdx.x;
+  const int c0 = blockIdx.y * 32;
+  if (i >= k) return;
+  const double lki = L[k + (size_t)i * ld];
+  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
+    const int c = c0 + cc;
+    if (c < n) Y[i + (size_t)c * ld] -= lki * Y[k + (size_t)c * ld];
+  }
+}
+
+__global__ void set_identity_kernel(double* __restrict__ Y, int ld, int n) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n * n) return;
   const int i = (int)(idx % n), j = (int)(idx / n);
-  if (i < j) A[idx] = A[(size_t)j + (size_t)i * n];
+  Y[i + (size_t)j * ld] = (i == j) ? 1.0 : 0.0;
+}
+
+// make the computed inverse exactly symmetric (upper <- lower)
+__global__ void mirror_lower_kernel(double* __restrict__ A, int ld, int n) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n * n) return;
+  const int i = (int)(idx % n), j = (int)(idx / n);
+  if (i < j) A[i + (size_t)j * ld] = A[j + (size_t)i * ld];
 }
 
 // Assemble W (row-major, ld = Dpad, pad zero) from its blocks (layers.cpp:149-162):
-//   [ DT          2 DGt r         -DGt        ]      DT  = D T        (n x n, col-major)
-//   [ GDT + G     2 GDGt r - I    -GDGt + 1/r ]      GD  = G D        (m x n)  DGt = GD'
-//   [ r G         -r              I           ]      GDT = GD T (m x n), GDGt (m x m)
-__global__ void assemble_w_kernel(int n, int m, int Dpad, const double* __restrict__ DT,
-                                  const double* __restrict__ GD, const double* __restrict__ GDT,
-                                  const double* __restrict__ GDGt, const double* __restrict__ Gs,
-                                  const double* __restrict__ rho, double* __restrict__ W) {
+//   [ DT          2 DGt r         -DGt        ]      DT  = D T        (n x n, ld_n)
+//   [ GDT + G     2 GDGt r - I    -GDGt + 1/r ]      GD  = G D        (m x n, ld_m)  DGt = GD'
+//   [ r G         -r              I           ]      GDT = GD T (m x n, ld_m), GDGt (m x m, ld_m)
+__global__ void assemble_w_kernel(int n, int m, int Dpad, int ld_n, int ld_m,
+                                  const double* __restrict__ DT, const double* __restrict__ GD,
+                                  const double* __restrict__ GDT, const double* __restrict__ GDGt,
+                                  const double* __restrict__ Gs, const double* __restrict__ rho,
+                                  double* __restrict__ W) {
   const int D = n + 2 * m;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)D * Dpad) return;
@@ -84,22 +152,22 @@ __global__ void assemble_w_kernel(int n, int m, int Dpad, const double* __restri
   double v = 0.0;
   if (c < D) {
     if (r < n) {
-      if (c < n) v = DT[r + (size_t)c * n];
-      else if (c < n + m) v = (2.0 * GD[(c - n) + (size_t)r * m]) * rho[c - n];
-      else v = -GD[(c - n - m) + (size_t)r * m];
+      if (c < n) v = DT[r + (size_t)c * ld_n];
+      else if (c < n + m) v = (2.0 * GD[(c - n) + (size_t)r * ld_m]) * rho[c - n];
+      else v = -GD[(c - n - m) + (size_t)r * ld_m];
     } else if (r < n + m) {
       const int i = r - n;
-      if (c < n) v = GDT[i + (size_t)c * m] + Gs[i + (size_t)c * m];
+      if (c < n) v = GDT[i + (size_t)c * ld_m] + Gs[i + (size_t)c * ld_m];
       else if (c < n + m) {
         const int j = c - n;
-        v = (2.0 * GDGt[i + (size_t)j * m]) * rho[j] - (i == j ? 1.0 : 0.0);
+        v = (2.0 * GDGt[i + (size_t)j * ld_m]) * rho[j] - (i == j ? 1.0 : 0.0);
       } else {
         const int j = c - n - m;
-        v = -GDGt[i + (size_t)j * m] + (i == j ? 1.0 / rho[j] : 0.0);
+        v = -GDGt[i + (size_t)j * ld_m] + (i == j ? 1.0 / rho[j] : 0.0);
       }
     } else {
       const int i = r - n - m;
-      if (c < n) v = rho[i] * Gs[i + (size_t)c * m];
+      if (c < n) v = rho[i] * Gs[i + (size_t)c * ld_m];
       else if (c < n + m) v = (c - n == i) ? -rho[i] : 0.0;
       else v = (c - n - m == i) ? 1.0 : 0.0;
     }
@@ -212,51 +280,62 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   if (device < 0) CQP_CUDA(cudaGetDevice(&device));
   CQP_CUDA(cudaSetDevice(device));
 
-  cublasHandle_t blas = nullptr;
-  cusolverDnHandle_t solver = nullptr;
   cqp_handle* h = nullptr;
-  std::vector<double*> temps;
+  DenseGemm* gemm_n = nullptr;  // N = n output columns
+  DenseGemm* gemm_m = nullptr;  // N = m output columns
+  cudaStream_t st0 = nullptr;
+  std::vector<void*> temps;
   auto cleanup = [&](int code) {
-    for (double* p : temps) cudaFree(p);
-    if (blas) cublasDestroy(blas);
-    if (solver) cusolverDnDestroy(solver);
+    for (void* p : temps) cudaFree(p);
+    dense_gemm_destroy(gemm_n);
+    dense_gemm_destroy(gemm_m);
+    if (st0) cudaStreamDestroy(st0);
     if (code != CQP_OK) { cqp_destroy(h); h = nullptr; }
     return code;
   };
   auto talloc = [&](double** p, size_t cnt) -> int {
     if (cudaMalloc(reinterpret_cast<void**>(p), sizeof(double) * (cnt ? cnt : 1)) != cudaSuccess) return (int)CQP_ERR_CUDA;
+    if (cudaMemset(*p, 0, sizeof(double) * (cnt ? cnt : 1)) != cudaSuccess) return (int)CQP_ERR_CUDA;
     temps.push_back(*p);
     return (int)CQP_OK;
   };
 #define TRY(expr) do { int rc__ = (expr); if (rc__) return cleanup(rc__); } while (0)
 #define TRYCUDA(expr) do { cudaError_t e__ = (expr); if (e__ != cudaSuccess) return cleanup(cuda_fail(e__, #expr)); } while (0)
 
-  if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS || cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS) {
-    set_error("cuBLAS/cuSOLVER initialisation failed");
-    return cleanup(CQP_ERR_CUDA);
-  }
+  const int ld_n = (n + 15) / 16 * 16, ld_m = (m + 15) / 16 * 16;      // K-padded leading dimensions
+  const int n128 = (n + 127) / 128 * 128, m128 = (m + 127) / 128 * 128;  // row-padded A operands
+  int* dfail = nullptr;
+  TRYCUDA(cudaMalloc(reinterpret_cast<void**>(&dfail), sizeof(int)));
+  temps.push_back(dfail);
+  TRYCUDA(cudaStreamCreateWithFlags(&st0, cudaStreamNonBlocking));
+
+  // In-place lower Cholesky of the n x n matrix A (leading dimension ld_n); fail flag on device.
+  auto cholesky = [&](double* A, cudaStream_t st) -> int {
+    CQP_CUDA(cudaMemsetAsync(dfail, 0, sizeof(int), st));
+    for (int j = 0; j < n; ++j) {
+      chol_scale_kernel<<<1, 256, 0, st>>>(A, ld_n, n, j, dfail);
+      const int rem = n - j - 1;
+      if (rem > 0) {
+        const int tiles = (rem + 31) / 32;
+        chol_update_kernel<<<dim3(tiles, tiles), dim3(32, 8), 0, st>>>(A, ld_n, n, j);
+      }
+    }
+    CQP_CUDA(cudaGetLastError());
+    return CQP_OK;
+  };
+  auto read_fail = [&](cudaStream_t st, int* out_flag) -> int {
+    CQP_CUDA(cudaMemcpyAsync(out_flag, dfail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CQP_CUDA(cudaStreamSynchronize(st));
+    return CQP_OK;
+  };
 
   // ---- PD check of H: LLT (problem.cpp:146-149) ----
-  double *dH = nullptr, *dwork = nullptr;
-  int* dinfo = nullptr;
-  TRY(talloc(&dH, (size_t)n * n));
-  TRYCUDA(cudaMalloc(reinterpret_cast<void**>(&dinfo), sizeof(int)));
-  temps.push_back(reinterpret_cast<double*>(dinfo));
-  int lwork_f = 0, lwork_i = 0;
-  if (cusolverDnDpotrf_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, n, dH, n, &lwork_f) != CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDpotri_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, n, dH, n, &lwork_i) != CUSOLVER_STATUS_SUCCESS) {
-    set_error("cuSOLVER workspace query failed");
-    return cleanup(CQP_ERR_CUDA);
-  }
-  const int lwork = std::max(lwork_f, lwork_i);
-  TRY(talloc(&dwork, (size_t)lwork));
-  TRYCUDA(cudaMemcpy(dH, H, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+  double* dH = nullptr;
+  TRY(talloc(&dH, (size_t)n * ld_n));
+  TRYCUDA(cudaMemcpy2D(dH, sizeof(double) * ld_n, H, sizeof(double) * n, sizeof(double) * n, n, cudaMemcpyHostToDevice));
+  TRY(cholesky(dH, st0));
   int info = 0;
-  if (cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, n, dH, n, dwork, lwork, dinfo) != CUSOLVER_STATUS_SUCCESS) {
-    set_error("cusolverDnDpotrf failed");
-    return cleanup(CQP_ERR_CUDA);
-  }
-  TRYCUDA(cudaMemcpy(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+  TRY(read_fail(st0, &info));
   if (info != 0) { set_error("H is not positive-definite"); return cleanup(CQP_ERR_NOT_PD_H); }
 
   // ---- bounds (problem.cpp:151-162) ----
@@ -293,78 +372,99 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   TRY(handle_alloc(&h, n, m, L, s, device));
   h->initial_index = initial_index;
   h->cost_scale = cost_scale;
-  CQP_BLAS(cublasSetStream(blas, h->stream));
-  CQP_SOLVER(cusolverDnSetStream(solver, h->stream));
+  cudaStream_t st = h->stream;
+  TRY(dense_gemm_create(&gemm_n, n, h->num_sms));
+  TRY(dense_gemm_create(&gemm_m, m, h->num_sms));
 
   const int D = h->D;
   const size_t nm = (size_t)n + m;
-  double *dHs, *dGs, *dRho, *drG, *dM, *dKkt, *dT, *dGD, *dGDGt, *dDT, *dGDT, *dscr;
-  TRY(talloc(&dHs, (size_t)n * n)); TRY(talloc(&dGs, (size_t)m * n)); TRY(talloc(&dRho, (size_t)m));
-  TRY(talloc(&drG, (size_t)m * n)); TRY(talloc(&dM, (size_t)n * n)); TRY(talloc(&dKkt, (size_t)n * n));
-  TRY(talloc(&dT, (size_t)n * n)); TRY(talloc(&dGD, (size_t)m * n)); TRY(talloc(&dGDGt, (size_t)m * m));
-  TRY(talloc(&dDT, (size_t)n * n)); TRY(talloc(&dGDT, (size_t)m * n));
+  // column-major, K-padded; matrices that also serve as a row-major A operand get padded rows
+  double *dHs, *dGs, *dGsrm, *dRho, *drG, *dM, *dKkt, *dY, *dT, *dGD, *dGDrm, *dGDGt, *dDT, *dGDT, *dscr;
+  TRY(talloc(&dHs, (size_t)n * ld_n));
+  TRY(talloc(&dGs, (size_t)n128 * ld_m));      // Gs (m x n, ld_m); as A operand it is Gs' row-major
+  TRY(talloc(&dGsrm, (size_t)m128 * ld_n));    // Gs row-major (m x n, ld_n)
+  TRY(talloc(&dRho, (size_t)m));
+  TRY(talloc(&drG, (size_t)n * ld_m));
+  TRY(talloc(&dM, (size_t)n * ld_n));
+  TRY(talloc(&dKkt, (size_t)n * ld_n));
+  TRY(talloc(&dY, (size_t)n128 * ld_n));       // D (symmetric: also its own row-major image)
+  TRY(talloc(&dT, (size_t)n * ld_n));
+  TRY(talloc(&dGD, (size_t)n * ld_m));
+  TRY(talloc(&dGDrm, (size_t)m128 * ld_n));
+  TRY(talloc(&dGDGt, (size_t)m * ld_m));
+  TRY(talloc(&dDT, (size_t)n * ld_n));
+  TRY(talloc(&dGDT, (size_t)n * ld_m));
   TRY(talloc(&dscr, std::max((size_t)n * n, (size_t)m * n)));
-  TRYCUDA(cudaMemcpyAsync(dHs, Hs.data(), sizeof(double) * Hs.size(), cudaMemcpyHostToDevice, h->stream));
-  TRYCUDA(cudaMemcpyAsync(dGs, Gs.data(), sizeof(double) * Gs.size(), cudaMemcpyHostToDevice, h->stream));
+  TRYCUDA(cudaMemcpy2DAsync(dHs, sizeof(double) * ld_n, Hs.data(), sizeof(double) * n, sizeof(double) * n, n, cudaMemcpyHostToDevice, st));
+  TRYCUDA(cudaMemcpy2DAsync(dGs, sizeof(double) * ld_m, Gs.data(), sizeof(double) * m, sizeof(double) * m, n, cudaMemcpyHostToDevice, st));
+  TRY(launch_transpose_pad(st, dGs, m, n, dGsrm, ld_n, ld_m));
 
   std::vector<double> rho_all((size_t)L * m);
-  const double one = 1.0, zero = 0.0;
   for (int k = 0; k < L; ++k) {
     // per-row penalties (layers.cpp:210-215; row_kind on the SCALED bounds, problem.hpp:45-47)
     double* rho = rho_all.data() + (size_t)k * m;
     for (int i = 0; i < m; ++i) rho[i] = ((cs[i] == ds[i]) ? 1e3 : 1.0) * grid[k];
-    TRYCUDA(cudaMemcpyAsync(dRho, rho, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream));
-    scale_rows_kernel<<<blocks_for((size_t)m * n), 256, 0, h->stream>>>(dGs, dRho, m, n, drG);
-    // M = Gs' (rho Gs)
-    CQP_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, n, n, m, &one, dGs, m, drG, m, &zero, dM, n));
-    kkt_and_t_kernel<<<blocks_for((size_t)n * n), 256, 0, h->stream>>>(dHs, dM, s.sigma, n, dKkt, dT);
-    // D = kkt^-1 via Cholesky (layers.cpp:126-130)
-    if (cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, n, dKkt, n, dwork, lwork, dinfo) != CUSOLVER_STATUS_SUCCESS) {
-      set_error("cusolverDnDpotrf failed"); return cleanup(CQP_ERR_CUDA);
+    TRYCUDA(cudaMemcpyAsync(dRho, rho, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+    scale_rows_kernel<<<blocks_for((size_t)m * n), 256, 0, st>>>(dGs, dRho, m, n, ld_m, drG);
+    // M = Gs' (rho Gs): A = Gs' row-major == Gs column-major (n rows of length m)
+    TRY(dense_gemm_run(gemm_n, st, dGs, ld_m, n, n128, drG, ld_m, dM, ld_n, 1.0));
+    kkt_and_t_kernel<<<blocks_for((size_t)n * n), 256, 0, st>>>(dHs, dM, s.sigma, n, ld_n, dKkt, dT);
+    // D = kkt^-1: Cholesky, then L Y = I and L' D = Y (layers.cpp:126-130)
+    TRY(cholesky(dKkt, st));
+    set_identity_kernel<<<blocks_for((size_t)n * n), 256, 0, st>>>(dY, ld_n, n);
+    for (int kk = 0; kk < n; ++kk) {
+      tri_scale_row_kernel<<<(kk + 1 + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, kk, kk + 1);
+      const int rem = n - kk - 1;
+      if (rem > 0)
+        fwd_update_kernel<<<dim3((rem + 31) / 32, (kk + 1 + 31) / 32), dim3(32, 8), 0, st>>>(dKkt, dY, ld_n, n, kk);
     }
-    TRYCUDA(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    TRYCUDA(cudaStreamSynchronize(h->stream));
+    for (int kk = n - 1; kk >= 0; --kk) {
+      tri_scale_row_kernel<<<(n + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, kk, n);
+      if (kk > 0)
+        bwd_update_kernel<<<dim3((kk + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, st>>>(dKkt, dY, ld_n, n, kk);
+    }
+    mirror_lower_kernel<<<blocks_for((size_t)n * n), 256, 0, st>>>(dY, ld_n, n);  // dY = D
+    TRY(read_fail(st, &info));
     if (info != 0) {
       set_error("KKT factorization failed: H + sigma I + G'rho G is not positive-definite");
       return cleanup(CQP_ERR_FACTORIZATION);
     }
-    if (cusolverDnDpotri(solver, CUBLAS_FILL_MODE_LOWER, n, dKkt, n, dwork, lwork, dinfo) != CUSOLVER_STATUS_SUCCESS) {
-      set_error("cusolverDnDpotri failed"); return cleanup(CQP_ERR_CUDA);
-    }
-    mirror_lower_kernel<<<blocks_for((size_t)n * n), 256, 0, h->stream>>>(dKkt, n);  // dKkt = D
-    // GD = Gs D ; GDGt = Gs (GD)' ; DT = D T ; GDT = GD T
-    CQP_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, &one, dGs, m, dKkt, n, &zero, dGD, m));
-    CQP_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_T, m, m, n, &one, dGs, m, dGD, m, &zero, dGDGt, m));
-    CQP_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, dKkt, n, dT, n, &zero, dDT, n));
-    CQP_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, m, n, n, &one, dGD, m, dT, n, &zero, dGDT, m));
-    assemble_w_kernel<<<blocks_for((size_t)D * h->Dpad), 256, 0, h->stream>>>(
-        n, m, h->Dpad, dDT, dGD, dGDT, dGDGt, dGs, dRho, h->W + (size_t)k * D * h->Dpad);
+    // GD = Gs D ; GDGt = Gs (GD)' ; DT = D T ; GDT = GD T   (layers.cpp:140-155)
+    TRY(dense_gemm_run(gemm_n, st, dGsrm, ld_n, m, m128, dY, ld_n, dGD, ld_m, 1.0));
+    TRY(launch_transpose_pad(st, dGD, m, n, dGDrm, ld_n, ld_m));
+    TRY(dense_gemm_run(gemm_m, st, dGsrm, ld_n, m, m128, dGDrm, ld_n, dGDGt, ld_m, 1.0));
+    TRY(dense_gemm_run(gemm_n, st, dY, ld_n, n, n128, dT, ld_n, dDT, ld_n, 1.0));
+    TRY(dense_gemm_run(gemm_n, st, dGDrm, ld_n, m, m128, dT, ld_n, dGDT, ld_m, 1.0));
+    assemble_w_kernel<<<blocks_for((size_t)D * h->Dpad), 256, 0, st>>>(
+        n, m, h->Dpad, ld_n, ld_m, dDT, dGD, dGDT, dGDGt, dGs, dRho, h->W + (size_t)k * D * h->Dpad);
     double* dg = h->Dk + (size_t)k * nm * h->npad;
-    TRY(launch_transpose_pad(h->stream, dKkt, n, n, dg, h->npad));
-    TRY(launch_transpose_pad(h->stream, dGD, m, n, dg + (size_t)n * h->npad, h->npad));
+    TRY(launch_transpose_pad(st, dY, n, n, dg, h->npad, ld_n));
+    TRY(launch_transpose_pad(st, dGD, m, n, dg + (size_t)n * h->npad, h->npad, ld_m));
     TRYCUDA(cudaGetLastError());
   }
-  TRYCUDA(cudaMemcpyAsync(h->rho_vec, rho_all.data(), sizeof(double) * rho_all.size(), cudaMemcpyHostToDevice, h->stream));
+  TRYCUDA(cudaMemcpyAsync(h->rho_vec, rho_all.data(), sizeof(double) * rho_all.size(), cudaMemcpyHostToDevice, st));
 
   // unscaled H, G, G' and scaled G in the solve kernel's row-major layout
-  TRYCUDA(cudaMemcpyAsync(dscr, H, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, h->stream));
-  TRY(launch_transpose_pad(h->stream, dscr, n, n, h->H, h->npad));
-  TRY(launch_transpose_pad(h->stream, dGs, m, n, h->Gs, h->npad));
-  TRYCUDA(cudaMemcpyAsync(drG, G, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, h->stream));
-  TRY(launch_transpose_pad(h->stream, drG, m, n, h->Gr, h->npad));
+  TRYCUDA(cudaMemcpyAsync(dscr, H, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, st));
+  TRY(launch_transpose_pad(st, dscr, n, n, h->H, h->npad));
+  TRY(launch_transpose_pad(st, dGs, m, n, h->Gs, h->npad, ld_m));
+  TRYCUDA(cudaStreamSynchronize(st));
+  TRYCUDA(cudaMemcpyAsync(dscr, G, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, st));
+  TRY(launch_transpose_pad(st, dscr, m, n, h->Gr, h->npad));
   {
     // G' (n x m) in the kernel's row-major padded layout
     std::vector<double> Gt_host((size_t)n * m);
     for (int j = 0; j < m; ++j)
       for (int i = 0; i < n; ++i) Gt_host[i + (size_t)j * n] = G[j + (size_t)i * m];
-    TRYCUDA(cudaMemcpyAsync(dGDT, Gt_host.data(), sizeof(double) * Gt_host.size(), cudaMemcpyHostToDevice, h->stream));
-    TRY(launch_transpose_pad(h->stream, dGDT, n, m, h->Gt, h->mpad));
-    TRYCUDA(cudaStreamSynchronize(h->stream));
+    TRYCUDA(cudaStreamSynchronize(st));
+    TRYCUDA(cudaMemcpyAsync(dscr, Gt_host.data(), sizeof(double) * Gt_host.size(), cudaMemcpyHostToDevice, st));
+    TRY(launch_transpose_pad(st, dscr, n, m, h->Gt, h->mpad));
+    TRYCUDA(cudaStreamSynchronize(st));
   }
   TRY(upload_small(h, grid.data(), E.data(), F.data()));
   TRY(upload_vectors(h, g, c, d));
   TRY(cold_start(h));
-  TRYCUDA(cudaStreamSynchronize(h->stream));
+  TRYCUDA(cudaStreamSynchronize(st));
   *out = h;
   return cleanup(CQP_OK);
 #undef TRY

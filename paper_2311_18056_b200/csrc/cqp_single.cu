@@ -768,13 +768,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 // ---- small helper kernels ---------------------------------------------------------------
 
 __global__ void transpose_pad_kernel(const double* __restrict__ src, int rows, int cols,
-                                     double* __restrict__ dst, int ld) {
-  // src column-major rows x cols -> dst row-major rows x ld (pad columns zeroed)
+                                     double* __restrict__ dst, int ld, int src_ld) {
+  // src column-major rows x cols (leading dimension src_ld) -> dst row-major rows x ld (pad zeroed)
   __shared__ double tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx: column block, by: row block
   for (int j = threadIdx.y; j < 32; j += blockDim.y) {
     const int r = by + threadIdx.x, c = bx + j;
-    tile[j][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)c * rows + r] : 0.0;
+    tile[j][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)c * src_ld + r] : 0.0;
   }
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -990,9 +990,9 @@ int launch_set_state(cqp_handle* h, int layer) {
 }
 
 int launch_transpose_pad(cudaStream_t st, const double* src, int rows, int cols, double* dst,
-                         int ld) {
+                         int ld, int src_ld) {
   dim3 grid((ld + 31) / 32, (rows + 31) / 32), block(32, 8);
-  transpose_pad_kernel<<<grid, block, 0, st>>>(src, rows, cols, dst, ld);
+  transpose_pad_kernel<<<grid, block, 0, st>>>(src, rows, cols, dst, ld, src_ld > 0 ? src_ld : rows);
   CQP_CUDA(cudaGetLastError());
   return CQP_OK;
 }
