@@ -1,0 +1,154 @@
+// Device-side helpers shared by the persistent single-QP kernels (cqp_single.cu: all-SM grid with
+// an L2 ring exchange; cqp_cluster.cu: one thread-block cluster with a DSMEM exchange).
+#pragma once
+
+#include <cfloat>
+#include <cmath>
+
+#include "cqp_internal.h"
+
+namespace cqp {
+namespace {
+
+constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ double nanmax(double best, double a) {
+  // max that keeps NaN once seen (the oracle's inf_norm propagates NaN the same way)
+  return (a > best || a != a) ? a : best;
+}
+
+// Watchdog: a spin that lasts longer than ~2 s records where it was stuck in host-mapped memory
+// and traps, so a protocol bug or a lost CTA becomes a CUDA error instead of a hung GPU.
+constexpr long long kSpinLimitCycles = 4000000000ll;
+
+__device__ __noinline__ void watchdog_fire(int* d, int where, int iter) {
+  if (d && atomicCAS(d, 0, 1) == 0) {
+    d[1] = where;
+    d[2] = iter;
+    d[3] = (int)blockIdx.x;
+    d[4] = (int)threadIdx.x;
+    __threadfence_system();
+  }
+  __trap();
+}
+
+__device__ __forceinline__ void progress(int* d, int role, int value) {
+#ifdef CQP_DEBUG_PROGRESS
+  if (d && blockIdx.x < 12) {
+    *((volatile int*)(d + 16 + blockIdx.x * 4 + role)) = value;
+  }
+#endif
+}
+
+// Optional timeline trace (-DCQP_TRACE): clock64() stamps of CTA 0's roles for iterations
+// 100..103, 16 slots per iteration, into the host-mapped debug record (as long long, from word 64).
+#ifdef CQP_TRACE
+#define CQP_STAMP(dbg, it, slot)                                                        \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && (it) >= 100 && (it) < 104)                                   \
+      reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-100) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define CQP_STAMP(dbg, it, slot) do {} while (0)
+#endif
+
+__device__ __forceinline__ bool is_sentinel(double x) {
+  return (unsigned long long)__double_as_longlong(x) == kSentinel;
+}
+
+__device__ __forceinline__ void publish(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void publish_release(double* p, double v) {
+  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
+  unsigned ok;
+  long long t0 = 0;
+  unsigned spins = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && (++spins & 0xFF) == 0) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
+    }
+  } while (!ok);
+}
+
+// ---- thread-block-cluster helpers (small problems: the whole W ladder slice set fits the shared
+// memory of one cluster, and the iterate is exchanged through distributed shared memory) ----
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned map_to_cta(unsigned local_smem_addr, unsigned cta_rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(cta_rank));
+  return r;
+}
+__device__ __forceinline__ void st_remote(unsigned cluster_addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cluster_addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
+  unsigned ok;
+  long long t0 = 0;
+  unsigned spins = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && (++spins & 0xFF) == 0) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
+    }
+  } while (!ok);
+}
+
+__device__ __forceinline__ double2 load_pair(const double* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// layers.cpp:38-50 with log10(grid) tabulated on the host.
+__device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L, double rho) {
+  const double target = log10(rho);
+  int best = 0;
+  double best_dist = INFINITY;
+  for (int k = 0; k < L; ++k) {
+    const double dist = fabs(log_grid[k] - target);
+    if (dist < best_dist - 1e-15) {
+      best = k;
+      best_dist = dist;
+    }
+  }
+  return best;
+}
+
+
+}  // namespace
+}  // namespace cqp

@@ -124,6 +124,7 @@ struct cqp_handle {
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)
+  int rpw = 0;      // cluster kernel: rows of W per warp
 };
 
 namespace cqp {
@@ -131,6 +132,9 @@ namespace cqp {
 // cqp_single.cu
 int configure_launch(cqp_handle* h);
 int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh);
+// cqp_cluster.cu : single thread-block cluster kernel for small problems (DSMEM exchange)
+int configure_cluster(cqp_handle* h);  // sets h->cluster = 1 and the launch shape when it fits
+int launch_cluster(cqp_handle* h, const RunParams& p);
 int launch_refresh_z(cqp_handle* h);
 int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int layer_index);
 int launch_set_state(cqp_handle* h, int layer);

@@ -35,133 +35,10 @@
 #include <cstdlib>
 
 #include "cqp_internal.h"
+#include "cqp_device.cuh"
 
 namespace cqp {
 namespace {
-
-constexpr unsigned long long kSentinel = 0xFFFFFFFFFFFFFFFFull;
-
-__device__ __forceinline__ double nanmax(double best, double a) {
-  // max that keeps NaN once seen (the oracle's inf_norm propagates NaN the same way)
-  return (a > best || a != a) ? a : best;
-}
-
-// Watchdog: a spin that lasts longer than ~2 s records where it was stuck in host-mapped memory
-// and traps, so a protocol bug or a lost CTA becomes a CUDA error instead of a hung GPU.
-constexpr long long kSpinLimitCycles = 4000000000ll;
-
-__device__ __noinline__ void watchdog_fire(int* d, int where, int iter) {
-  if (d && atomicCAS(d, 0, 1) == 0) {
-    d[1] = where;
-    d[2] = iter;
-    d[3] = (int)blockIdx.x;
-    d[4] = (int)threadIdx.x;
-    __threadfence_system();
-  }
-  __trap();
-}
-
-__device__ __forceinline__ void progress(int* d, int role, int value) {
-#ifdef CQP_DEBUG_PROGRESS
-  if (d && blockIdx.x < 12) {
-    *((volatile int*)(d + 16 + blockIdx.x * 4 + role)) = value;
-  }
-#endif
-}
-
-// Optional timeline trace (-DCQP_TRACE): clock64() stamps of CTA 0's roles for iterations
-// 100..103, 16 slots per iteration, into the host-mapped debug record (as long long, from word 64).
-#ifdef CQP_TRACE
-#define CQP_STAMP(dbg, it, slot)                                                        \
-  do {                                                                                  \
-    if (blockIdx.x == 0 && (it) >= 100 && (it) < 104)                                   \
-      reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-100) * 16 + (slot)] = clock64(); \
-  } while (0)
-#else
-#define CQP_STAMP(dbg, it, slot) do {} while (0)
-#endif
-
-__device__ __forceinline__ bool is_sentinel(double x) {
-  return (unsigned long long)__double_as_longlong(x) == kSentinel;
-}
-
-__device__ __forceinline__ void publish(double* p, double v) {
-  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-__device__ __forceinline__ void publish_release(double* p, double v) {
-  asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
-  unsigned ok;
-  long long t0 = 0;
-  unsigned spins = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (!ok && (++spins & 0xFF) == 0) {
-      if (t0 == 0) t0 = clock64();
-      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
-    }
-  } while (!ok);
-}
-
-// ---- thread-block-cluster helpers (small problems: the whole W ladder slice set fits the shared
-// memory of one cluster, and the iterate is exchanged through distributed shared memory) ----
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned map_to_cta(unsigned local_smem_addr, unsigned cta_rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(cta_rank));
-  return r;
-}
-__device__ __forceinline__ void st_remote(unsigned cluster_addr, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(cluster_addr), "d"(v) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, int parity, int* dbg, int where, int iter) {
-  unsigned ok;
-  long long t0 = 0;
-  unsigned spins = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (!ok && (++spins & 0xFF) == 0) {
-      if (t0 == 0) t0 = clock64();
-      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, where, iter);
-    }
-  } while (!ok);
-}
-
-__device__ __forceinline__ double2 load_pair(const double* p) {
-  double2 v;
-  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p)
-               : "memory");
-  return v;
-}
 
 // Loader warps: fetch the whole iterate (nc2 column pairs) from ring slot `q` into shared memory
 // `xs`.  All loads of a batch are in flight together; only entries still holding the sentinel are
@@ -301,7 +178,7 @@ struct Smem {
   double* sb;    // Rp  bias rows
   double* slo;   // Rp
   double* shi;   // Rp
-  double* sval;  // 128 + Rp scratch (cluster mode stages the CTA's rows of v here)
+  double* sval;  // 128 + Rp scratch
   unsigned long long* bars;  // full[2], xready[2], go
 };
 
@@ -475,27 +352,9 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
   __syncthreads();
 }
 
-// layers.cpp:38-50 with log10(grid) tabulated on the host.
-__device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L, double rho) {
-  const double target = log10(rho);
-  int best = 0;
-  double best_dist = INFINITY;
-  for (int k = 0; k < L; ++k) {
-    const double dist = fabs(log_grid[k] - target);
-    if (dist < best_dist - 1e-15) {
-      best = k;
-      best_dist = dist;
-    }
-  }
-  return best;
-}
-
-// CL = false: all-SM grid, iterate exchanged through the L2 ring (cooperative launch).
-// CL = true : ONE thread-block cluster of p.G CTAs; every CTA keeps a full copy of the iterate
-//             in shared memory and the publisher warp writes its rows straight into every peer's
-//             copy (st.shared::cluster) followed by a remote mbarrier arrive: no L2 round trip,
-//             no polling.  Used when the W slices of one ladder level fit the cluster's SMEM.
-template <int RB, bool CL>
+// All-SM grid, iterate exchanged through the L2 ring (cooperative launch).  Small problems whose
+// ladder level fits one thread-block cluster's shared memory use cqp_cluster.cu instead.
+template <int RB>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
@@ -510,13 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if (t == 0) {
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
-    mbar_init(&xready[0], CL ? p.G : kLoaderWarps);
-    mbar_init(&xready[1], CL ? p.G : kLoaderWarps);
+    mbar_init(&xready[0], kLoaderWarps);
+    mbar_init(&xready[1], kLoaderWarps);
     mbar_init(go, 1);
-  }
-  if (CL) {
-    __syncthreads();
-    cluster_sync_all();  // every peer's barriers exist before anyone arrives on them remotely
   }
   const int n = p.n, m = p.m, D = p.D;
   const int row0 = blockIdx.x * p.R;
@@ -566,7 +421,6 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     s.xs[p.Dpad + i] = 0.0;
   }
   __syncthreads();
-  if (CL) cluster_sync_all();  // peers may write into xs[1] as soon as they finish iteration 1
 
   int n_trace = 1, n_hist = 0;
   if (blockIdx.x == 0 && t == 0) {
@@ -585,10 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     double* part = s.spart + (size_t)b * kComputeWarps * Rcap;
     if (compute) {
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 1); CQP_STAMP(p.dbg, i, 0); }
-      if (i > 1) {
-        if (CL) mbar_wait_cluster(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
-        else mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
-      }
+      if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 2); CQP_STAMP(p.dbg, i, 1); }  // v_{i-1} landed
       if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 10);
       const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
@@ -613,29 +464,6 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 1); CQP_STAMP(p.dbg, i, 4); }
       mbar_wait(&full[b], par, p.dbg, 2, i);
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
-      if (CL) {
-        // rows of v_i -> s.sval (local), then lane j delivers them to peer j's copy xs[b] and
-        // arrives on peer j's xready[b] (release at cluster scope orders the stores before it)
-        for (int r = lane; r < nrows; r += 32) {
-          double x = 0.0;
-#pragma unroll
-          for (int w = 0; w < kComputeWarps; ++w) x += part[w * Rcap + r];
-          x += s.sb[r];
-          const double lo = s.slo[r], hi = s.shi[r];
-          x = x < lo ? lo : x;
-          x = x > hi ? hi : x;
-          s.sval[r] = x;
-        }
-        __syncwarp();
-        if (lane == 0) CQP_STAMP(p.dbg, i, 6);
-        if (lane < p.G) {
-          const unsigned xdst = map_to_cta(smem_u32(s.xs + (size_t)b * p.Dpad + row0), (unsigned)lane);
-          for (int r = 0; r < nrows; ++r) st_remote(xdst + 8u * (unsigned)r, s.sval[r]);
-          mbar_arrive_remote(map_to_cta(smem_u32(&xready[b]), (unsigned)lane));
-        }
-        __syncwarp();
-        if (lane == 0) CQP_STAMP(p.dbg, i, 7);
-      } else {
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
       for (int r = lane; r < nrows; r += 32) {
@@ -663,8 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
       if (p.fence_mode == 0) __threadfence();
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 3); CQP_STAMP(p.dbg, i, 7); }
-      }
-    } else if (!CL) {
+    } else {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
@@ -759,10 +586,6 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       p.state[0] = layer;
     }
   }
-  if (CL) {
-    __syncthreads();
-    cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
-  }
 }
 
 // ---- small helper kernels ---------------------------------------------------------------
@@ -831,53 +654,12 @@ __global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
 
 template <int RB>
 int launch_run_rb(cqp_handle* h, RunParams& p) {
-  if (h->cluster) {
-    auto fn = run_kernel<RB, true>;
-    CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-    if (h->G > 8) CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(h->G);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = (size_t)h->smem_bytes;
-    cfg.stream = h->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)h->G;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CQP_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
-    return CQP_OK;
-  }
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->smem_bytes));
   void* args[] = {&p};
-  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, false>, dim3(h->G), dim3(kThreads),
+  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB>, dim3(h->G), dim3(kThreads),
                                        args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
-}
-
-// Can a single cluster of `C` CTAs hold one ladder level (and does the device schedule it)?
-template <int RB>
-bool cluster_fits(int C, int smem_bytes) {
-  auto fn = run_kernel<RB, true>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return false;
-  if (C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(C);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = (size_t)smem_bytes;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) { cudaGetLastError(); return false; }
-  return clusters >= 1;
 }
 
 }  // namespace
@@ -885,25 +667,13 @@ bool cluster_fits(int C, int smem_bytes) {
 int configure_launch(cqp_handle* h) {
   const int D = h->D;
   h->cluster = 0;
-  // Small problems CAN run as one thread-block cluster (16 CTAs, else 8) that keeps W_k in its
-  // shared memory and exchanges the iterate through DSMEM.  Measured on B200 (round 1) this mode
-  // is correct but slower than the all-SM grid (4.1 vs 2.4 us/iteration at D = 300: the
-  // release-ordered remote stores and the 16-row butterflies dominate), so it is opt-in
-  // (CQP_ENABLE_CLUSTER=1) until the push is rewritten with st.async.
-  const char* enable_cluster = std::getenv("CQP_ENABLE_CLUSTER");
+  // Small problems (one ladder level fits the shared memory of ONE thread-block cluster) run the
+  // cluster kernel of cqp_cluster.cu: the iterate never leaves the SMs.  CQP_FORCE_TIER=0/1 pins
+  // the all-SM grid kernel (tests, A/B measurements).
   const char* force_tier = std::getenv("CQP_FORCE_TIER");
-  if (D >= 64 && enable_cluster && enable_cluster[0] == '1' && !(force_tier && force_tier[0] == '1')) {
-    for (int C : {16, 8}) {
-      const int R = (D + C - 1) / C;
-      const int rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
-      const size_t need = smem_doubles(R, rb, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
-      if (need > (size_t)kMaxSmemBytes) continue;
-      const bool ok = rb == 4 ? cluster_fits<4>(C, (int)need) : (rb == 8 ? cluster_fits<8>(C, (int)need) : cluster_fits<16>(C, (int)need));
-      if (!ok) continue;
-      h->cluster = 1; h->R = R; h->G = C; h->rb = rb; h->w_smem = 1; h->smem_bytes = (int)need;
-      return CQP_OK;
-    }
-  }
+  const bool force_grid = force_tier && (force_tier[0] == '0' || force_tier[0] == '1');
+  if (!force_grid && configure_cluster(h) == CQP_OK && h->cluster) return CQP_OK;
+  h->cluster = 0;
   int G = h->num_sms;
   int R = (D + G - 1) / G;
   if (R < 1) R = 1;
@@ -954,8 +724,9 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.barrier_next = h->barrier + ((h->launch_parity + 1) & 1);
   h->launch_parity ^= 1;
   p.dbg = h->dbg_dev;
+  if (h->cluster) return launch_cluster(h, p);
   // few iterations: copying the W slice into shared memory costs as much as streaming it once
-  if (total_iters < 4 && !h->cluster) p.w_smem = 0;
+  if (total_iters < 4) p.w_smem = 0;
   switch (h->rb) {
     case 4: return launch_run_rb<4>(h, p);
     case 8: return launch_run_rb<8>(h, p);
