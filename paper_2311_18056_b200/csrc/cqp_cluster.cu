@@ -9,10 +9,15 @@
 // a DSMEM store (~215 cycles) that carries its own completion signal:
 //   * CTA r of the C-CTA cluster keeps rows [r R, r R + R) of W_k resident in shared memory and a
 //     full double-buffered copy of the iterate (xs[2][Dpad]).
-//   * All 16 warps are compute warps and own WHOLE rows (warp w: local rows [w RPW, w RPW + RPW)),
-//     lanes stride over column pairs (16-byte LDS, conflict-free), two FMA chains per row, a
-//     5-step xor butterfly; there is no cross-warp reduction, no publisher warp and no CTA-wide
-//     barrier in the iteration loop.
+//   * All 16 warps are compute warps and own WHOLE rows, so there is no cross-warp reduction, no
+//     publisher warp and no CTA-wide barrier in the iteration loop.  Two layouts:
+//       - register mode (R <= 32, D <= 512): 16 lanes per row, 2 rows per warp; every lane keeps
+//         its NPT column pairs of W_k in REGISTERS for the whole solve (a rho switch reloads
+//         them), so an iteration reads only x from shared memory (both half-warps read the same
+//         16 addresses: one 256-byte broadcast wavefront per LDS) and needs a 4-step butterfly;
+//       - shared-memory mode (larger R): W slice resident in shared memory, warp w owns local rows
+//         [w RPW, w RPW + RPW), lanes stride over column pairs (16-byte LDS, conflict-free), two
+//         FMA chains per row, a 5-step butterfly.
 //   * The warp that finished a row adds the bias, clamps and pushes the value into every CTA's
 //     copy with st.async.shared::cluster ... mbarrier::complete_tx::bytes (lane -> peer lane % C).
 //     Each CTA's xready[parity] mbarrier expects exactly 8 D bytes per iteration, so "v_i is
@@ -88,40 +93,99 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ Mrow, 
   return warp_sum(a0 + a1);
 }
 
+// Three row dots of one residual step at once: H[rh, :] . y, G'[rh, :] . lambda, G[rg, :] . y (a
+// null row pointer yields 0).  Each sum has the same fixed order as warp_row_dot; all global loads
+// of a trip are issued before the first FMA and the three butterflies interleave.  The rows may
+// live in shared memory (hg_smem) or in global memory: generic loads.
+__device__ __forceinline__ void warp_row_dot3(const double* __restrict__ Hrow, const double* __restrict__ Gtrow,
+                                              const double* __restrict__ Grow, const double* __restrict__ y,
+                                              const double* __restrict__ lam, int npad, int mpad, int lane,
+                                              double& hy, double& gtl, double& gy) {
+  const double2* h2 = reinterpret_cast<const double2*>(Hrow);
+  const double2* t2 = reinterpret_cast<const double2*>(Gtrow);
+  const double2* g2 = reinterpret_cast<const double2*>(Grow);
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  const double2* l2 = reinterpret_cast<const double2*>(lam);
+  const int nn2 = npad >> 1, nm2 = mpad >> 1, top = max(nn2, nm2);
+  const double2 zero = make_double2(0.0, 0.0);
+  double a[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  for (int c2 = lane; c2 < top; c2 += 64) {
+    const int d2 = c2 + 32;
+    const bool n0 = c2 < nn2, n1 = d2 < nn2, m0 = c2 < nm2, m1 = d2 < nm2;
+    const double2 wh0 = (Hrow && n0) ? h2[c2] : zero, wh1 = (Hrow && n1) ? h2[d2] : zero;
+    const double2 wt0 = (Gtrow && m0) ? t2[c2] : zero, wt1 = (Gtrow && m1) ? t2[d2] : zero;
+    const double2 wg0 = (Grow && n0) ? g2[c2] : zero, wg1 = (Grow && n1) ? g2[d2] : zero;
+    const double2 y0 = n0 ? y2[c2] : zero, y1 = n1 ? y2[d2] : zero;
+    const double2 l0 = m0 ? l2[c2] : zero, l1 = m1 ? l2[d2] : zero;
+    a[0][0] = fma(wh0.x, y0.x, a[0][0]); a[0][0] = fma(wh0.y, y0.y, a[0][0]);
+    a[0][1] = fma(wh1.x, y1.x, a[0][1]); a[0][1] = fma(wh1.y, y1.y, a[0][1]);
+    a[1][0] = fma(wt0.x, l0.x, a[1][0]); a[1][0] = fma(wt0.y, l0.y, a[1][0]);
+    a[1][1] = fma(wt1.x, l1.x, a[1][1]); a[1][1] = fma(wt1.y, l1.y, a[1][1]);
+    a[2][0] = fma(wg0.x, y0.x, a[2][0]); a[2][0] = fma(wg0.y, y0.y, a[2][0]);
+    a[2][1] = fma(wg1.x, y1.x, a[2][1]); a[2][1] = fma(wg1.y, y1.y, a[2][1]);
+  }
+  double v0 = a[0][0] + a[0][1], v1 = a[1][0] + a[1][1], v2 = a[2][0] + a[2][1];
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, w);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, w);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, w);
+  }
+  hy = v0; gtl = v1; gy = v2;
+}
+
 struct ClSmem {
-  double* sW;     // R * Dpad  this CTA's rows of W_k
-  double* xs;     // 2 * Dpad  full iterate, double buffered by iteration parity (peers write here)
+  double* sW;     // R * Dpad  this CTA's rows of W_k (shared-memory mode only)
+  double* xs;     // 2 * xs_stride  full iterate, double buffered by iteration parity (peers write here)
+  double* sH;     // pern * npad   this CTA's rows of H   (hg_smem only; else read from global)
+  double* sGt;    // pern * mpad   ... of G'
+  double* sG;     // perm * npad   ... of G
   double* uy;     // npad      unscaled y (also scratch for g_s)
   double* uz;     // mpad
   double* ul;     // mpad
+  double* sE;     // npad      scaling.E   (constant for the launch)
+  double* sF;     // mpad      scaling.F
+  double* sg;     // npad      unscaled g
   double* sb;     // Rp  bias rows
   double* slo;    // Rp
   double* shi;    // Rp
+  double* sgrid;  // 2 * 16   grid values, then log10(grid) (L <= 16; else read from global)
   double* wmax;   // kClWarps * 8   per-warp partial maxima
   double* cmax;   // 8              this CTA's maxima / the cluster-wide result
   double* norms;  // 2 * 16 * 8     per-CTA maxima of a residual pass, by pass parity (peers write here)
   unsigned long long* bars;  // xready[2], nbar[2]
 };
 
-__host__ __device__ inline size_t cl_smem_doubles(int R, int Dpad, int npad, int mpad) {
+// Shared-memory doubles: `wrows` rows of W (0 in register mode), the iterate copies, and the
+// (optional) rows of H, G', G a CTA needs for the residual checks.
+__host__ __device__ inline size_t cl_smem_doubles(int R, int wrows, int Dpad, int xs_stride, int npad, int mpad,
+                                                  int hg_rows_n, int hg_rows_m) {
   const int Rp = (R + 1) & ~1;
-  return (size_t)R * Dpad + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad + 3 * (size_t)Rp + kClWarps * 8 + 8 +
-         2 * 16 * 8 + 8;
+  return (size_t)wrows * Dpad + 2 * (size_t)xs_stride + 3 * (size_t)npad + 3 * (size_t)mpad + 3 * (size_t)Rp +
+         (size_t)hg_rows_n * (npad + mpad) + (size_t)hg_rows_m * npad + 32 + kClWarps * 8 + 8 + 2 * 16 * 8 + 8;
 }
 
 __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& p) {
   ClSmem s;
   double* base = reinterpret_cast<double*>(raw);
   const int Rp = (p.R + 1) & ~1;
+  const int pern = p.hg_smem ? (p.n + p.G - 1) / p.G : 0, perm = p.hg_smem ? (p.m + p.G - 1) / p.G : 0;
   s.sW = base;
-  s.xs = s.sW + (size_t)p.R * p.Dpad;
-  s.uy = s.xs + 2 * p.Dpad;
+  s.xs = s.sW + (p.w_smem ? (size_t)p.R * p.Dpad : 0);
+  s.sH = s.xs + 2 * p.xs_stride;
+  s.sGt = s.sH + (size_t)pern * p.npad;
+  s.sG = s.sGt + (size_t)pern * p.mpad;
+  s.uy = s.sG + (size_t)perm * p.npad;
   s.uz = s.uy + p.npad;
   s.ul = s.uz + p.mpad;
-  s.sb = s.ul + p.mpad;
+  s.sE = s.ul + p.mpad;
+  s.sF = s.sE + p.npad;
+  s.sg = s.sF + p.mpad;
+  s.sb = s.sg + p.npad;
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
-  s.wmax = s.shi + Rp;
+  s.sgrid = s.shi + Rp;
+  s.wmax = s.sgrid + 32;
   s.cmax = s.wmax + kClWarps * 8;
   s.norms = s.cmax + 8;
   s.bars = reinterpret_cast<unsigned long long*>(s.norms + 2 * 16 * 8);
@@ -134,7 +198,7 @@ __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& 
 __device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int row0, int nrows) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   __syncthreads();
-  {
+  if (p.w_smem) {
     const double2* src = reinterpret_cast<const double2*>(p.W + ((size_t)k * p.D + row0) * p.Dpad);
     double2* dst = reinterpret_cast<double2*>(s.sW);
     const int count = nrows * (p.Dpad >> 1);
@@ -149,7 +213,7 @@ __device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int ro
     }
     for (; i < count; i += kClThreads) dst[i] = __ldg(src + i);
   }
-  for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * p.g[i]) : 0.0;
+  for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < p.n) ? p.cost_scale * (s.sE[i] * s.sg[i]) : 0.0;
   __syncthreads();
   const int nm = p.n + p.m;
   const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
@@ -172,17 +236,17 @@ __device__ void cl_residual_pass(const RunParams& p, const ClSmem& s, const doub
   unsigned long long* nbar = s.bars + 2;
   __syncthreads();
   // unscale (layers.hpp:57-59)
-  for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? p.E[i] * xs[i] : 0.0;
+  for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? s.sE[i] * xs[i] : 0.0;
   for (int i = t; i < p.mpad; i += kClThreads) {
     double z = 0.0, l = 0.0;
     if (i < m) {
-      z = xs[n + i] / p.F[i];
+      z = xs[n + i] / s.sF[i];
       if (final) {  // solver.cpp:94  z = clamp(z, p.c, p.d) in original units
         const double lo = p.c[i], hi = p.d[i];
         z = z < lo ? lo : z;
         z = z > hi ? hi : z;
       }
-      l = (p.F[i] * xs[n + m + i]) / p.cost_scale;
+      l = (s.sF[i] * xs[n + m + i]) / p.cost_scale;
     }
     s.uz[i] = z;
     s.ul[i] = l;
@@ -190,31 +254,38 @@ __device__ void cl_residual_pass(const RunParams& p, const ClSmem& s, const doub
   __syncthreads();
 
   double mx[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  {  // rows of H and G' owned by this CTA (warp per row)
-    const int per = (n + C - 1) / C;
-    const int h0 = (int)rank * per;
-    const int h1 = min(n, h0 + per);
-    for (int row = h0 + warp; row < h1; row += kClWarps) {
-      const double hy = warp_row_dot(p.H + (size_t)row * p.npad, s.uy, p.npad, lane);
-      const double gtl = warp_row_dot(p.Gt + (size_t)row * p.mpad, s.ul, p.mpad, lane);
-      const double gi = p.g[row];
-      const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
-      mx[6] = nanmax(mx[6], fabs(gi));
-      mx[1] = nanmax(mx[1], fabs(dual));
-      mx[2] = nanmax(mx[2], fabs(hy));
-      mx[3] = nanmax(mx[3], fabs(gtl));
-    }
-  }
-  {  // rows of G owned by this CTA
-    const int per = (m + C - 1) / C;
-    const int g0 = (int)rank * per;
-    const int g1 = min(m, g0 + per);
-    for (int row = g0 + warp; row < g1; row += kClWarps) {
-      const double gy = warp_row_dot(p.Gr + (size_t)row * p.npad, s.uy, p.npad, lane);
-      const double z = s.uz[row];
-      mx[0] = nanmax(mx[0], fabs(gy - z));
-      mx[4] = nanmax(mx[4], fabs(gy));
-      mx[5] = nanmax(mx[5], fabs(z));
+  {
+    // CTA `rank` owns rows [h0, h1) of H and G' and rows [g0, g1) of G; warp w takes the j-th row
+    // of both ranges together (j = w, w + 16, ...) so that the three row reads are in flight at
+    // once and the three butterflies interleave.
+    const int pern = (n + C - 1) / C, perm = (m + C - 1) / C;
+    const int h0 = (int)rank * pern, h1 = min(n, h0 + pern);
+    const int g0 = (int)rank * perm, g1 = min(m, g0 + perm);
+    const int trips = max(pern, perm);
+    for (int j = warp; j < trips; j += kClWarps) {
+      const int rh = h0 + j, rg = g0 + j;
+      const bool vh = rh < h1, vg = rg < g1;
+      if (!vh && !vg) break;
+      double hy, gtl, gy;
+      const double* Hrow = p.hg_smem ? s.sH + (size_t)j * p.npad : p.H + (size_t)rh * p.npad;
+      const double* Trow = p.hg_smem ? s.sGt + (size_t)j * p.mpad : p.Gt + (size_t)rh * p.mpad;
+      const double* Grow = p.hg_smem ? s.sG + (size_t)j * p.npad : p.Gr + (size_t)rg * p.npad;
+      warp_row_dot3(vh ? Hrow : nullptr, vh ? Trow : nullptr, vg ? Grow : nullptr, s.uy, s.ul, p.npad, p.mpad,
+                    lane, hy, gtl, gy);
+      if (vh) {
+        const double gi = s.sg[rh];
+        const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
+        mx[6] = nanmax(mx[6], fabs(gi));
+        mx[1] = nanmax(mx[1], fabs(dual));
+        mx[2] = nanmax(mx[2], fabs(hy));
+        mx[3] = nanmax(mx[3], fabs(gtl));
+      }
+      if (vg) {
+        const double z = s.uz[rg];
+        mx[0] = nanmax(mx[0], fabs(gy - z));
+        mx[4] = nanmax(mx[4], fabs(gy));
+        mx[5] = nanmax(mx[5], fabs(z));
+      }
     }
   }
   if (lane == 0) {
@@ -244,9 +315,12 @@ __device__ void cl_residual_pass(const RunParams& p, const ClSmem& s, const doub
   __syncthreads();
 }
 
-template <int RPW>
+// NPT == 0: shared-memory mode with RPW rows per warp; NPT > 0: register mode (RPW unused), each
+// lane keeps NPT column pairs of its row in registers.
+template <int RPW, int NPT>
 __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool kReg = NPT > 0;
   const ClSmem s = cl_carve(smem_raw, p);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int C = p.G;  // cluster size == grid size
@@ -268,14 +342,35 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   const int nrows = (int)(((long long)(rank + 1) * D) / C) - row0;
   int layer = p.state[0];
 
+  for (int i = t; i < p.npad; i += kClThreads) {
+    s.sE[i] = (i < n) ? p.E[i] : 1.0;
+    s.sg[i] = (i < n) ? p.g[i] : 0.0;
+  }
+  for (int i = t; i < p.mpad; i += kClThreads) s.sF[i] = (i < m) ? p.F[i] : 1.0;
+  const bool grid_smem = p.L <= 16;
+  if (grid_smem && t < p.L) {
+    s.sgrid[t] = p.grid[t];
+    s.sgrid[16 + t] = p.log_grid[t];
+  }
+  const double* grid_v = grid_smem ? s.sgrid : p.grid;
+  const double* grid_log = grid_smem ? s.sgrid + 16 : p.log_grid;
+  if (p.hg_smem) {  // the rows of H, G', G this CTA needs at every residual check
+    const int pern = (n + C - 1) / C, perm = (m + C - 1) / C;
+    const int h0 = (int)rank * pern, g0 = (int)rank * perm;
+    const int cn = max(0, min(pern, n - h0)), cm = max(0, min(perm, m - g0));
+    for (int i = t; i < cn * p.npad; i += kClThreads) s.sH[i] = __ldg(p.H + (size_t)h0 * p.npad + i);
+    for (int i = t; i < cn * p.mpad; i += kClThreads) s.sGt[i] = __ldg(p.Gt + (size_t)h0 * p.mpad + i);
+    for (int i = t; i < cm * p.npad; i += kClThreads) s.sG[i] = __ldg(p.Gr + (size_t)g0 * p.npad + i);
+  }
+  __syncthreads();
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
   // (layers.cpp:182-186, 223-226)
   for (int r = t; r < nrows; r += kClThreads) {
     const int row = row0 + r;
     double lo = -INFINITY, hi = INFINITY;
     if (row >= n && row < n + m) {
-      lo = p.F[row - n] * p.c[row - n];
-      hi = p.F[row - n] * p.d[row - n];
+      lo = s.sF[row - n] * p.c[row - n];
+      hi = s.sF[row - n] * p.d[row - n];
     }
     s.slo[r] = lo;
     s.shi[r] = hi;
@@ -298,12 +393,48 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     cluster_sync_all();  // release/acquire at cluster scope: the peers' rows of z_s are visible
   }
 
+  // ---- work split inside the CTA ----
+  const int nc2 = p.Dpad >> 1;
+  const int XS = p.xs_stride;
+  // register mode: lanes [0,16) of warp w own local row 2w, lanes [16,32) row 2w + 1; lane `sub` of a
+  // row covers column pairs sub, sub + 16, ...  and pushes the finished row to peer `sub`.
+  // shared-memory mode: warp w owns local rows [w RPW, w RPW + RPW); lane (peer = lane % C,
+  // lane / C) pushes rows lane / C, lane / C + 32 / C, ... of the warp to `peer`.
+  const int sub = kReg ? (lane & 15) : lane / C;
+  const int peer = kReg ? (lane & 15) : (lane & (C - 1));
+  const int wr0 = kReg ? 2 * warp : warp * RPW;                               // first local row of this warp
+  const int nr = max(0, min(kReg ? 2 : RPW, nrows - wr0));                    // rows this warp owns
+  const int lr = wr0 + (lane >> 4);                                           // register mode: this lane's row
+  const bool has_row = kReg && lr < nrows;
+  const bool pusher = kReg && has_row && peer < C;
+  unsigned push_mask = 0;  // shared-memory mode, bit r: this lane pushes the warp's r-th row
+  if (!kReg) {
+    const int step = 32 / C;  // C is 8 or 16: a power of two
+    for (int r = 0; r < nr; ++r)
+      if (((r - sub) & (step - 1)) == 0) push_mask |= 1u << r;
+  }
+  const unsigned peer_xs = map_to_cta(smem_u32(s.xs), (unsigned)(peer < C ? peer : 0));
+  const unsigned peer_bar = map_to_cta(smem_u32(&xready[0]), (unsigned)(peer < C ? peer : 0));
+
+  double2 wreg[kReg ? NPT : 1];
+  auto load_registers = [&](int k) {  // register mode: this lane's column pairs of W_k[row0 + lr, :]
+    if (kReg) {
+      const double2* src = reinterpret_cast<const double2*>(p.W + ((size_t)k * D + row0 + (has_row ? lr : 0)) * p.Dpad);
+#pragma unroll
+      for (int j = 0; j < (kReg ? NPT : 1); ++j) {
+        const int c2 = (lane & 15) + 16 * j;
+        wreg[j] = (has_row && c2 < nc2) ? __ldg(src + c2) : make_double2(0.0, 0.0);
+      }
+    }
+  };
+
   cl_load_layer(p, s, layer, row0, nrows);
+  load_registers(layer);
 
   // v_0 -> xs[0]; pad slots of both copies stay zero for the whole launch
-  for (int i = t; i < p.Dpad; i += kClThreads) {
+  for (int i = t; i < XS; i += kClThreads) {
     s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
-    s.xs[p.Dpad + i] = 0.0;
+    s.xs[XS + i] = 0.0;
   }
   __syncthreads();
   cluster_sync_all();  // peers write into xs[1] as soon as they finish iteration 1
@@ -314,16 +445,8 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     p.trace[1] = layer;
   }
 
-  // per-lane push target: peer = lane % C gets rows {lane / C, lane / C + 32 / C, ...} of this warp
-  const int peer = lane & (C - 1);
-  const int sub = lane / C, step = 32 / C;
-  const unsigned peer_xs = map_to_cta(smem_u32(s.xs), (unsigned)peer);
-  const unsigned peer_bar = map_to_cta(smem_u32(&xready[0]), (unsigned)peer);
-  const int wr0 = warp * RPW;                       // first local row of this warp
-  const int nr = max(0, min(RPW, nrows - wr0));     // rows this warp owns
-  const int nc2 = p.Dpad >> 1;
-
   bool converged = false;
+  int until_check = p.check_interval;
   int iters_done = 0;
   int have = 0;  // v_have has been awaited (and its barrier re-armed) already
   for (int i = 1; i <= p.total_iters; ++i) {
@@ -332,6 +455,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     // Warps without rows (nr == 0) skip the loop's waits: a warp that pushes nothing does not hold
     // the cluster back, so the barrier could run two phases ahead of it; they rejoin at the checks.
     // Warp 0 always owns rows (nrows >= 1), so thread 0 re-arms every phase.
+    if (t == 0) CQP_STAMP(p.dbg, i, 0);
     if (i > 1 && have != i - 1 && nr > 0) {
       mbar_wait_cluster(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);  // v_{i-1} landed
       // Safe to re-arm without a CTA barrier: the next phase of this barrier carries v_{i+1}, which
@@ -339,66 +463,101 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
       // this wait) pushed its rows of v_i.
       if (t == 0) mbar_arm(&xready[b ^ 1], xbytes);
     }
+    if (t == 0) CQP_STAMP(p.dbg, i, 1);
     if (nr > 0) {
-      const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
-      const double2* w2 = reinterpret_cast<const double2*>(s.sW);
-      size_t roff[RPW];
+      const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * XS);
+      if constexpr (kReg) {
+        double a0 = 0.0, a1 = 0.0;
+        const double2* xl = x2 + (lane & 15);
 #pragma unroll
-      for (int r = 0; r < RPW; ++r) roff[r] = (size_t)min(wr0 + r, nrows - 1) * nc2;  // duplicates are not pushed
-      double a0[RPW], a1[RPW];
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) a0[r] = a1[r] = 0.0;
-      int c2 = lane;
-      for (; c2 + 32 < nc2; c2 += 64) {
-        const double2 x0 = x2[c2], x1 = x2[c2 + 32];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const double2 w0 = w2[roff[r] + c2], w1 = w2[roff[r] + c2 + 32];
-          a0[r] = fma(w0.x, x0.x, a0[r]);
-          a0[r] = fma(w0.y, x0.y, a0[r]);
-          a1[r] = fma(w1.x, x1.x, a1[r]);
-          a1[r] = fma(w1.y, x1.y, a1[r]);
+        for (int j = 0; j < NPT; j += 2) {
+          const double2 x0 = xl[16 * j];
+          a0 = fma(wreg[j].x, x0.x, a0);
+          a0 = fma(wreg[j].y, x0.y, a0);
+          if (j + 1 < NPT) {
+            const double2 x1 = xl[16 * (j + 1)];
+            a1 = fma(wreg[j + 1].x, x1.x, a1);
+            a1 = fma(wreg[j + 1].y, x1.y, a1);
+          }
         }
-      }
-      if (c2 < nc2) {
-        const double2 x0 = x2[c2];
+        if (t == 0) CQP_STAMP(p.dbg, i, 3);
+        double tot = a0 + a1;
 #pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const double2 w0 = w2[roff[r] + c2];
-          a0[r] = fma(w0.x, x0.x, a0[r]);
-          a0[r] = fma(w0.y, x0.y, a0[r]);
-        }
-      }
-      double tot[RPW];
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) tot[r] = a0[r] + a1[r];
-#pragma unroll
-      for (int w = 16; w >= 1; w >>= 1) {
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) tot[r] += __shfl_xor_sync(0xffffffffu, tot[r], w);
-      }
-      // every lane holds the RPW row sums; lane (peer, sub) pushes rows sub, sub + step, ...
-      const unsigned xdst = peer_xs + 8u * (unsigned)(b * p.Dpad + row0 + wr0);
-      const unsigned bdst = peer_bar + 8u * (unsigned)b;
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) {
-        if (r < nr && ((r - sub) % step) == 0 && r >= sub) {
-          double x = tot[r] + s.sb[wr0 + r];
-          const double lo = s.slo[wr0 + r], hi = s.shi[wr0 + r];
+        for (int w = 8; w >= 1; w >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);
+        if (t == 0) CQP_STAMP(p.dbg, i, 2);
+        if (pusher) {
+          double x = tot + s.sb[lr];
+          const double lo = s.slo[lr], hi = s.shi[lr];
           x = x < lo ? lo : x;
           x = x > hi ? hi : x;
-          st_async_f64(xdst + 8u * (unsigned)r, x, bdst);
+          st_async_f64(peer_xs + 8u * (unsigned)(b * XS + row0 + lr), x, peer_bar + 8u * (unsigned)b);
+        }
+      } else {
+        const double2* w2 = reinterpret_cast<const double2*>(s.sW);
+        size_t roff[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) roff[r] = (size_t)min(wr0 + r, nrows - 1) * nc2;  // duplicates are not pushed
+        double a0[RPW], a1[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) a0[r] = a1[r] = 0.0;
+        int c2 = lane;
+        for (; c2 + 32 < nc2; c2 += 64) {
+          const double2 x0 = x2[c2], x1 = x2[c2 + 32];
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) {
+            const double2 w0 = w2[roff[r] + c2], w1 = w2[roff[r] + c2 + 32];
+            a0[r] = fma(w0.x, x0.x, a0[r]);
+            a0[r] = fma(w0.y, x0.y, a0[r]);
+            a1[r] = fma(w1.x, x1.x, a1[r]);
+            a1[r] = fma(w1.y, x1.y, a1[r]);
+          }
+        }
+        if (c2 < nc2) {
+          const double2 x0 = x2[c2];
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) {
+            const double2 w0 = w2[roff[r] + c2];
+            a0[r] = fma(w0.x, x0.x, a0[r]);
+            a0[r] = fma(w0.y, x0.y, a0[r]);
+          }
+        }
+        if (t == 0) CQP_STAMP(p.dbg, i, 3);
+        double tot[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) tot[r] = a0[r] + a1[r];
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) tot[r] += __shfl_xor_sync(0xffffffffu, tot[r], w);
+        }
+        if (t == 0) CQP_STAMP(p.dbg, i, 2);
+        // every lane holds the RPW row sums; lane (peer, sub) pushes rows sub, sub + step, ...
+        const unsigned xdst = peer_xs + 8u * (unsigned)(b * XS + row0 + wr0);
+        const unsigned bdst = peer_bar + 8u * (unsigned)b;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          if ((push_mask >> r) & 1u) {
+            double x = tot[r] + s.sb[wr0 + r];
+            const double lo = s.slo[wr0 + r], hi = s.shi[wr0 + r];
+            x = x < lo ? lo : x;
+            x = x > hi ? hi : x;
+            st_async_f64(xdst + 8u * (unsigned)r, x, bdst);
+          }
         }
       }
+      if (t == 0) CQP_STAMP(p.dbg, i, 6);
     }
     iters_done = i;
-    if (i % p.check_interval != 0) continue;
+    if (--until_check != 0) continue;
+    until_check = p.check_interval;
 
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     mbar_wait_cluster(&xready[b], ((i - 1) >> 1) & 1, p.dbg, 2, i);  // v_i
     have = i;
     double nrm[7];
-    cl_residual_pass(p, s, s.xs + (size_t)b * p.Dpad, false, pass++, rank, C, nrm);
+    if (t == 0) CQP_STAMP(p.dbg, i, 4);
+    cl_residual_pass(p, s, s.xs + (size_t)b * XS, false, pass++, rank, C, nrm);
+    if (t == 0) CQP_STAMP(p.dbg, i, 5);
     // (the pass begins with a CTA barrier, so every warp is past its wait on xready[b])
     if (t == 0) mbar_arm(&xready[b], xbytes);
     const double r_prim = nrm[0], r_dual = nrm[1];
@@ -410,7 +569,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
     ++n_hist;
     if (p.adaptive) {
-      const double rho_cur = p.grid[layer];
+      const double rho_cur = grid_v[layer];
       double rho_nom = rho_cur;
       if (!(r_prim == 0.0 || r_dual == 0.0)) {
         const double g_norm = nrm[6];
@@ -421,7 +580,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
         den = den < 1e-4 ? 1e-4 : den;
         rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
       }
-      const int cand_near = nearest_grid_index(p.log_grid, p.L, rho_nom);
+      const int cand_near = nearest_grid_index(grid_log, p.L, rho_nom);
       const double qa = rho_nom / rho_cur, qb = rho_cur / rho_nom;
       const double ratio = qa < qb ? qb : qa;
       const int cand = ratio >= p.threshold ? cand_near : layer;
@@ -433,8 +592,10 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
         }
         ++n_trace;
         cl_load_layer(p, s, layer, row0, nrows);
+        load_registers(layer);
       }
     }
+    if (t == 0) CQP_STAMP(p.dbg, i, 7);
     if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
       converged = true;
       break;
@@ -446,7 +607,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   if (iters_done >= 1 && have != iters_done)
     mbar_wait_cluster(&xready[bf], ((iters_done - 1) >> 1) & 1, p.dbg, 3, iters_done);
   double nrm[7];
-  const double* xfinal = s.xs + (size_t)bf * p.Dpad;
+  const double* xfinal = s.xs + (size_t)bf * XS;
   cl_residual_pass(p, s, xfinal, true, pass++, rank, C, nrm);
   // between-launch invariant: p.vq slot 0 = iterate (slots 1..3 keep the grid kernel's sentinel)
   for (int r = t; r < nrows; r += kClThreads) p.vq[row0 + r] = xfinal[row0 + r];
@@ -475,9 +636,9 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
 }
 
-template <int RPW>
+template <int RPW, int NPT>
 int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr) {
-  auto fn = cluster_kernel<RPW>;
+  auto fn = cluster_kernel<RPW, NPT>;
   CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
   if (h->G > 8) CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cfg = cudaLaunchConfig_t{};
@@ -494,28 +655,41 @@ int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribu
   return CQP_OK;
 }
 
-template <int RPW>
-int cluster_launch_rpw(cqp_handle* h, const RunParams& p) {
+enum class ClOp { Launch, Fits };
+
+// Launch, or ask whether the device schedules one cluster of h->G CTAs with h->smem_bytes each.
+template <int RPW, int NPT>
+int cluster_do(ClOp op, cqp_handle* h, const RunParams* p) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
-  int rc = cluster_launch_cfg<RPW>(h, cfg, attr);
+  int rc = cluster_launch_cfg<RPW, NPT>(h, cfg, attr);
+  if (op == ClOp::Fits) {
+    int clusters = 0;
+    if (rc != CQP_OK || cudaOccupancyMaxActiveClusters(&clusters, cluster_kernel<RPW, NPT>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return clusters >= 1;
+  }
   if (rc) return rc;
-  CQP_CUDA(cudaLaunchKernelEx(&cfg, cluster_kernel<RPW>, p));
+  CQP_CUDA(cudaLaunchKernelEx(&cfg, cluster_kernel<RPW, NPT>, *p));
   return CQP_OK;
 }
 
-// Does the device schedule one cluster of h->G CTAs with h->smem_bytes each?
-template <int RPW>
-bool cluster_fits(cqp_handle* h) {
-  cudaLaunchConfig_t cfg;
-  cudaLaunchAttribute attr[1];
-  if (cluster_launch_cfg<RPW>(h, cfg, attr) != CQP_OK) { cudaGetLastError(); return false; }
-  int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, cluster_kernel<RPW>, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
+int cluster_dispatch(ClOp op, cqp_handle* h, const RunParams* p) {
+  switch (h->npt) {
+    case 4: return cluster_do<1, 4>(op, h, p);
+    case 8: return cluster_do<1, 8>(op, h, p);
+    case 12: return cluster_do<1, 12>(op, h, p);
+    case 16: return cluster_do<1, 16>(op, h, p);
+    default: break;
   }
-  return clusters >= 1;
+  switch (h->rpw) {
+    case 1: return cluster_do<1, 0>(op, h, p);
+    case 2: return cluster_do<2, 0>(op, h, p);
+    case 3: return cluster_do<3, 0>(op, h, p);
+    default: return cluster_do<4, 0>(op, h, p);
+  }
 }
 
 }  // namespace
@@ -524,30 +698,49 @@ int configure_cluster(cqp_handle* h) {
   h->cluster = 0;
   const int D = h->D;
   if (D < 32) return CQP_OK;  // the balanced row split needs D >= C; tiny problems use the grid kernel
-  const char* only = std::getenv("CQP_CLUSTER_SIZE");  // test hook: pin the cluster size (16 or 8)
+  const char* only = std::getenv("CQP_CLUSTER_SIZE");  // test hooks: pin the cluster size (16 or 8),
+  const char* mode = std::getenv("CQP_CLUSTER_MODE");  // "smem" forbids the register mode
+  const bool allow_reg = !(mode && mode[0] == 's');
   for (int C : {16, 8}) {
     if (only && std::atoi(only) != C) continue;
     const int R = (D + C - 1) / C;
-    const int rpw = (R + kClWarps - 1) / kClWarps;
-    if (rpw > kClMaxRpw) continue;
-    const size_t need = cl_smem_doubles(R, h->Dpad, h->npad, h->mpad) * sizeof(double);
-    if (need > (size_t)kMaxSmemBytes) continue;
-    h->R = R; h->G = C; h->rpw = rpw; h->smem_bytes = (int)need; h->w_smem = 1; h->rb = 0;
-    const bool ok = rpw == 1 ? cluster_fits<1>(h) : rpw == 2 ? cluster_fits<2>(h) : rpw == 3 ? cluster_fits<3>(h) : cluster_fits<4>(h);
-    if (!ok) continue;
-    h->cluster = 1;
-    return CQP_OK;
+    const int pern = (h->n + C - 1) / C, perm = (h->m + C - 1) / C;
+    // register mode: 2 rows per warp (R <= 32), 16 lanes per row, NPT = ceil(nc2 / 16) <= 16 pairs per lane
+    const int np = ((h->Dpad >> 1) + 15) / 16;
+    for (int reg = allow_reg ? 1 : 0; reg >= 0; --reg) {
+      int npt = 0, rpw = 0, xs_stride = h->Dpad;
+      if (reg) {
+        if (R > 2 * kClWarps || np > 16) continue;
+        npt = (np + 3) / 4 * 4;
+        xs_stride = 32 * npt;
+      } else {
+        rpw = (R + kClWarps - 1) / kClWarps;
+        if (rpw > kClMaxRpw) continue;
+      }
+      const int wrows = reg ? 0 : R;
+      size_t need = cl_smem_doubles(R, wrows, h->Dpad, xs_stride, h->npad, h->mpad, pern, perm) * sizeof(double);
+      int hg = 1;
+      if (need > (size_t)kMaxSmemBytes) {  // no room to cache the residual rows: read them through L2
+        hg = 0;
+        need = cl_smem_doubles(R, wrows, h->Dpad, xs_stride, h->npad, h->mpad, 0, 0) * sizeof(double);
+      }
+      if (need > (size_t)kMaxSmemBytes) continue;
+      h->R = R; h->G = C; h->rpw = rpw; h->npt = npt; h->xs_stride = xs_stride; h->hg_smem = hg;
+      h->smem_bytes = (int)need; h->w_smem = reg ? 0 : 1; h->rb = 0;
+      if (!cluster_dispatch(ClOp::Fits, h, nullptr)) continue;
+      h->cluster = 1;
+      return CQP_OK;
+    }
   }
   return CQP_OK;
 }
 
-int launch_cluster(cqp_handle* h, const RunParams& p) {
-  switch (h->rpw) {
-    case 1: return cluster_launch_rpw<1>(h, p);
-    case 2: return cluster_launch_rpw<2>(h, p);
-    case 3: return cluster_launch_rpw<3>(h, p);
-    default: return cluster_launch_rpw<4>(h, p);
-  }
+int launch_cluster(cqp_handle* h, const RunParams& p0) {
+  RunParams p = p0;
+  p.w_smem = h->w_smem;
+  p.xs_stride = h->xs_stride;
+  p.hg_smem = h->hg_smem;
+  return cluster_dispatch(ClOp::Launch, h, &p);
 }
 
 }  // namespace cqp

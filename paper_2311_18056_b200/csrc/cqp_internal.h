@@ -51,7 +51,10 @@ struct RunParams {
   int L;
   int R;        // rows of W owned by one CTA
   int G;        // CTAs
-  int w_smem;   // 1: W slice resident in shared memory; 0: streamed from global (L2/HBM)
+  int w_smem;   // 1: W slice resident in shared memory; 0: streamed from global (L2/HBM) [grid kernel]
+                //    / kept in registers [cluster kernel, register mode]
+  int xs_stride;  // cluster kernel: doubles between the two shared-memory copies of the iterate
+  int hg_smem;    // cluster kernel: the CTA's rows of H, G', G are cached in shared memory
   const double* W;    // [L][D][Dpad] row-major
   const double* Dk;   // [L][n+m][npad]  rows 0..n: D_k, rows n..n+m: G D_k (bias operator)
   const double* H;    // [n][npad]   unscaled
@@ -124,7 +127,9 @@ struct cqp_handle {
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)
-  int rpw = 0;      // cluster kernel: rows of W per warp
+  int rpw = 0;      // cluster kernel, shared-memory mode: rows of W per warp
+  int npt = 0;      // cluster kernel, register mode: column pairs of W per lane (0: shared-memory mode)
+  int xs_stride = 0, hg_smem = 0;
 };
 
 namespace cqp {

@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
   bool converged = false;
   int iters_done = 0;
+  int until_check = p.check_interval;
   const int nc2 = p.Dpad >> 1;
   constexpr int shift = 5 - Log2<RB>::v;
   for (int i = 1; i <= p.total_iters; ++i) {
@@ -502,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 3);
     }
     iters_done = i;
-    if (i % p.check_interval != 0) continue;
+    if (--until_check != 0) continue;  // (a countdown: no integer division in the loop)
+    until_check = p.check_interval;
 
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     double nr[7];

@@ -71,7 +71,7 @@ elif stage.startswith("trace"):
     w = (C.c_int * 256)()
     s._L.cqp_debug_words(s._h, w)
     ll = np.frombuffer(bytes(w), dtype=np.int64)[32:]
-    names = {0: "c:start", 1: "c:x ready", 3: "c:fma done", 2: "c:dots done", 10: "c15:x ready", 11: "c15:done", 4: "p:start", 5: "p:partials ready", 6: "p:published", 7: "p:done", 8: "l:go seen", 9: "l:fetched"}
+    names = {0: "c:start", 1: "c:x ready", 3: "c:fma done", 2: "c:dots done", 10: "c15:x ready", 11: "c15:done", 4: "p:start|check begin", 5: "p:partials ready|pass done", 6: "p:published", 7: "p:done|check end", 8: "l:go seen", 9: "l:fetched"}
     t00 = ll[0]
     for it in range(4):
         row = ll[it * 16:(it + 1) * 16]
