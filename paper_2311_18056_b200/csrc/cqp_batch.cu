@@ -89,8 +89,12 @@ constexpr int gemm_smem_bytes() {
 // C[col][row] = epilogue(A[a_index] (BM x K) . B(cols) (K x BN)) for every (slot tile, sub-tile,
 // m-tile) work item; persistent CTAs stride over the items.  WM x WN warps, warp tile
 // (BM/WM) x (BN/WN) made of 8x8 DMMA tiles.  Operand tiles are [rows][16] doubles whose
-// 16-byte chunks are XOR-swizzled with (row & 7): the 8-byte fragment loads of a warp (8 rows x
-// 4 consecutive k) then hit 32 distinct banks per half-warp.
+// 16-byte chunks are XOR-swizzled with 2 (row & 3): the 8-byte fragment loads of a half-warp (4
+// rows x 4 consecutive k = 2 chunks per row) then hit 8 distinct chunks = all 32 banks (ncu:
+// shared-memory load bank conflicts 42 % of wavefronts with the (row & 7) swizzle, 0.4 % with this
+// one).  Scheduling is static striding on purpose: a dynamic work counter with a split tail was
+// measured 7 % SLOWER (the 3-4 CTAs of an SM share its tensor pipe, so CTA-level quantisation
+// is already smoothed at SM level, and half-size tail items re-read A).
 template <int BM, int BN, int WM, int WN, int MINB>
 __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const GemmParams p) {
   constexpr int T = WM * WN * 32;
@@ -120,34 +124,69 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
     if (tid < BN) cols_s[tid] = p.cols[slot0 + tid];
     __syncthreads();
 
+    // per-thread copy plan, invariant over k: chunk ch = tid + i T -> tile row r = ch >> 3, 16-byte
+    // chunk c = ch & 7 of the row's 16 doubles (hoisted out of the k loop: the column lookup and
+    // the address arithmetic were 8 % of the issue slots)
+    constexpr int ACH = (BM * 8 + T - 1) / T, BCH = (BN * 8 + T - 1) / T;
+    const double* asrc[ACH];
+    int adst[ACH];
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
+      asrc[i] = A + (size_t)r * p.lda + c * 2;
+      adst[i] = r * BK + ((c ^ ((r & 3) << 1)) << 1);
+    }
+    const double* bsrc[BCH];
+    int bdst[BCH], bbytes[BCH];
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
+      const int col = (ch < BN * 8) ? cols_s[r] : -1;
+      bsrc[i] = p.Bm + (size_t)(col < 0 ? 0 : col) * p.ldb + c * 2;
+      bdst[i] = r * BK + ((c ^ ((r & 3) << 1)) << 1);
+      bbytes[i] = col < 0 ? 0 : 16;
+    }
     auto issue = [&](int kt, int stage) {
       const int k0 = kt * BK;
       double* as = As + stage * BM * BK;
       double* bs = Bs + stage * BN * BK;
 #pragma unroll
-      for (int ch = tid; ch < BM * 8; ch += T) {
-        const int r = ch >> 3, c = ch & 7;
-        cp_async16(as + r * BK + ((c ^ (r & 7)) << 1), A + (size_t)r * p.lda + k0 + c * 2, 16);
-      }
+      for (int i = 0; i < ACH; ++i)
+        if ((BM * 8) % T == 0 || tid + i * T < BM * 8) cp_async16(as + adst[i], asrc[i] + k0, 16);
 #pragma unroll
-      for (int ch = tid; ch < BN * 8; ch += T) {
-        const int r = ch >> 3, c = ch & 7;
-        const int col = cols_s[r];
-        const double* src = p.Bm + (size_t)(col < 0 ? 0 : col) * p.ldb + k0 + c * 2;
-        cp_async16(bs + r * BK + ((c ^ (r & 7)) << 1), src, col < 0 ? 0 : 16);
-      }
+      for (int i = 0; i < BCH; ++i)
+        if ((BN * 8) % T == 0 || tid + i * T < BN * 8) cp_async16(bs + bdst[i], bsrc[i] + k0, bbytes[i]);
     };
-
-    double acc[MI][NI][2];
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s < p.k_tiles) issue(s, s);
       cp_async_commit();
+    }
+    // Accumulators start from the bias (mode 1: v = bias + W s; alpha is 1 there), so its global
+    // loads overlap the pipeline fill instead of serialising the epilogue.  The clamp bounds of
+    // this thread's elements are prefetched into L1 for the same reason (they are read-only for
+    // the whole solve; only rows of the z block have any).
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = cols_s[warp_n * TN + ni * 8 + 2 * t4 + j];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+          const int row = m0 + warp_m * TM + mi * 8 + g;
+          double init = 0.0;
+          if (p.mode == 1 && col >= 0 && row < p.nm) {
+            init = p.bias[(size_t)col * p.ld_bias + row];
+            if (row >= p.n && g == 0) {  // one prefetch per 64-byte run of 8 rows
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lo + (size_t)col * p.ld_lohi + row - p.n));
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.hi + (size_t)col * p.ld_lohi + row - p.n));
+            }
+          }
+          acc[mi][ni][j] = init;
+        }
+      }
     }
     for (int kt = 0; kt < p.k_tiles; ++kt) {
       cp_async_wait<STAGES - 2>();
@@ -160,7 +199,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         const int e = ks * 4 + t4;
-        const int off = (((e >> 1) ^ g) << 1) | (e & 1);  // rows are 8-aligned + g, so r & 7 == g
+        const int off = (((e >> 1) ^ ((g & 3) << 1)) << 1) | (e & 1);  // rows are 8-aligned + g, so r & 7 == g
         double a[MI], b[NI];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) a[mi] = as[(mi * 8 + g) * BK + off];
@@ -186,9 +225,9 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
         for (int mi = 0; mi < MI; ++mi) {
           const int row = m0 + warp_m * TM + mi * 8 + g;
           if (row >= p.M) continue;
-          double v = p.alpha * acc[mi][ni][j];
+          double v = acc[mi][ni][j];
+          if (p.mode != 1) v *= p.alpha;
           if (p.mode == 1 && row < p.nm) {
-            v += p.bias[(size_t)col * p.ld_bias + row];
             if (row >= p.n) {
               const double lo = p.lo[(size_t)col * p.ld_lohi + row - p.n];
               const double hi = p.hi[(size_t)col * p.ld_lohi + row - p.n];
