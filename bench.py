@@ -21,6 +21,8 @@ collective; only a small result summary is gathered).
            reference: -O3 -DNDEBUG, no -march) on a bounded sample of the same instances
   single_qp = configs[1]: single-QP solve time (p50 us) per size through cqp_solve, next to the
            CPU oracle, with the achieved shared-memory streaming rate 8 D^2 bytes / iteration
+  mpc_steps = configs[0], [2], [3]: receding-horizon control step (fused cqp_mpc_step) wall/kernel
+           p50 and the W streaming rate next to the HBM peak
 """
 from __future__ import annotations
 
@@ -179,7 +181,7 @@ def single_qp_sweep(S, problems, repeats: int = 7):
     kernel-only and through-the-API wall time, next to the CPU oracle on the same inputs."""
     from oracle import oracle as O
     out = []
-    for nu in (10, 30, 50):
+    for nu in (10, 18, 30, 50):
         wl = problems.config2(nu, seed=0)
         base = wl.base_problem()
         q = wl.problem_at(wl.x0(10.0))
@@ -207,6 +209,43 @@ def single_qp_sweep(S, problems, repeats: int = 7):
                     "gpu_kernel_us_p50": k50, "gpu_wall_us_p50": w50, "cpu_us_p50": c50,
                     "speedup_wall": c50 / w50, "us_per_iteration": k50 / it,
                     "smem_stream_GBs": 8.0 * D * D * it / (k50 * 1e-6) / 1e9, "launch": gs.launch_info()})
+        gs.close()
+    return out
+
+
+def mpc_step_section(S, problems, peaks):
+    """configs[0], [2], [3]: receding-horizon step {instantiate (host), update_vectors, refresh_z,
+    fixed_iters(k)} (bench.cpp:157-185) through the fused cqp_mpc_step: host wall p50 per step
+    (upload + one launch + download), kernel p50, and the W streaming rate 8 D^2 k / kernel time
+    next to the HBM peak (the robot-sized W levels, 54 and 133 MB, are L2/HBM streamed)."""
+    out = []
+    for name, make, k in (("config1 nu=10 N=10", lambda: problems.config1(seed=0), 1),
+                          ("atlas-sized nx=58 nu=29 N=30", lambda: problems.config3_atlas(30, seed=0), 2),
+                          ("quadruped-sized nx=52 nu=32 N=30", lambda: problems.config4_quadruped(30, seed=0), 15)):
+        wl = make()
+        base = wl.base_problem()
+        gs = S.Solver(base.H, base.g, base.G, base.c, base.d)
+        x = wl.x0(1.0)
+        q = wl.problem_at(x)
+        gs.update_vectors(q.g, q.c, q.d); gs.cold_start()
+        r0 = gs.solve()                                   # initial solve to tolerance (PAPER.md:790)
+        A, B, K, nu = wl.sys.A, wl.sys.B, wl.tmpl.K, wl.sys.nu
+        wall, ker = [], []
+        for t in range(120):
+            q = wl.problem_at(x)
+            t1 = time.perf_counter()
+            rep = gs.mpc_step(q.g, q.c, q.d, k)
+            wall.append((time.perf_counter() - t1) * 1e6); ker.append(rep.kernel_us)
+            u = np.clip(-K @ x + rep.solution.y[:nu], wl.limits.u_lo, wl.limits.u_hi)
+            x = A @ x + B @ u
+        D = base.n + 2 * base.m
+        w50, k50 = statistics.median(wall[20:]), statistics.median(ker[20:])
+        out.append({"workload": name, "n": base.n, "m": base.m, "D": D, "iters_per_step": k,
+                    "initial_solve_iterations": r0.solution.iterations, "initial_solve_kernel_us": r0.kernel_us,
+                    "step_wall_us_p50": w50, "step_kernel_us_p50": k50, "step_hz": 1e6 / w50,
+                    "W_stream_GBs": 8.0 * D * D * k / (k50 * 1e-6) / 1e9,
+                    "W_stream_frac_of_hbm_peak": 8.0 * D * D * k / (k50 * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                    "launch": gs.launch_info()})
         gs.close()
     return out
 
@@ -289,6 +328,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     parity_ok = bool(np.array_equal(np.array(cpu_iters), out["iterations"][:sample]))
 
     single_qp = single_qp_sweep(S, problems) if world == 1 and not args.no_single else None
+    mpc_steps = mpc_step_section(S, problems, peaks) if world == 1 and not args.no_single else None
 
     line = {
         "metric": METRIC, "value": value, "unit": "QP/s", "n_gpus": world, "steps": args.steps,
@@ -315,6 +355,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     }
     if single_qp is not None:
         line["single_qp"] = single_qp
+    if mpc_steps is not None:
+        line["mpc_steps"] = mpc_steps
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -243,6 +243,7 @@ int cqp_create_from_layers(cqp_handle** out, int n, int m, int L, const double* 
   }
   if ((rc = upload_small(h, grid_values, E, F))) return fail(rc);
   if ((rc = upload_vectors(h, g, c, d))) return fail(rc);
+  if ((rc = prepare_streaming(h))) return fail(rc);
   if ((rc = cold_start(h))) return fail(rc);
   CQP_CUDA(cudaStreamSynchronize(h->stream));
   cudaFree(scratch);
@@ -254,7 +255,7 @@ void cqp_destroy(cqp_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  cudaFree(h->W); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
+  cudaFree(h->W); cudaFree(h->Wt); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
   cudaFree(h->Gs); cudaFree(h->E); cudaFree(h->F); cudaFree(h->dgrid); cudaFree(h->dlog_grid);
   cudaFree(h->g); cudaFree(h->vq); cudaFree(h->state); cudaFree(h->barrier);
   cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp); cudaFree(h->dres);

@@ -43,10 +43,13 @@ __device__ __forceinline__ void progress(int* d, int role, int value) {
 // Optional timeline trace (-DCQP_TRACE): clock64() stamps of CTA 0's roles for iterations
 // 100..103, 16 slots per iteration, into the host-mapped debug record (as long long, from word 64).
 #ifdef CQP_TRACE
+#ifndef CQP_TRACE_AT
+#define CQP_TRACE_AT 100
+#endif
 #define CQP_STAMP(dbg, it, slot)                                                        \
   do {                                                                                  \
-    if (blockIdx.x == 0 && (it) >= 100 && (it) < 104)                                   \
-      reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-100) * 16 + (slot)] = clock64(); \
+    if (blockIdx.x == 0 && (it) >= CQP_TRACE_AT && (it) < CQP_TRACE_AT + 4)                                   \
+      reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-CQP_TRACE_AT) * 16 + (slot)] = clock64(); \
   } while (0)
 #else
 #define CQP_STAMP(dbg, it, slot) do {} while (0)

@@ -19,6 +19,10 @@ constexpr int kComputeWarps = kComputeThreads / 32;
 constexpr int kLoaderWarps = 3;         // the only warps that poll L2 for the iterate
 constexpr int kLoaderThreads = kLoaderWarps * 32;
 constexpr int kThreads = kComputeThreads + 32 + kLoaderThreads;  // + 1 publisher warp + loaders
+// W streaming ring of the L2/HBM tier: a stage holds 16 rows x 128 column pairs (32 KB)
+constexpr int kStageRows = 16, kStagePairs = 128;
+constexpr int kStageDoubles = kStageRows * kStagePairs * 2;
+constexpr int kMaxStages = 6;
 constexpr int kWarps = kThreads / 32;
 
 inline int pad2(int x) { return (x + 1) & ~1; }
@@ -53,9 +57,14 @@ struct RunParams {
   int G;        // CTAs
   int w_smem;   // 1: W slice resident in shared memory; 0: streamed from global (L2/HBM) [grid kernel]
                 //    / kept in registers [cluster kernel, register mode]
+  int wdoubles;       // grid kernel: shared-memory doubles reserved for W (resident slice or ring)
+  int stream_stages;  // grid kernel, w_smem == 0: stages of the cp.async.bulk ring (0: plain global loads)
   int xs_stride;  // cluster kernel: doubles between the two shared-memory copies of the iterate
   int hg_smem;    // cluster kernel: the CTA's rows of H, G', G are cached in shared memory
   const double* W;    // [L][D][Dpad] row-major
+  const double* Wt;   // same data re-tiled for the L2/HBM tier's streamer (null: stream row segments):
+                      // per CTA slice, per 16-row super-block, per 128-pair chunk: [nv rows][cw pairs]
+                      // contiguous, so one cp.async.bulk moves a whole ring stage
   const double* Dk;   // [L][n+m][npad]  rows 0..n: D_k, rows n..n+m: G D_k (bias operator)
   const double* H;    // [n][npad]   unscaled
   const double* Gr;   // [m][npad]   unscaled G, row-major
@@ -104,6 +113,7 @@ struct cqp_handle {
   std::vector<double> grid, E_host, F_host;
   // device memory
   double *W = nullptr, *Dk = nullptr;  // Dk: [L][n+m][npad] = [D_k; G D_k]
+  double* Wt = nullptr;                // tier 1 only: W re-tiled for contiguous streaming (built lazily)
   double *H = nullptr, *Gr = nullptr, *Gt = nullptr, *Gs = nullptr;
   double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;
   double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
@@ -126,6 +136,8 @@ struct cqp_handle {
   int* dbg_dev = nullptr;
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
+  int stream_stages = 0;  // tier 1: stages of the W streaming ring that fit the shared memory
+  int wdoubles = 0;       // shared-memory doubles reserved for W (resident slice or ring)
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)
   int rpw = 0;      // cluster kernel, shared-memory mode: rows of W per warp
   int npt = 0;      // cluster kernel, register mode: column pairs of W per lane (0: shared-memory mode)
@@ -137,6 +149,7 @@ namespace cqp {
 // cqp_single.cu
 int configure_launch(cqp_handle* h);
 int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh);
+int prepare_streaming(cqp_handle* h);  // L2/HBM tier: re-tile the ladder for contiguous streaming
 // cqp_cluster.cu : single thread-block cluster kernel for small problems (DSMEM exchange)
 int configure_cluster(cqp_handle* h);  // sets h->cluster = 1 and the launch shape when it fits
 int launch_cluster(cqp_handle* h, const RunParams& p);

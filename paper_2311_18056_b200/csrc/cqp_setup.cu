@@ -463,6 +463,7 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   }
   TRY(upload_small(h, grid.data(), E.data(), F.data()));
   TRY(upload_vectors(h, g, c, d));
+  TRY(prepare_streaming(h));
   TRY(cold_start(h));
   TRYCUDA(cudaStreamSynchronize(st));
   *out = h;

@@ -29,6 +29,7 @@
 //     behind one grid barrier), and every CTA takes the identical rho decision; a switch
 //     reloads the W slice and recomputes the bias rows b = -[D_k; G D_k] g_s it owns.
 //   * Nothing is launched per iteration; the host sees one launch and one result download.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
@@ -42,20 +43,22 @@ namespace {
 
 // Loader warps: fetch the whole iterate (nc2 column pairs) from ring slot `q` into shared memory
 // `xs`.  All loads of a batch are in flight together; only entries still holding the sentinel are
-// re-polled.  `lt` is the thread's index among the kLoaderThreads loader threads.
-__device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int nc2, int lt, int* dbg, int iter) {
-  constexpr int U = 8;
+// re-polled.  `lt` is the thread's index among the `nfetch` fetching threads (the loader warps; in the
+// L2/HBM tier also the compute warps, which would otherwise idle through the exchange).
+template <int U>
+__device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int nc2, int lt, int nfetch, int* dbg,
+                                              int iter) {
   double2* xs2 = reinterpret_cast<double2*>(xs);
-  for (int base = lt; base < nc2; base += kLoaderThreads * U) {
+  for (int base = lt; base < nc2; base += nfetch * U) {
     double2 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int c2 = base + u * kLoaderThreads;
+      const int c2 = base + u * nfetch;
       if (c2 < nc2) v[u] = load_pair(q + 2 * c2);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int c2 = base + u * kLoaderThreads;
+      const int c2 = base + u * nfetch;
       if (c2 < nc2) {
         long long t0 = 0;
         unsigned spins = 0;
@@ -168,7 +171,7 @@ __device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, i
 }
 
 struct Smem {
-  double* sW;    // R * Dpad   (tier 0 only)
+  double* sW;    // R * Dpad resident slice (tier 0) / streaming ring (tier 1); p.wdoubles doubles
   double* xs;    // 2 * Dpad   iterate (cache space), double buffered by iteration parity
   double* uy;    // npad       unscaled y   (also scratch for g_s)
   double* uz;    // mpad       unscaled z
@@ -179,17 +182,19 @@ struct Smem {
   double* slo;   // Rp
   double* shi;   // Rp
   double* sval;  // 128 + Rp scratch
-  unsigned long long* bars;  // full[2], xready[2], go
+  unsigned long long* bars;  // full[2], xready[2], go, (pad), wfull[kMaxStages], wempty[kMaxStages]
 };
 
 __host__ __device__ inline int round_up(int x, int q) { return (x + q - 1) / q * q; }
 
+// `wdoubles`: doubles reserved at the front for W: the resident slice R * Dpad (tier 0) or the
+// streaming ring stages * kStageDoubles (tier 1).
 __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad, int mpad,
-                                               int w_smem) {
+                                               size_t wdoubles) {
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
-  return (size_t)(w_smem ? (size_t)R * Dpad : 0) + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad +
-         kWarps * 16 + 2 * (size_t)kComputeWarps * Rcap + 4 * (size_t)Rp + 128 + 8;
+  return wdoubles + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
+         2 * (size_t)kComputeWarps * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
 }
 
 template <int RB>
@@ -199,7 +204,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   const int Rp = (p.R + 1) & ~1;
   const int Rcap = round_up(p.R, RB);
   s.sW = base;
-  s.xs = base + (p.w_smem ? (size_t)p.R * p.Dpad : 0);
+  s.xs = base + p.wdoubles;
   s.uy = s.xs + 2 * p.Dpad;
   s.uz = s.uy + p.npad;
   s.ul = s.uz + p.mpad;
@@ -209,7 +214,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
-  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128 + Rp);
+  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128 + Rp);  // 8 + 2 kMaxStages words
   return s;
 }
 
@@ -354,7 +359,9 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
 
 // All-SM grid, iterate exchanged through the L2 ring (cooperative launch).  Small problems whose
 // ladder level fits one thread-block cluster's shared memory use cqp_cluster.cu instead.
-template <int RB>
+// STREAM selects the L2/HBM tier's code (W through the cp.async.bulk ring) at compile time, so the
+// shared-memory-resident tier keeps its registers.
+template <int RB, bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
@@ -362,16 +369,29 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // warp roles: [0,16) compute, 16 publisher, [17,21) loaders
   const bool compute = warp < kComputeWarps;
   const bool publisher = warp == kComputeWarps;
-  const int lt = t - (kComputeThreads + 32);  // loader thread index (>= 0 for loader warps)
+  const int lt = t - (kComputeThreads + 32);  // loader thread index (in [0, kLoaderThreads) for loader warps)
+  const bool loader = lt >= 0 && lt < kLoaderThreads;
   unsigned long long* full = s.bars;        // [2] compute -> publisher: partials of iteration i
   unsigned long long* xready = s.bars + 2;  // [2] loaders -> compute: v_i is in xs[i&1]
   unsigned long long* go = s.bars + 4;      //     publisher -> loaders: v_i rows published
+  unsigned long long* wfull = s.bars + 8;                 // [NS] streamer -> compute: stage holds a W chunk
+  unsigned long long* wempty = s.bars + 8 + kMaxStages;   // [NS] compute -> streamer: stage consumed
+  // L2/HBM tier: W_k is streamed through a shared-memory ring by the publisher warp with
+  // cp.async.bulk (mbarrier complete_tx), kStageRows rows x kStagePairs column pairs per stage; the
+  // ring runs ahead of the compute warps, also across iterations (W does not depend on v).
+  const int NS = STREAM ? p.stream_stages : 1;  // (1: keeps the dead % NS of the other tier well defined)
+  constexpr bool streaming = STREAM;
   if (t == 0) {
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
-    mbar_init(&xready[0], kLoaderWarps);
-    mbar_init(&xready[1], kLoaderWarps);
+    mbar_init(&xready[0], kLoaderWarps + (STREAM ? kComputeWarps : 0));
+    mbar_init(&xready[1], kLoaderWarps + (STREAM ? kComputeWarps : 0));
     mbar_init(go, 1);
+    for (int k = 0; k < (STREAM ? NS : 0); ++k) {
+      mbar_init(&wfull[k], 1);
+      mbar_init(&wempty[k], kComputeWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
   }
   const int n = p.n, m = p.m, D = p.D;
   const int row0 = blockIdx.x * p.R;
@@ -433,6 +453,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   int until_check = p.check_interval;
   const int nc2 = p.Dpad >> 1;
   constexpr int shift = 5 - Log2<RB>::v;
+  unsigned wcnt = 0;  // chunks of the W stream consumed (compute) / issued (streamer) so far
+  const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
+  const int nfetch = streaming ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
   for (int i = 1; i <= p.total_iters; ++i) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
     const int b = i & 1;
@@ -445,6 +468,38 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 10);
       const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
       const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
+      if (streaming) {
+        // thread (pc = t & 127, rq = t >> 7): column pair pc of the chunk, rows 4 rq .. 4 rq + 3 of
+        // the 16-row super-block; the 4 warps that share rq leave 4 partials per row
+        const int pc = t & (kStagePairs - 1), rq = t >> 7;
+        for (int rb0 = 0; rb0 < nrows; rb0 += kStageRows) {
+          const int nv = min(kStageRows, nrows - rb0);
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
+            const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
+            mbar_wait(&wfull[stage], (int)ph, p.dbg, 7, i);
+            const double2* st = reinterpret_cast<const double2*>(s.sW) + (size_t)stage * (kStageDoubles / 2);
+            const int c2 = c0 + pc;
+            const int cw = p.Wt ? min(kStagePairs, nc2 - c0) : kStagePairs;  // stage row stride (pairs)
+            if (c2 < nc2) {
+              const double2 xv = x2[c2];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                if (4 * rq + j < nv) {
+                  const double2 w = st[(4 * rq + j) * cw + pc];
+                  acc[j] = fma(w.x, xv.x, acc[j]);
+                  acc[j] = fma(w.y, xv.y, acc[j]);
+                }
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wempty[stage]);
+          }
+          const double total = warp_butterfly<4>(acc, lane);  // lane 8 j holds row 4 rq + j
+          const int row = rb0 + 4 * rq + (lane >> 3);
+          if ((lane & 7) == 0 && row < nrows) part[(warp & 3) * Rcap + row] = total;
+        }
+      } else
       for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
         const int nv = min(RB, nrows - rb0);
         double acc[RB];
@@ -461,8 +516,52 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 11);
       if (lane == 0) mbar_arrive(&full[b]);
       if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
+      if (streaming) {
+        // L2/HBM tier: large iterate, idle compute warps: they fetch v_i together with the loaders
+        // (xs[b] held v_{i-2}, which every warp finished reading before any warp entered iteration i)
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, t, nfetch, p.dbg, i);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xready[b]);
+      }
     } else if (publisher) {
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 1); CQP_STAMP(p.dbg, i, 4); }
+      // L2/HBM tier: this warp is also the W streamer.  It issues the chunks of iteration i (paced
+      // by the compute warps through wempty), publishes v_i, and then starts on iteration i + 1
+      // at once, so the first NS chunks of the next iteration load during the iterate exchange.
+      if (streaming) {
+        for (int rb0 = 0; rb0 < nrows; rb0 += kStageRows) {
+          const int nv = min(kStageRows, nrows - rb0);
+          for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
+            const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
+            mbar_wait(&wempty[stage], (int)(ph ^ 1u), p.dbg, 8, i);  // (a fresh barrier passes at once)
+            const unsigned bytes = 16u * (unsigned)min(kStagePairs, nc2 - c0);
+            if (lane == 0) {
+              asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(
+                               smem_u32(&wfull[stage])),
+                           "r"(bytes * (unsigned)nv)
+                           : "memory");
+            }
+            __syncwarp();
+            if (p.Wt) {  // re-tiled W: the whole stage is one contiguous block
+              if (lane == 0) {
+                const double* src = p.Wt + (size_t)layer * D * p.Dpad + 2 * ((size_t)(row0 + rb0) * nc2 + (size_t)nv * c0);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(s.sW + (size_t)stage * kStageDoubles)),
+                    "l"(src), "r"(bytes * (unsigned)nv), "r"(smem_u32(&wfull[stage]))
+                    : "memory");
+              }
+            } else if (lane < nv) {
+              const double* src = p.W + ((size_t)layer * D + row0 + rb0 + lane) * p.Dpad + 2 * (size_t)c0;
+              const unsigned dst = smem_u32(s.sW + (size_t)stage * kStageDoubles + (size_t)lane * (2 * kStagePairs));
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                  "l"(src), "r"(bytes), "r"(smem_u32(&wfull[stage]))
+                  : "memory");
+            }
+          }
+        }
+      }
       mbar_wait(&full[b], par, p.dbg, 2, i);
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
@@ -470,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       for (int r = lane; r < nrows; r += 32) {
         double x = 0.0;
 #pragma unroll
-        for (int w = 0; w < kComputeWarps; ++w) x += part[w * Rcap + r];
+        for (int w = 0; w < npart; ++w) x += part[w * Rcap + r];
         x += s.sb[r];
         const double lo = s.slo[r], hi = s.shi[r];
         x = x < lo ? lo : x;
@@ -492,11 +591,15 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
       if (p.fence_mode == 0) __threadfence();
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 3); CQP_STAMP(p.dbg, i, 7); }
-    } else {
+    } else if (loader) {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
-      fetch_iterate(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, p.dbg, i);
+      if (streaming)
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, kComputeThreads + lt, nfetch,
+                         p.dbg, i);
+      else
+        fetch_iterate<8>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, nfetch, p.dbg, i);
       __syncwarp();
       if (lt == 0) CQP_STAMP(p.dbg, i, 9);
       if (lane == 0) mbar_arrive(&xready[b]);
@@ -654,14 +757,35 @@ __global__ void warm_scale_kernel(const double* __restrict__ y, const double* __
 
 __global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
 
-template <int RB>
-int launch_run_rb(cqp_handle* h, RunParams& p) {
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+// Row-major W_k ([D][Dpad]) -> the streaming layout of the L2/HBM tier (RunParams::Wt): inside the
+// R-row slice of every CTA, every 16-row super-block (nv valid rows) stores its 128-pair column
+// chunks one after the other, each as [nv][cw] pairs.  One thread per (row, column pair).
+__global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int D, int nc2, int R) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)D * nc2) return;
+  const int row = (int)(idx / nc2), c2 = (int)(idx - (size_t)row * nc2);
+  const int b = row / R, lr = row - b * R;
+  const int nrows = min(R, D - b * R);
+  const int sb = lr / kStageRows, r = lr - sb * kStageRows;
+  const int nv = min(kStageRows, nrows - sb * kStageRows);
+  const int c = c2 / kStagePairs, pc = c2 - c * kStagePairs;
+  const int cw = min(kStagePairs, nc2 - c * kStagePairs);
+  dst[(size_t)(b * R + sb * kStageRows) * nc2 + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = src[idx];
+}
+
+template <int RB, bool STREAM>
+int launch_run_rb2(cqp_handle* h, RunParams& p) {
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->smem_bytes));
   void* args[] = {&p};
-  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB>, dim3(h->G), dim3(kThreads),
+  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, STREAM>, dim3(h->G), dim3(kThreads),
                                        args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
+}
+
+template <int RB>
+int launch_run_rb(cqp_handle* h, RunParams& p) {
+  return (!p.w_smem && p.stream_stages > 0) ? launch_run_rb2<RB, true>(h, p) : launch_run_rb2<RB, false>(h, p);
 }
 
 }  // namespace
@@ -683,15 +807,43 @@ int configure_launch(cqp_handle* h) {
   h->R = R;
   h->G = G;
   h->rb = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
-  size_t need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 1) * sizeof(double);
+  h->wdoubles = R * h->Dpad;
+  h->stream_stages = 0;
+  size_t need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, (size_t)h->wdoubles) * sizeof(double);
   h->w_smem = need <= (size_t)kMaxSmemBytes ? 1 : 0;
   if (force_tier && force_tier[0] == '1') h->w_smem = 0;  // test hook: stream W from L2/HBM
-  if (!h->w_smem) need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
-  if (need > (size_t)kMaxSmemBytes) {
-    set_error("problem too large for the persistent kernel's shared-memory vectors");
-    return CQP_ERR_CAPACITY;
+  if (!h->w_smem) {
+    // L2/HBM tier: give the rest of the shared memory to the W streaming ring
+    const size_t base = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
+    if (base > (size_t)kMaxSmemBytes) {
+      set_error("problem too large for the persistent kernel's shared-memory vectors");
+      return CQP_ERR_CAPACITY;
+    }
+    int stages = (int)(((size_t)kMaxSmemBytes - base) / (kStageDoubles * sizeof(double)));
+    if (stages > kMaxStages) stages = kMaxStages;
+    if (stages < 2) stages = 0;  // no room: plain global loads
+    if (const char* e = std::getenv("CQP_STREAM_STAGES")) stages = std::min(stages, std::atoi(e));  // A/B knob
+    h->stream_stages = stages;
+    h->wdoubles = stages * kStageDoubles;
+    need = base + (size_t)h->wdoubles * sizeof(double);
   }
   h->smem_bytes = (int)need;
+  return CQP_OK;
+}
+
+// L2/HBM tier: build the streaming copy of the ladder (RunParams::Wt).  Called once W is complete
+// (end of handle creation); launch_run re-checks so that a handle never streams a stale copy.
+int prepare_streaming(cqp_handle* h) {
+  if (h->cluster || h->w_smem || h->stream_stages <= 0 || h->Wt || std::getenv("CQP_NO_RETILE")) return CQP_OK;
+  const size_t per = (size_t)h->D * h->Dpad;
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Wt), sizeof(double) * per * h->L));
+  const size_t pairs = per / 2;
+  for (int k = 0; k < h->L; ++k) {
+    retile_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, h->stream>>>(
+        reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per * k), h->D,
+        h->Dpad >> 1, h->R);
+    CQP_CUDA(cudaGetLastError());
+  }
   return CQP_OK;
 }
 
@@ -727,8 +879,19 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   h->launch_parity ^= 1;
   p.dbg = h->dbg_dev;
   if (h->cluster) return launch_cluster(h, p);
-  // few iterations: copying the W slice into shared memory costs as much as streaming it once
-  if (total_iters < 4) p.w_smem = 0;
+  int rc_stream = prepare_streaming(h);  // (no-op unless the ladder was replaced)
+  if (rc_stream) return rc_stream;
+  p.Wt = (!h->w_smem) ? h->Wt : nullptr;
+  p.wdoubles = h->wdoubles;
+  p.stream_stages = h->stream_stages;
+  // few iterations: copying the W slice into shared memory costs as much as streaming it once;
+  // the ring then lives in the (unused) slice region
+  if (total_iters < 4 && p.w_smem) {
+    p.w_smem = 0;
+    int stages = h->wdoubles / kStageDoubles;
+    if (stages > kMaxStages) stages = kMaxStages;
+    p.stream_stages = stages >= 2 ? stages : 0;
+  }
   switch (h->rb) {
     case 4: return launch_run_rb<4>(h, p);
     case 8: return launch_run_rb<8>(h, p);

@@ -340,8 +340,8 @@ def test_closed_loop_protocol_matches_oracle(G, oracle, P, k):
 
 # ---- tiers ---------------------------------------------------------------------------------------
 def test_all_kernel_modes_agree(G, oracle, P, monkeypatch):
-    """tier 0 (all-SM grid, W in shared memory) and tier 1 (W streamed from L2/HBM) run the same
-    arithmetic in the same order: bit for bit.  Tier 2 (one thread-block cluster, DSMEM exchange;
+    """tier 0 (all-SM grid, W in shared memory), tier 1 (W streamed from L2/HBM through a
+    cp.async.bulk ring) and tier 2 (one thread-block cluster, DSMEM exchange;
     the default for small problems) sums each row in a different order: same counts, traces and
     history indices, values within rounding."""
     wl = P.config2(14, seed=2)
@@ -369,11 +369,14 @@ def test_all_kernel_modes_agree(G, oracle, P, monkeypatch):
     monkeypatch.delenv("CQP_CLUSTER_SIZE", raising=False)
     a, b, c, c8 = reports
     assert c8.solution.iterations == c.solution.iterations and rel_err(c8.solution.y, c.solution.y) <= 1e-9
-    assert np.array_equal(a.solution.y, b.solution.y) and a.residual_history == b.residual_history
+    # tier 1 streams W through a shared-memory ring: each row is summed as 4 partials instead of 16
+    assert b.solution.iterations == a.solution.iterations and b.solution.rho_trace == a.solution.rho_trace
+    assert rel_err(b.solution.y, a.solution.y) <= 1e-9 and rel_err(b.solution.lam, a.solution.lam) <= 1e-9
     assert c.solution.iterations == a.solution.iterations and c.solution.rho_trace == a.solution.rho_trace
     assert [(h[0], h[3]) for h in c.residual_history] == [(h[0], h[3]) for h in a.residual_history]
     assert rel_err(c.solution.y, a.solution.y) <= 1e-9 and rel_err(c.solution.lam, a.solution.lam) <= 1e-9
     os_.update_vectors(q.g, q.c, q.d); os_.cold_start()
     ro = os_.solve()
     assert_report_parity(a, ro)
+    assert_report_parity(b, ro)
     assert_report_parity(c, ro)

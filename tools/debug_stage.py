@@ -61,10 +61,15 @@ elif stage.startswith("watch"):
     os._exit(0)
 elif stage.startswith("trace"):
     import ctypes as C
-    nu = int(stage[5:])
-    wl = problems.config2(nu, 0); base = wl.base_problem()
+    if stage[5:] == "quad":
+        wl = problems.config4_quadruped(30, 0)
+    elif stage[5:] == "atlas":
+        wl = problems.config3_atlas(30, 0)
+    else:
+        wl = problems.config2(int(stage[5:]), 0)
+    base = wl.base_problem()
     s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
-    q = wl.problem_at(wl.x0(10.0)); s.update_vectors(q.g, q.c, q.d)
+    q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
     print(s.launch_info())
     for _ in range(2):
         s.cold_start(); r = s.fixed_iters(1000)
