@@ -496,10 +496,11 @@ struct cqp_batch {
   int ld_s = 0, ld_n = 0, ld_m = 0, ld_nm = 0;
   int Dm_pad = 0, nm_mpad = 0, n_mpad = 0, m_mpad = 0;
   int grid_ctas[4] = {0, 0, 0, 0};  // persistent grid per tile configuration
-  // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/):
-  // 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size (less wave quantisation, 12
-  // warps/SM), 64x32 wins below ~3400 columns, 32x32 for the last few dozen columns.
-  int thr_big = 1 << 30, thr_mid = 3400, thr_small = 96;
+  // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
+  // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
+  // (less wave quantisation, 12 warps/SM), 64x32 wins below ~3400 columns, 32x32 (6 CTAs/SM: more
+  // warps to keep the tensor pipe fed when the grid no longer fills) below ~1000.
+  int thr_big = 1 << 30, thr_mid = 3400, thr_small = 1000;
   int force_cfg = -1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;

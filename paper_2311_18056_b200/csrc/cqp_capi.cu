@@ -33,13 +33,15 @@ size_t result_bytes(int n, int m, int cap) {
 
 int ensure_result_capacity(cqp_handle* h, int cap) {
   if (cap <= h->res_cap) return CQP_OK;
-  if (h->dres) cudaFree(h->dres);
+  // The result record lives in host-mapped pinned memory: the kernel writes it straight over PCIe
+  // (posted writes, a few KB), so a solve needs no device->host copy after the launch.
+  if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->hres) cudaFreeHost(h->hres);
   h->dres = h->hres = nullptr;
   h->res_cap = cap;
   h->res_bytes = result_bytes(h->n, h->m, cap);
-  CQP_CUDA(cudaMalloc(&h->dres, h->res_bytes));
-  CQP_CUDA(cudaMallocHost(&h->hres, h->res_bytes));
+  CQP_CUDA(cudaHostAlloc(&h->hres, h->res_bytes, cudaHostAllocMapped));
+  CQP_CUDA(cudaHostGetDevicePointer(&h->dres, h->hres, 0));
   return CQP_OK;
 }
 
@@ -258,7 +260,7 @@ void cqp_destroy(cqp_handle* h) {
   cudaFree(h->W); cudaFree(h->Wt); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
   cudaFree(h->Gs); cudaFree(h->E); cudaFree(h->F); cudaFree(h->dgrid); cudaFree(h->dlog_grid);
   cudaFree(h->g); cudaFree(h->vq); cudaFree(h->state); cudaFree(h->barrier);
-  cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp); cudaFree(h->dres);
+  cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp);  // (dres aliases the mapped hres)
   if (h->hres) cudaFreeHost(h->hres);
   if (h->hstage) cudaFreeHost(h->hstage);
   if (h->dbg_host) cudaFreeHost(h->dbg_host);
@@ -312,7 +314,6 @@ static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh
   CQP_CUDA(cudaEventRecord(h->ev0, h->stream));
   if ((rc = launch_run(h, early_exit, total, refresh))) return rc;
   CQP_CUDA(cudaEventRecord(h->ev1, h->stream));
-  CQP_CUDA(cudaMemcpyAsync(h->hres, h->dres, h->res_bytes, cudaMemcpyDeviceToHost, h->stream));
   {
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {

@@ -125,8 +125,8 @@ struct cqp_handle {
   double* rho_vec = nullptr;  // [L][m]
   double* dtmp = nullptr;     // Dpad scratch (warm start staging)
   // result buffer (device) and its pinned host mirror
-  void* dres = nullptr;
-  void* hres = nullptr;
+  void* dres = nullptr;  // device alias of hres
+  void* hres = nullptr;  // host-mapped pinned result record, written by the kernel
   size_t res_bytes = 0;
   int res_cap = 0;
   // pinned staging for update_vectors: [g; c; d]

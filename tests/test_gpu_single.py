@@ -150,6 +150,31 @@ def test_dense_qp_parity_with_device_offline_stage(G, oracle, n, seeds):
         assert_report_parity(gs.solve(), os_.solve(), res_rel=0.5, res_abs=1e-7)
 
 
+def test_cluster_kernel_layouts(G, oracle, P):
+    """The cluster tier picks its layout from D: register mode with NPT = 4/8/12/16 column pairs per
+    lane (D <= 512), shared-memory mode with 1-4 rows per warp above, residual rows cached in shared
+    memory or read through L2 when they do not fit.  One parity solve per layout, odd D included."""
+    cases = [("dense", 35), ("dense", 90), ("dense", 130), ("dense", 200), ("mpc", 21)]
+    for kind, size in cases:
+        if kind == "dense":
+            p = oracle.gen_random_dense_qp(size, 7)
+            q = p
+        else:
+            wl = P.config2(size, seed=1)
+            p = wl.base_problem()
+            q = wl.problem_at(wl.x0(3.0))
+        gs, os_ = make_pair(oracle, G, p, from_layers=True)
+        assert gs.launch_info()["tier"] == 2, (kind, size, gs.launch_info())
+        for s in (gs, os_):
+            s.update_vectors(q.g, q.c, q.d)
+            s.cold_start()
+        assert_report_parity(gs.solve(), os_.solve())
+        # fixed_iters composes bit for bit in this tier too (tests/test_solver.cpp:211-233)
+        gs.cold_start(); gs.fixed_iters(7); va = gs.state
+        gs.cold_start(); gs.fixed_iters(3); gs.fixed_iters(4)
+        assert np.array_equal(gs.state, va)
+
+
 # ---- the BASELINE.json MPC configs ---------------------------------------------------------------
 @pytest.mark.parametrize("nu,hard,unstable", [(10, 1.0, False), (10, 10.0, False), (10, 10.0, True),
                                              (30, 1.0, False), (30, 10.0, False), (50, 10.0, False)])

@@ -37,7 +37,14 @@ def launch_summary(name):
             for k, v in sorted(tot.items(), key=lambda kv: -kv[1])]
 
 
-KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+KEYS = ["gpu__time_duration.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
@@ -64,20 +71,21 @@ def full_summary(rep):
 def main():
     os.makedirs(OUT, exist_ok=True)
     summary = {}
-    for name in ("launches_batch.csv", "launches_single.csv"):
+    prefix = sys.argv[2] if len(sys.argv) > 2 else ""      # e.g. "s2_": files of a later session
+    for name in (prefix + "launches_batch.csv", prefix + "launches_single.csv"):
         if os.path.exists(os.path.join(SRC, name)):
             summary[name] = launch_summary(name)[:12]
-    for rep in ("prof_dmma.ncu-rep", "prof_single.ncu-rep"):
-        if os.path.exists(os.path.join(SRC, rep)):
-            summary[rep] = full_summary(rep)
+    for rep in sorted(f for f in os.listdir(SRC) if f.startswith(prefix + "prof_") and f.endswith(".ncu-rep")):
+        summary[rep] = full_summary(rep)
     json.dump(summary, open(os.path.join(OUT, f"{TAG}_ncu_summary.json"), "w"), indent=1)
     # per-launch DRAM traffic of the dominant batched kernel, for bench.py's roofline.traffic
-    if "prof_dmma.ncu-rep" in summary and summary["prof_dmma.ncu-rep"]:
+    dm = prefix + "prof_dmma.ncu-rep"
+    if dm in summary and summary[dm]:
         def to_bytes(s):
             v, unit = s.split()[0].replace(",", ""), s.split()[1] if len(s.split()) > 1 else "byte"
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             return float(v) * mult
-        recs = summary["prof_dmma.ncu-rep"]
+        recs = summary[dm]
         traffic = sum(to_bytes(r["dram__bytes_read.sum"]) + to_bytes(r["dram__bytes_write.sum"]) for r in recs) / len(recs)
         json.dump({"dram_bytes_per_launch": traffic, "captures": len(recs), "source": f"{TAG}_ncu_summary.json"},
                   open(os.path.join(OUT, "dmma_gemm_traffic.json"), "w"), indent=1)
