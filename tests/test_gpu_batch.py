@@ -89,3 +89,27 @@ def test_batch_max_iters_and_capacity(G, oracle, P):
         assert rel_err(out["y"][:, j], s.y) <= 1e-6
     with pytest.raises(MemoryError):
         batch.solve(np.zeros((base.n, 65)), np.zeros((base.m, 65)), np.ones((base.m, 65)))
+
+
+def test_persistent_round_kernel_is_bit_identical(G, P, monkeypatch):
+    """CQP_BATCH_PERSISTENT=1 (opt-in): one cooperative launch per check round, strips of columns
+    owned by CTA teams.  Same tile arithmetic per output element as the launch-per-iteration
+    path, so every output must agree bit for bit -- with enough columns (>= 576) for the teams to
+    be used, heterogeneous iteration counts and rho switches."""
+    wl = P.config2(10, seed=5)
+    base = wl.base_problem()
+    B = 1500
+    g, c, d, _ = P.batch_instances(wl, B, lo=0.3, hi=10.0)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CQP_BATCH_PERSISTENT", flag)
+        single = G.Solver(base.H, base.g, base.G, base.c, base.d)
+        batch = G.BatchSolver(single, capacity=B)
+        outs.append(batch.solve(g, c, d))
+        batch.close(); single.close()
+    monkeypatch.delenv("CQP_BATCH_PERSISTENT", raising=False)
+    a, b = outs
+    assert b["launches"] < a["launches"]                      # the round kernel really ran
+    assert len(set(a["iterations"].tolist())) > 3 and a["n_switches"].max() >= 1
+    for key in ("iterations", "status", "final_index", "n_switches", "y", "z", "lam", "r_prim", "r_dual"):
+        assert np.array_equal(a[key], b[key]), key
