@@ -214,9 +214,10 @@ def single_qp_sweep(S, problems, repeats: int = 7):
 
 
 def mpc_step_section(S, problems, peaks):
-    """configs[0], [2], [3]: receding-horizon step {instantiate (host), update_vectors, refresh_z,
-    fixed_iters(k)} (bench.cpp:157-185) through the fused cqp_mpc_step: host wall p50 per step
-    (upload + one launch + download), kernel p50, and the W streaming rate 8 D^2 k / kernel time
+    """configs[0], [2], [3]: receding-horizon step {instantiate, update_vectors, refresh_z,
+    fixed_iters(k), control extraction} (bench.cpp:157-185) through cqp_mpc_step_x0 (template on the
+    device: upload x0, one launch, download u0): host wall p50 per step through the Python wrapper
+    and through the C ABI alone, kernel p50, and the W streaming rate 8 D^2 k / kernel time
     next to the HBM peak (the robot-sized W levels, 54 and 133 MB, are L2/HBM streamed)."""
     out = []
     for name, make, k in (("config1 nu=10 N=10", lambda: problems.config1(seed=0), 1),
@@ -230,12 +231,22 @@ def mpc_step_section(S, problems, peaks):
         gs.update_vectors(q.g, q.c, q.d); gs.cold_start()
         r0 = gs.solve()                                   # initial solve to tolerance
         A, B, K, nu = wl.sys.A, wl.sys.B, wl.tmpl.K, wl.sys.nu
-        wall, ker = [], []
+        # (a) template on the device: a step uploads x0 and downloads u0 (cqp_mpc_step_x0)
+        gs.set_mpc_template(wl.tmpl, wl.limits)
+        wall, ker, cabi = [], [], []
         for t in range(120):
+            t1 = time.perf_counter()
+            u, rep = gs.mpc_step_x0(x, k)
+            wall.append((time.perf_counter() - t1) * 1e6); ker.append(rep.kernel_us); cabi.append(rep.wall_ms * 1e3)
+            x = A @ x + B @ u
+        # (b) host-side instantiate (untimed), step uploads g, c, d (cqp_mpc_step)
+        x = wl.x0(1.0)
+        wall_gcd = []
+        for t in range(60):
             q = wl.problem_at(x)
             t1 = time.perf_counter()
             rep = gs.mpc_step(q.g, q.c, q.d, k)
-            wall.append((time.perf_counter() - t1) * 1e6); ker.append(rep.kernel_us)
+            wall_gcd.append((time.perf_counter() - t1) * 1e6)
             u = np.clip(-K @ x + rep.solution.y[:nu], wl.limits.u_lo, wl.limits.u_hi)
             x = A @ x + B @ u
         D = base.n + 2 * base.m
@@ -243,6 +254,8 @@ def mpc_step_section(S, problems, peaks):
         out.append({"workload": name, "n": base.n, "m": base.m, "D": D, "iters_per_step": k,
                     "initial_solve_iterations": r0.solution.iterations, "initial_solve_kernel_us": r0.kernel_us,
                     "step_wall_us_p50": w50, "step_kernel_us_p50": k50, "step_hz": 1e6 / w50,
+                    "step_cabi_wall_us_p50": statistics.median(cabi[20:]),
+                    "step_wall_us_p50_host_instantiate": statistics.median(wall_gcd[10:]),
                     "W_stream_GBs": 8.0 * D * D * k / (k50 * 1e-6) / 1e9,
                     "W_stream_frac_of_hbm_peak": 8.0 * D * D * k / (k50 * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6650.0),
                     "launch": gs.launch_info()})

@@ -154,6 +154,22 @@ CQP_API int cqp_fixed_iters(cqp_handle *h, int k, cqp_result *out);
 CQP_API int cqp_mpc_step(cqp_handle *h, const double *g, const double *c, const double *d,
                          int k, cqp_result *out);
 
+/* Condensed-MPC template on the device: mpc::instantiate (mpc.cpp:260-270) and the control
+ * extraction of the closed loop (bench.cpp:169-175) move behind the boundary, so that a control
+ * step uploads x0 (nx doubles) instead of g, c, d (n + 2m doubles) and downloads u0.
+ * offset_g: n x nx, offset_c: m x nx, K: nu x nx (column-major, CondensedTemplate fields,
+ * mpc.hpp); c_base, d_base: m; u_lo, u_hi: nu (BoxLimits).  nu <= n. */
+CQP_API int cqp_mpc_set_template(cqp_handle *h, int nx, int nu, const double *offset_g,
+                                 const double *offset_c, const double *c_base,
+                                 const double *d_base, const double *K, const double *u_lo,
+                                 const double *u_hi);
+
+/* One receding-horizon control step from the measured state (bench.cpp:157-175):
+ *   p = instantiate(tmpl, x0); update_vectors(p.g, p.c, p.d); refresh_z(); fixed_iters(k);
+ *   u0 = clamp(-K x0 + y[0:nu], u_lo, u_hi)
+ * all on the device.  u0 (nu) and out may be NULL. */
+CQP_API int cqp_mpc_step_x0(cqp_handle *h, const double *x0, int k, double *u0, cqp_result *out);
+
 /* Solver::state() / layer_index(), solver.hpp:126-127: v (n+2m, cache space) and the index. */
 CQP_API int cqp_get_state(cqp_handle *h, double *v, int *layer_index);
 

@@ -1,5 +1,6 @@
 // C ABI of libcqp_b200.so (include/cqp_b200.h): handle management, uploads, result download.
 // Mirrors the reference's Solver lifecycle (/root/reference/proj/src/solver.cpp:180-218).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -28,7 +29,7 @@ int dev_alloc(T** p, size_t count) {
 
 size_t result_bytes(int n, int m, int cap) {
   return sizeof(DevResultHead) + sizeof(int) * 4 * (size_t)cap + sizeof(double) * 2 * (size_t)cap +
-         sizeof(double) * ((size_t)n + 2 * (size_t)m);
+         sizeof(double) * ((size_t)n + 2 * (size_t)m) + sizeof(double) * (size_t)n /* u0, nu <= n */;
 }
 
 int ensure_result_capacity(cqp_handle* h, int cap) {
@@ -150,6 +151,7 @@ int upload_vectors(cqp_handle* h, const double* g, const double* c, const double
   std::memcpy(h->hstage + n + m, d, sizeof(double) * m);
   h->c_host.assign(c, c + m);
   h->d_host.assign(d, d + m);
+  h->vectors_device_only = false;
   CQP_CUDA(cudaMemcpyAsync(h->g, h->hstage, sizeof(double) * ((size_t)n + 2 * (size_t)m),
                            cudaMemcpyHostToDevice, h->stream));
   return CQP_OK;
@@ -263,6 +265,9 @@ void cqp_destroy(cqp_handle* h) {
   cudaFree(h->partial); cudaFree(h->rho_vec); cudaFree(h->dtmp);  // (dres aliases the mapped hres)
   if (h->hres) cudaFreeHost(h->hres);
   if (h->hstage) cudaFreeHost(h->hstage);
+  if (h->hx0) cudaFreeHost(h->hx0);
+  cudaFree(h->mpc_og); cudaFree(h->mpc_oc); cudaFree(h->mpc_cb); cudaFree(h->mpc_db);
+  cudaFree(h->mpc_K); cudaFree(h->mpc_ulo); cudaFree(h->mpc_uhi); cudaFree(h->mpc_x0);
   if (h->dbg_host) cudaFreeHost(h->dbg_host);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -308,7 +313,8 @@ int cqp_refresh_z(cqp_handle* h) {
 }
 
 static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh, cqp_result* out,
-                         std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now()) {
+                         std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(),
+                         double* u0 = nullptr) {
   int rc = ensure_result_capacity(h, total / h->s.check_interval + 2);
   if (rc) return rc;
   CQP_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -334,7 +340,8 @@ static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh
   const double* hist_r = reinterpret_cast<const double*>(base + off); off += sizeof(double) * 2 * (size_t)cap;
   const double* y = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->n;
   const double* z = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->m;
-  const double* lam = reinterpret_cast<const double*>(base + off);
+  const double* lam = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  if (u0) std::memcpy(u0, base + off, sizeof(double) * (size_t)h->mpc_nu);
   if (out) {
     out->status = head->status;
     out->iterations = head->iterations;
@@ -384,6 +391,66 @@ int cqp_mpc_step(cqp_handle* h, const double* g, const double* c, const double* 
   int rc = upload_vectors(h, g, c, d);
   if (rc) return rc;
   return run_and_fetch(h, false, k, true, out, t0);
+}
+
+int cqp_mpc_set_template(cqp_handle* h, int nx, int nu, const double* offset_g, const double* offset_c,
+                         const double* c_base, const double* d_base, const double* K, const double* u_lo,
+                         const double* u_hi) {
+  if (!h || !offset_g || !offset_c || !c_base || !d_base || !K || !u_lo || !u_hi) {
+    set_error("mpc_set_template: null argument");
+    return CQP_ERR_ARGUMENT;
+  }
+  if (nx < 1 || nu < 1 || nu > h->n) { set_error("mpc_set_template: bad dimensions"); return CQP_ERR_DIMENSION; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));
+  const int n = h->n, m = h->m;
+  cudaFree(h->mpc_og); cudaFree(h->mpc_oc); cudaFree(h->mpc_cb); cudaFree(h->mpc_db);
+  cudaFree(h->mpc_K); cudaFree(h->mpc_ulo); cudaFree(h->mpc_uhi); cudaFree(h->mpc_x0);
+  if (h->hx0) cudaFreeHost(h->hx0);
+  h->mpc_og = h->mpc_oc = h->mpc_cb = h->mpc_db = h->mpc_K = h->mpc_ulo = h->mpc_uhi = h->mpc_x0 = h->hx0 = nullptr;
+  h->mpc_nx = nx; h->mpc_nu = nu; h->mpc_nxpad = pad2(nx);
+  int rc;
+  if ((rc = dev_alloc(&h->mpc_og, (size_t)n * h->mpc_nxpad))) return rc;
+  if ((rc = dev_alloc(&h->mpc_oc, (size_t)m * h->mpc_nxpad))) return rc;
+  if ((rc = dev_alloc(&h->mpc_cb, (size_t)m))) return rc;
+  if ((rc = dev_alloc(&h->mpc_db, (size_t)m))) return rc;
+  if ((rc = dev_alloc(&h->mpc_K, (size_t)nu * h->mpc_nxpad))) return rc;
+  if ((rc = dev_alloc(&h->mpc_ulo, (size_t)nu))) return rc;
+  if ((rc = dev_alloc(&h->mpc_uhi, (size_t)nu))) return rc;
+  if ((rc = dev_alloc(&h->mpc_x0, (size_t)nx))) return rc;
+  CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->hx0), sizeof(double) * nx));
+  double* scratch = nullptr;
+  const size_t big = (size_t)std::max(std::max(n, m), nu) * nx;
+  if ((rc = dev_alloc(&scratch, big))) return rc;
+  auto done = [&](int code) { cudaStreamSynchronize(h->stream); cudaFree(scratch); return code; };
+  if ((rc = upload_transposed(h, offset_g, n, nx, h->mpc_og, h->mpc_nxpad, scratch))) return done(rc);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+  if ((rc = upload_transposed(h, offset_c, m, nx, h->mpc_oc, h->mpc_nxpad, scratch))) return done(rc);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return done(CQP_ERR_CUDA);
+  if ((rc = upload_transposed(h, K, nu, nx, h->mpc_K, h->mpc_nxpad, scratch))) return done(rc);
+  if (cudaMemcpyAsync(h->mpc_cb, c_base, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+      cudaMemcpyAsync(h->mpc_db, d_base, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+      cudaMemcpyAsync(h->mpc_ulo, u_lo, sizeof(double) * nu, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+      cudaMemcpyAsync(h->mpc_uhi, u_hi, sizeof(double) * nu, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    return done(cuda_fail(cudaGetLastError(), "mpc_set_template upload"));
+  return done(CQP_OK);
+}
+
+int cqp_mpc_step_x0(cqp_handle* h, const double* x0, int k, double* u0, cqp_result* out) {
+  if (!h || !x0) { set_error("mpc_step_x0: null argument"); return CQP_ERR_ARGUMENT; }
+  if (!h->mpc_og) { set_error("mpc_step_x0: no template (call cqp_mpc_set_template first)"); return CQP_ERR_ARGUMENT; }
+  if (k < 1) { set_error("mpc_step_x0: k must be >= 1"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  std::memcpy(h->hx0, x0, sizeof(double) * h->mpc_nx);
+  CQP_CUDA(cudaMemcpyAsync(h->mpc_x0, h->hx0, sizeof(double) * h->mpc_nx, cudaMemcpyHostToDevice, h->stream));
+  int rc = launch_instantiate(h);
+  if (rc) return rc;
+  h->vectors_device_only = true;
+  h->mpc_extract = true;
+  rc = run_and_fetch(h, false, k, true, out, t0, u0);
+  h->mpc_extract = false;
+  return rc;
 }
 
 int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
@@ -442,6 +509,13 @@ int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, dou
                     int* initial_index, double* c_tilde, double* d_tilde) {
   if (!h) return CQP_ERR_ARGUMENT;
   const int n = h->n, m = h->m;
+  if (h->vectors_device_only && (c_tilde || d_tilde)) {  // c, d came from the device-side instantiate
+    CQP_CUDA(cudaSetDevice(h->device));
+    h->c_host.resize(m); h->d_host.resize(m);
+    CQP_CUDA(cudaMemcpyAsync(h->c_host.data(), h->c, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
+    CQP_CUDA(cudaMemcpyAsync(h->d_host.data(), h->d, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
+    CQP_CUDA(cudaStreamSynchronize(h->stream));
+  }
   if (E) std::memcpy(E, h->E_host.data(), sizeof(double) * n);
   if (F) std::memcpy(F, h->F_host.data(), sizeof(double) * m);
   if (cost_scale) *cost_scale = h->cost_scale;

@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   // between-launch invariant: p.vq slot 0 = iterate (slots 1..3 keep the grid kernel's sentinel)
   for (int r = t; r < nrows; r += kClThreads) p.vq[row0 + r] = xfinal[row0 + r];
   if (rank == 0) {
+    mpc_extract_control(p, s.uy, t);
     if (p.Dpad != D && t == 0) p.vq[D] = 0.0;
     for (int i = t; i < n; i += kClThreads) p.out_y[i] = s.uy[i];
     for (int i = t; i < m; i += kClThreads) {

@@ -153,5 +153,19 @@ __device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L,
 }
 
 
+// Control extraction of the closed loop (bench.cpp:169-175): u0 = clamp(-K x + y[0:nu], u_lo, u_hi).
+// `y` is the unscaled primal solution in shared memory; executed by one CTA (threads t < nu).
+__device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t) {
+  if (!p.mpc_K || t >= p.mpc_nu) return;
+  const double* Krow = p.mpc_K + (size_t)t * p.mpc_nxpad;
+  double kx = 0.0;
+  for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], p.mpc_x0[j], kx);
+  double u = -kx + y[t];
+  const double lo = p.mpc_ulo[t], hi = p.mpc_uhi[t];
+  u = u < lo ? lo : u;
+  u = u > hi ? hi : u;
+  p.out_u[t] = u;
+}
+
 }  // namespace
 }  // namespace cqp

@@ -89,6 +89,13 @@ struct RunParams {
   int do_refresh;     // run Solver::refresh_z before the first iteration
   int fence_mode;     // 0: fence after re-arm (default); 1: none; 2: release-store publish
   int cap;            // capacity of the record arrays
+  // receding-horizon control extraction (null Kt: none): u0 = clamp(-K x0 + y[0:nu], u_lo, u_hi)
+  const double* mpc_K;   // [nu][nxpad] row-major
+  const double* mpc_x0;  // nx
+  const double* mpc_ulo; // nu
+  const double* mpc_uhi; // nu
+  int mpc_nx, mpc_nxpad, mpc_nu;
+  double* out_u;         // nu (in the result record)
   DevResultHead* head;
   int* trace;         // [cap][2]
   int* hist_i;        // [cap][2]  (iteration, grid index)
@@ -132,6 +139,15 @@ struct cqp_handle {
   // pinned staging for update_vectors: [g; c; d]
   double* hstage = nullptr;
   std::vector<double> c_host, d_host;  // current unscaled bounds (for cqp_get_scaling)
+  // condensed-MPC template on the device (cqp_mpc_set_template): instantiate() and the control
+  // extraction of the closed loop run on the device, a step uploads only x0
+  int mpc_nx = 0, mpc_nxpad = 0, mpc_nu = 0;
+  double *mpc_og = nullptr, *mpc_oc = nullptr;   // offset_g [n][nxpad], offset_c [m][nxpad] row-major
+  double *mpc_cb = nullptr, *mpc_db = nullptr;   // c_base, d_base (m)
+  double *mpc_K = nullptr, *mpc_ulo = nullptr, *mpc_uhi = nullptr, *mpc_x0 = nullptr;
+  double* hx0 = nullptr;                          // pinned staging of x0
+  bool vectors_device_only = false;               // c/d were last set by the device-side instantiate
+  bool mpc_extract = false;                       // the next launch also extracts the control
   int* dbg_host = nullptr;  // host-mapped watchdog record (16 ints)
   int* dbg_dev = nullptr;
   // launch configuration
@@ -161,6 +177,7 @@ int launch_transpose_pad(cudaStream_t st, const double* src_colmajor, int rows, 
 int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, int cols, int ld,
                        double* dst_colmajor);
 int launch_bias(cqp_handle* h, int k, double* b_out);  // b_out: device, D doubles
+int launch_instantiate(cqp_handle* h);                  // g, c, d <- template(x0) on the device
 
 // cqp_batch.cu : dense DMMA GEMM with an identity slot map, used by the offline stage
 struct DenseGemm;

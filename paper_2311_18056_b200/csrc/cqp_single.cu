@@ -671,6 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     }
   }
   if (blockIdx.x == 0) {
+    mpc_extract_control(p, s.uy, t);
     for (int i = t; i < n; i += kThreads) p.out_y[i] = s.uy[i];
     for (int i = t; i < m; i += kThreads) {
       p.out_z[i] = s.uz[i];
@@ -756,6 +757,29 @@ __global__ void warm_scale_kernel(const double* __restrict__ y, const double* __
 }
 
 __global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
+
+// mpc::instantiate on the device (mpc.cpp:260-270): g = offset_g x0, shift = offset_c x0,
+// c = c_base - shift, d = d_base - shift.  One warp per row of [offset_g; offset_c].
+__global__ void instantiate_kernel(const double* __restrict__ og, const double* __restrict__ oc,
+                                   const double* __restrict__ cb, const double* __restrict__ db,
+                                   const double* __restrict__ x0, int n, int m, int nx, int nxpad,
+                                   double* __restrict__ g, double* __restrict__ c, double* __restrict__ d) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n + m) return;
+  const double* M = row < n ? og + (size_t)row * nxpad : oc + (size_t)(row - n) * nxpad;
+  double acc = 0.0;
+  for (int j = lane; j < nx; j += 32) acc = fma(M[j], x0[j], acc);
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+  if (lane == 0) {
+    if (row < n) {
+      g[row] = acc;
+    } else {
+      c[row - n] = cb[row - n] - acc;
+      d[row - n] = db[row - n] - acc;
+    }
+  }
+}
 
 // Row-major W_k ([D][Dpad]) -> the streaming layout of the L2/HBM tier (RunParams::Wt): inside the
 // R-row slice of every CTA, every 16-row super-block (nv valid rows) stores its 128-pair column
@@ -869,7 +893,12 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.hist_r = reinterpret_cast<double*>(base + off); off += sizeof(double) * 2 * (size_t)h->res_cap;
   p.out_y = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->n;
   p.out_z = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->m;
-  p.out_lam = reinterpret_cast<double*>(base + off);
+  p.out_lam = reinterpret_cast<double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  p.out_u = reinterpret_cast<double*>(base + off);
+  if (h->mpc_extract) {
+    p.mpc_K = h->mpc_K; p.mpc_x0 = h->mpc_x0; p.mpc_ulo = h->mpc_ulo; p.mpc_uhi = h->mpc_uhi;
+    p.mpc_nx = h->mpc_nx; p.mpc_nxpad = h->mpc_nxpad; p.mpc_nu = h->mpc_nu;
+  }
   p.fence_mode = 0;
   if (const char* fm = std::getenv("CQP_FENCE_MODE")) p.fence_mode = std::atoi(fm);  // experiment knob
   // grid-barrier counters ping-pong between launches: this launch counts on barrier[parity]
@@ -917,6 +946,14 @@ int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int l
   set_state_kernel<<<1, 1, 0, h->stream>>>(h->state, layer_index);
   CQP_CUDA(cudaGetLastError());
   return launch_refresh_z(h);
+}
+
+int launch_instantiate(cqp_handle* h) {
+  const int rows = h->n + h->m, threads = 256, rows_per_block = threads / 32;
+  instantiate_kernel<<<(rows + rows_per_block - 1) / rows_per_block, threads, 0, h->stream>>>(
+      h->mpc_og, h->mpc_oc, h->mpc_cb, h->mpc_db, h->mpc_x0, h->n, h->m, h->mpc_nx, h->mpc_nxpad, h->g, h->c, h->d);
+  CQP_CUDA(cudaGetLastError());
+  return CQP_OK;
 }
 
 int launch_set_state(cqp_handle* h, int layer) {

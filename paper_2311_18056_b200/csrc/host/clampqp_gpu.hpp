@@ -262,8 +262,32 @@ class Solver {
   }
   cqp_handle* native_handle() { return h_; }
 
+  /// Condensed-MPC template on the device (mpc.hpp CondensedTemplate fields + BoxLimits):
+  /// afterwards mpc_step(x0, k, &u0) instantiates the step QP (mpc.cpp:260-270) and extracts the
+  /// control (bench.cpp:169-175) on the device; a step uploads x0 and downloads u0.
+  void set_mpc_template(const Mat& offset_g, const Mat& offset_c, const Vec& c_base, const Vec& d_base,
+                        const Mat& K, const Vec& u_lo, const Vec& u_hi) {
+    const Index nx = offset_g.cols(), nu = K.rows();
+    if (offset_g.rows() != problem_.num_vars() || offset_c.rows() != problem_.num_constraints() ||
+        offset_c.cols() != nx || K.cols() != nx || c_base.size() != problem_.num_constraints() ||
+        d_base.size() != c_base.size() || u_lo.size() != nu || u_hi.size() != nu) {
+      throw std::invalid_argument("set_mpc_template: dimension mismatch");
+    }
+    detail::check(cqp_mpc_set_template(h_, static_cast<int>(nx), static_cast<int>(nu), offset_g.data(),
+                                       offset_c.data(), c_base.data(), d_base.data(), K.data(), u_lo.data(),
+                                       u_hi.data()));
+    mpc_nx_ = nx; mpc_nu_ = nu;
+  }
+  SolveReport mpc_step(const Vec& x0, int k, Vec* u0) {
+    if (k < 1) throw std::invalid_argument("mpc_step: k must be >= 1");
+    if (mpc_nx_ == 0 || x0.size() != mpc_nx_) throw std::invalid_argument("mpc_step: x0 dimension mismatch");
+    if (u0) *u0 = Vec(mpc_nu_);
+    return run(k, nullptr, nullptr, nullptr, x0.data(), u0 ? u0->data() : nullptr);
+  }
+
  private:
-  SolveReport run(int k, const double* g, const double* c, const double* d) {
+  SolveReport run(int k, const double* g, const double* c, const double* d, const double* x0 = nullptr,
+                  double* u0 = nullptr) {
     const Index n = problem_.num_vars(), m = problem_.num_constraints();
     const int total = k > 0 ? k : settings_.max_iters;
     const int cap = total / settings_.check_interval + 2;
@@ -275,7 +299,8 @@ class Solver {
     r.y = rep.solution.y.data(); r.z = rep.solution.z.data(); r.lambda = rep.solution.lambda.data();
     r.rho_trace = trace.data(); r.rho_trace_cap = cap;
     r.history = hist.data(); r.history_cap = cap;
-    if (g) detail::check(cqp_mpc_step(h_, g, c, d, k, &r));
+    if (x0) detail::check(cqp_mpc_step_x0(h_, x0, k, u0, &r));
+    else if (g) detail::check(cqp_mpc_step(h_, g, c, d, k, &r));
     else if (k > 0) detail::check(cqp_fixed_iters(h_, k, &r));
     else detail::check(cqp_solve(h_, &r));
     rep.solution.status = r.status == CQP_SOLVED ? SolveStatus::Solved
@@ -291,6 +316,7 @@ class Solver {
   QProblem problem_;
   SolverSettings settings_;
   cqp_handle* h_ = nullptr;
+  Index mpc_nx_ = 0, mpc_nu_ = 0;
 };
 
 }  // namespace clampqp

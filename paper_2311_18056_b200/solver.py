@@ -238,6 +238,31 @@ class Solver:
         _raise(self._L.cqp_mpc_step(self._h, _p(g), _p(c), _p(d), int(k), C.byref(res)))
         return self._report(res, bufs)
 
+    def set_mpc_template(self, tmpl, limits) -> None:
+        """Hand the condensed-MPC template (mpc.hpp CondensedTemplate: offset_g, offset_c, c_base,
+        d_base, K) and the control limits to the device, so that `mpc_step_x0` can instantiate the
+        step QP (mpc.cpp:260-270) and extract the control (bench.cpp:169-175) there."""
+        f = lambda a: np.asfortranarray(np.asarray(a, dtype=np.float64))  # noqa: E731
+        og, oc, K = f(tmpl.offset_g), f(tmpl.offset_c), f(tmpl.K)
+        nx, nu = og.shape[1], K.shape[0]
+        if og.shape != (self.n, nx) or oc.shape != (self.m, nx) or K.shape != (nu, nx):
+            raise ValueError("set_mpc_template: dimension mismatch")
+        cb, db = _vec(tmpl.c_base, self.m, "set_mpc_template"), _vec(tmpl.d_base, self.m, "set_mpc_template")
+        ulo, uhi = _vec(limits.u_lo, nu, "set_mpc_template"), _vec(limits.u_hi, nu, "set_mpc_template")
+        _raise(self._L.cqp_mpc_set_template(self._h, nx, nu, _p(og), _p(oc), _p(cb), _p(db), _p(K), _p(ulo), _p(uhi)))
+        self._mpc_nx, self._mpc_nu = nx, nu
+
+    def mpc_step_x0(self, x0, k: int):
+        """(u0, report) of one control step from the measured state x0; everything between the
+        upload of x0 and the download of u0 runs on the device."""
+        if k < 1:
+            raise ValueError("mpc_step_x0: k must be >= 1")
+        x0 = _vec(x0, getattr(self, "_mpc_nx", -1), "mpc_step_x0")
+        u0 = np.empty(self._mpc_nu)
+        res, bufs = self._result(k // self.settings.check_interval + 2)
+        _raise(self._L.cqp_mpc_step_x0(self._h, _p(x0), int(k), _p(u0), C.byref(res)))
+        return u0, self._report(res, bufs)
+
     # ---- accessors, solver.hpp:123-127 ----
     @property
     def state(self) -> np.ndarray:

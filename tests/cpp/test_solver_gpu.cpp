@@ -143,6 +143,29 @@ int main() {
       CHECK(ra.solution.iterations == 2 && rb.solution.iterations == 2);
     }
   }
+  // instantiate + control extraction on the device: a 1-D "template" with nx = 2
+  //   g = offset_g x0, c = c_base - offset_c x0, d = d_base - offset_c x0, u0 = clamp(-K x0 + y)
+  {
+    Solver a(box_1d()), b(box_1d());
+    const Mat og{{-1.0, 0.5}}, oc{{0.25, -0.125}}, K{{0.5, 0.25}};
+    const Vec cb{0.0}, db{0.5}, ulo{-0.2}, uhi{0.3};
+    b.set_mpc_template(og, oc, cb, db, K, ulo, uhi);
+    for (int t = 0; t < 5; ++t) {
+      const Vec x0{1.0 + 0.25 * t, -0.5 + 0.125 * t};   // dyadic values: the tiny dots are exact
+      const double shift = 0.25 * x0[0] - 0.125 * x0[1];
+      const Vec g{-1.0 * x0[0] + 0.5 * x0[1]}, c{0.0 - shift}, d{0.5 - shift};
+      a.update_vectors(g, c, d); a.refresh_z();
+      const SolveReport ra = a.fixed_iters(3);
+      Vec u0;
+      const SolveReport rb = b.mpc_step(x0, 3, &u0);
+      CHECK(ra.solution.y[0] == rb.solution.y[0]);
+      CHECK(ra.solution.lambda[0] == rb.solution.lambda[0]);
+      double u = -(0.5 * x0[0] + 0.25 * x0[1]) + ra.solution.y[0];
+      u = u < -0.2 ? -0.2 : (u > 0.3 ? 0.3 : u);
+      CHECK(std::fabs(u0[0] - u) <= 1e-15);
+    }
+    CHECK_THROWS_AS(b.mpc_step(Vec{1.0}, 1, nullptr), std::invalid_argument);
+  }
   if (failures == 0) std::printf("ALL C++ HOST-MIRROR CHECKS PASSED\n");
   return failures == 0 ? 0 : 1;
 }

@@ -62,7 +62,19 @@ def test_robot_sized_parity_with_oracle(G, oracle, P, name, k, hard):
     rg, ro = gpu.solve(), cpu.solve()
     assert ro.solution.status == oracle.SOLVED
     assert_report_parity(rg, ro)
-    closed_loop(wl, gpu, cpu, k, 5, x0)
+    x5 = closed_loop(wl, gpu, cpu, k, 5, x0)
+    # the same loop with instantiate + control extraction on the device (upload x0, download u0)
+    gpu.set_mpc_template(wl.tmpl, wl.limits)
+    A, B, K, nu = wl.sys.A, wl.sys.B, wl.tmpl.K, wl.sys.nu
+    x = x5
+    for _ in range(3):
+        q = wl.problem_at(x)
+        cpu.update_vectors(q.g, q.c, q.d); cpu.refresh_z(); ro = cpu.fixed_iters(k)
+        u_ref = np.clip(-K @ x + ro.solution.y[:nu], wl.limits.u_lo, wl.limits.u_hi)
+        u0, rg = gpu.mpc_step_x0(x, k)
+        assert rel_err(rg.solution.y, ro.solution.y) <= 1e-9 and rel_err(rg.solution.lam, ro.solution.lam) <= 1e-9
+        assert np.abs(u0 - u_ref).max() <= 1e-9 * max(1.0, np.abs(u_ref).max())
+        x = A @ x + B @ u_ref
 
 
 def test_quadruped_full_size_properties(G, P):

@@ -363,6 +363,42 @@ def test_closed_loop_protocol_matches_oracle(G, oracle, P, k):
         x = A @ x + B @ u
 
 
+@pytest.mark.parametrize("k", [1, 15])
+def test_closed_loop_from_x0_on_device(G, oracle, P, k):
+    """cqp_mpc_set_template + cqp_mpc_step_x0: instantiate (mpc.cpp:260-270) and the control
+    extraction (bench.cpp:169-175) on the device; the step uploads x0 and downloads u0.  Against
+    the oracle driven by the host-side instantiate, over a closed loop that hits the limits."""
+    wl = P.config1(seed=3)
+    base = wl.base_problem()
+    gs, os_ = make_pair(oracle, G, base)
+    gs.set_mpc_template(wl.tmpl, wl.limits)
+    x = wl.x0(1.0)
+    A, B, K, nu = wl.sys.A, wl.sys.B, wl.tmpl.K, wl.sys.nu
+    clipped = 0
+    for step in range(25):
+        q = wl.problem_at(x)
+        os_.update_vectors(q.g, q.c, q.d); os_.refresh_z(); ro = os_.fixed_iters(k)
+        u_ref_raw = -K @ x + ro.solution.y[:nu]
+        u_ref = np.clip(u_ref_raw, wl.limits.u_lo, wl.limits.u_hi)
+        clipped += int(np.any(u_ref != u_ref_raw))
+        u0, rg = gs.mpc_step_x0(x, k)
+        assert rg.solution.iterations == k
+        assert rel_err(rg.solution.y, ro.solution.y) <= 1e-9
+        assert rel_err(rg.solution.lam, ro.solution.lam) <= 1e-9
+        assert rel_err(rg.solution.z, ro.solution.z) <= 1e-9
+        assert abs(rg.solution.r_prim - ro.solution.r_prim) <= 1e-9 * max(1.0, ro.solution.r_prim)
+        assert np.abs(u0 - u_ref).max() <= 1e-9 * max(1.0, np.abs(u_ref).max())
+        assert np.all(u0 >= wl.limits.u_lo) and np.all(u0 <= wl.limits.u_hi)
+        x = A @ x + B @ u_ref
+    assert clipped > 0                                   # the clamp in the control law was exercised
+    # the device-side c, d are what the host-side instantiate produces
+    sc = gs.scaling()
+    Fv = os_.cache.F
+    assert np.abs(sc["c_tilde"][base.n:base.n + base.m] - Fv * q.c).max() <= 1e-12 * max(1.0, np.abs(q.c).max())
+    with pytest.raises(ValueError):
+        gs.mpc_step_x0(np.zeros(3), k)
+
+
 # ---- tiers ---------------------------------------------------------------------------------------
 def test_all_kernel_modes_agree(G, oracle, P, monkeypatch):
     """tier 0 (all-SM grid, W in shared memory), tier 1 (W streamed from L2/HBM through a
