@@ -58,6 +58,7 @@ struct RunParams {
   int w_smem;   // 1: W slice resident in shared memory; 0: streamed from global (L2/HBM) [grid kernel]
                 //    / kept in registers [cluster kernel, register mode]
   int wdoubles;       // grid kernel: shared-memory doubles reserved for W (resident slice or ring)
+  int sb_rows;        // grid kernel, streaming: rows per super-block of the W stream (<= kStageRows)
   int stream_stages;  // grid kernel, w_smem == 0: stages of the cp.async.bulk ring (0: plain global loads)
   int xs_stride;  // cluster kernel: doubles between the two shared-memory copies of the iterate
   int hg_smem;    // cluster kernel: the CTA's rows of H, G', G are cached in shared memory

@@ -51,25 +51,35 @@ __device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int n
   double2* xs2 = reinterpret_cast<double2*>(xs);
   for (int base = lt; base < nc2; base += nfetch * U) {
     double2 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c2 = base + u * nfetch;
-      if (c2 < nc2) v[u] = load_pair(q + 2 * c2);
-    }
+    unsigned pending = 0;  // bit u: entry u of this batch is not in shared memory yet
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int c2 = base + u * nfetch;
       if (c2 < nc2) {
-        long long t0 = 0;
-        unsigned spins = 0;
-        while (is_sentinel(v[u].x) || is_sentinel(v[u].y)) {
-          v[u] = load_pair(q + 2 * c2);
-          if ((++spins & 0x3FF) == 0) {
-            if (t0 == 0) t0 = clock64();
-            else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 100 + c2, iter);
-          }
+        v[u] = load_pair(q + 2 * c2);
+        pending |= 1u << u;
+      }
+    }
+    long long t0 = 0;
+    unsigned spins = 0;
+    while (pending) {
+      // one pass over the batch: store what has landed, then re-issue ALL armed entries back to
+      // back, so that a re-poll round costs one L2 round trip, not one per entry
+      unsigned again = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if ((pending >> u) & 1u) {
+          if (is_sentinel(v[u].x) || is_sentinel(v[u].y)) again |= 1u << u;
+          else xs2[base + u * nfetch] = v[u];
         }
-        xs2[c2] = v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((again >> u) & 1u) v[u] = load_pair(q + 2 * (base + u * nfetch));
+      pending = again;
+      if (pending && (++spins & 0x3FF) == 0) {
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 100 + base, iter);
       }
     }
   }
@@ -454,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   const int nc2 = p.Dpad >> 1;
   constexpr int shift = 5 - Log2<RB>::v;
   unsigned wcnt = 0;  // chunks of the W stream consumed (compute) / issued (streamer) so far
+  const int sbr = STREAM ? p.sb_rows : kStageRows;  // rows per super-block of the W stream (<= kStageRows)
   const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
   const int nfetch = streaming ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
   for (int i = 1; i <= p.total_iters; ++i) {
@@ -472,12 +483,18 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         // thread (pc = t & 127, rq = t >> 7): column pair pc of the chunk, rows 4 rq .. 4 rq + 3 of
         // the 16-row super-block; the 4 warps that share rq leave 4 partials per row
         const int pc = t & (kStagePairs - 1), rq = t >> 7;
-        for (int rb0 = 0; rb0 < nrows; rb0 += kStageRows) {
-          const int nv = min(kStageRows, nrows - rb0);
+        for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
+          const int nv = min(sbr, nrows - rb0);
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
           for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
             const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
             mbar_wait(&wfull[stage], (int)ph, p.dbg, 7, i);
+#ifdef CQP_TRACE_CHUNKS
+            if (t == 0 && blockIdx.x == 0 && i == CQP_TRACE_AT) {
+              const int ci = (rb0 / sbr) * ((nc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
+              if (ci < 48) reinterpret_cast<volatile long long*>(p.dbg + 64)[ci] = clock64();
+            }
+#endif
             const double2* st = reinterpret_cast<const double2*>(s.sW) + (size_t)stage * (kStageDoubles / 2);
             const int c2 = c0 + pc;
             const int cw = p.Wt ? min(kStagePairs, nc2 - c0) : kStagePairs;  // stage row stride (pairs)
@@ -518,7 +535,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
       if (streaming) {
         // L2/HBM tier: large iterate, idle compute warps: they fetch v_i together with the loaders
-        // (xs[b] held v_{i-2}, which every warp finished reading before any warp entered iteration i)
+        // (xs[b] held v_{i-2}, which every warp finished reading before any warp entered iteration i).
+        // Like the loaders they start polling only once this CTA has published its own rows: earlier
+        // polls cannot succeed and would compete with the W prefetch for L2 bandwidth.
+        mbar_wait(go, (i - 1) & 1, p.dbg, 9, i);
         fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, t, nfetch, p.dbg, i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xready[b]);
@@ -529,8 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       // by the compute warps through wempty), publishes v_i, and then starts on iteration i + 1
       // at once, so the first NS chunks of the next iteration load during the iterate exchange.
       if (streaming) {
-        for (int rb0 = 0; rb0 < nrows; rb0 += kStageRows) {
-          const int nv = min(kStageRows, nrows - rb0);
+        for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
+          const int nv = min(sbr, nrows - rb0);
           for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
             const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
             mbar_wait(&wempty[stage], (int)(ph ^ 1u), p.dbg, 8, i);  // (a fresh barrier passes at once)
@@ -544,7 +564,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
             __syncwarp();
             if (p.Wt) {  // re-tiled W: the whole stage is one contiguous block
               if (lane == 0) {
-                const double* src = p.Wt + (size_t)layer * D * p.Dpad + 2 * ((size_t)(row0 + rb0) * nc2 + (size_t)nv * c0);
+                // (rows of the re-tiled copy are padded to 8 pairs = 128 B, so every block is 128 B aligned)
+                const int nc2p = (nc2 + 7) & ~7;
+                const double* src = p.Wt + 2 * ((size_t)layer * D * nc2p + (size_t)(row0 + rb0) * nc2p + (size_t)nv * c0);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         smem_u32(s.sW + (size_t)stage * kStageDoubles)),
@@ -782,19 +804,21 @@ __global__ void instantiate_kernel(const double* __restrict__ og, const double* 
 }
 
 // Row-major W_k ([D][Dpad]) -> the streaming layout of the L2/HBM tier (RunParams::Wt): inside the
-// R-row slice of every CTA, every 16-row super-block (nv valid rows) stores its 128-pair column
+// R-row slice of every CTA, every super-block of sbr <= 16 rows (nv valid rows) stores its 128-pair column
 // chunks one after the other, each as [nv][cw] pairs.  One thread per (row, column pair).
-__global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int D, int nc2, int R) {
+__global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int D, int nc2, int R,
+                              int sbr) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)D * nc2) return;
   const int row = (int)(idx / nc2), c2 = (int)(idx - (size_t)row * nc2);
   const int b = row / R, lr = row - b * R;
   const int nrows = min(R, D - b * R);
-  const int sb = lr / kStageRows, r = lr - sb * kStageRows;
-  const int nv = min(kStageRows, nrows - sb * kStageRows);
+  const int sb = lr / sbr, r = lr - sb * sbr;
+  const int nv = min(sbr, nrows - sb * sbr);
   const int c = c2 / kStagePairs, pc = c2 - c * kStagePairs;
   const int cw = min(kStagePairs, nc2 - c * kStagePairs);
-  dst[(size_t)(b * R + sb * kStageRows) * nc2 + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = src[idx];
+  const int nc2p = (nc2 + 7) & ~7;  // slices start on 128-byte boundaries (bulk copies are faster aligned)
+  dst[(size_t)(b * R + sb * sbr) * nc2p + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = src[idx];
 }
 
 template <int RB, bool STREAM>
@@ -855,17 +879,28 @@ int configure_launch(cqp_handle* h) {
   return CQP_OK;
 }
 
+// Rows per super-block of the W stream: the R rows of a CTA are cut into ceil(R / 16) equal parts
+// (R = 18 -> 9 + 9 rather than 16 + 2, so that no ring stage is nearly empty).
+static int stream_sb_rows(int R) {
+  if (const char* e = std::getenv("CQP_SB_BALANCE")) if (e[0] == '0') return kStageRows;  // A/B knob
+  const int nsb = (R + kStageRows - 1) / kStageRows;
+  return (R + nsb - 1) / nsb;
+}
+
 // L2/HBM tier: build the streaming copy of the ladder (RunParams::Wt).  Called once W is complete
 // (end of handle creation); launch_run re-checks so that a handle never streams a stale copy.
 int prepare_streaming(cqp_handle* h) {
   if (h->cluster || h->w_smem || h->stream_stages <= 0 || h->Wt || std::getenv("CQP_NO_RETILE")) return CQP_OK;
   const size_t per = (size_t)h->D * h->Dpad;
-  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Wt), sizeof(double) * per * h->L));
+  const int nc2p = ((h->Dpad >> 1) + 7) & ~7;
+  const size_t per_t = (size_t)h->D * nc2p * 2;  // re-tiled level: rows padded to 128 bytes
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Wt), sizeof(double) * per_t * h->L));
+  CQP_CUDA(cudaMemsetAsync(h->Wt, 0, sizeof(double) * per_t * h->L, h->stream));
   const size_t pairs = per / 2;
   for (int k = 0; k < h->L; ++k) {
     retile_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, h->stream>>>(
-        reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per * k), h->D,
-        h->Dpad >> 1, h->R);
+        reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per_t * k), h->D,
+        h->Dpad >> 1, h->R, stream_sb_rows(h->R));
     CQP_CUDA(cudaGetLastError());
   }
   return CQP_OK;
@@ -913,6 +948,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.Wt = (!h->w_smem) ? h->Wt : nullptr;
   p.wdoubles = h->wdoubles;
   p.stream_stages = h->stream_stages;
+  p.sb_rows = stream_sb_rows(h->R);
   // few iterations: copying the W slice into shared memory costs as much as streaming it once;
   // the ring then lives in the (unused) slice region
   if (total_iters < 4 && p.w_smem) {

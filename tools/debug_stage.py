@@ -59,6 +59,20 @@ elif stage.startswith("watch"):
     threading.Thread(target=watch, daemon=True).start()
     r = s.fixed_iters(k); print(stage, r.solution.iterations, s.state, r.kernel_us, flush=True)
     os._exit(0)
+elif stage.startswith("chunks"):
+    import ctypes as C
+    wl = problems.config3_atlas(30, 0) if stage[6:] == "atlas" else problems.config4_quadruped(30, 0)
+    base = wl.base_problem()
+    s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
+    q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
+    for _ in range(2):
+        s.cold_start(); r = s.fixed_iters(300)
+    w = (C.c_int * 256)()
+    s._L.cqp_debug_words(s._h, w)
+    ll = np.frombuffer(bytes(w), dtype=np.int64)[32:80]
+    ll = ll[ll != 0]
+    print(s.launch_info(), "chunk-ready stamps (cycles since the first):", [int(x - ll[0]) for x in ll])
+    print("us/iter", r.kernel_us / 300)
 elif stage.startswith("trace"):
     import ctypes as C
     if stage[5:] == "quad":
