@@ -442,9 +442,7 @@ int cqp_mpc_step_x0(cqp_handle* h, const double* x0, int k, double* u0, cqp_resu
   if (k < 1) { set_error("mpc_step_x0: k must be >= 1"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
   const auto t0 = std::chrono::steady_clock::now();
-  std::memcpy(h->hx0, x0, sizeof(double) * h->mpc_nx);
-  CQP_CUDA(cudaMemcpyAsync(h->mpc_x0, h->hx0, sizeof(double) * h->mpc_nx, cudaMemcpyHostToDevice, h->stream));
-  int rc = launch_instantiate(h);
+  int rc = launch_instantiate(h, x0);
   if (rc) return rc;
   h->vectors_device_only = true;
   h->mpc_extract = true;

@@ -23,6 +23,7 @@ constexpr int kThreads = kComputeThreads + 32 + kLoaderThreads;  // + 1 publishe
 constexpr int kStageRows = 16, kStagePairs = 128;
 constexpr int kStageDoubles = kStageRows * kStagePairs * 2;
 constexpr int kMaxStages = 6;
+constexpr int kMaxInlineX0 = 128;  // x0 of an MPC step rides in the kernel parameters up to this size
 constexpr int kWarps = kThreads / 32;
 
 inline int pad2(int x) { return (x + 1) & ~1; }
@@ -178,7 +179,7 @@ int launch_transpose_pad(cudaStream_t st, const double* src_colmajor, int rows, 
 int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, int cols, int ld,
                        double* dst_colmajor);
 int launch_bias(cqp_handle* h, int k, double* b_out);  // b_out: device, D doubles
-int launch_instantiate(cqp_handle* h);                  // g, c, d <- template(x0) on the device
+int launch_instantiate(cqp_handle* h, const double* x0_host);  // g, c, d <- template(x0) on the device
 
 // cqp_batch.cu : dense DMMA GEMM with an identity slot map, used by the offline stage
 struct DenseGemm;

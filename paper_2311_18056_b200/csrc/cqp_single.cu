@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "cqp_internal.h"
 #include "cqp_device.cuh"
@@ -562,6 +563,12 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
                            : "memory");
             }
             __syncwarp();
+#ifdef CQP_TRACE_CHUNKS
+            if (lane == 0 && blockIdx.x == 0 && i == CQP_TRACE_AT) {
+              const int ci = (rb0 / sbr) * ((nc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
+              if (ci < 48) reinterpret_cast<volatile long long*>(p.dbg + 64)[48 + ci] = clock64();
+            }
+#endif
             if (p.Wt) {  // re-tiled W: the whole stage is one contiguous block
               if (lane == 0) {
                 // (rows of the re-tiled copy are padded to 8 pairs = 128 B, so every block is 128 B aligned)
@@ -782,11 +789,19 @@ __global__ void set_state_kernel(int* state, int layer) { state[0] = layer; }
 
 // mpc::instantiate on the device (mpc.cpp:260-270): g = offset_g x0, shift = offset_c x0,
 // c = c_base - shift, d = d_base - shift.  One warp per row of [offset_g; offset_c].
+struct X0Arg {
+  double x[kMaxInlineX0];  // x0 travels in the kernel's parameter block: no host->device copy per step
+};
+
+template <bool INLINE>
 __global__ void instantiate_kernel(const double* __restrict__ og, const double* __restrict__ oc,
                                    const double* __restrict__ cb, const double* __restrict__ db,
-                                   const double* __restrict__ x0, int n, int m, int nx, int nxpad,
+                                   double* __restrict__ x0_dev, const X0Arg xa, int n, int m, int nx, int nxpad,
                                    double* __restrict__ g, double* __restrict__ c, double* __restrict__ d) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const double* x0 = INLINE ? xa.x : x0_dev;
+  if (INLINE && blockIdx.x == 0)  // keep a device copy for the control extraction of the run kernel
+    for (int j = threadIdx.x; j < nx; j += blockDim.x) x0_dev[j] = xa.x[j];
   if (row >= n + m) return;
   const double* M = row < n ? og + (size_t)row * nxpad : oc + (size_t)(row - n) * nxpad;
   double acc = 0.0;
@@ -984,10 +999,22 @@ int launch_warm_start(cqp_handle* h, const double* dy, const double* dlam, int l
   return launch_refresh_z(h);
 }
 
-int launch_instantiate(cqp_handle* h) {
+int launch_instantiate(cqp_handle* h, const double* x0_host) {
   const int rows = h->n + h->m, threads = 256, rows_per_block = threads / 32;
-  instantiate_kernel<<<(rows + rows_per_block - 1) / rows_per_block, threads, 0, h->stream>>>(
-      h->mpc_og, h->mpc_oc, h->mpc_cb, h->mpc_db, h->mpc_x0, h->n, h->m, h->mpc_nx, h->mpc_nxpad, h->g, h->c, h->d);
+  const int blocks = (rows + rows_per_block - 1) / rows_per_block;
+  X0Arg xa;
+  if (h->mpc_nx <= kMaxInlineX0) {
+    std::memcpy(xa.x, x0_host, sizeof(double) * h->mpc_nx);
+    instantiate_kernel<true><<<blocks, threads, 0, h->stream>>>(h->mpc_og, h->mpc_oc, h->mpc_cb, h->mpc_db, h->mpc_x0,
+                                                               xa, h->n, h->m, h->mpc_nx, h->mpc_nxpad, h->g, h->c,
+                                                               h->d);
+  } else {
+    std::memcpy(h->hx0, x0_host, sizeof(double) * h->mpc_nx);
+    CQP_CUDA(cudaMemcpyAsync(h->mpc_x0, h->hx0, sizeof(double) * h->mpc_nx, cudaMemcpyHostToDevice, h->stream));
+    instantiate_kernel<false><<<blocks, threads, 0, h->stream>>>(h->mpc_og, h->mpc_oc, h->mpc_cb, h->mpc_db,
+                                                                h->mpc_x0, xa, h->n, h->m, h->mpc_nx, h->mpc_nxpad,
+                                                                h->g, h->c, h->d);
+  }
   CQP_CUDA(cudaGetLastError());
   return CQP_OK;
 }

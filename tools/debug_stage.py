@@ -69,9 +69,11 @@ elif stage.startswith("chunks"):
         s.cold_start(); r = s.fixed_iters(300)
     w = (C.c_int * 256)()
     s._L.cqp_debug_words(s._h, w)
-    ll = np.frombuffer(bytes(w), dtype=np.int64)[32:80]
-    ll = ll[ll != 0]
-    print(s.launch_info(), "chunk-ready stamps (cycles since the first):", [int(x - ll[0]) for x in ll])
+    al = np.frombuffer(bytes(w), dtype=np.int64)
+    ll = al[32:80]; ll = ll[ll != 0]
+    pl = al[80:128]; pl = pl[pl != 0]
+    print(s.launch_info(), "consumer chunk-ready stamps (cycles since the first):", [int(x - ll[0]) for x in ll])
+    print("producer issue stamps (same origin):", [int(x - ll[0]) for x in pl])
     print("us/iter", r.kernel_us / 300)
 elif stage.startswith("trace"):
     import ctypes as C

@@ -42,18 +42,24 @@ __global__ void __launch_bounds__(544, 1) stream(const double* __restrict__ W, s
   const unsigned char* base = reinterpret_cast<const unsigned char*>(W) + (size_t)blockIdx.x * slice_bytes;
   unsigned cnt = 0;
   double acc = 0.0;
+  long long prof[4] = {0, 0, 0, 0};
   for (int rep = 0; rep < reps; ++rep) {
     if (warp == 16) {  // producer
       for (int c = 0; c < chunks; ++c, ++cnt) {
         const unsigned stage = cnt % NS, ph = (cnt / NS) & 1;
+        const long long c0 = clock64();
         mbar_wait(&empty[stage], ph ^ 1);
+        const long long c1 = clock64();
         if (lane == 0)
           asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smem_u32(&full[stage])), "r"(kStageBytes) : "memory");
         __syncwarp();
+        const long long c2 = clock64();
         const unsigned dst0 = smem_u32(ring) + stage * kStageBytes;
         if (MODE == 1) {
           if (lane == 0)
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst0), "l"(base + (size_t)c * kStageBytes), "r"(kStageBytes), "r"(smem_u32(&full[stage])) : "memory");
+          const long long c3 = clock64();
+          if (lane == 0 && blockIdx.x == 0 && sink) { prof[0] += c1 - c0; prof[1] += c2 - c1; prof[2] += c3 - c2; prof[3] += 1; }
         } else {
           // row-major slice: rows of row_doubles*8 bytes; a stage covers NR rows x SEG bytes
           constexpr int NR = MODE == 0 ? 16 : 4, SEG = kStageBytes / NR;
@@ -81,6 +87,9 @@ __global__ void __launch_bounds__(544, 1) stream(const double* __restrict__ W, s
     }
   }
   if (acc == 1.2345) sink[0] = acc;
+  if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 16 * 32 && prof[3] > 0)
+    printf("    producer per chunk: wait(empty) %lld, expect_tx %lld, bulk issue %lld cycles (%lld chunks)\n",
+           prof[0] / prof[3], prof[1] / prof[3], prof[2] / prof[3], prof[3]);
 }
 
 template <int MODE>
