@@ -176,6 +176,26 @@ def measure_dgemm_peak():
     return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
 
 
+def measure_hbm_copy_peak():
+    """STREAM-style device copy (read + write bytes / time), the HBM denominator when the driver's
+    MEASURED_PEAKS.json is absent: 2 GiB buffers, best of 5."""
+    import torch
+    n = 1 << 28  # doubles: 2 GiB
+    a = torch.empty(n, dtype=torch.float64, device="cuda").normal_()
+    b = torch.empty_like(a)
+    for _ in range(2):
+        b.copy_(a)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); b.copy_(a); e1.record(); torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 8 * n / (best * 1e-3) / 1e9
+
+
 def single_qp_sweep(S, problems, repeats: int = 7):
     """configs[0..1]: single-QP solve time per size (p50 over repeats, cold_start before each),
     kernel-only and through-the-API wall time, next to the CPU oracle on the same inputs."""
@@ -341,6 +361,10 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     parity_ok = bool(np.array_equal(np.array(cpu_iters), out["iterations"][:sample]))
 
     single_qp = single_qp_sweep(S, problems) if world == 1 and not args.no_single else None
+    hbm_measured = measure_hbm_copy_peak() if world == 1 and not args.no_single else None
+    if hbm_measured is not None and "measured" not in peak_src:
+        peaks = dict(peaks, hbm_gbs=hbm_measured)
+        peak_src = "device copy measured in this run (MEASURED_PEAKS.json absent)"
     mpc_steps = mpc_step_section(S, problems, peaks) if world == 1 and not args.no_single else None
 
     line = {
@@ -364,12 +388,19 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         "cpu_baseline": {"value": cpu_qps, "unit": "QP/s", "cores": cores, "kind": "port",
                          "sample": f"{sample} of the {BATCH} instances, one oracle Solver per thread (-O3 -DNDEBUG build)",
                          "iteration_counts_match_gpu": parity_ok},
-        "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "source": peak_src},
+        "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "source": peak_src, "hbm_copy_gbs_this_run": hbm_measured},
     }
     if single_qp is not None:
         line["single_qp"] = single_qp
     if mpc_steps is not None:
         line["mpc_steps"] = mpc_steps
+        big = mpc_steps[-1]      # quadruped-sized: the HBM-streamed tier of the single-QP kernel
+        line["roofline_single_qp_stream"] = {
+            "bound": "hbm", "achieved": big["W_stream_GBs"], "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+            "frac": big["W_stream_frac_of_hbm_peak"], "traffic": 134.0e6,
+            "kernel": "run_kernel<16, true> (persistent single-QP kernel, W through the cp.async.bulk ring)",
+            "algorithmic": f"8*D^2 = {8 * big['D'] ** 2} bytes per iteration x {big['iters_per_step']} iterations per step / step kernel time (includes refresh_z, bias and epilogue residual passes)",
+            "peak_source": peak_src, "traffic_source": "ncu dram__bytes_read per iteration, profiles/r01s2_ncu_summary.json"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

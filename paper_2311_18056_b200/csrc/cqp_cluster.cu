@@ -679,9 +679,13 @@ int cluster_do(ClOp op, cqp_handle* h, const RunParams* p) {
 
 int cluster_dispatch(ClOp op, cqp_handle* h, const RunParams* p) {
   switch (h->npt) {
+    case 2: return cluster_do<1, 2>(op, h, p);
     case 4: return cluster_do<1, 4>(op, h, p);
+    case 6: return cluster_do<1, 6>(op, h, p);
     case 8: return cluster_do<1, 8>(op, h, p);
+    case 10: return cluster_do<1, 10>(op, h, p);
     case 12: return cluster_do<1, 12>(op, h, p);
+    case 14: return cluster_do<1, 14>(op, h, p);
     case 16: return cluster_do<1, 16>(op, h, p);
     default: break;
   }
@@ -712,7 +716,7 @@ int configure_cluster(cqp_handle* h) {
       int npt = 0, rpw = 0, xs_stride = h->Dpad;
       if (reg) {
         if (R > 2 * kClWarps || np > 16) continue;
-        npt = (np + 3) / 4 * 4;
+        npt = (np + 1) / 2 * 2;
         xs_stride = 32 * npt;
       } else {
         rpw = (R + kClWarps - 1) / kClWarps;

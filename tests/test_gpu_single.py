@@ -151,7 +151,7 @@ def test_dense_qp_parity_with_device_offline_stage(G, oracle, n, seeds):
 
 
 def test_cluster_kernel_layouts(G, oracle, P):
-    """The cluster tier picks its layout from D: register mode with NPT = 4/8/12/16 column pairs per
+    """The cluster tier picks its layout from D: register mode with NPT = 2..16 column pairs per
     lane (D <= 512), shared-memory mode with 1-4 rows per warp above, residual rows cached in shared
     memory or read through L2 when they do not fit.  One parity solve per layout, odd D included."""
     cases = [("dense", 35), ("dense", 90), ("dense", 130), ("dense", 200), ("mpc", 21)]
