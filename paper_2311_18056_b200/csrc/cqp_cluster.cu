@@ -234,6 +234,7 @@ __device__ void cl_residual_pass(const RunParams& p, const ClSmem& s, const doub
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int n = p.n, m = p.m;
   unsigned long long* nbar = s.bars + 2;
+  asm volatile("cp.async.wait_all;" ::: "memory");  // the cached rows of H, G', G (first pass only: a no-op later)
   __syncthreads();
   // unscale (layers.hpp:57-59)
   for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? s.sE[i] * xs[i] : 0.0;
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   unsigned long long* nbar = s.bars + 2;  // [2]: the norms of residual pass `pass` are complete
   const int n = p.n, m = p.m, D = p.D;
   const unsigned xbytes = 8u * (unsigned)D;
+  CQP_STAMP0(p.dbg, 0);
   if (t == 0) {
     for (int k = 0; k < 4; ++k) mbar_init(&s.bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -358,9 +360,16 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     const int pern = (n + C - 1) / C, perm = (m + C - 1) / C;
     const int h0 = (int)rank * pern, g0 = (int)rank * perm;
     const int cn = max(0, min(pern, n - h0)), cm = max(0, min(perm, m - g0));
-    for (int i = t; i < cn * p.npad; i += kClThreads) s.sH[i] = __ldg(p.H + (size_t)h0 * p.npad + i);
-    for (int i = t; i < cn * p.mpad; i += kClThreads) s.sGt[i] = __ldg(p.Gt + (size_t)h0 * p.mpad + i);
-    for (int i = t; i < cm * p.npad; i += kClThreads) s.sG[i] = __ldg(p.Gr + (size_t)g0 * p.npad + i);
+    // asynchronous (cp.async, 16 B): the rows are first needed at the first residual pass, which
+    // waits for them; the prologue does not
+    auto copy_async = [&](double* dst, const double* src, int doubles) {
+      for (int i = 2 * t; i < doubles; i += 2 * kClThreads)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + i)), "l"(src + i) : "memory");
+    };
+    copy_async(s.sH, p.H + (size_t)h0 * p.npad, cn * p.npad);
+    copy_async(s.sGt, p.Gt + (size_t)h0 * p.mpad, cn * p.mpad);
+    copy_async(s.sG, p.Gr + (size_t)g0 * p.npad, cm * p.npad);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   __syncthreads();
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
@@ -376,22 +385,10 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     s.shi[r] = hi;
   }
   __syncthreads();
-  cluster_sync_all();  // every peer's barriers are initialised and armed before anyone pushes
-
-  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in p.vq (slot 0)
-  if (p.do_refresh) {
-    for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? __ldcg(p.vq + i) : 0.0;
-    __syncthreads();
-    const int per = (m + C - 1) / C;
-    const int g0 = (int)rank * per;
-    const int g1 = min(m, g0 + per);
-    for (int row = g0 + warp; row < g1; row += kClWarps) {
-      const double zs = warp_row_dot(p.Gs + (size_t)row * p.npad, s.uy, p.npad, lane);
-      if (lane == 0) __stcg(p.vq + n + row, zs);
-    }
-    __syncthreads();
-    cluster_sync_all();  // release/acquire at cluster scope: the peers' rows of z_s are visible
-  }
+  CQP_STAMP0(p.dbg, 1);
+  // (No cluster barrier here: nobody pushes into a peer before the barrier that follows the v_0
+  // load below, and that one also orders every peer's mbarrier initialisation before the pushes.)
+  CQP_STAMP0(p.dbg, 2);
 
   // ---- work split inside the CTA ----
   const int nc2 = p.Dpad >> 1;
@@ -428,8 +425,26 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
   };
 
+  load_registers(layer);  // (global loads into registers: their latency overlaps refresh_z and the bias rows)
+
+  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in p.vq (slot 0)
+  if (p.do_refresh) {
+    for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? __ldcg(p.vq + i) : 0.0;
+    __syncthreads();
+    const int per = (m + C - 1) / C;
+    const int g0 = (int)rank * per;
+    const int g1 = min(m, g0 + per);
+    for (int row = g0 + warp; row < g1; row += kClWarps) {
+      const double zs = warp_row_dot(p.Gs + (size_t)row * p.npad, s.uy, p.npad, lane);
+      if (lane == 0) __stcg(p.vq + n + row, zs);
+    }
+    __syncthreads();
+    cluster_sync_all();  // release/acquire at cluster scope: the peers' rows of z_s are visible
+  }
+
+  CQP_STAMP0(p.dbg, 3);
   cl_load_layer(p, s, layer, row0, nrows);
-  load_registers(layer);
+  CQP_STAMP0(p.dbg, 4);
 
   // v_0 -> xs[0]; pad slots of both copies stay zero for the whole launch
   for (int i = t; i < XS; i += kClThreads) {
@@ -438,6 +453,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   }
   __syncthreads();
   cluster_sync_all();  // peers write into xs[1] as soon as they finish iteration 1
+  CQP_STAMP0(p.dbg, 5);
 
   int n_trace = 1, n_hist = 0, pass = 0;
   if (rank == 0 && t == 0) {
@@ -603,12 +619,15 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   }
 
   // ---- epilogue (solver.cpp:90-99) ----
+  CQP_STAMP0(p.dbg, 6);
   const int bf = iters_done & 1;
   if (iters_done >= 1 && have != iters_done)
     mbar_wait_cluster(&xready[bf], ((iters_done - 1) >> 1) & 1, p.dbg, 3, iters_done);
   double nrm[7];
   const double* xfinal = s.xs + (size_t)bf * XS;
+  CQP_STAMP0(p.dbg, 7);
   cl_residual_pass(p, s, xfinal, true, pass++, rank, C, nrm);
+  CQP_STAMP0(p.dbg, 8);
   // between-launch invariant: p.vq slot 0 = iterate (slots 1..3 keep the grid kernel's sentinel)
   for (int r = t; r < nrows; r += kClThreads) p.vq[row0 + r] = xfinal[row0 + r];
   if (rank == 0) {
@@ -634,7 +653,9 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
   }
   __syncthreads();
+  CQP_STAMP0(p.dbg, 9);
   cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
+  CQP_STAMP0(p.dbg, 10);
 }
 
 template <int RPW, int NPT>

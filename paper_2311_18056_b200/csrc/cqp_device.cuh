@@ -51,8 +51,15 @@ __device__ __forceinline__ void progress(int* d, int role, int value) {
     if (blockIdx.x == 0 && (it) >= CQP_TRACE_AT && (it) < CQP_TRACE_AT + 4)                                   \
       reinterpret_cast<volatile long long*>((dbg) + 64)[((it)-CQP_TRACE_AT) * 16 + (slot)] = clock64(); \
   } while (0)
+// prologue / epilogue stamps of CTA 0 (fixed slots 48..63 of the same record)
+#define CQP_STAMP0(dbg, slot)                                                                   \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0)                                                    \
+      reinterpret_cast<volatile long long*>((dbg) + 64)[48 + (slot)] = clock64();               \
+  } while (0)
 #else
 #define CQP_STAMP(dbg, it, slot) do {} while (0)
+#define CQP_STAMP0(dbg, slot) do {} while (0)
 #endif
 
 __device__ __forceinline__ bool is_sentinel(double x) {

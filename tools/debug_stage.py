@@ -59,6 +59,20 @@ elif stage.startswith("watch"):
     threading.Thread(target=watch, daemon=True).start()
     r = s.fixed_iters(k); print(stage, r.solution.iterations, s.state, r.kernel_us, flush=True)
     os._exit(0)
+elif stage.startswith("fixed"):
+    import ctypes as C
+    wl = problems.config1(0); base = wl.base_problem()
+    s = S.Solver(base.H, base.g, base.G, base.c, base.d)
+    q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
+    s.cold_start(); s.solve()
+    for _ in range(3):
+        r = s.mpc_step(q.g, q.c, q.d, int(stage[5:]))
+    w = (C.c_int * 256)()
+    s._L.cqp_debug_words(s._h, w)
+    al = np.frombuffer(bytes(w), dtype=np.int64)[32 + 48:32 + 64]
+    names = ["entry", "vectors+rows cached", "cluster sync 1", "refresh_z done", "layer + W regs", "v0 + cluster sync", "loop done", "final v arrived", "residual pass", "outputs written", "exit sync"]
+    print(s.launch_info(), "kernel_us", r.kernel_us)
+    print("  ".join(f"{names[i]}@{int(al[i] - al[0])}" for i in range(11) if al[i]))
 elif stage.startswith("chunks"):
     import ctypes as C
     wl = problems.config3_atlas(30, 0) if stage[6:] == "atlas" else problems.config4_quadruped(30, 0)
