@@ -160,6 +160,44 @@ __device__ __forceinline__ int nearest_grid_index(const double* log_grid, int L,
 }
 
 
+// One warp: M[row, :] . x with M row-major in global memory and x in shared memory (pad entries of
+// both zero), U 16-byte loads per lane in flight: an n = 870 row (14 column pairs per lane) costs
+// two L2 round trips instead of one per pair.  Fixed order: lane l takes pairs l, l + 32, ...
+template <int U>
+__device__ __forceinline__ double warp_row_dot_mlp(const double* __restrict__ Mrow, const double* __restrict__ x,
+                                                   int ncols_pad, int lane) {
+  const double2* m2 = reinterpret_cast<const double2*>(Mrow);
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const int nc2 = ncols_pad >> 1;
+  double a0 = 0.0, a1 = 0.0;
+  for (int base = lane; base < nc2; base += 32 * U) {
+    double2 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c2 = base + 32 * u;
+      w[u] = c2 < nc2 ? __ldg(m2 + c2) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c2 = base + 32 * u;
+      if (c2 < nc2) {
+        const double2 xv = x2[c2];
+        if (u & 1) {
+          a1 = fma(w[u].x, xv.x, a1);
+          a1 = fma(w[u].y, xv.y, a1);
+        } else {
+          a0 = fma(w[u].x, xv.x, a0);
+          a0 = fma(w[u].y, xv.y, a0);
+        }
+      }
+    }
+  }
+  double v = a0 + a1;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) v += __shfl_xor_sync(0xffffffffu, v, w);
+  return v;
+}
+
 // Control extraction of the closed loop (bench.cpp:169-175): u0 = clamp(-K x + y[0:nu], u_lo, u_hi).
 // `y` is the unscaled primal solution in shared memory; executed by one CTA (threads t < nu).
 __device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t) {

@@ -153,41 +153,13 @@ __device__ __forceinline__ void fma_rows(const double* __restrict__ M, int ld, i
   }
 }
 
-// Whole-CTA helper for the non-hot paths (bias rows, residual checks, refresh_z):
-// returns, in threads 0..nvalid-1, M[r, :] . x for r < nvalid <= RB.  M row-major with even
-// leading dimension (shared or global), x in shared memory, pad entries zero.
-// Contains two __syncthreads(); must be called by all kThreads threads.
-template <int RB>
-__device__ __forceinline__ double block_rows_dot(const double* __restrict__ M, int ld, int nvalid,
-                                                 const double* __restrict__ x, int ncols_pad,
-                                                 double* sred) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  double acc[RB];
-#pragma unroll
-  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-  const int nc2 = ncols_pad >> 1;
-  const double2* x2 = reinterpret_cast<const double2*>(x);
-  for (int c2 = t; c2 < nc2; c2 += kThreads) fma_rows<RB>(M, ld, nvalid, c2, x2[c2], acc);
-  constexpr int shift = 5 - Log2<RB>::v;
-  const double total = warp_butterfly<RB>(acc, lane);
-  if ((lane & ((1 << shift) - 1)) == 0) sred[warp * RB + (lane >> shift)] = total;
-  __syncthreads();
-  double s = 0.0;
-  if (t < RB) {
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += sred[w * RB + t];
-  }
-  __syncthreads();
-  return s;
-}
-
 struct Smem {
   double* sW;    // R * Dpad resident slice (tier 0) / streaming ring (tier 1); p.wdoubles doubles
   double* xs;    // 2 * Dpad   iterate (cache space), double buffered by iteration parity
   double* uy;    // npad       unscaled y   (also scratch for g_s)
   double* uz;    // mpad       unscaled z
   double* ul;    // mpad       unscaled lambda
-  double* sred;  // kWarps * 16          (block_rows_dot)
+  double* sred;  // kWarps * 16          (all-CTA reduction of the residual norms)
   double* spart; // 2 * kComputeWarps * Rcap   per-warp partials of the hot loop, by parity
   double* sb;    // Rp  bias rows
   double* slo;   // Rp
@@ -248,14 +220,14 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
   __syncthreads();
   const int nm = p.n + p.m;
   const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
-  for (int rb0 = 0; rb0 < nrows; rb0 += RB) {
-    const int first = row0 + rb0;
-    const int nv = min(RB, nrows - rb0);
-    const int nv_dot = max(0, min(nv, nm - first));  // rows that have a D/GD row
-    double sum = 0.0;
-    if (first < nm)
-      sum = block_rows_dot<RB>(DG + (size_t)first * p.npad, p.npad, nv_dot, s.uy, p.npad, s.sred);
-    if (t < nv) s.sb[rb0 + t] = (t < nv_dot) ? -sum : 0.0;
+  {  // warp per row, 8 loads per lane in flight (these GEMVs are one-shot: latency, not bandwidth)
+    const int lane = t & 31, warp = t >> 5;
+    for (int r = warp; r < nrows; r += kWarps) {
+      const int row = row0 + r;
+      double bias = 0.0;
+      if (row < nm) bias = -warp_row_dot_mlp<8>(DG + (size_t)row * p.npad, s.uy, p.npad, lane);
+      if (lane == 0) s.sb[r] = bias;
+    }
   }
   __syncthreads();
 }
@@ -290,54 +262,57 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
 
   double mx[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const int G = p.G;
-  // rows of H and G' owned by this CTA
-  {
-    const int per = (n + G - 1) / G;
-    const int h0 = blockIdx.x * per;
-    const int nh = max(0, min(per, n - h0));
-    for (int rb0 = 0; rb0 < nh; rb0 += RB) {
-      const int nv = min(RB, nh - rb0);
-      const int row = h0 + rb0;
-      const double hy = block_rows_dot<RB>(p.H + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
-      const double gtl = block_rows_dot<RB>(p.Gt + (size_t)row * p.mpad, p.mpad, nv, s.ul, p.mpad, s.sred);
-      if (t < nv) {
-        const double gi = p.g[row + t];
-        const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
-        mx[6] = nanmax(mx[6], fabs(gi));
-        mx[1] = nanmax(mx[1], fabs(dual));
-        mx[2] = nanmax(mx[2], fabs(hy));
-        mx[3] = nanmax(mx[3], fabs(gtl));
-      }
+  const int lane = t & 31, warp = t >> 5;
+  // This CTA owns rows [h0, h0 + cn) of H and G' and rows [g0, g0 + cm) of G: 2 cn + cm independent
+  // row dots, one warp each (8 loads per lane in flight), all in parallel; results meet in shared
+  // memory (s.sval) and thread r combines row r.
+  const int pern = (n + G - 1) / G, perm = (m + G - 1) / G;
+  const int h0 = blockIdx.x * pern, g0 = blockIdx.x * perm;
+  const int cn = max(0, min(pern, n - h0)), cm = max(0, min(perm, m - g0));
+  const int cap3 = 40;  // rows of one kind that fit s.sval (3 * 40 <= 128); larger shares loop
+  for (int c0 = 0; c0 < max(cn, cm); c0 += cap3) {
+    const int bn = max(0, min(cap3, cn - c0)), bm = max(0, min(cap3, cm - c0));
+    for (int d = warp; d < 2 * bn + bm; d += kWarps) {
+      double val;
+      if (d < bn) val = warp_row_dot_mlp<8>(p.H + (size_t)(h0 + c0 + d) * p.npad, s.uy, p.npad, lane);
+      else if (d < 2 * bn) val = warp_row_dot_mlp<8>(p.Gt + (size_t)(h0 + c0 + d - bn) * p.mpad, s.ul, p.mpad, lane);
+      else val = warp_row_dot_mlp<8>(p.Gr + (size_t)(g0 + c0 + d - 2 * bn) * p.npad, s.uy, p.npad, lane);
+      if (lane == 0) s.sval[d] = val;
     }
-  }
-  // rows of G owned by this CTA
-  {
-    const int per = (m + G - 1) / G;
-    const int g0 = blockIdx.x * per;
-    const int ng = max(0, min(per, m - g0));
-    for (int rb0 = 0; rb0 < ng; rb0 += RB) {
-      const int nv = min(RB, ng - rb0);
-      const int row = g0 + rb0;
-      const double gy = block_rows_dot<RB>(p.Gr + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
-      if (t < nv) {
-        const double z = s.uz[row + t];
-        mx[0] = nanmax(mx[0], fabs(gy - z));
-        mx[4] = nanmax(mx[4], fabs(gy));
-        mx[5] = nanmax(mx[5], fabs(z));
-      }
+    __syncthreads();
+    if (t < bn) {
+      const int row = h0 + c0 + t;
+      const double hy = s.sval[t], gtl = s.sval[bn + t];
+      const double gi = p.g[row];
+      const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
+      mx[6] = nanmax(mx[6], fabs(gi));
+      mx[1] = nanmax(mx[1], fabs(dual));
+      mx[2] = nanmax(mx[2], fabs(hy));
+      mx[3] = nanmax(mx[3], fabs(gtl));
     }
+    if (t < bm) {
+      const double gy = s.sval[2 * bn + t];
+      const double z = s.uz[g0 + c0 + t];
+      mx[0] = nanmax(mx[0], fabs(gy - z));
+      mx[4] = nanmax(mx[4], fabs(gy));
+      mx[5] = nanmax(mx[5], fabs(z));
+    }
+    __syncthreads();
   }
-  // combine the RB threads that hold values, publish, exchange
-  if (t < RB) {
+  // the threads t < 40 hold values: warps 0 and 1 reduce them, then two lanes meet in shared memory
+  if (warp < 2) {
 #pragma unroll
-    for (int k = 0; k < 7; ++k) s.sval[t * 7 + k] = mx[k];
+    for (int k = 0; k < 7; ++k) {
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) mx[k] = nanmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], w));
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) s.sval[warp * 8 + k] = mx[k];
+    }
   }
   __syncthreads();
-  if (t < 7) {
-    double best = 0.0;
-    for (int r = 0; r < RB; ++r) best = nanmax(best, s.sval[r * 7 + t]);
-    __stcg(p.partial + (size_t)blockIdx.x * 8 + t, best);
-  }
+  if (t < 7) __stcg(p.partial + (size_t)blockIdx.x * 8 + t, nanmax(s.sval[t], s.sval[8 + t]));
   grid_barrier(p.barrier, epoch, G, p.dbg);
   // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
   // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant)
@@ -434,12 +409,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     __syncthreads();
     const int per = (m + p.G - 1) / p.G;
     const int g0 = blockIdx.x * per;
-    const int ng = max(0, min(per, m - g0));
-    for (int rb0 = 0; rb0 < ng; rb0 += RB) {
-      const int nv = min(RB, ng - rb0);
-      const int row = g0 + rb0;
-      const double zs = block_rows_dot<RB>(p.Gs + (size_t)row * p.npad, p.npad, nv, s.uy, p.npad, s.sred);
-      if (t < nv) __stcg(v + n + row + t, zs);
+    const int g1 = min(m, g0 + per);
+    for (int row = g0 + warp; row < g1; row += kWarps) {
+      const double zs = warp_row_dot_mlp<8>(p.Gs + (size_t)row * p.npad, s.uy, p.npad, lane);
+      if (lane == 0) __stcg(v + n + row, zs);
     }
     grid_barrier(p.barrier, epoch, p.G, p.dbg);
   }
