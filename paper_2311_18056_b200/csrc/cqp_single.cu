@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // L2/HBM tier: W_k is streamed through a shared-memory ring by the publisher warp with
   // cp.async.bulk (mbarrier complete_tx), kStageRows rows x kStagePairs column pairs per stage; the
   // ring runs ahead of the compute warps, also across iterations (W does not depend on v).
-  const int NS = STREAM ? p.stream_stages : 1;  // (1: keeps the dead % NS of the other tier well defined)
+  const int NS = STREAM ? p.stream_stages : 1;
   constexpr bool streaming = STREAM;
   if (t == 0) {
     mbar_init(&full[0], kComputeWarps);
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   int until_check = p.check_interval;
   const int nc2 = p.Dpad >> 1;
   constexpr int shift = 5 - Log2<RB>::v;
-  unsigned wcnt = 0;  // chunks of the W stream consumed (compute) / issued (streamer) so far
+  unsigned wstage = 0, wphase = 0;  // ring position of the next W chunk to consume (compute) / issue (streamer)
   const int sbr = STREAM ? p.sb_rows : kStageRows;  // rows per super-block of the W stream (<= kStageRows)
   const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
   const int nfetch = streaming ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
@@ -460,8 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
-            const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
+          for (int c0 = 0; c0 < nc2; c0 += kStagePairs) {
+            const unsigned stage = wstage, ph = wphase;  // (stage, phase) advance without integer division
+            if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wfull[stage], (int)ph, p.dbg, 7, i);
 #ifdef CQP_TRACE_CHUNKS
             if (t == 0 && blockIdx.x == 0 && i == CQP_TRACE_AT) {
@@ -525,8 +526,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (streaming) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
-          for (int c0 = 0; c0 < nc2; c0 += kStagePairs, ++wcnt) {
-            const unsigned stage = wcnt % (unsigned)NS, ph = (wcnt / (unsigned)NS) & 1u;
+          for (int c0 = 0; c0 < nc2; c0 += kStagePairs) {
+            const unsigned stage = wstage, ph = wphase;
+            if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wempty[stage], (int)(ph ^ 1u), p.dbg, 8, i);  // (a fresh barrier passes at once)
             const unsigned bytes = 16u * (unsigned)min(kStagePairs, nc2 - c0);
             if (lane == 0) {
