@@ -741,8 +741,8 @@ struct cqp_batch {
   // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
   // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
   // (less wave quantisation, 12 warps/SM), 64x32 wins below ~3400 columns, 32x32 (6 CTAs/SM: more
-  // warps to keep the tensor pipe fed when the grid no longer fills) below ~1000.
-  int thr_big = 1 << 30, thr_mid = 3400, thr_small = 1000;
+  // warps to keep the tensor pipe fed when the grid no longer fills) below ~1400.
+  int thr_big = 1 << 30, thr_mid = 3400, thr_small = 1400;
   int force_cfg = -1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;
