@@ -1,34 +1,43 @@
-// Single-QP solve path: one persistent cooperative sm_100a kernel per solve()/fixed_iters().
+// Single-QP solve path, all-SM tiers: one persistent cooperative sm_100a kernel per
+// solve() / fixed_iters() / mpc_step().  (Problems whose ladder level fits ONE thread-block
+// cluster's shared memory, D <~ 650, run the cluster kernel of cqp_cluster.cu instead.)
 //
 // Replaces the reference's run_loop (/root/reference/proj/src/solver.cpp:43-105) and the
 // helpers it calls (iterate :109-117, residuals :119-124, rho_nominal :126-134,
 // select_layer :136-142 + nearest_grid_index layers.cpp:38-50), plus the per-MPC-step
-// vector update (layers.cpp:177-187) and z refresh (solver.cpp:197-200).
+// vector update (layers.cpp:177-187), z refresh (solver.cpp:197-200), mpc::instantiate
+// (mpc.cpp:260-270) and the control extraction of the closed loop (bench.cpp:169-175).
 //
-// Design (DESIGN.md section 3):
-//   * W_k (D x D, D = n + 2m) is stored row-major; CTA b owns rows [b*R, b*R + R) and keeps
-//     that slice resident in shared memory (tier 0) or streams it from L2/HBM (tier 1).
+// Design (DESIGN.md section 3.2):
+//   * W_k (D x D, D = n + 2m) is stored row-major; CTA b owns rows [b*R, b*R + R) and either keeps
+//     that slice resident in shared memory (tier 0, run_kernel<RB, false>) or streams it from
+//     L2/HBM through a shared-memory ring of cp.async.bulk stages fed from a re-tiled copy of the
+//     ladder (tier 1, run_kernel<RB, true>; one contiguous <= 32 KB block per stage).
 //   * The iterate is exchanged through L2 WITHOUT a grid barrier: four D-vectors q[0..3] form a
 //     ring; iteration i reads v_{i-1} from q[(i-1)&3] and writes v_i to q[i&3].  A slot that has
 //     not been written yet holds a sentinel bit pattern (all ones, a NaN no arithmetic
 //     produces), so the data word is its own "ready" flag (8-byte accesses are single-copy
-//     atomic).  Each compute thread owns a fixed set of column pairs, polls exactly the x
-//     entries it needs into registers and starts its FMAs as soon as they land.
+//     atomic).
 //   * Warp roles inside a CTA (no CTA-wide barrier in the iteration loop):
-//       - 16 compute warps form the R dot products (x from shared memory, 16-byte LDS/LDG of
-//         W, FP64 FMA), reduce them with a shuffle butterfly and hand per-warp partials to
+//       - 16 compute warps form the R dot products (x from shared memory, 16-byte LDS of W,
+//         FP64 FMA), reduce them with a shuffle butterfly and hand per-warp partials to
 //       - 1 publisher warp, which sums the partials in a FIXED order (bit-reproducible run to
 //         run), adds the bias, clamps, stores the rows to q[i&3], wakes the loaders, re-arms
-//         its rows of q[(i+2)&3] with the sentinel and fences (off the critical path);
-//       - 4 loader warps, the only threads that poll L2: they fetch v_i into a double-buffered
-//         shared-memory copy (all loads in flight, re-polling only the entries still armed).
-//     Hand-offs use parity-split mbarriers (full[2], xready[2], go), so a role can run at most
-//     one phase ahead and arrivals of different iterations never mix.
+//         its rows of q[(i+2)&3] with the sentinel and fences (off the critical path); in tier 1
+//         it is also the producer of the W ring and runs ahead of the compute warps, across
+//         iterations too (W does not depend on v);
+//       - 3 loader warps poll L2 for v_i into a double-buffered shared-memory copy: all loads in
+//         flight, every re-poll round re-issues ALL still-armed entries back to back (one L2 round
+//         trip per round); in tier 1 the otherwise idle compute warps fetch along.
+//     Hand-offs use parity-split mbarriers (full[2], xready[2], go, wfull[], wempty[]), so a role
+//     can run at most one phase ahead and arrivals of different iterations never mix.
 //   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
-//     problem (H y, G' lambda, G y spread over the CTAs, seven max-norms exchanged through L2
-//     behind one grid barrier), and every CTA takes the identical rho decision; a switch
-//     reloads the W slice and recomputes the bias rows b = -[D_k; G D_k] g_s it owns.
-//   * Nothing is launched per iteration; the host sees one launch and one result download.
+//     problem (H y, G' lambda, G y as independent warp-per-row dots spread over the CTAs, seven
+//     max-norms exchanged through L2 behind one grid barrier), and every CTA takes the identical
+//     rho decision; a switch reloads the W slice and recomputes the bias rows
+//     b = -[D_k; G D_k] g_s it owns.
+//   * Nothing is launched per iteration; the result record is written straight into host-mapped
+//     memory, so the host sees one launch and one stream synchronisation per call.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
