@@ -198,6 +198,12 @@ CQP_API int cqp_debug_words(const cqp_handle *h, int *out256);
 CQP_API int cqp_launch_info(const cqp_handle *h, int *ctas, int *rows_per_cta, int *tier,
                             int *smem_bytes);
 
+/* Page-locked host memory for the caller's input / output buffers (cudaMallocHost / cudaFreeHost):
+ * copies from and to pinned buffers run at full PCIe rate and asynchronously; pageable buffers
+ * are staged by the driver.  Optional: every entry point accepts any host pointer. */
+CQP_API int cqp_pinned_alloc(void **out, unsigned long long bytes);
+CQP_API void cqp_pinned_free(void *p);
+
 /* ---- batched path: many QPs sharing (H, G) and therefore the W ladder ---------------------
  * (MPC instances that differ in x0, i.e. in g, c, d).  Semantically B independent
  * `solve()` calls from a cold start (solver.cpp:158-166), one per column. */

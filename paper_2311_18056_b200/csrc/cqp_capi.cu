@@ -527,6 +527,17 @@ int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, dou
   return CQP_OK;
 }
 
+int cqp_pinned_alloc(void** out, unsigned long long bytes) {
+  if (!out) return CQP_ERR_ARGUMENT;
+  *out = nullptr;
+  CQP_CUDA(cudaMallocHost(out, bytes ? (size_t)bytes : 1));
+  return CQP_OK;
+}
+
+void cqp_pinned_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int cqp_debug_words(const cqp_handle* h, int* out256) {
   if (!h || !out256) return CQP_ERR_ARGUMENT;
   for (int i = 0; i < 256; ++i) out256[i] = ((volatile int*)h->dbg_host)[i];

@@ -314,11 +314,25 @@ class BatchSolver:
         self.capacity = int(capacity)
         _raise(self._L.cqp_batch_create(C.byref(self._b), solver._h, self.capacity))
         self.n, self.m = solver.n, solver.m
+        self._pinned = []     # page-locked output buffers, allocated once (views are returned)
+        self._out = None
+
+    def _pinned_array(self, shape, dtype, order="C"):
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        ptr = C.c_void_p()
+        _raise(self._L.cqp_pinned_alloc(C.byref(ptr), max(nbytes, 1)))
+        self._pinned.append(ptr)
+        buf = (C.c_char * max(nbytes, 1)).from_address(ptr.value)
+        return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape, order=order)
 
     def close(self) -> None:
         b, self._b = getattr(self, "_b", None), C.c_void_p()
         if b:
             self._L.cqp_batch_destroy(b)
+        self._out = None
+        for ptr in getattr(self, "_pinned", []):
+            self._L.cqp_pinned_free(ptr)
+        self._pinned = []
 
     def __del__(self):
         try:
@@ -333,11 +347,18 @@ class BatchSolver:
         if g.ndim != 2 or g.shape[0] != self.n or c.shape != (self.m, g.shape[1]) or d.shape != c.shape:
             raise ValueError("batch solve: dimension mismatch")
         B = g.shape[1]
-        y = np.empty((self.n, B), order="F"); z = np.empty((self.m, B), order="F")
-        lam = np.empty((self.m, B), order="F")
-        status = np.empty(B, dtype=np.int32); iters = np.empty(B, dtype=np.int32)
-        final = np.empty(B, dtype=np.int32); nsw = np.empty(B, dtype=np.int32)
-        rp = np.empty(B); rd = np.empty(B)
+        if B > self.capacity:
+            raise MemoryError("batch solve: B exceeds the batch capacity")
+        if self._out is None:
+            # page-locked result buffers for `capacity` columns, reused by every solve: the arrays
+            # returned below are views that the NEXT solve overwrites (copy them to keep them)
+            cap = self.capacity
+            self._out = (self._pinned_array((self.n, cap), np.float64, "F"), self._pinned_array((self.m, cap), np.float64, "F"),
+                         self._pinned_array((self.m, cap), np.float64, "F"), self._pinned_array((cap,), np.int32),
+                         self._pinned_array((cap,), np.int32), self._pinned_array((cap,), np.int32),
+                         self._pinned_array((cap,), np.int32), self._pinned_array((cap,), np.float64),
+                         self._pinned_array((cap,), np.float64))
+        y, z, lam, status, iters, final, nsw, rp, rd = (a[..., :B] for a in self._out)
         ms = C.c_double()
         ip = lambda a: a.ctypes.data_as(_lib.c_int_p)  # noqa: E731
         _raise(self._L.cqp_batch_solve(self._b, B, _p(g), _p(c), _p(d), _p(y), _p(z), _p(lam),

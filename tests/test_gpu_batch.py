@@ -62,6 +62,7 @@ def test_batch_matches_per_column_oracle(G, oracle, P, nu, B, unstable):
         assert abs(out["r_dual"][j] - s.r_dual) <= 2e-3 * s.r_dual + 1e-9
         assert np.all(out["z"][:, j] >= c[:, j]) and np.all(out["z"][:, j] <= d[:, j])
     # second call on the same batch object (buffers are reused) and the single-QP kernel agree
+    out = {k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in out.items()}  # (views of reused pinned buffers)
     out2 = batch.solve(g, c, d)
     assert np.array_equal(out2["iterations"], out["iterations"]) and np.array_equal(out2["y"], out["y"])
     single.update_vectors(g[:, 0], c[:, 0], d[:, 0]); single.cold_start()
@@ -105,7 +106,7 @@ def test_persistent_round_kernel_is_bit_identical(G, P, monkeypatch):
         monkeypatch.setenv("CQP_BATCH_PERSISTENT", flag)
         single = G.Solver(base.H, base.g, base.G, base.c, base.d)
         batch = G.BatchSolver(single, capacity=B)
-        outs.append(batch.solve(g, c, d))
+        outs.append({k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in batch.solve(g, c, d).items()})
         batch.close(); single.close()
     monkeypatch.delenv("CQP_BATCH_PERSISTENT", raising=False)
     a, b = outs
