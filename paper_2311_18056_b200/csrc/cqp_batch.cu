@@ -81,9 +81,9 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int ST = STAGES>
 constexpr int gemm_smem_bytes() {
-  return STAGES * (BM + BN) * BK * (int)sizeof(double) + BN * (int)sizeof(int);
+  return ST * (BM + BN) * BK * (int)sizeof(double) + BN * (int)sizeof(int);
 }
 
 // C[col][row] = epilogue(A[a_index] (BM x K) . B(cols) (K x BN)) for every (slot tile, sub-tile,
@@ -95,19 +95,25 @@ constexpr int gemm_smem_bytes() {
 // one).  Scheduling is static striding on purpose: a dynamic work counter with a split tail was
 // measured 7 % SLOWER (the 3-4 CTAs of an SM share its tensor pipe, so CTA-level quantisation
 // is already smoothed at SM level, and half-size tail items re-read A).
-template <int BM, int BN, int WM, int WN, int MINB>
-__global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const GemmParams p) {
-  constexpr int T = WM * WN * 32;
+// KS > 1 (last rounds, few columns left): KS warp groups share one tile and split the k steps of
+// every k-tile among them (group kg takes ks = kg, kg + KS, ...); their partial accumulators meet
+// in shared memory after the k loop and group 0 adds them in a fixed order.  With a handful of
+// items per SM a tile's K loop is a latency chain (barrier -> LDS -> DMMA per k step); KS groups
+// walk it KS k steps at a time.
+template <int BM, int BN, int WM, int WN, int MINB, int ST = STAGES, int KS = 1>
+__global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(const GemmParams p) {
+  constexpr int T = WM * WN * 32 * KS;
   constexpr int TM = BM / WM, TN = BN / WN, MI = TM / 8, NI = TN / 8;
   constexpr int SUB = SLOT_TILE / BN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
-  double* Bs = As + STAGES * BM * BK;
-  int* cols_s = reinterpret_cast<int*>(Bs + STAGES * BN * BK);
+  double* Bs = As + ST * BM * BK;
+  int* cols_s = reinterpret_cast<int*>(Bs + ST * BN * BK);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int warp_m = warp % WM, warp_n = warp / WM;
+  const int kg = warp / (WM * WN), warp_in = warp - kg * (WM * WN);  // k-split group, warp within it
+  const int warp_m = warp_in % WM, warp_n = warp_in / WM;
   const int m_tiles = p.M_pad / BM;
   const int total = (*p.n_tiles) * SUB * m_tiles;
 
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
     };
 
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
+    for (int s = 0; s < ST - 1; ++s) {
       if (s < p.k_tiles) issue(s, s);
       cp_async_commit();
     }
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
         for (int mi = 0; mi < MI; ++mi) {
           const int row = m0 + warp_m * TM + mi * 8 + g;
           double init = 0.0;
-          if (p.mode == 1 && col >= 0 && row < p.nm) {
+          if (p.mode == 1 && col >= 0 && row < p.nm && kg == 0) {
             init = p.bias[(size_t)col * p.ld_bias + row];
             if (row >= p.n && g == 0) {  // one prefetch per 64-byte run of 8 rows
               asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lo + (size_t)col * p.ld_lohi + row - p.n));
@@ -189,15 +195,16 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
       }
     }
     for (int kt = 0; kt < p.k_tiles; ++kt) {
-      cp_async_wait<STAGES - 2>();
+      cp_async_wait<ST - 2>();
       __syncthreads();
-      const int next = kt + STAGES - 1;
-      if (next < p.k_tiles) issue(next, next % STAGES);
+      const int next = kt + ST - 1;
+      if (next < p.k_tiles) issue(next, next % ST);
       cp_async_commit();
-      const double* as = As + (kt % STAGES) * BM * BK + (warp_m * TM) * BK;
-      const double* bs = Bs + (kt % STAGES) * BN * BK + (warp_n * TN) * BK;
+      const double* as = As + (kt % ST) * BM * BK + (warp_m * TM) * BK;
+      const double* bs = Bs + (kt % ST) * BN * BK + (warp_n * TN) * BK;
 #pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
+      for (int ks0 = 0; ks0 < BK / 4; ks0 += KS) {
+        const int ks = ks0 + kg;
         const int e = ks * 4 + t4;
         const int off = (((e >> 1) ^ ((g & 3) << 1)) << 1) | (e & 1);  // rows are 8-aligned + g, so r & 7 == g
         double a[MI], b[NI];
@@ -212,6 +219,36 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dmma_gemm_kernel(const Gem
       }
     }
     cp_async_wait<0>();
+    if (KS > 1) {
+      // partial accumulators of groups 1 .. KS-1 -> shared memory (the stage buffers are free now),
+      // group 0 adds them in group order and runs the epilogue alone
+      __syncthreads();
+      double* red = As;  // [KS - 1][WM * WN * 32][MI * NI * 2]
+      constexpr int PER = MI * NI * 2;
+      if (kg > 0) {
+        double* mine = red + ((size_t)(kg - 1) * (WM * WN * 32) + warp_in * 32 + lane) * PER;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            mine[(mi * NI + ni) * 2] = acc[mi][ni][0];
+            mine[(mi * NI + ni) * 2 + 1] = acc[mi][ni][1];
+          }
+      }
+      __syncthreads();
+      if (kg > 0) continue;
+#pragma unroll
+      for (int q = 1; q < KS; ++q) {
+        const double* theirs = red + ((size_t)(q - 1) * (WM * WN * 32) + warp_in * 32 + lane) * PER;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            acc[mi][ni][0] += theirs[(mi * NI + ni) * 2];
+            acc[mi][ni][1] += theirs[(mi * NI + ni) * 2 + 1];
+          }
+      }
+    }
 
     // epilogue: C fragment (row = g, cols 2*t4, 2*t4+1) of each 8x8 sub-tile
 #pragma unroll
@@ -737,13 +774,18 @@ struct cqp_batch {
   int n = 0, m = 0, D = 0, L = 0;
   int ld_s = 0, ld_n = 0, ld_m = 0, ld_nm = 0;
   int Dm_pad = 0, nm_mpad = 0, n_mpad = 0, m_mpad = 0;
-  int grid_ctas[4] = {0, 0, 0, 0};  // persistent grid per tile configuration
+  int grid_ctas[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // persistent grid per tile configuration
   // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
   // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
   // (less wave quantisation, 12 warps/SM), 64x32 wins below ~3400 columns, 32x32 (6 CTAs/SM: more
   // warps to keep the tensor pipe fed when the grid no longer fills) below ~1400.
   int thr_big = 1 << 30, thr_mid = 3400, thr_small = 1400;
   int force_cfg = -1;
+  int small_cfg = 3;  // 32x32 tiles
+  // below thr_tiny columns: 32x32 tiles with 4 k-split warp groups (cfg 4; cfg 5 has 2).  Measured
+  // (B200, D = 1500): a round of <= 58 columns takes 0.62 instead of 0.72 ms; between 100 and 300
+  // columns the split is slower (the groups share the 4 DMMA pipes of their SM), so it stops at 64.
+  int tiny_cfg = 4, thr_tiny = 64;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evc0 = nullptr, evc1 = nullptr;
   float last_total_ms = 0.f, last_compute_ms = 0.f;
@@ -793,11 +835,15 @@ struct GemmConfig {
   int threads;
   int smem;
 };
-const GemmConfig kConfigs[4] = {
+constexpr int kNumConfigs = 6;
+const GemmConfig kConfigs[kNumConfigs] = {
     {dmma_gemm_kernel<128, 128, 2, 4, 1>, 256, gemm_smem_bytes<128, 128>()},
     {dmma_gemm_kernel<64, 64, 2, 2, 3>, 128, gemm_smem_bytes<64, 64>()},
     {dmma_gemm_kernel<64, 32, 2, 2, 4>, 128, gemm_smem_bytes<64, 32>()},
     {dmma_gemm_kernel<32, 32, 2, 2, 6>, 128, gemm_smem_bytes<32, 32>()},
+    // deeper pipelines for the latency-bound last rounds (CQP_BATCH_FORCE_CFG / thresholds)
+    {dmma_gemm_kernel<32, 32, 2, 2, 2, STAGES, 4>, 512, gemm_smem_bytes<32, 32>()},   // 4 k-split groups
+    {dmma_gemm_kernel<32, 32, 2, 2, 3, STAGES, 2>, 256, gemm_smem_bytes<32, 32>()},   // 2 k-split groups
 };
 
 // Tile shape for a round with (at most) `active` columns still iterating.
@@ -806,7 +852,8 @@ int pick_config(const cqp_batch* b, int active) {
   if (active >= b->thr_big) return 0;
   if (active >= b->thr_mid) return 1;
   if (active >= b->thr_small) return 2;
-  return 3;
+  if (active >= b->thr_tiny) return b->small_cfg;
+  return b->tiny_cfg;
 }
 
 int launch_gemm(cqp_batch* b, const GemmParams& p, int cfg) {
@@ -902,7 +949,7 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CQP_ERR_CUDA);
   cudaEventCreate(&b->ev0); cudaEventCreate(&b->ev1);
   cudaEventCreate(&b->evc0); cudaEventCreate(&b->evc1);
-  for (int cfg = 0; cfg < 4; ++cfg) {
+  for (int cfg = 0; cfg < kNumConfigs; ++cfg) {
     const GemmConfig& gc = kConfigs[cfg];
     if (cudaFuncSetAttribute(gc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gc.smem) != cudaSuccess)
       return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dmma_gemm_kernel)"));
@@ -923,6 +970,8 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   }
   if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
   if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
+  if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
+  if (const char* e = std::getenv("CQP_BATCH_TINY")) std::sscanf(e, "%d,%d", &b->tiny_cfg, &b->thr_tiny);
   int rc;
   const size_t cap = (size_t)capacity;
   const size_t slot_cap = cap + (size_t)L * SLOT_TILE, tile_cap = slot_cap / SLOT_TILE + L;
