@@ -90,6 +90,7 @@ struct RunParams {
   int check_interval, adaptive, early_exit, total_iters;
   int do_refresh;     // run Solver::refresh_z before the first iteration
   int fence_mode;     // 0: fence after re-arm (default); 1: none; 2: release-store publish
+  int poll_delay_ns;  // the fetching warps pause this long after `go` before their first poll of v_i
   int cap;            // capacity of the record arrays
   // receding-horizon control extraction (null Kt: none): u0 = clamp(-K x0 + y[0:nu], u_lo, u_hi)
   const double* mpc_K;   // [nu][nxpad] row-major

@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         // Like the loaders they start polling only once this CTA has published its own rows: earlier
         // polls cannot succeed and would compete with the W prefetch for L2 bandwidth.
         mbar_wait(go, (i - 1) & 1, p.dbg, 9, i);
+        if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);
         fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, t, nfetch, p.dbg, i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xready[b]);
@@ -607,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     } else if (loader) {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
+      if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);  // (see launch_run)
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
       if (streaming)
         fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, kComputeThreads + lt, nfetch,
@@ -934,6 +936,12 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
     p.mpc_nx = h->mpc_nx; p.mpc_nxpad = h->mpc_nxpad; p.mpc_nu = h->mpc_nu;
   }
   p.fence_mode = 0;
+  // The other CTAs publish within a few hundred ns of this one: a first poll issued right at `go`
+  // mostly finds sentinels and costs a second L2 round trip, and the extra polling traffic slows the
+  // publishes themselves.  A short pause before the first poll is a net win (B200, D = 900 / 1500:
+  // 2.90 -> 2.60 / 4.11 -> 3.78 us per iteration at 100-200 ns; 400 ns is too long).
+  p.poll_delay_ns = 150;
+  if (const char* e = std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = std::atoi(e);
   if (const char* fm = std::getenv("CQP_FENCE_MODE")) p.fence_mode = std::atoi(fm);  // experiment knob
   // grid-barrier counters ping-pong between launches: this launch counts on barrier[parity]
   // (zeroed by the previous launch, or at allocation) and zeroes the other one.
