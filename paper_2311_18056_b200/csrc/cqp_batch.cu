@@ -822,6 +822,7 @@ template <typename T>
 int balloc(T** p, size_t count) {
   CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1)));
   CQP_CUDA(cudaMemset(*p, 0, sizeof(T) * (count ? count : 1)));
+  CQP_CUDA(cudaStreamSynchronize(0));  // legacy-stream memset vs the batch's non-blocking stream
   return CQP_OK;
 }
 
@@ -903,6 +904,7 @@ int dense_gemm_create(DenseGemm** out, int N, int num_sms) {
   CQP_CUDA(cudaMemcpy(g->cols, cols.data(), sizeof(int) * slots, cudaMemcpyHostToDevice));
   CQP_CUDA(cudaMemcpy(g->tiles, td.data(), sizeof(TileDesc) * tiles, cudaMemcpyHostToDevice));
   CQP_CUDA(cudaMemcpy(g->n_tiles, &tiles, sizeof(int), cudaMemcpyHostToDevice));
+  CQP_CUDA(cudaStreamSynchronize(0));  // pageable sources: the DMAs may outlive the calls
   const GemmConfig& gc = kConfigs[1];
   CQP_CUDA(cudaFuncSetAttribute(gc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, gc.smem));
   int occ = 0;

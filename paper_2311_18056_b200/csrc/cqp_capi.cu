@@ -116,6 +116,7 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->state, 2))) return rc;
   if ((rc = dev_alloc(&h->barrier, 2))) return rc;
   CQP_CUDA(cudaMemset(h->barrier, 0, 2 * sizeof(unsigned)));
+  CQP_CUDA(cudaStreamSynchronize(0));  // legacy-stream memset vs the handle's non-blocking stream
   if ((rc = dev_alloc(&h->partial, 8 * (size_t)(h->num_sms + 1)))) return rc;
   if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
   if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
@@ -244,6 +245,7 @@ int cqp_create_from_layers(cqp_handle** out, int n, int m, int L, const double* 
         rho[(size_t)k * m + i] = (eq ? 1e3 : 1.0) * grid_values[k];
       }
     CQP_CUDA(cudaMemcpy(h->rho_vec, rho.data(), sizeof(double) * rho.size(), cudaMemcpyHostToDevice));
+    CQP_CUDA(cudaStreamSynchronize(0));  // (pageable source: the DMA may outlive the call)
   }
   if ((rc = upload_small(h, grid_values, E, F))) return fail(rc);
   if ((rc = upload_vectors(h, g, c, d))) return fail(rc);

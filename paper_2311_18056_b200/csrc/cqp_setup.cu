@@ -296,6 +296,9 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   auto talloc = [&](double** p, size_t cnt) -> int {
     if (cudaMalloc(reinterpret_cast<void**>(p), sizeof(double) * (cnt ? cnt : 1)) != cudaSuccess) return (int)CQP_ERR_CUDA;
     if (cudaMemset(*p, 0, sizeof(double) * (cnt ? cnt : 1)) != cudaSuccess) return (int)CQP_ERR_CUDA;
+    // cudaMemset runs on the legacy default stream, which does NOT order against the
+    // cudaStreamNonBlocking streams the kernels below use: wait for it here
+    if (cudaStreamSynchronize(0) != cudaSuccess) return (int)CQP_ERR_CUDA;
     temps.push_back(*p);
     return (int)CQP_OK;
   };
@@ -333,6 +336,10 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   double* dH = nullptr;
   TRY(talloc(&dH, (size_t)n * ld_n));
   TRYCUDA(cudaMemcpy2D(dH, sizeof(double) * ld_n, H, sizeof(double) * n, sizeof(double) * n, n, cudaMemcpyHostToDevice));
+  // (a synchronous copy from pageable memory may return before its DMA has landed, and the legacy
+  // stream does not order against st0: without this wait the factorisation could read a partial H
+  // and report a spurious non-positive pivot)
+  TRYCUDA(cudaStreamSynchronize(0));
   TRY(cholesky(dH, st0));
   int info = 0;
   TRY(read_fail(st0, &info));
