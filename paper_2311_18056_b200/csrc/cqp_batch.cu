@@ -62,6 +62,15 @@ struct GemmParams {
   const double* lo;    // [col][ld_lohi], rows n..nm-1
   const double* hi;
   int ld_lohi;
+  // Structured layer (mode 1 only; split == 0: plain dense layer).  The third block row of W is
+  // [rho G, -diag(rho), I] (/root/reference/proj/src/layers.cpp:159-161): of its D columns only
+  // the first n are dense.  The padded copy of W therefore stores rows 0 .. n+m-1 at padded rows
+  // 0 .. split-1 and rows n+m .. D-1 (their first n columns; the rest zeroed) at padded rows
+  // split ..; tiles of the second part run k_tiles3 = ceil(n / 16) k-tiles instead of k_tiles and
+  // get the two diagonal terms  -rho_i z_i + lambda_i  as the accumulator's start value.
+  int split;             // padded row where the lambda block starts (multiple of 128), 0 = dense
+  int k_tiles3;
+  const double* negrho;  // [a_index][m]: W(n+m+i, n+i) = -rho_i
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -117,14 +126,31 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
   const int m_tiles = p.M_pad / BM;
   const int total = (*p.n_tiles) * SUB * m_tiles;
 
+  // Structured layer: the short lambda-row tiles (k_tiles3 k-tiles) are ordered after all the long
+  // ones, so that the static striding hands every CTA a similar mix (longest-first).
+  const int m_long = (p.split > 0) ? p.split / BM : m_tiles, m_short = m_tiles - m_long;
+  const int total_long = (*p.n_tiles) * SUB * m_long;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int ns = item / m_tiles, mt = item - ns * m_tiles;
+    int ns, mt;
+    if (item < total_long) {
+      ns = item / m_long;
+      mt = item - ns * m_long;
+    } else {
+      const int j = item - total_long;
+      ns = j / m_short;
+      mt = m_long + (j - ns * m_short);
+    }
     const int nt = ns / SUB, sub = ns - nt * SUB;
     const TileDesc td = p.tiles[nt];
     const int slot0 = td.slot0 + sub * BN;
     if (p.cols[slot0] < 0) continue;  // padding slots sit at the end of a bucket: empty sub-tile
     const int m0 = mt * BM;
-    if (m0 >= p.M) continue;
+    // padded row m0 -> actual row; valid rows of this part end at row_end; k-tiles of this part
+    const bool blk3 = p.split > 0 && m0 >= p.split;
+    const int row0 = blk3 ? m0 - p.split + p.nm : m0;
+    const int row_end = (p.split > 0 && !blk3) ? p.nm : p.M;
+    const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
+    if (row0 >= row_end) continue;
     const double* A = p.A + (size_t)td.a_index * p.a_stride + (size_t)m0 * p.lda;
     __syncthreads();  // previous item's readers of cols_s / smem are done
     if (tid < BN) cols_s[tid] = p.cols[slot0 + tid];
@@ -166,7 +192,7 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
 
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-      if (s < p.k_tiles) issue(s, s);
+      if (s < k_tiles) issue(s, s);
       cp_async_commit();
     }
     // Accumulators start from the bias (mode 1: v = bias + W s; alpha is 1 there), so its global
@@ -181,24 +207,30 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
         const int col = cols_s[warp_n * TN + ni * 8 + 2 * t4 + j];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
-          const int row = m0 + warp_m * TM + mi * 8 + g;
+          const int row = row0 + warp_m * TM + mi * 8 + g;
           double init = 0.0;
-          if (p.mode == 1 && col >= 0 && row < p.nm && kg == 0) {
-            init = p.bias[(size_t)col * p.ld_bias + row];
-            if (row >= p.n && g == 0) {  // one prefetch per 64-byte run of 8 rows
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lo + (size_t)col * p.ld_lohi + row - p.n));
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.hi + (size_t)col * p.ld_lohi + row - p.n));
+          if (p.mode == 1 && col >= 0 && kg == 0) {
+            if (row < p.nm) {
+              init = p.bias[(size_t)col * p.ld_bias + row];
+              if (row >= p.n && g == 0) {  // one prefetch per 64-byte run of 8 rows
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lo + (size_t)col * p.ld_lohi + row - p.n));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.hi + (size_t)col * p.ld_lohi + row - p.n));
+              }
+            } else if (blk3 && row < p.M) {  // lambda row i: the diagonal blocks (3,2) = -rho, (3,3) = I
+              const double* v = p.Bm + (size_t)col * p.ldb;
+              const int i = row - p.nm;
+              init = fma(p.negrho[(size_t)td.a_index * (p.M - p.nm) + i], v[p.n + i], v[row]);
             }
           }
           acc[mi][ni][j] = init;
         }
       }
     }
-    for (int kt = 0; kt < p.k_tiles; ++kt) {
+    for (int kt = 0; kt < k_tiles; ++kt) {
       cp_async_wait<ST - 2>();
       __syncthreads();
       const int next = kt + ST - 1;
-      if (next < p.k_tiles) issue(next, next % ST);
+      if (next < k_tiles) issue(next, next % ST);
       cp_async_commit();
       const double* as = As + (kt % ST) * BM * BK + (warp_m * TM) * BK;
       const double* bs = Bs + (kt % ST) * BN * BK + (warp_n * TN) * BK;
@@ -260,8 +292,8 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
         double* crow = p.C + (size_t)col * p.ldc;
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
-          const int row = m0 + warp_m * TM + mi * 8 + g;
-          if (row >= p.M) continue;
+          const int row = row0 + warp_m * TM + mi * 8 + g;
+          if (row >= row_end) continue;
           double v = acc[mi][ni][j];
           if (p.mode != 1) v *= p.alpha;
           if (p.mode == 1 && row < p.nm) {
@@ -279,210 +311,6 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
   }
 }
 
-// ---- persistent round kernel ---------------------------------------------------------------
-// The columns of S are independent QPs: iteration i + 1 of a column strip depends only on
-// iteration i of the SAME strip.  So a whole check round (25 iterations) runs as ONE cooperative
-// launch: the grid is cut into teams of `team` CTAs, a team owns a strip of <= 64 same-rho columns
-// and runs all iterations of the round on it, its CTAs splitting the row tiles and synchronising
-// with each other only (one counter per strip).  No launch per iteration, no grid-wide wave tail,
-// teams drift freely.  Strip widths are chosen by batch_regroup_kernel so that the strips fill
-// the teams.  Same tile code and k order per output element as dmma_gemm_kernel<64, 64, 2, 2>:
-// results are bit-identical to the per-iteration launches.
-// STATUS: correct (tests/test_gpu_batch.py passes with CQP_BATCH_PERSISTENT=1) but OPT-IN: measured
-// on B200 at B = 4096 it is slower than 25 launches per round (420 vs 308 ms per solve).  A 56-wide
-// strip costs as much as a 64-wide one with the 2 x 2 warp grid (4 + 3 column groups), so the 74
-// strips are 15 % more tile work than the 1536 tiles of the launch-per-iteration path, whose own
-// wave tail costs only ~3 %; and with fewer columns a round's time is set by the per-item K-loop
-// latency, not by the strip width.  Kept for the next round (4 x 1 warp grid, K-split for narrow
-// strips).
-struct StripDesc {
-  int slot0;    // first slot of the strip
-  int ncols;    // valid columns (<= 64)
-  int a_index;  // ladder index of the strip's bucket
-  int pad;
-};
-
-struct RoundParams {
-  GemmParams g;          // A = W ladder, bias / bounds; Bm and C are set per iteration
-  double* S0;            // iteration `it` reads (it even ? S0 : S1) and writes the other one
-  double* S1;
-  const StripDesc* strips;
-  const int* n_strips;
-  int* team_ctr;         // [strip] arrivals of the strip's team (zeroed by the regroup kernel)
-  int team;              // CTAs per team
-  int steps;             // iterations of this round
-};
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void __launch_bounds__(128, 3) dmma_round_kernel(const RoundParams rp) {
-  constexpr int BM = 64, BN = 64, WM = 2, WN = 2, T = WM * WN * 32;
-  constexpr int TM = BM / WM, MI = TM / 8, NI = 4;  // up to 4 column groups of 8 per warp
-  const GemmParams& p = rp.g;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* As = reinterpret_cast<double*>(smem_raw);
-  double* Bs = As + STAGES * BM * BK;
-  int* cols_s = reinterpret_cast<int*>(Bs + STAGES * BN * BK);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int warp_m = warp % WM, warp_n = warp / WM;
-  const int m_tiles = (p.M + BM - 1) / BM;
-  const int n_teams = (int)gridDim.x / rp.team;
-  const int team_id = (int)blockIdx.x / rp.team, member = (int)blockIdx.x - team_id * rp.team;
-  if (team_id >= n_teams) return;
-  const int n_strips = *rp.n_strips;
-
-  for (int sidx = team_id; sidx < n_strips; sidx += n_teams) {
-    const StripDesc sd = rp.strips[sidx];
-    const int ngroups = (sd.ncols + 7) >> 3;            // column groups of 8 in the strip
-    const int gpw = (ngroups + WN - 1) / WN;             // groups per warp column
-    const int g0 = warp_n * gpw;                         // this warp's first group
-    const int nw = max(0, min(gpw, ngroups - g0));       // ... and how many it has (<= NI)
-    const double* Abase = p.A + (size_t)sd.a_index * p.a_stride;
-    __syncthreads();
-    if (tid < BN) cols_s[tid] = (tid < ngroups * 8) ? p.cols[sd.slot0 + tid] : -1;
-    __syncthreads();
-    // B copy plan (invariant over k, row tiles and iterations up to the buffer base)
-    constexpr int ACH = BM * 8 / T, BCH = BN * 8 / T;
-    size_t boff[BCH];
-    int bdst[BCH], bbytes[BCH];
-    bool bon[BCH];
-#pragma unroll
-    for (int i = 0; i < BCH; ++i) {
-      const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
-      const int col = cols_s[r];
-      boff[i] = (size_t)(col < 0 ? 0 : col) * p.ldb + c * 2;
-      bdst[i] = r * BK + ((c ^ ((r & 3) << 1)) << 1);
-      bbytes[i] = col < 0 ? 0 : 16;
-      bon[i] = r < ngroups * 8;
-    }
-    int adst[ACH];
-#pragma unroll
-    for (int i = 0; i < ACH; ++i) {
-      const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
-      adst[i] = r * BK + ((c ^ ((r & 3) << 1)) << 1);
-    }
-
-    for (int it = 0; it < rp.steps; ++it) {
-      const double* Sin = (it & 1) ? rp.S1 : rp.S0;
-      double* Sout = (it & 1) ? rp.S0 : rp.S1;
-      for (int mt = member; mt < m_tiles; mt += rp.team) {
-        const int m0 = mt * BM;
-        const double* A = Abase + (size_t)m0 * p.lda;
-        __syncthreads();  // previous item's readers of the stage buffers are done
-        auto issue = [&](int kt, int stage) {
-          const int k0 = kt * BK;
-          double* as = As + stage * BM * BK;
-          double* bs = Bs + stage * BN * BK;
-#pragma unroll
-          for (int i = 0; i < ACH; ++i) {
-            const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
-            cp_async16(as + adst[i], A + (size_t)r * p.lda + c * 2 + k0, 16);
-          }
-#pragma unroll
-          for (int i = 0; i < BCH; ++i)
-            if (bon[i]) cp_async16(bs + bdst[i], Sin + boff[i] + k0, bbytes[i]);
-        };
-#pragma unroll
-        for (int s = 0; s < STAGES - 1; ++s) {
-          if (s < p.k_tiles) issue(s, s);
-          cp_async_commit();
-        }
-        double acc[MI][NI][2];
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int col = ni < nw ? cols_s[(g0 + ni) * 8 + 2 * t4 + j] : -1;
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi) {
-              const int row = m0 + warp_m * TM + mi * 8 + g;
-              double init = 0.0;
-              if (col >= 0 && row < p.nm) {
-                init = p.bias[(size_t)col * p.ld_bias + row];
-                if (row >= p.n && g == 0) {
-                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p.lo + (size_t)col * p.ld_lohi + row - p.n));
-                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p.hi + (size_t)col * p.ld_lohi + row - p.n));
-                }
-              }
-              acc[mi][ni][j] = init;
-            }
-          }
-        }
-        for (int kt = 0; kt < p.k_tiles; ++kt) {
-          cp_async_wait<STAGES - 2>();
-          __syncthreads();
-          const int next = kt + STAGES - 1;
-          if (next < p.k_tiles) issue(next, next % STAGES);
-          cp_async_commit();
-          const double* as = As + (kt % STAGES) * BM * BK + (warp_m * TM) * BK;
-          const double* bs = Bs + (kt % STAGES) * BN * BK + (g0 * 8) * BK;
-#pragma unroll
-          for (int ks = 0; ks < BK / 4; ++ks) {
-            const int e = ks * 4 + t4;
-            const int off = (((e >> 1) ^ ((g & 3) << 1)) << 1) | (e & 1);
-            double a[MI], b[NI];
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi) a[mi] = as[(mi * 8 + g) * BK + off];
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) b[ni] = ni < nw ? bs[(ni * 8 + g) * BK + off] : 0.0;
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) {
-              if (ni < nw) {
-#pragma unroll
-                for (int mi = 0; mi < MI; ++mi) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-              }
-            }
-          }
-        }
-        cp_async_wait<0>();
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          if (ni >= nw) continue;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int col = cols_s[(g0 + ni) * 8 + 2 * t4 + j];
-            if (col < 0) continue;
-            double* crow = Sout + (size_t)col * p.ldc;
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi) {
-              const int row = m0 + warp_m * TM + mi * 8 + g;
-              if (row >= p.M) continue;
-              double v = acc[mi][ni][j];
-              if (row < p.nm && row >= p.n) {
-                const double lo = p.lo[(size_t)col * p.ld_lohi + row - p.n];
-                const double hi = p.hi[(size_t)col * p.ld_lohi + row - p.n];
-                v = v < lo ? lo : v;
-                v = v > hi ? hi : v;
-              }
-              crow[row] = v;
-            }
-          }
-        }
-      }
-      if (it + 1 < rp.steps) {
-        // team barrier: every CTA of the team has written its rows of iteration `it`
-        __syncthreads();
-        if (tid == 0) {
-          __threadfence();
-          atomicAdd(rp.team_ctr + sidx, 1);
-          const int want = rp.team * (it + 1);
-          long long t0 = clock64();
-          while (ld_acquire_gpu(rp.team_ctr + sidx) < want) {
-            if (clock64() - t0 > 8000000000ll) __trap();  // ~4 s: a lost team mate must not hang the box
-          }
-        }
-        __syncthreads();
-      }
-    }
-  }
-}
-
 // dst[a][r][c] (rows_pad x ld_dst, zero padded) <- src[a][r][c] (rows x ld_src, first `cols`)
 __global__ void repad_kernel(const double* __restrict__ src, int rows, int cols, int ld_src,
                              size_t src_stride, double* __restrict__ dst, int rows_pad, int ld_dst,
@@ -495,6 +323,15 @@ __global__ void repad_kernel(const double* __restrict__ src, int rows, int cols,
   const int r = (int)(rem / ld_dst), c = (int)(rem % ld_dst);
   dst[(size_t)a * dst_stride + rem] =
       (r < rows && c < cols) ? src[(size_t)a * src_stride + (size_t)r * ld_src + c] : 0.0;
+}
+
+// negrho[a][i] = W_a(n+m+i, n+i) = -rho_i: the diagonal of block (3,2) (layers.cpp:160)
+__global__ void extract_negrho_kernel(const double* __restrict__ W, int ld, size_t stride, int n, int m,
+                                      double* __restrict__ negrho, int count) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * count) return;
+  const int a = idx / m, i = idx - a * m;
+  negrho[idx] = W[(size_t)a * stride + (size_t)(n + m + i) * ld + n + i];
 }
 
 struct BatchDev {
@@ -540,12 +377,6 @@ struct BatchDev {
   TileDesc* tiles;   // [tile_cap]
   int* n_tiles;
   int* n_active;
-  // strips of the persistent round kernel (see dmma_round_kernel)
-  StripDesc* strips;
-  int* n_strips;
-  int* team_ctr;
-  int strip_cap;
-  int n_teams_next;  // teams of the NEXT round's launch (0: per-iteration launches, no strips needed)
   // settings
   double eps_prim, eps_dual, threshold;
   int adaptive, max_iters;
@@ -691,7 +522,6 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
 __global__ void batch_regroup_kernel(BatchDev b) {
   __shared__ int warp_sums[32];
   __shared__ int base_s, slot_base_s, total_active_s;
-  __shared__ int bucket_count[64], bucket_base[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (tid == 0) { slot_base_s = 0; total_active_s = 0; }
   __syncthreads();
@@ -719,7 +549,6 @@ __global__ void batch_regroup_kernel(BatchDev b) {
     }
     const int count = base_s;
     const int padded = (count + SLOT_TILE - 1) / SLOT_TILE * SLOT_TILE;
-    if (tid == 0 && k < 64) { bucket_count[k] = count; bucket_base[k] = slot_base_s; }
     for (int i = count + tid; i < padded; i += blockDim.x) b.cols[slot_base_s + i] = -1;
     for (int t = tid; t < padded / SLOT_TILE; t += blockDim.x) {
       b.tiles[n_tiles + t].slot0 = slot_base_s + t * SLOT_TILE;
@@ -731,36 +560,6 @@ __global__ void batch_regroup_kernel(BatchDev b) {
     __syncthreads();
   }
   if (tid == 0) { *b.n_tiles = n_tiles; *b.n_active = total_active_s; }
-  // Strips for the persistent round kernel: the narrowest width w (multiple of 8, <= 64) whose
-  // strip count fits p passes over the teams, for the smallest such p.  Every bucket is cut into
-  // strips of w slots (the last one of a bucket may be narrower); padding slots stay -1.
-  if (tid == 0 && b.n_teams_next > 0) {
-    const int L = b.L < 64 ? b.L : 64;
-    int w = 64;
-    for (int pass = 1; pass <= 64; ++pass) {
-      bool found = false;
-      for (int cand = 8; cand <= 64; cand += 8) {
-        int cnt = 0;
-        for (int k = 0; k < L; ++k) cnt += (bucket_count[k] + cand - 1) / cand;
-        if (cnt <= pass * b.n_teams_next) { w = cand; found = true; break; }
-      }
-      if (found) break;
-    }
-    int ns = 0;
-    for (int k = 0; k < L; ++k) {
-      for (int off = 0; off < bucket_count[k] && ns < b.strip_cap; off += w) {
-        StripDesc sd;
-        sd.slot0 = bucket_base[k] + off;
-        sd.ncols = min(w, bucket_count[k] - off);
-        sd.a_index = k;
-        sd.pad = 0;
-        b.strips[ns] = sd;
-        b.team_ctr[ns] = 0;
-        ++ns;
-      }
-    }
-    *b.n_strips = ns;
-  }
 }
 
 }  // namespace
@@ -774,6 +573,10 @@ struct cqp_batch {
   int n = 0, m = 0, D = 0, L = 0;
   int ld_s = 0, ld_n = 0, ld_m = 0, ld_nm = 0;
   int Dm_pad = 0, nm_mpad = 0, n_mpad = 0, m_mpad = 0;
+  // Structured layer: the lambda rows of W only multiply y (see GemmParams::split).  Default on;
+  // CQP_BATCH_DENSE=1 keeps the plain dense layer for A/B runs.
+  int split = 0;
+  double* negrho = nullptr;
   int grid_ctas[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // persistent grid per tile configuration
   // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
   // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
@@ -806,12 +609,6 @@ struct cqp_batch {
   int* cols = nullptr;
   TileDesc* tiles = nullptr;
   int *n_tiles = nullptr, *n_active = nullptr;
-  StripDesc* strips = nullptr;   // persistent round kernel: strip list, its length, team counters
-  int* n_strips = nullptr;
-  int* team_ctr = nullptr;
-  int strip_cap = 0;
-  int round_grid = 0;            // resident CTAs of dmma_round_kernel (3 per SM)
-  int persistent = 0;            // CQP_BATCH_PERSISTENT=1 opts in (measured slower, see dmma_round_kernel)
   int* h_active = nullptr;  // pinned, one word per round
   int h_active_cap = 0;
 };
@@ -945,8 +742,12 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   const int n = b->n, m = b->m, D = b->D, L = b->L, nm = n + m;
   b->ld_s = round_up_i(D, BK); b->ld_n = round_up_i(n, BK); b->ld_m = round_up_i(m, BK);
   b->ld_nm = round_up_i(nm, 2);
-  b->Dm_pad = round_up_i(D, 128); b->nm_mpad = round_up_i(nm, 128);
+  b->nm_mpad = round_up_i(nm, 128);
   b->n_mpad = round_up_i(n, 128); b->m_mpad = round_up_i(m, 128);
+  int dense = 0;
+  if (const char* e = std::getenv("CQP_BATCH_DENSE")) dense = std::atoi(e);
+  b->split = dense ? 0 : b->nm_mpad;
+  b->Dm_pad = dense ? round_up_i(D, 128) : b->nm_mpad + b->m_mpad;
   auto fail = [&](int rc) { cqp_batch_destroy(b); return rc; };
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(CQP_ERR_CUDA);
   cudaEventCreate(&b->ev0); cudaEventCreate(&b->ev1);
@@ -960,16 +761,6 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
       return fail(cuda_fail(cudaGetLastError(), "occupancy(dmma_gemm_kernel)"));
     b->grid_ctas[cfg] = occ * h->num_sms;
   }
-  {
-    const int smem = gemm_smem_bytes<64, 64>();
-    if (cudaFuncSetAttribute(dmma_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(dmma_round_kernel)"));
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dmma_round_kernel, 128, smem) != cudaSuccess || occ < 1)
-      return fail(cuda_fail(cudaGetLastError(), "occupancy(dmma_round_kernel)"));
-    b->round_grid = occ * h->num_sms;
-    if (const char* e = std::getenv("CQP_BATCH_PERSISTENT")) b->persistent = std::atoi(e);
-  }
   if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
   if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
@@ -979,6 +770,7 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   const size_t slot_cap = cap + (size_t)L * SLOT_TILE, tile_cap = slot_cap / SLOT_TILE + L;
 #define BA(ptr, count) if ((rc = balloc(&b->ptr, (count)))) return fail(rc)
   BA(Wb, (size_t)L * b->Dm_pad * b->ld_s);
+  BA(negrho, (size_t)L * m);
   BA(DGb, (size_t)L * b->nm_mpad * b->ld_n);
   BA(Hb, (size_t)b->n_mpad * b->ld_n);
   BA(Gb, (size_t)b->m_mpad * b->ld_n);
@@ -991,12 +783,20 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   BA(layer, cap); BA(active, cap); BA(iters, cap); BA(status, cap); BA(nsw, cap);
   BA(rp, cap); BA(rd, cap); BA(out_y, cap * n); BA(out_z, cap * m); BA(out_l, cap * m);
   BA(cols, slot_cap); BA(tiles, tile_cap); BA(n_tiles, 1); BA(n_active, 1);
-  b->strip_cap = (int)(slot_cap / 8 + L);
-  BA(strips, b->strip_cap); BA(n_strips, 1); BA(team_ctr, b->strip_cap);
 #undef BA
   // shared matrices: handle layouts (row-major, even ld) -> tile-padded copies
-  if ((rc = repad(b, h->W, D, D, h->Dpad, (size_t)D * h->Dpad, b->Wb, b->Dm_pad, b->ld_s,
-                  (size_t)b->Dm_pad * b->ld_s, L))) return fail(rc);
+  if (b->split == 0) {
+    if ((rc = repad(b, h->W, D, D, h->Dpad, (size_t)D * h->Dpad, b->Wb, b->Dm_pad, b->ld_s,
+                    (size_t)b->Dm_pad * b->ld_s, L))) return fail(rc);
+  } else {
+    // rows 0 .. n+m-1 in full; rows n+m .. D-1 from padded row `split` on, first n columns only
+    if ((rc = repad(b, h->W, nm, D, h->Dpad, (size_t)D * h->Dpad, b->Wb, b->nm_mpad, b->ld_s,
+                    (size_t)b->Dm_pad * b->ld_s, L))) return fail(rc);
+    if ((rc = repad(b, h->W + (size_t)nm * h->Dpad, m, n, h->Dpad, (size_t)D * h->Dpad,
+                    b->Wb + (size_t)b->split * b->ld_s, b->m_mpad, b->ld_s, (size_t)b->Dm_pad * b->ld_s, L))) return fail(rc);
+    extract_negrho_kernel<<<(m * L + 255) / 256, 256, 0, b->stream>>>(h->W, h->Dpad, (size_t)D * h->Dpad, n, m, b->negrho, L);
+    if (cudaGetLastError() != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "extract_negrho_kernel"));
+  }
   if ((rc = repad(b, h->Dk, nm, n, h->npad, (size_t)nm * h->npad, b->DGb, b->nm_mpad, b->ld_n,
                   (size_t)b->nm_mpad * b->ld_n, L))) return fail(rc);
   if ((rc = repad(b, h->H, n, n, h->npad, 0, b->Hb, b->n_mpad, b->ld_n, 0, 1))) return fail(rc);
@@ -1011,10 +811,10 @@ void cqp_batch_destroy(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
-                  b->tiles, b->n_tiles, b->n_active, b->strips, b->n_strips, b->team_ctr};
+                  b->tiles, b->n_tiles, b->n_active};
   for (void* p : ptrs) cudaFree(p);
   if (b->h_active) cudaFreeHost(b->h_active);
   for (cudaEvent_t e : b->round_events) cudaEventDestroy(e);
@@ -1074,8 +874,6 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   bd.nsw = b->nsw; bd.rp = b->rp; bd.rd = b->rd;
   bd.out_y = b->out_y; bd.out_z = b->out_z; bd.out_l = b->out_l;
   bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
-  bd.strips = b->strips; bd.n_strips = b->n_strips; bd.team_ctr = b->team_ctr; bd.strip_cap = b->strip_cap;
-  bd.n_teams_next = 0;
   bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
   bd.adaptive = s.adaptive_rho; bd.max_iters = s.max_iters;
 
@@ -1101,6 +899,7 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     p.Bm = Sin; p.ldb = b->ld_s; p.C = Sout; p.ldc = b->ld_s; p.mode = 1;
     p.bias = b->bias; p.ld_bias = b->ld_nm; p.nm = nm; p.n = n;
     p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
+    p.split = b->split; p.k_tiles3 = b->ld_n / BK; p.negrho = b->negrho;
     return launch_gemm(b, p, cfg);
   };
   auto gemm_plain = [&](const double* A, int M, int m_pad, int lda, const double* Bm, int ldb, double* C, int ldc, int cfg) {
@@ -1110,35 +909,7 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     return launch_gemm(b, p, cfg);
   };
 
-  // Persistent round kernel: CTAs per team for a round that starts with (at most) `active` columns;
-  // 0 = per-iteration launches (too few columns to fill even the widest teams).  A team of T CTAs
-  // splits the 64-row tiles of W; fewer columns -> fewer, larger teams.
-  auto team_size = [&](int active) {
-    if (!b->persistent || b->D < 256) return 0;
-    for (int T : {6, 12, 24})
-      if (active >= 32 * (b->round_grid / T)) return T;
-    return 0;
-  };
-  auto launch_round = [&](double* S0, double* S1, int team, int steps) {
-    RoundParams rp{};
-    rp.g = base;
-    rp.g.A = b->Wb; rp.g.a_stride = (size_t)b->Dm_pad * b->ld_s; rp.g.lda = b->ld_s; rp.g.M = b->D;
-    rp.g.M_pad = b->Dm_pad; rp.g.k_tiles = b->ld_s / BK; rp.g.ldb = b->ld_s; rp.g.ldc = b->ld_s; rp.g.mode = 1;
-    rp.g.bias = b->bias; rp.g.ld_bias = b->ld_nm; rp.g.nm = nm; rp.g.n = n;
-    rp.g.lo = b->lo; rp.g.hi = b->hi; rp.g.ld_lohi = b->ld_m;
-    rp.S0 = S0; rp.S1 = S1; rp.strips = b->strips; rp.n_strips = b->n_strips; rp.team_ctr = b->team_ctr;
-    rp.team = team; rp.steps = steps;
-    void* args[] = {&rp};
-    const int grid = (b->round_grid / team) * team;
-    b->last_launches += 1;
-    CQP_CUDA(cudaLaunchCooperativeKernel((const void*)dmma_round_kernel, dim3(grid), dim3(128), args,
-                                         (size_t)gemm_smem_bytes<64, 64>(), st));
-    return (int)CQP_OK;
-  };
-
   int rc;
-  int team_next = team_size(B);  // team size of the round whose regroup is enqueued next
-  bd.n_teams_next = team_next ? b->round_grid / team_next : 0;
   batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
   CQP_CUDA(cudaGetLastError());
   b->last_launches += 2;  // prepare, regroup
@@ -1155,16 +926,10 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     const int steps = (r < full_rounds) ? interval : rem;
     // the host knows the active count with a lag of two rounds; it only decreases
     const int cfg = pick_config(b, r >= 2 ? b->h_active[r - 2] : B);
-    const int team = team_next;  // (its strips were built by the regroup kernel enqueued last)
     CQP_CUDA(cudaEventRecord(b->it0[r], st));
-    if (team > 0) {
-      if ((rc = launch_round(Sa, Sb, team, steps))) return rc;
-      if (steps & 1) std::swap(Sa, Sb);
-    } else {
-      for (int k = 0; k < steps; ++k) {
-        if ((rc = gemm_iter(Sa, Sb, cfg))) return rc;
-        std::swap(Sa, Sb);
-      }
+    for (int k = 0; k < steps; ++k) {
+      if ((rc = gemm_iter(Sa, Sb, cfg))) return rc;
+      std::swap(Sa, Sb);
     }
     CQP_CUDA(cudaEventRecord(b->it1[r], st));
     rounds_done = r + 1;
@@ -1179,8 +944,6 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m, cfg))) return rc;
     batch_decide_kernel<<<(B + 7) / 8, 256, 0, st>>>(bd, it, r < full_rounds ? 1 : 0, 1);
     CQP_CUDA(cudaGetLastError());
-    team_next = team_size(r >= 2 ? b->h_active[r - 2] : B);  // what the host knows now (it only shrinks)
-    bd.n_teams_next = team_next ? b->round_grid / team_next : 0;
     batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
     CQP_CUDA(cudaGetLastError());
     CQP_CUDA(cudaMemcpyAsync(&b->h_active[r], b->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1215,7 +978,11 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     b->round_ms[r] = ms;
     b->round_active[r] = (int)active;
     b->last_gemm_ms += ms;
-    b->last_gemm_flops += 2.0 * (double)b->D * (double)b->D * active * steps;
+    // executed flops: the structured layer skips the zeros of blocks (3,2), (3,3) (4 m^2 flop) and
+    // keeps their diagonals (2 FMA per lambda row)
+    const double per_col = b->split ? 2.0 * ((double)nm * b->D + (double)m * n) + 4.0 * m
+                                    : 2.0 * (double)b->D * (double)b->D;
+    b->last_gemm_flops += per_col * active * steps;
   }
   cudaEventElapsedTime(&b->last_total_ms, b->ev0, b->ev1);
   cudaEventElapsedTime(&b->last_compute_ms, b->evc0, b->evc1);
