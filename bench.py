@@ -14,8 +14,9 @@ collective; only a small result summary is gathered).
   e2e    = QPs/s through the C-ABI call cqp_batch_solve with HOST buffers: host->device copy of
            (g, c, d), the solve, device->host copy of (y, z, lambda, status, ...) all inside the
            timed region
-  roofline = the iteration GEMM (dmma_gemm_kernel): algorithmic 2 D^2 flop per active column per
-           iteration / CUDA-event time of those launches, against the FP64 GEMM rate cuBLAS
+  roofline = the iteration GEMM (dmma_gemm_kernel): EXECUTED flop per active column per iteration
+           (2 ((n+m) D + m n): the zero blocks (3,2), (3,3) of W are skipped, so less than the
+           dense 2 D^2) / CUDA-event time of those launches, against the FP64 GEMM rate cuBLAS
            reaches on this GPU measured in the same run (MEASURED_PEAKS.json has no FP64 entry)
   cpu_baseline = the CPU oracle (a restatement of the reference solver, compiled like the
            reference: -O3 -DNDEBUG, no -march) on a bounded sample of the same instances
@@ -159,6 +160,13 @@ def reference_arm(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def read_stream_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "stream_traffic.json"))).get("dram_bytes_per_iteration")
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def measure_dgemm_peak():
     import torch
     a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
@@ -223,12 +231,13 @@ def single_qp_sweep(S, problems, repeats: int = 7):
             cpu_ms.append(ro.wall_ms)
         D = 3 * base.n
         it = rep.solution.iterations
+        info = gs.launch_info()
         k50, w50, c50 = statistics.median(ker), statistics.median(wall), statistics.median(cpu_ms) * 1e3
         out.append({"nu": nu, "D": D, "iterations": it, "cpu_iterations": ro.solution.iterations,
                     "rho_trace_equal": rep.solution.rho_trace == ro.solution.rho_trace,
                     "gpu_kernel_us_p50": k50, "gpu_wall_us_p50": w50, "cpu_us_p50": c50,
                     "speedup_wall": c50 / w50, "us_per_iteration": k50 / it,
-                    "smem_stream_GBs": 8.0 * D * D * it / (k50 * 1e-6) / 1e9, "launch": gs.launch_info()})
+                    "smem_stream_GBs": info["w_bytes_per_iteration"] * it / (k50 * 1e-6) / 1e9, "launch": info})
         gs.close()
     return out
 
@@ -270,15 +279,18 @@ def mpc_step_section(S, problems, peaks):
             u = np.clip(-K @ x + rep.solution.y[:nu], wl.limits.u_lo, wl.limits.u_hi)
             x = A @ x + B @ u
         D = base.n + 2 * base.m
+        info = gs.launch_info()
+        wbytes = info["w_bytes_per_iteration"]      # bytes of W one iteration reads (structured: < 8 D^2)
         w50, k50 = statistics.median(wall[20:]), statistics.median(ker[20:])
         out.append({"workload": name, "n": base.n, "m": base.m, "D": D, "iters_per_step": k,
                     "initial_solve_iterations": r0.solution.iterations, "initial_solve_kernel_us": r0.kernel_us,
                     "step_wall_us_p50": w50, "step_kernel_us_p50": k50, "step_hz": 1e6 / w50,
                     "step_cabi_wall_us_p50": statistics.median(cabi[20:]),
                     "step_wall_us_p50_host_instantiate": statistics.median(wall_gcd[10:]),
-                    "W_stream_GBs": 8.0 * D * D * k / (k50 * 1e-6) / 1e9,
-                    "W_stream_frac_of_hbm_peak": 8.0 * D * D * k / (k50 * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6650.0),
-                    "launch": gs.launch_info()})
+                    "W_bytes_per_iteration": wbytes, "dense_W_bytes_per_iteration": 8.0 * D * D,
+                    "W_stream_GBs": wbytes * k / (k50 * 1e-6) / 1e9,
+                    "W_stream_frac_of_hbm_peak": wbytes * k / (k50 * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                    "launch": info})
         gs.close()
     return out
 
@@ -344,6 +356,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     dgemm_peak = measure_dgemm_peak()
     achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12
     D = n + 2 * m
+    flop_col = 2 * ((n + m) * D + m * n) + 4 * m     # executed per active column per iteration
+    dense_equiv = achieved * (2 * D * D) / flop_col   # what a dense-W kernel would need for the same solves
     traffic = None
     prof = os.path.join(ROOT, "profiles", "dmma_gemm_traffic.json")
     if os.path.exists(prof):
@@ -393,7 +407,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
                      "frac": achieved / dgemm_peak, "traffic": traffic,
                      "kernel": "dmma_gemm_kernel (iteration GEMM, FP64 DMMA.8x8x4)",
-                     "algorithmic": f"2*D^2 = {2 * D * D} flop per active column per iteration; {gemm_fl:.4g} flop in {gemm_ms:.1f} ms over {args.steps} steps",
+                     "algorithmic": f"executed 2*((n+m)*D + m*n) + 4*m = {flop_col} flop per active column per iteration (the zero blocks (3,2), (3,3) of W are skipped; dense W would be 2*D^2 = {2 * D * D}); {gemm_fl:.4g} flop in {gemm_ms:.1f} ms over {args.steps} steps",
+                     "dense_equivalent_tflops": dense_equiv,
                      "peak_source": "cuBLAS DGEMM 8192^3 via torch.matmul, best of 5, measured in this run (no FP64 entry in MEASURED_PEAKS.json)",
                      "gemm_share_of_step": gemm_ms / comp_ms if comp_ms else None},
         "cpu_baseline": {"value": cpu_qps, "unit": "QP/s", "cores": cores, "kind": "port",
@@ -410,10 +425,10 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         big = mpc_steps[-1]      # quadruped-sized: the HBM-streamed tier of the single-QP kernel
         line["roofline_single_qp_stream"] = {
             "bound": "hbm", "achieved": big["W_stream_GBs"], "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-            "frac": big["W_stream_frac_of_hbm_peak"], "traffic": 134.0e6,
+            "frac": big["W_stream_frac_of_hbm_peak"], "traffic": read_stream_traffic(),
             "kernel": "run_kernel<16, true> (persistent single-QP kernel, W through the cp.async.bulk ring)",
-            "algorithmic": f"8*D^2 = {8 * big['D'] ** 2} bytes per iteration x {big['iters_per_step']} iterations per step / step kernel time (includes refresh_z, bias and epilogue residual passes)",
-            "peak_source": peak_src, "traffic_source": "ncu dram__bytes_read per iteration, profiles/r01s2_ncu_summary.json"}
+            "algorithmic": f"{big['W_bytes_per_iteration']:.0f} bytes of W per iteration (lambda rows streamed as rho*G only; dense 8*D^2 = {8 * big['D'] ** 2}) x {big['iters_per_step']} iterations per step / step kernel time (includes refresh_z, bias and epilogue residual passes)",
+            "peak_source": peak_src, "traffic_source": "ncu dram__bytes_read per iteration, profiles/stream_traffic.json"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -198,6 +198,12 @@ CQP_API int cqp_debug_words(const cqp_handle *h, int *out256);
 CQP_API int cqp_launch_info(const cqp_handle *h, int *ctas, int *rows_per_cta, int *tier,
                             int *smem_bytes);
 
+/* Bytes of W_k one iteration of the persistent kernel reads (the roofline numerator of the
+ * matvec path): 8 D^2 for the dense layer (solver.cpp:60); the L2/HBM tier streams the lambda rows
+ * [rho G, -diag(rho), I] (layers.cpp:159-161) as their first n columns only, 8 ((n+m) D + m n),
+ * and reports structured = 1. */
+CQP_API int cqp_layer_traffic(const cqp_handle *h, double *w_bytes_per_iteration, int *structured);
+
 /* Page-locked host memory for the caller's input / output buffers (cudaMallocHost / cudaFreeHost):
  * copies from and to pinned buffers run at full PCIe rate and asynchronously; pageable buffers
  * are staged by the driver.  Optional: every entry point accepts any host pointer. */

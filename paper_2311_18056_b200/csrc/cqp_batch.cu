@@ -71,6 +71,10 @@ struct GemmParams {
   int split;             // padded row where the lambda block starts (multiple of 128), 0 = dense
   int k_tiles3;
   const double* negrho;  // [a_index][m]: W(n+m+i, n+i) = -rho_i
+  // Dynamic scheduling (null: static striding): CTAs take their first item by blockIdx and every
+  // further one from this counter (zero at launch).  The next index is fetched while the current
+  // item is being computed, so the atomic's latency never shows.
+  int* work_ctr;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -130,7 +134,10 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
   // ones, so that the static striding hands every CTA a similar mix (longest-first).
   const int m_long = (p.split > 0) ? p.split / BM : m_tiles, m_short = m_tiles - m_long;
   const int total_long = (*p.n_tiles) * SUB * m_long;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+  __shared__ int next_item_s;
+  for (int item = blockIdx.x; item < total;) {
+    int fetched = 0;
+    if (tid == 0) fetched = p.work_ctr ? (int)gridDim.x + atomicAdd(p.work_ctr, 1) : item + (int)gridDim.x;
     int ns, mt;
     if (item < total_long) {
       ns = item / m_long;
@@ -143,16 +150,15 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
     const int nt = ns / SUB, sub = ns - nt * SUB;
     const TileDesc td = p.tiles[nt];
     const int slot0 = td.slot0 + sub * BN;
-    if (p.cols[slot0] < 0) continue;  // padding slots sit at the end of a bucket: empty sub-tile
     const int m0 = mt * BM;
     // padded row m0 -> actual row; valid rows of this part end at row_end; k-tiles of this part
     const bool blk3 = p.split > 0 && m0 >= p.split;
     const int row0 = blk3 ? m0 - p.split + p.nm : m0;
     const int row_end = (p.split > 0 && !blk3) ? p.nm : p.M;
     const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
-    if (row0 >= row_end) continue;
+    // (padding slots sit at the end of a bucket: a sub-tile whose first slot is empty is empty)
+    if (row0 < row_end && p.cols[slot0] >= 0) {
     const double* A = p.A + (size_t)td.a_index * p.a_stride + (size_t)m0 * p.lda;
-    __syncthreads();  // previous item's readers of cols_s / smem are done
     if (tid < BN) cols_s[tid] = p.cols[slot0 + tid];
     __syncthreads();
 
@@ -268,7 +274,7 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
           }
       }
       __syncthreads();
-      if (kg > 0) continue;
+      if (kg == 0) {
 #pragma unroll
       for (int q = 1; q < KS; ++q) {
         const double* theirs = red + ((size_t)(q - 1) * (WM * WN * 32) + warp_in * 32 + lane) * PER;
@@ -280,9 +286,11 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
             acc[mi][ni][1] += theirs[(mi * NI + ni) * 2 + 1];
           }
       }
+      }
     }
 
     // epilogue: C fragment (row = g, cols 2*t4, 2*t4+1) of each 8x8 sub-tile
+    if (KS == 1 || kg == 0) {
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
@@ -308,6 +316,12 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
         }
       }
     }
+    }
+    }  // item not empty
+    __syncthreads();  // this item's readers of cols_s / the stage buffers are done
+    if (tid == 0) next_item_s = fetched;
+    __syncthreads();
+    item = next_item_s;
   }
 }
 
@@ -577,6 +591,12 @@ struct cqp_batch {
   // CQP_BATCH_DENSE=1 keeps the plain dense layer for A/B runs.
   int split = 0;
   double* negrho = nullptr;
+  // one work counter per GEMM launch of a solve (dynamic scheduling), zeroed when the solve starts.
+  // OPT-IN (CQP_BATCH_DYNAMIC=1): measured slower than static striding on B200 (B = 4096, same
+  // box: 304.9 vs 288.5 ms per solve), as was an earlier variant with a split tail.
+  int* work_ctrs = nullptr;
+  int work_ctr_cap = 0, work_ctr_next = 0;
+  int dynamic = 0;
   int grid_ctas[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // persistent grid per tile configuration
   // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
   // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
@@ -654,9 +674,11 @@ int pick_config(const cqp_batch* b, int active) {
   return b->tiny_cfg;
 }
 
-int launch_gemm(cqp_batch* b, const GemmParams& p, int cfg) {
+int launch_gemm(cqp_batch* b, const GemmParams& p0, int cfg) {
   b->last_launches += 1;
   const GemmConfig& c = kConfigs[cfg];
+  GemmParams p = p0;
+  p.work_ctr = (b->dynamic && b->work_ctr_next < b->work_ctr_cap) ? b->work_ctrs + b->work_ctr_next++ : nullptr;
   c.fn<<<b->grid_ctas[cfg], c.threads, c.smem, b->stream>>>(p);
   CQP_CUDA(cudaGetLastError());
   return CQP_OK;
@@ -763,6 +785,7 @@ int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   }
   if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
   if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
+  if (const char* e = std::getenv("CQP_BATCH_DYNAMIC")) b->dynamic = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_TINY")) std::sscanf(e, "%d,%d", &b->tiny_cfg, &b->thr_tiny);
   int rc;
@@ -811,7 +834,7 @@ void cqp_batch_destroy(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
                   b->tiles, b->n_tiles, b->n_active};
@@ -856,7 +879,18 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
     b->it1.push_back(e1);
   }
   cudaStream_t st = b->stream;
+  {
+    const int need = rounds * (interval + 4) + 8;  // GEMM launches of one solve
+    if (b->work_ctr_cap < need) {
+      cudaFree(b->work_ctrs);
+      b->work_ctrs = nullptr; b->work_ctr_cap = 0;
+      CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&b->work_ctrs), sizeof(int) * need));
+      b->work_ctr_cap = need;
+    }
+    b->work_ctr_next = 0;
+  }
   CQP_CUDA(cudaEventRecord(b->ev0, st));
+  CQP_CUDA(cudaMemsetAsync(b->work_ctrs, 0, sizeof(int) * b->work_ctr_cap, st));
   CQP_CUDA(cudaMemcpyAsync(b->g, g_cols, sizeof(double) * (size_t)n * B, cudaMemcpyHostToDevice, st));
   CQP_CUDA(cudaMemcpyAsync(b->c, c_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));
   CQP_CUDA(cudaMemcpyAsync(b->d, d_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));

@@ -563,4 +563,12 @@ int cqp_launch_info(const cqp_handle* h, int* ctas, int* rows_per_cta, int* tier
   return CQP_OK;
 }
 
+int cqp_layer_traffic(const cqp_handle* h, double* w_bytes_per_iteration, int* structured) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  const double D = h->D, n = h->n, m = h->m;
+  if (w_bytes_per_iteration) *w_bytes_per_iteration = h->structured ? 8.0 * ((n + m) * D + m * n) : 8.0 * D * D;
+  if (structured) *structured = h->structured;
+  return CQP_OK;
+}
+
 }  // extern "C"

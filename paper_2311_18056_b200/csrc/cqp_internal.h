@@ -61,6 +61,14 @@ struct RunParams {
   int wdoubles;       // grid kernel: shared-memory doubles reserved for W (resident slice or ring)
   int sb_rows;        // grid kernel, streaming: rows per super-block of the W stream (<= kStageRows)
   int stream_stages;  // grid kernel, w_smem == 0: stages of the cp.async.bulk ring (0: plain global loads)
+  // grid kernel, L2/HBM tier, structured layer: the lambda rows of W, [rho G, -diag(rho), I]
+  // (layers.cpp:159-161), are streamed as their first n columns only; the two diagonal terms are
+  // added by the publisher.  CTAs [0, G12) own R12 rows each of the first n + m rows, the other CTAs
+  // R3 lambda rows each (R12 * D ~ R3 * n: equal bytes per CTA).  R = max(R12, R3) sizes the buffers.
+  int structured;
+  int G12, R12, R3;
+  int sb_rows3;          // rows per super-block of the W stream in the lambda-row CTAs
+  size_t wt_level_pairs; // double2 elements per ladder level of Wt
   int xs_stride;  // cluster kernel: doubles between the two shared-memory copies of the iterate
   int hg_smem;    // cluster kernel: the CTA's rows of H, G', G are cached in shared memory
   const double* W;    // [L][D][Dpad] row-major
@@ -74,6 +82,7 @@ struct RunParams {
   const double* Gs;   // [m][npad]   scaled G, row-major (refresh_z)
   const double* E;    // n
   const double* F;    // m
+  const double* rho_vec;  // [L][m] penalty of every constraint row per ladder level
   double cost_scale;
   const double* grid;      // L
   const double* log_grid;  // L  (log10 of the grid values, computed on the host)
@@ -155,6 +164,7 @@ struct cqp_handle {
   int* dbg_dev = nullptr;
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
+  int structured = 0, G12 = 0, R12 = 0, R3 = 0;  // tier 1: structured layer partition (RunParams)
   int stream_stages = 0;  // tier 1: stages of the W streaming ring that fit the shared memory
   int wdoubles = 0;       // shared-memory doubles reserved for W (resident slice or ring)
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)

@@ -235,6 +235,7 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
       const int row = row0 + r;
       double bias = 0.0;
       if (row < nm) bias = -warp_row_dot_mlp<8>(DG + (size_t)row * p.npad, s.uy, p.npad, lane);
+      else if (p.structured) bias = -p.rho_vec[(size_t)k * p.m + (row - nm)];  // W(row, row - m), see the publisher
       if (lane == 0) s.sb[r] = bias;
     }
   }
@@ -389,8 +390,31 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
   }
   const int n = p.n, m = p.m, D = p.D;
-  const int row0 = blockIdx.x * p.R;
-  const int nrows = max(0, min(p.R, D - row0));
+  const int nc2 = p.Dpad >> 1;
+  const int nc2p = (nc2 + 7) & ~7;  // rows of the re-tiled copy are padded to 8 pairs = 128 B
+  // rows this CTA owns; L2/HBM tier: column pairs it streams per row (wc2), pair offset of its slice
+  // inside a level of Wt (wslice) with row pitch wpitch, rows per super-block (sbr)
+  int row0 = blockIdx.x * p.R;
+  int nrows = max(0, min(p.R, D - row0));
+  int wc2 = nc2, wpitch = nc2p, sbr = STREAM ? p.sb_rows : kStageRows;
+  size_t wslice = (size_t)row0 * nc2p;
+  const bool structured = STREAM && p.structured;
+  if (structured) {
+    const int nm = n + m;
+    if ((int)blockIdx.x < p.G12) {
+      row0 = blockIdx.x * p.R12;
+      nrows = max(0, min(p.R12, nm - row0));
+      wslice = (size_t)row0 * nc2p;
+    } else {
+      const int r3 = ((int)blockIdx.x - p.G12) * p.R3;
+      row0 = nm + r3;
+      nrows = max(0, min(p.R3, m - r3));
+      wc2 = (n + 1) >> 1;
+      wpitch = (wc2 + 7) & ~7;
+      wslice = (size_t)nm * nc2p + (size_t)r3 * wpitch;
+      sbr = p.sb_rows3;
+    }
+  }
   const int Rcap = round_up(p.R, RB);
   const bool owns_pad = (p.Dpad != D) && (row0 + nrows == D);  // last CTA also drives the pad slot
   unsigned epoch = 0;
@@ -444,10 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   bool converged = false;
   int iters_done = 0;
   int until_check = p.check_interval;
-  const int nc2 = p.Dpad >> 1;
   constexpr int shift = 5 - Log2<RB>::v;
   unsigned wstage = 0, wphase = 0;  // ring position of the next W chunk to consume (compute) / issue (streamer)
-  const int sbr = STREAM ? p.sb_rows : kStageRows;  // rows per super-block of the W stream (<= kStageRows)
   const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
   const int nfetch = streaming ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
   for (int i = 1; i <= p.total_iters; ++i) {
@@ -469,20 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int c0 = 0; c0 < nc2; c0 += kStagePairs) {
+          for (int c0 = 0; c0 < wc2; c0 += kStagePairs) {
             const unsigned stage = wstage, ph = wphase;  // (stage, phase) advance without integer division
             if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wfull[stage], (int)ph, p.dbg, 7, i);
 #ifdef CQP_TRACE_CHUNKS
             if (t == 0 && blockIdx.x == 0 && i == CQP_TRACE_AT) {
-              const int ci = (rb0 / sbr) * ((nc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
+              const int ci = (rb0 / sbr) * ((wc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
               if (ci < 48) reinterpret_cast<volatile long long*>(p.dbg + 64)[ci] = clock64();
             }
 #endif
             const double2* st = reinterpret_cast<const double2*>(s.sW) + (size_t)stage * (kStageDoubles / 2);
             const int c2 = c0 + pc;
-            const int cw = p.Wt ? min(kStagePairs, nc2 - c0) : kStagePairs;  // stage row stride (pairs)
-            if (c2 < nc2) {
+            const int cw = p.Wt ? min(kStagePairs, wc2 - c0) : kStagePairs;  // stage row stride (pairs)
+            if (c2 < wc2) {
               const double2 xv = x2[c2];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -536,11 +558,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (streaming) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
-          for (int c0 = 0; c0 < nc2; c0 += kStagePairs) {
+          for (int c0 = 0; c0 < wc2; c0 += kStagePairs) {
             const unsigned stage = wstage, ph = wphase;
             if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wempty[stage], (int)(ph ^ 1u), p.dbg, 8, i);  // (a fresh barrier passes at once)
-            const unsigned bytes = 16u * (unsigned)min(kStagePairs, nc2 - c0);
+            const unsigned bytes = 16u * (unsigned)min(kStagePairs, wc2 - c0);
             if (lane == 0) {
               asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(
                                smem_u32(&wfull[stage])),
@@ -550,15 +572,14 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
             __syncwarp();
 #ifdef CQP_TRACE_CHUNKS
             if (lane == 0 && blockIdx.x == 0 && i == CQP_TRACE_AT) {
-              const int ci = (rb0 / sbr) * ((nc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
+              const int ci = (rb0 / sbr) * ((wc2 + kStagePairs - 1) / kStagePairs) + c0 / kStagePairs;
               if (ci < 48) reinterpret_cast<volatile long long*>(p.dbg + 64)[48 + ci] = clock64();
             }
 #endif
             if (p.Wt) {  // re-tiled W: the whole stage is one contiguous block
               if (lane == 0) {
-                // (rows of the re-tiled copy are padded to 8 pairs = 128 B, so every block is 128 B aligned)
-                const int nc2p = (nc2 + 7) & ~7;
-                const double* src = p.Wt + 2 * ((size_t)layer * D * nc2p + (size_t)(row0 + rb0) * nc2p + (size_t)nv * c0);
+                // (row pitches are multiples of 8 pairs = 128 B, so every block is 128 B aligned)
+                const double* src = p.Wt + 2 * ((size_t)layer * p.wt_level_pairs + wslice + (size_t)rb0 * wpitch + (size_t)nv * c0);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         smem_u32(s.sW + (size_t)stage * kStageDoubles)),
@@ -580,11 +601,14 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
+      const double* xprev = s.xs + (size_t)(b ^ 1) * p.Dpad;  // v_{i-1} (complete: the compute warps read it)
       for (int r = lane; r < nrows; r += 32) {
         double x = 0.0;
 #pragma unroll
         for (int w = 0; w < npart; ++w) x += part[w * Rcap + r];
-        x += s.sb[r];
+        // structured layer, lambda row j: + W(row, n + j) z_j + W(row, n + m + j) lambda_j = -rho_j z_j + lambda_j
+        if (structured && row0 + r >= n + m) x += fma(s.sb[r], xprev[row0 + r - m], xprev[row0 + r]);
+        else x += s.sb[r];
         const double lo = s.slo[r], hi = s.shi[r];
         x = x < lo ? lo : x;
         x = x > hi ? hi : x;
@@ -805,21 +829,48 @@ __global__ void instantiate_kernel(const double* __restrict__ og, const double* 
 }
 
 // Row-major W_k ([D][Dpad]) -> the streaming layout of the L2/HBM tier (RunParams::Wt): inside the
-// R-row slice of every CTA, every super-block of sbr <= 16 rows (nv valid rows) stores its 128-pair column
+// row slice of every CTA, every super-block of sbr <= 16 rows (nv valid rows) stores its 128-pair column
 // chunks one after the other, each as [nv][cw] pairs.  One thread per (row, column pair).
-__global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int D, int nc2, int R,
-                              int sbr) {
+// Structured layer (G12 > 0): rows < nm are cut into slices of R12 rows with all nc2 pairs; the
+// lambda rows follow in slices of R3 rows with only their first ceil(n / 2) pairs (the dense
+// block rho G; columns >= n are dropped / zeroed: the publisher adds the two diagonal terms).
+struct RetilePlan {
+  int D, nc2, n, nm;
+  int G12, R12, R3;    // G12 == 0: uniform slices of R12 rows
+  int sbr12, sbr3;
+};
+
+__global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, const RetilePlan q) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)D * nc2) return;
-  const int row = (int)(idx / nc2), c2 = (int)(idx - (size_t)row * nc2);
-  const int b = row / R, lr = row - b * R;
-  const int nrows = min(R, D - b * R);
+  if (idx >= (size_t)q.D * q.nc2) return;
+  const int row = (int)(idx / q.nc2), c2 = (int)(idx - (size_t)row * q.nc2);
+  const int nc2p = (q.nc2 + 7) & ~7;  // slices start on 128-byte boundaries (bulk copies are faster aligned)
+  int lr, nrows, sbr, wc2 = q.nc2, pitch = nc2p;
+  size_t slice;
+  double2 val = src[idx];
+  if (q.G12 > 0 && row >= q.nm) {
+    wc2 = (q.n + 1) >> 1;
+    if (c2 >= wc2) return;
+    if (2 * c2 + 1 >= q.n) val.y = 0.0;  // odd n: the pair's second column belongs to block (3,2)
+    pitch = (wc2 + 7) & ~7;
+    const int r3 = row - q.nm, b = r3 / q.R3;
+    lr = r3 - b * q.R3;
+    nrows = min(q.R3, (q.D - q.nm) - b * q.R3);
+    slice = (size_t)q.nm * nc2p + (size_t)(b * q.R3) * pitch;
+    sbr = q.sbr3;
+  } else {
+    const int limit = q.G12 > 0 ? q.nm : q.D;
+    const int b = row / q.R12;
+    lr = row - b * q.R12;
+    nrows = min(q.R12, limit - b * q.R12);
+    slice = (size_t)(b * q.R12) * nc2p;
+    sbr = q.sbr12;
+  }
   const int sb = lr / sbr, r = lr - sb * sbr;
   const int nv = min(sbr, nrows - sb * sbr);
   const int c = c2 / kStagePairs, pc = c2 - c * kStagePairs;
-  const int cw = min(kStagePairs, nc2 - c * kStagePairs);
-  const int nc2p = (nc2 + 7) & ~7;  // slices start on 128-byte boundaries (bulk copies are faster aligned)
-  dst[(size_t)(b * R + sb * sbr) * nc2p + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = src[idx];
+  const int cw = min(kStagePairs, wc2 - c * kStagePairs);
+  dst[slice + (size_t)(sb * sbr) * pitch + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = val;
 }
 
 template <int RB, bool STREAM>
@@ -849,6 +900,7 @@ int configure_launch(cqp_handle* h) {
   const bool force_grid = force_tier && (force_tier[0] == '0' || force_tier[0] == '1');
   if (!force_grid && configure_cluster(h) == CQP_OK && h->cluster) return CQP_OK;
   h->cluster = 0;
+  h->structured = 0;
   int G = h->num_sms;
   int R = (D + G - 1) / G;
   if (R < 1) R = 1;
@@ -875,6 +927,36 @@ int configure_launch(cqp_handle* h) {
     h->stream_stages = stages;
     h->wdoubles = stages * kStageDoubles;
     need = base + (size_t)h->wdoubles * sizeof(double);
+    // Structured layer: the lambda rows are streamed as n columns instead of D, so they go to
+    // fewer CTAs with more rows each: pick G12 + G3 <= G that minimises the largest per-CTA
+    // byte count max(R12 D, R3 n).  CQP_SINGLE_DENSE=1 keeps the dense layer (A/B runs).
+    const char* dense = std::getenv("CQP_SINGLE_DENSE");
+    const int n = h->n, m = h->m, nm = n + m;
+    if (stages >= 2 && !(dense && dense[0] == '1') && !std::getenv("CQP_NO_RETILE") && m >= 1 && n >= 2 && G >= 2) {
+      long long best = -1;
+      int bestR12 = 0, bestR3 = 0;
+      for (int g12 = 1; g12 < G; ++g12) {
+        const int r12 = (nm + g12 - 1) / g12, r3 = (m + (G - g12) - 1) / (G - g12);
+        const long long cost = std::max((long long)r12 * D, (long long)r3 * n);
+        if (best < 0 || cost < best) { best = cost; bestR12 = r12; bestR3 = r3; }
+      }
+      const int Rs = std::max(bestR12, bestR3);
+      const size_t base_s = smem_doubles(Rs, 16, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
+      int stages_s = base_s > (size_t)kMaxSmemBytes ? 0 : (int)(((size_t)kMaxSmemBytes - base_s) / (kStageDoubles * sizeof(double)));
+      stages_s = std::min(stages_s, stages);
+      const bool force = std::getenv("CQP_FORCE_STRUCTURED") != nullptr;  // tests: also where it does not pay
+      if (stages_s >= 2 && (best < (long long)R * D || force)) {
+        h->structured = 1;
+        h->R12 = bestR12; h->R3 = bestR3;
+        h->G12 = (nm + bestR12 - 1) / bestR12;
+        h->G = h->G12 + (m + bestR3 - 1) / bestR3;
+        h->R = Rs;
+        h->rb = 16;
+        h->stream_stages = stages_s;
+        h->wdoubles = stages_s * kStageDoubles;
+        need = base_s + (size_t)h->wdoubles * sizeof(double);
+      }
+    }
   }
   h->smem_bytes = (int)need;
   return CQP_OK;
@@ -888,20 +970,34 @@ static int stream_sb_rows(int R) {
   return (R + nsb - 1) / nsb;
 }
 
+// double2 elements of one re-tiled ladder level (rows padded to 8 pairs = 128 bytes)
+static size_t wt_level_pairs(const cqp_handle* h) {
+  const int nc2p = ((h->Dpad >> 1) + 7) & ~7;
+  if (!h->structured) return (size_t)h->D * nc2p;
+  const int wp3 = (((h->n + 1) >> 1) + 7) & ~7;
+  return (size_t)(h->n + h->m) * nc2p + (size_t)h->m * wp3;
+}
+
 // L2/HBM tier: build the streaming copy of the ladder (RunParams::Wt).  Called once W is complete
 // (end of handle creation); launch_run re-checks so that a handle never streams a stale copy.
 int prepare_streaming(cqp_handle* h) {
   if (h->cluster || h->w_smem || h->stream_stages <= 0 || h->Wt || std::getenv("CQP_NO_RETILE")) return CQP_OK;
   const size_t per = (size_t)h->D * h->Dpad;
-  const int nc2p = ((h->Dpad >> 1) + 7) & ~7;
-  const size_t per_t = (size_t)h->D * nc2p * 2;  // re-tiled level: rows padded to 128 bytes
+  const size_t per_t = 2 * wt_level_pairs(h);  // re-tiled level: rows padded to 128 bytes
   CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Wt), sizeof(double) * per_t * h->L));
   CQP_CUDA(cudaMemsetAsync(h->Wt, 0, sizeof(double) * per_t * h->L, h->stream));
   const size_t pairs = per / 2;
+  RetilePlan q{};
+  q.D = h->D; q.nc2 = h->Dpad >> 1; q.n = h->n; q.nm = h->n + h->m;
+  if (h->structured) {
+    q.G12 = h->G12; q.R12 = h->R12; q.R3 = h->R3;
+    q.sbr12 = stream_sb_rows(h->R12); q.sbr3 = stream_sb_rows(h->R3);
+  } else {
+    q.G12 = 0; q.R12 = h->R; q.R3 = 1; q.sbr12 = stream_sb_rows(h->R); q.sbr3 = 1;
+  }
   for (int k = 0; k < h->L; ++k) {
     retile_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, h->stream>>>(
-        reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per_t * k), h->D,
-        h->Dpad >> 1, h->R, stream_sb_rows(h->R));
+        reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per_t * k), q);
     CQP_CUDA(cudaGetLastError());
   }
   return CQP_OK;
@@ -955,7 +1051,12 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.Wt = (!h->w_smem) ? h->Wt : nullptr;
   p.wdoubles = h->wdoubles;
   p.stream_stages = h->stream_stages;
-  p.sb_rows = stream_sb_rows(h->R);
+  p.sb_rows = stream_sb_rows(h->structured ? h->R12 : h->R);
+  p.structured = (h->structured && p.Wt) ? 1 : 0;
+  p.G12 = h->G12; p.R12 = h->R12; p.R3 = h->R3;
+  p.sb_rows3 = h->structured ? stream_sb_rows(h->R3) : 1;
+  p.wt_level_pairs = wt_level_pairs(h);
+  p.rho_vec = h->rho_vec;
   // few iterations: copying the W slice into shared memory costs as much as streaming it once;
   // the ring then lives in the (unused) slice region
   if (total_iters < 4 && p.w_smem) {

@@ -299,7 +299,10 @@ class Solver:
     def launch_info(self) -> dict:
         a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         _raise(self._L.cqp_launch_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
-        return {"ctas": a.value, "rows_per_cta": b.value, "tier": c.value, "smem_bytes": d.value}
+        wb, st = C.c_double(), C.c_int()
+        _raise(self._L.cqp_layer_traffic(self._h, C.byref(wb), C.byref(st)))
+        return {"ctas": a.value, "rows_per_cta": b.value, "tier": c.value, "smem_bytes": d.value,
+                "w_bytes_per_iteration": wb.value, "structured": st.value}
 
 
 class BatchSolver:

@@ -52,7 +52,8 @@ def test_robot_sized_parity_with_oracle(G, oracle, P, name, k, hard):
     base = wl.base_problem()
     cpu = oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), variant="v3")
     gpu = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=oracle_layers(cpu.cache))
-    assert gpu.launch_info()["tier"] == 1          # W streamed from L2/HBM
+    info = gpu.launch_info()
+    assert info["tier"] == 1 and info["structured"] == 1   # W streamed from L2/HBM, lambda rows as rho G only
     # initial solve to tolerance from a hard start, then the receding-horizon loop
     x0 = wl.x0(hard)
     q = wl.problem_at(x0)

@@ -441,3 +441,39 @@ def test_all_kernel_modes_agree(G, oracle, P, monkeypatch):
     assert_report_parity(a, ro)
     assert_report_parity(b, ro)
     assert_report_parity(c, ro)
+
+
+@pytest.mark.parametrize("n", [51, 201])
+def test_structured_stream_layer_matches_dense_and_oracle(G, oracle, monkeypatch, n):
+    """L2/HBM tier, structured layer: the lambda rows of W, [rho G, -diag(rho), I]
+    (layers.cpp:159-161), are streamed as their first n columns and the two diagonal terms are
+    added by the publisher.  Forced here on small problems (odd n: a column pair straddles the
+    y / z boundary; equality rows: rho differs per row) and compared with the dense layer and the
+    oracle: identical counts, traces, history indices; values within rounding."""
+    p = oracle.gen_random_dense_qp(n, 3)
+    monkeypatch.setenv("CQP_FORCE_TIER", "1")
+    reports = []
+    for env, want in ((("CQP_SINGLE_DENSE", "1"), 0), (("CQP_FORCE_STRUCTURED", "1"), 1)):
+        monkeypatch.delenv("CQP_SINGLE_DENSE", raising=False)
+        monkeypatch.delenv("CQP_FORCE_STRUCTURED", raising=False)
+        monkeypatch.setenv(*env)
+        gs, os_ = make_pair(oracle, G, p, from_layers=True)
+        info = gs.launch_info()
+        assert info["tier"] == 1 and info["structured"] == want
+        D = p.n + 2 * p.m
+        assert info["w_bytes_per_iteration"] == (8.0 * ((p.n + p.m) * D + p.m * p.n) if want else 8.0 * D * D)
+        reports.append(gs.solve())
+        gs.cold_start(); gs.fixed_iters(7); va = gs.state
+        gs.cold_start(); gs.fixed_iters(3); gs.fixed_iters(4)
+        assert np.array_equal(gs.state, va)
+        gs.close()
+    for k in ("CQP_FORCE_TIER", "CQP_SINGLE_DENSE", "CQP_FORCE_STRUCTURED"):
+        monkeypatch.delenv(k, raising=False)
+    dense, struct = reports
+    ro = os_.solve()
+    assert len(ro.solution.rho_trace) > 1 or n < 100   # the larger one switches rho
+    assert_report_parity(dense, ro)
+    assert_report_parity(struct, ro)
+    assert struct.solution.iterations == dense.solution.iterations
+    assert rel_err(struct.solution.y, dense.solution.y) <= 1e-9
+    assert rel_err(struct.solution.lam, dense.solution.lam) <= 1e-9
