@@ -117,3 +117,40 @@ def test_structured_layer_matches_dense_layer(G, P, monkeypatch):
         assert np.array_equal(a[key], b[key]), key
     for key in ("y", "z", "lam"):
         assert rel_err(a[key], b[key]) <= 1e-9, key
+
+
+def test_lanes_match_one_batch(G, oracle, P, monkeypatch):
+    """Batches of >= 1024 columns are cut into two sub-batches that run concurrently on their own
+    streams (their GEMM launches fill each other's wave tails).  Columns are independent QPs, so
+    counts, traces and statuses must equal the single-lane run; values agree to rounding only
+    (the tile shape / k-split of a round follows the lane's active-column count, which changes
+    the summation order).  A sample of columns is checked against the oracle as well."""
+    wl = P.config2(10, seed=5)
+    base = wl.base_problem()
+    B = 1100
+    g, c, d, _ = P.batch_instances(wl, B, lo=0.3, hi=10.0)
+    outs = []
+    for lanes in ("1", "2", "3"):
+        monkeypatch.setenv("CQP_BATCH_LANES", lanes)
+        single = G.Solver(base.H, base.g, base.G, base.c, base.d)
+        batch = G.BatchSolver(single, capacity=B)
+        outs.append({k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in batch.solve(g, c, d).items()})
+        small = batch.solve(g[:, :100], c[:, :100], d[:, :100])     # small batch on a multi-lane object: one lane
+        assert np.array_equal(small["iterations"], outs[0]["iterations"][:100])
+        assert rel_err(small["y"], outs[0]["y"][:, :100]) <= 1e-9
+        batch.close(); single.close()
+    monkeypatch.delenv("CQP_BATCH_LANES", raising=False)
+    a = outs[0]
+    assert len(set(a["iterations"].tolist())) > 3 and a["n_switches"].max() >= 1
+    for b in outs[1:]:
+        for key in ("iterations", "status", "final_index", "n_switches"):
+            assert np.array_equal(a[key], b[key]), key
+        for key in ("y", "z", "lam"):
+            assert rel_err(a[key], b[key]) <= 1e-9, key
+        assert b["compute_ms"] > 0 and b["gemm_ms"] > 0 and b["gemm_flops"] == a["gemm_flops"]
+    cpu = oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), variant="v3")
+    for j in list(range(0, B, 97)) + [B - 1]:
+        cpu.update_vectors(g[:, j], c[:, j], d[:, j]); cpu.cold_start()
+        s = cpu.solve().solution
+        assert outs[1]["iterations"][j] == s.iterations and outs[1]["status"][j] == s.status
+        assert rel_err(outs[1]["y"][:, j], s.y) <= 1e-6 and rel_err(outs[1]["lam"][:, j], s.lam) <= 1e-6

@@ -89,6 +89,17 @@ def main():
         traffic = sum(to_bytes(r["dram__bytes_read.sum"]) + to_bytes(r["dram__bytes_write.sum"]) for r in recs) / len(recs)
         json.dump({"dram_bytes_per_launch": traffic, "captures": len(recs), "source": f"{TAG}_ncu_summary.json"},
                   open(os.path.join(OUT, "dmma_gemm_traffic.json"), "w"), indent=1)
+    # DRAM bytes per iteration of the streamed single-QP tier (tools/profile_tier1.py runs
+    # fixed_iters(100)), for bench.py's roofline_single_qp_stream.traffic
+    t1 = prefix + "prof_tier1.ncu-rep"
+    if t1 in summary and summary[t1]:
+        def to_bytes1(s):
+            v, unit = s.split()[0].replace(",", ""), s.split()[1] if len(s.split()) > 1 else "byte"
+            return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+        r = summary[t1][0]
+        json.dump({"dram_bytes_per_iteration": (to_bytes1(r["dram__bytes_read.sum"]) + to_bytes1(r["dram__bytes_write.sum"])) / 100.0,
+                   "iterations_in_capture": 100, "source": f"{TAG}_ncu_summary.json"},
+                  open(os.path.join(OUT, "stream_traffic.json"), "w"), indent=1)
     print(json.dumps(summary, indent=1)[:3000])
 
 
