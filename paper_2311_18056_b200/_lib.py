@@ -10,7 +10,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcqp_b200.so")
+# CQP_B200_LIB: load another build of the same library (tools/: instrumented -DCQP_TRACE builds)
+LIB_PATH = os.environ.get("CQP_B200_LIB") or os.path.join(_HERE, "libcqp_b200.so")
 
 c_double_p = C.POINTER(C.c_double)
 c_int_p = C.POINTER(C.c_int)

@@ -68,6 +68,12 @@ struct RunParams {
   int structured;
   int G12, R12, R3;
   int sb_rows3;          // rows per super-block of the W stream in the lambda-row CTAs
+  int nparts;            // per-row partial sums kept per parity: 16 (one per compute warp) or, for handles
+                         // that always stream, 4
+  int stage_doubles;     // doubles per ring stage (re-tiled stream: h->stage_doubles; row segments: kStageDoubles)
+  int cw12, cw3;         // column pairs per ring stage (chunk width): a stage holds nv rows x cw pairs
+                         // <= 32 KB, so super-blocks of fewer than 16 rows take wider chunks (one bulk
+                         // copy per stage: the fewer and larger the copies, the higher the streaming rate)
   size_t wt_level_pairs; // double2 elements per ladder level of Wt
   int xs_stride;  // cluster kernel: doubles between the two shared-memory copies of the iterate
   int hg_smem;    // cluster kernel: the CTA's rows of H, G', G are cached in shared memory
@@ -165,6 +171,9 @@ struct cqp_handle {
   // launch configuration
   int R = 0, G = 0, w_smem = 0, rb = 0, smem_bytes = 0;
   int structured = 0, G12 = 0, R12 = 0, R3 = 0;  // tier 1: structured layer partition (RunParams)
+  int cw12 = 128, cw3 = 128;                      // tier 1: chunk widths Wt was re-tiled with
+  int stage_doubles = 4096;                       // tier 1: doubles per ring stage of the re-tiled stream
+  int nparts = 16;                                // per-row partial sums per parity (RunParams::nparts)
   int stream_stages = 0;  // tier 1: stages of the W streaming ring that fit the shared memory
   int wdoubles = 0;       // shared-memory doubles reserved for W (resident slice or ring)
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)

@@ -182,11 +182,11 @@ __host__ __device__ inline int round_up(int x, int q) { return (x + q - 1) / q *
 // `wdoubles`: doubles reserved at the front for W: the resident slice R * Dpad (tier 0) or the
 // streaming ring stages * kStageDoubles (tier 1).
 __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad, int mpad,
-                                               size_t wdoubles) {
+                                               size_t wdoubles, int nparts = kComputeWarps) {
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
   return wdoubles + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
-         2 * (size_t)kComputeWarps * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
+         2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
 }
 
 template <int RB>
@@ -202,7 +202,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.ul = s.uz + p.mpad;
   s.sred = s.ul + p.mpad;
   s.spart = s.sred + kWarps * 16;
-  s.sb = s.spart + 2 * kComputeWarps * Rcap;
+  s.sb = s.spart + 2 * p.nparts * Rcap;
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   int row0 = blockIdx.x * p.R;
   int nrows = max(0, min(p.R, D - row0));
   int wc2 = nc2, wpitch = nc2p, sbr = STREAM ? p.sb_rows : kStageRows;
+  int cwp = (STREAM && p.Wt) ? p.cw12 : kStagePairs;  // column pairs per ring stage
   size_t wslice = (size_t)row0 * nc2p;
   const bool structured = STREAM && p.structured;
   if (structured) {
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       wpitch = (wc2 + 7) & ~7;
       wslice = (size_t)nm * nc2p + (size_t)r3 * wpitch;
       sbr = p.sb_rows3;
+      cwp = p.cw3;
     }
   }
   const int Rcap = round_up(p.R, RB);
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
     const int b = i & 1;
     const int par = ((i - 1) >> 1) & 1;  // phase parity of the k-th use of a [2]-split barrier
-    double* part = s.spart + (size_t)b * kComputeWarps * Rcap;
+    double* part = s.spart + (size_t)b * p.nparts * Rcap;
     if (compute) {
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 1); CQP_STAMP(p.dbg, i, 0); }
       if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int c0 = 0; c0 < wc2; c0 += kStagePairs) {
+          for (int c0 = 0; c0 < wc2; c0 += cwp) {
             const unsigned stage = wstage, ph = wphase;  // (stage, phase) advance without integer division
             if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wfull[stage], (int)ph, p.dbg, 7, i);
@@ -501,15 +503,15 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
               if (ci < 48) reinterpret_cast<volatile long long*>(p.dbg + 64)[ci] = clock64();
             }
 #endif
-            const double2* st = reinterpret_cast<const double2*>(s.sW) + (size_t)stage * (kStageDoubles / 2);
-            const int c2 = c0 + pc;
-            const int cw = p.Wt ? min(kStagePairs, wc2 - c0) : kStagePairs;  // stage row stride (pairs)
-            if (c2 < wc2) {
-              const double2 xv = x2[c2];
+            const double2* st = reinterpret_cast<const double2*>(s.sW) + (size_t)stage * (p.stage_doubles / 2);
+            const int cw = p.Wt ? min(cwp, wc2 - c0) : kStagePairs;  // stage row stride (pairs)
+            const int cend = p.Wt ? cw : min(kStagePairs, wc2 - c0);
+            for (int pp = pc; pp < cend; pp += kStagePairs) {  // (chunks wider than 128 pairs: several passes)
+              const double2 xv = x2[c0 + pp];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 if (4 * rq + j < nv) {
-                  const double2 w = st[(4 * rq + j) * cw + pc];
+                  const double2 w = st[(4 * rq + j) * cw + pp];
                   acc[j] = fma(w.x, xv.x, acc[j]);
                   acc[j] = fma(w.y, xv.y, acc[j]);
                 }
@@ -558,11 +560,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (streaming) {
         for (int rb0 = 0; rb0 < nrows; rb0 += sbr) {
           const int nv = min(sbr, nrows - rb0);
-          for (int c0 = 0; c0 < wc2; c0 += kStagePairs) {
+          for (int c0 = 0; c0 < wc2; c0 += cwp) {
             const unsigned stage = wstage, ph = wphase;
             if (++wstage == (unsigned)NS) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&wempty[stage], (int)(ph ^ 1u), p.dbg, 8, i);  // (a fresh barrier passes at once)
-            const unsigned bytes = 16u * (unsigned)min(kStagePairs, wc2 - c0);
+            const unsigned bytes = 16u * (unsigned)min(cwp, wc2 - c0);
             if (lane == 0) {
               asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(
                                smem_u32(&wfull[stage])),
@@ -582,13 +584,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
                 const double* src = p.Wt + 2 * ((size_t)layer * p.wt_level_pairs + wslice + (size_t)rb0 * wpitch + (size_t)nv * c0);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(s.sW + (size_t)stage * kStageDoubles)),
+                        smem_u32(s.sW + (size_t)stage * p.stage_doubles)),
                     "l"(src), "r"(bytes * (unsigned)nv), "r"(smem_u32(&wfull[stage]))
                     : "memory");
               }
             } else if (lane < nv) {
               const double* src = p.W + ((size_t)layer * D + row0 + rb0 + lane) * p.Dpad + 2 * (size_t)c0;
-              const unsigned dst = smem_u32(s.sW + (size_t)stage * kStageDoubles + (size_t)lane * (2 * kStagePairs));
+              const unsigned dst = smem_u32(s.sW + (size_t)stage * p.stage_doubles + (size_t)lane * (2 * kStagePairs));
               asm volatile(
                   "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                   "l"(src), "r"(bytes), "r"(smem_u32(&wfull[stage]))
@@ -838,6 +840,7 @@ struct RetilePlan {
   int D, nc2, n, nm;
   int G12, R12, R3;    // G12 == 0: uniform slices of R12 rows
   int sbr12, sbr3;
+  int cw12, cw3;       // chunk width (column pairs per ring stage) of the two slice kinds
 };
 
 __global__ void retile_kernel(const double2* __restrict__ src, double2* __restrict__ dst, const RetilePlan q) {
@@ -845,7 +848,7 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
   if (idx >= (size_t)q.D * q.nc2) return;
   const int row = (int)(idx / q.nc2), c2 = (int)(idx - (size_t)row * q.nc2);
   const int nc2p = (q.nc2 + 7) & ~7;  // slices start on 128-byte boundaries (bulk copies are faster aligned)
-  int lr, nrows, sbr, wc2 = q.nc2, pitch = nc2p;
+  int lr, nrows, sbr, wc2 = q.nc2, pitch = nc2p, cwp = q.cw12;
   size_t slice;
   double2 val = src[idx];
   if (q.G12 > 0 && row >= q.nm) {
@@ -858,6 +861,7 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
     nrows = min(q.R3, (q.D - q.nm) - b * q.R3);
     slice = (size_t)q.nm * nc2p + (size_t)(b * q.R3) * pitch;
     sbr = q.sbr3;
+    cwp = q.cw3;
   } else {
     const int limit = q.G12 > 0 ? q.nm : q.D;
     const int b = row / q.R12;
@@ -868,9 +872,9 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
   }
   const int sb = lr / sbr, r = lr - sb * sbr;
   const int nv = min(sbr, nrows - sb * sbr);
-  const int c = c2 / kStagePairs, pc = c2 - c * kStagePairs;
-  const int cw = min(kStagePairs, wc2 - c * kStagePairs);
-  dst[slice + (size_t)(sb * sbr) * pitch + (size_t)nv * (c * kStagePairs) + (size_t)r * cw + pc] = val;
+  const int c = c2 / cwp, pc = c2 - c * cwp;
+  const int cw = min(cwp, wc2 - c * cwp);
+  dst[slice + (size_t)(sb * sbr) * pitch + (size_t)nv * (c * cwp) + (size_t)r * cw + pc] = val;
 }
 
 template <int RB, bool STREAM>
@@ -901,6 +905,7 @@ int configure_launch(cqp_handle* h) {
   if (!force_grid && configure_cluster(h) == CQP_OK && h->cluster) return CQP_OK;
   h->cluster = 0;
   h->structured = 0;
+  h->nparts = kComputeWarps;
   int G = h->num_sms;
   int R = (D + G - 1) / G;
   if (R < 1) R = 1;
@@ -920,13 +925,42 @@ int configure_launch(cqp_handle* h) {
       set_error("problem too large for the persistent kernel's shared-memory vectors");
       return CQP_ERR_CAPACITY;
     }
-    int stages = (int)(((size_t)kMaxSmemBytes - base) / (kStageDoubles * sizeof(double)));
-    if (stages > kMaxStages) stages = kMaxStages;
-    if (stages < 2) stages = 0;  // no room: plain global loads
-    if (const char* e = std::getenv("CQP_STREAM_STAGES")) stages = std::min(stages, std::atoi(e));  // A/B knob
+    // Ring plan: everything the vectors leave free goes to the ring, cut into a FEW LARGE stages
+    // (one cp.async.bulk each).  Measured on B200: the per-SM streaming rate grows with the bytes in
+    // flight (quadruped-sized: 3 x 30 KB were latency-bound at 66 GB/s per SM) and with the copy
+    // size (Atlas-sized, same bytes in flight: 4 x 28 KB 7.3 us per iteration, 2 x 64 KB 6.2 us).
+    const bool no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
+    int want_stages = 3;
+    if (const char* e = std::getenv("CQP_STREAM_STAGES")) want_stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
+    auto plan_ring = [&](size_t base_bytes, int& stages, int& stage_doubles) {
+      stages = 0;
+      stage_doubles = kStageDoubles;
+      if (base_bytes >= (size_t)kMaxSmemBytes) return;
+      const size_t avail = (size_t)kMaxSmemBytes - base_bytes;
+      if (no_retile) {  // row-segment streaming: fixed 16 x 128-pair stages
+        stages = std::min(kMaxStages, (int)(avail / (kStageDoubles * sizeof(double))));
+        if (stages < 2) stages = 0;
+        return;
+      }
+      for (int ns = want_stages; ns >= 2; --ns) {
+        const size_t sb = (avail / ns) & ~(size_t)127;
+        if (sb >= kStageDoubles * sizeof(double)) { stages = ns; stage_doubles = (int)(sb / sizeof(double)); return; }
+      }
+    };
+    // handles that always stream keep 4 partial sums per row instead of 16
+    int stages = 0;
+    h->nparts = 4;
+    size_t base_used = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0, 4) * sizeof(double);
+    plan_ring(base_used, stages, h->stage_doubles);
+    if (stages < 2) {  // no room for a ring: plain global loads, 16 partials
+      h->nparts = kComputeWarps;
+      base_used = base;
+      stages = 0;
+      h->stage_doubles = kStageDoubles;
+    }
     h->stream_stages = stages;
-    h->wdoubles = stages * kStageDoubles;
-    need = base + (size_t)h->wdoubles * sizeof(double);
+    h->wdoubles = stages * h->stage_doubles;
+    need = base_used + (size_t)h->wdoubles * sizeof(double);
     // Structured layer: the lambda rows are streamed as n columns instead of D, so they go to
     // fewer CTAs with more rows each: pick G12 + G3 <= G that minimises the largest per-CTA
     // byte count max(R12 D, R3 n).  CQP_SINGLE_DENSE=1 keeps the dense layer (A/B runs).
@@ -941,9 +975,9 @@ int configure_launch(cqp_handle* h) {
         if (best < 0 || cost < best) { best = cost; bestR12 = r12; bestR3 = r3; }
       }
       const int Rs = std::max(bestR12, bestR3);
-      const size_t base_s = smem_doubles(Rs, 16, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
-      int stages_s = base_s > (size_t)kMaxSmemBytes ? 0 : (int)(((size_t)kMaxSmemBytes - base_s) / (kStageDoubles * sizeof(double)));
-      stages_s = std::min(stages_s, stages);
+      const size_t base_s = smem_doubles(Rs, 16, h->Dpad, h->npad, h->mpad, 0, 4) * sizeof(double);
+      int stages_s = 0, stage_doubles_s = kStageDoubles;
+      plan_ring(base_s, stages_s, stage_doubles_s);
       const bool force = std::getenv("CQP_FORCE_STRUCTURED") != nullptr;  // tests: also where it does not pay
       if (stages_s >= 2 && (best < (long long)R * D || force)) {
         h->structured = 1;
@@ -953,7 +987,8 @@ int configure_launch(cqp_handle* h) {
         h->R = Rs;
         h->rb = 16;
         h->stream_stages = stages_s;
-        h->wdoubles = stages_s * kStageDoubles;
+        h->stage_doubles = stage_doubles_s;
+        h->wdoubles = stages_s * h->stage_doubles;
         need = base_s + (size_t)h->wdoubles * sizeof(double);
       }
     }
@@ -968,6 +1003,17 @@ static int stream_sb_rows(int R) {
   if (const char* e = std::getenv("CQP_SB_BALANCE")) if (e[0] == '0') return kStageRows;  // A/B knob
   const int nsb = (R + kStageRows - 1) / kStageRows;
   return (R + nsb - 1) / nsb;
+}
+
+// Column pairs per ring stage for super-blocks of up to `sbr` rows streaming `wc2` pairs per row: as
+// wide as the 32 KB stage allows (multiple of 8 pairs = 128 B), then evened out over the chunks of
+// a row so that no stage is nearly empty.  CQP_WIDE_CHUNKS=0 keeps 128-pair chunks (A/B runs).
+static int stream_chunk_pairs(int sbr, int wc2, int stage_doubles) {
+  if (const char* e = std::getenv("CQP_WIDE_CHUNKS")) if (e[0] == '0') return kStagePairs;
+  const int cwmax = ((stage_doubles / 2) / sbr) & ~7;
+  const int nch = (wc2 + cwmax - 1) / cwmax;
+  const int even = (((wc2 + nch - 1) / nch) + 7) & ~7;
+  return std::max(kStagePairs, std::min(even, cwmax));
 }
 
 // double2 elements of one re-tiled ladder level (rows padded to 8 pairs = 128 bytes)
@@ -995,6 +1041,8 @@ int prepare_streaming(cqp_handle* h) {
   } else {
     q.G12 = 0; q.R12 = h->R; q.R3 = 1; q.sbr12 = stream_sb_rows(h->R); q.sbr3 = 1;
   }
+  q.cw12 = h->cw12 = stream_chunk_pairs(q.sbr12, q.nc2, h->stage_doubles);
+  q.cw3 = h->cw3 = stream_chunk_pairs(q.sbr3, (h->n + 1) >> 1, h->stage_doubles);
   for (int k = 0; k < h->L; ++k) {
     retile_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, h->stream>>>(
         reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per_t * k), q);
@@ -1055,6 +1103,9 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.structured = (h->structured && p.Wt) ? 1 : 0;
   p.G12 = h->G12; p.R12 = h->R12; p.R3 = h->R3;
   p.sb_rows3 = h->structured ? stream_sb_rows(h->R3) : 1;
+  p.cw12 = h->cw12; p.cw3 = h->cw3;  // (what prepare_streaming re-tiled Wt with)
+  p.stage_doubles = p.Wt ? h->stage_doubles : kStageDoubles;
+  p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;
   // few iterations: copying the W slice into shared memory costs as much as streaming it once;

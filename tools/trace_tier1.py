@@ -1,0 +1,23 @@
+"""Scratch (GPU box): timeline of CTA 0's warp roles in the L2/HBM tier, iterations 100..103, from a
+-DCQP_TRACE build (CQP_B200_LIB=build/trace/libcqp_b200.so).  Times in us relative to the first stamp."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2311_18056_b200 import problems, solver as S, _lib
+NAMES = {0: "cmp:start", 1: "cmp:v landed", 10: "cmp15:v landed", 2: "cmp:done", 11: "cmp15:done", 4: "pub:start",
+         5: "pub:full", 6: "pub:published", 7: "pub:rearmed", 8: "ldr:go", 9: "ldr:fetched"}
+which = sys.argv[1] if len(sys.argv) > 1 else "quad"
+wl = problems.config4_quadruped(30, 0) if which == "quad" else problems.config3_atlas(30, 0)
+base = wl.base_problem()
+s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
+q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
+for _ in range(2):
+    s.cold_start(); r = s.fixed_iters(120)
+print(which, s.launch_info(), "kernel_us", r.kernel_us, "us/iter", r.kernel_us / 120)
+words = (C.c_int * 256)()
+_lib.load().cqp_debug_words(s._h, words)
+st = np.frombuffer(bytes(words), dtype=np.int64)[32:32 + 64].reshape(4, 16)
+t0 = st[0][0]
+for it in range(4):
+    ev = sorted((int(st[it][k]), NAMES[k]) for k in NAMES if st[it][k] > 0)
+    print("iter", 100 + it, " ".join(f"{n}@{(t - t0) / 1965.0:.2f}" for t, n in ev))
