@@ -42,7 +42,25 @@ __device__ __forceinline__ void progress(int* d, int role, int value) {
 
 // Optional timeline trace (-DCQP_TRACE): clock64() stamps of CTA 0's roles for iterations
 // 100..103, 16 slots per iteration, into the host-mapped debug record (as long long, from word 64).
-#ifdef CQP_TRACE
+#if defined(CQP_TRACE_TWO)
+// Two-CTA variant (tools/trace_tier1.py two): CTA 0 and the LAST CTA (a lambda-row CTA of the
+// structured partition) stamp iterations AT, AT+1 with %globaltimer (ns, common to all SMs).
+#ifndef CQP_TRACE_AT
+#define CQP_TRACE_AT 100
+#endif
+__device__ __forceinline__ long long cqp_globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CQP_STAMP(dbg, it, slot)                                                                          \
+  do {                                                                                                    \
+    if ((blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (it) >= CQP_TRACE_AT && (it) < CQP_TRACE_AT + 2) \
+      reinterpret_cast<volatile long long*>((dbg) + 64)[(blockIdx.x == 0 ? 0 : 32) + ((it)-CQP_TRACE_AT) * 16 + (slot)] = \
+          cqp_globaltimer();                                                                              \
+  } while (0)
+#define CQP_STAMP0(dbg, slot) do {} while (0)
+#elif defined(CQP_TRACE)
 #ifndef CQP_TRACE_AT
 #define CQP_TRACE_AT 100
 #endif

@@ -164,10 +164,9 @@ __device__ __forceinline__ void fma_rows(const double* __restrict__ M, int ld, i
 
 struct Smem {
   double* sW;    // R * Dpad resident slice (tier 0) / streaming ring (tier 1); p.wdoubles doubles
-  double* xs;    // 2 * Dpad   iterate (cache space), double buffered by iteration parity
-  double* uy;    // npad       unscaled y   (also scratch for g_s)
-  double* uz;    // mpad       unscaled z
-  double* ul;    // mpad       unscaled lambda
+  double* xs;    // 2 * XS     iterate (cache space), double buffered by iteration parity; XS = xs_stride()
+                 // The unscaled y / z / lambda of a residual pass (and the g_s scratch of load_layer)
+                 // live in whichever of the two buffers does NOT hold the current iterate: see scratch().
   double* sred;  // kWarps * 16          (all-CTA reduction of the residual norms)
   double* spart; // 2 * kComputeWarps * Rcap   per-warp partials of the hot loop, by parity
   double* sb;    // Rp  bias rows
@@ -179,13 +178,26 @@ struct Smem {
 
 __host__ __device__ inline int round_up(int x, int q) { return (x + q - 1) / q * q; }
 
+// Doubles between the two shared-memory copies of the iterate: room for D entries, and for the
+// three separately padded vectors [uy (npad); uz (mpad); ul (mpad)] that alias the idle copy.
+__host__ __device__ inline int xs_stride(int Dpad, int npad, int mpad) {
+  const int v = npad + 2 * mpad;
+  return v > Dpad ? v : Dpad;
+}
+
+struct Scratch {
+  double* uy;  // npad  unscaled y (also scratch for g_s)
+  double* uz;  // mpad  unscaled z
+  double* ul;  // mpad  unscaled lambda
+};
+
 // `wdoubles`: doubles reserved at the front for W: the resident slice R * Dpad (tier 0) or the
 // streaming ring stages * kStageDoubles (tier 1).
 __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad, int mpad,
                                                size_t wdoubles, int nparts = kComputeWarps) {
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
-  return wdoubles + 2 * (size_t)Dpad + npad + 2 * (size_t)mpad + kWarps * 16 +
+  return wdoubles + 2 * (size_t)xs_stride(Dpad, npad, mpad) + kWarps * 16 +
          2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
 }
 
@@ -197,10 +209,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   const int Rcap = round_up(p.R, RB);
   s.sW = base;
   s.xs = base + p.wdoubles;
-  s.uy = s.xs + 2 * p.Dpad;
-  s.uz = s.uy + p.npad;
-  s.ul = s.uz + p.mpad;
-  s.sred = s.ul + p.mpad;
+  s.sred = s.xs + 2 * xs_stride(p.Dpad, p.npad, p.mpad);
   s.spart = s.sred + kWarps * 16;
   s.sb = s.spart + 2 * p.nparts * Rcap;
   s.slo = s.sb + Rp;
@@ -210,12 +219,28 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   return s;
 }
 
+// The scratch vectors alias the copy of the iterate that is idle while `cur` (one of the two
+// copies, or null before the first iterate is loaded) is the current one.  Idle means: iteration i
+// has completed everywhere in this CTA (its readers of v_{i-1} are done) and the fetch of v_{i+1},
+// which overwrites that copy, has not been released yet -- true during a residual pass, the layer
+// switch that follows it, the prologue and the epilogue.
+__device__ __forceinline__ Scratch scratch(const RunParams& p, const Smem& s, const double* cur) {
+  const int XS = xs_stride(p.Dpad, p.npad, p.mpad);
+  double* base = (cur == s.xs + XS) ? s.xs : s.xs + XS;
+  Scratch q;
+  q.uy = base;
+  q.uz = base + p.npad;
+  q.ul = q.uz + p.mpad;
+  return q;
+}
+
 // Makes layer k current for this CTA: W slice -> shared memory (tier 0), bias rows for the
 // rows it owns: b = -[D_k; G D_k] g_s, 0 on the lambda rows (layers.cpp:168-175).
 // Uses s.uy as scratch for g_s = cost_scale * E o g (layers.cpp:181).
 template <int RB>
-__device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows) {
+__device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows, const double* cur) {
   const int t = threadIdx.x;
+  const Scratch sc = scratch(p, s, cur);
   __syncthreads();
   if (p.w_smem) {
     const double2* src =
@@ -225,7 +250,7 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
     for (int i = t; i < count; i += kThreads) dst[i] = __ldg(src + i);
   }
   for (int i = t; i < p.npad; i += kThreads)
-    s.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * p.g[i]) : 0.0;
+    sc.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * p.g[i]) : 0.0;
   __syncthreads();
   const int nm = p.n + p.m;
   const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
@@ -234,7 +259,7 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
     for (int r = warp; r < nrows; r += kWarps) {
       const int row = row0 + r;
       double bias = 0.0;
-      if (row < nm) bias = -warp_row_dot_mlp<8>(DG + (size_t)row * p.npad, s.uy, p.npad, lane);
+      if (row < nm) bias = -warp_row_dot_mlp<8>(DG + (size_t)row * p.npad, sc.uy, p.npad, lane);
       else if (p.structured) bias = -p.rho_vec[(size_t)k * p.m + (row - nm)];  // W(row, row - m), see the publisher
       if (lane == 0) s.sb[r] = bias;
     }
@@ -251,9 +276,10 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
                               unsigned& epoch, double (&out)[7]) {
   const int t = threadIdx.x;
   const int n = p.n, m = p.m;
+  const Scratch sc = scratch(p, s, xs);
   __syncthreads();
   // unscale (layers.hpp:57-59)
-  for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? p.E[i] * xs[i] : 0.0;
+  for (int i = t; i < p.npad; i += kThreads) sc.uy[i] = (i < n) ? p.E[i] * xs[i] : 0.0;
   for (int i = t; i < p.mpad; i += kThreads) {
     double z = 0.0, l = 0.0;
     if (i < m) {
@@ -265,8 +291,8 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
       }
       l = (p.F[i] * xs[n + m + i]) / p.cost_scale;
     }
-    s.uz[i] = z;
-    s.ul[i] = l;
+    sc.uz[i] = z;
+    sc.ul[i] = l;
   }
   __syncthreads();
 
@@ -284,9 +310,9 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     const int bn = max(0, min(cap3, cn - c0)), bm = max(0, min(cap3, cm - c0));
     for (int d = warp; d < 2 * bn + bm; d += kWarps) {
       double val;
-      if (d < bn) val = warp_row_dot_mlp<8>(p.H + (size_t)(h0 + c0 + d) * p.npad, s.uy, p.npad, lane);
-      else if (d < 2 * bn) val = warp_row_dot_mlp<8>(p.Gt + (size_t)(h0 + c0 + d - bn) * p.mpad, s.ul, p.mpad, lane);
-      else val = warp_row_dot_mlp<8>(p.Gr + (size_t)(g0 + c0 + d - 2 * bn) * p.npad, s.uy, p.npad, lane);
+      if (d < bn) val = warp_row_dot_mlp<8>(p.H + (size_t)(h0 + c0 + d) * p.npad, sc.uy, p.npad, lane);
+      else if (d < 2 * bn) val = warp_row_dot_mlp<8>(p.Gt + (size_t)(h0 + c0 + d - bn) * p.mpad, sc.ul, p.mpad, lane);
+      else val = warp_row_dot_mlp<8>(p.Gr + (size_t)(g0 + c0 + d - 2 * bn) * p.npad, sc.uy, p.npad, lane);
       if (lane == 0) s.sval[d] = val;
     }
     __syncthreads();
@@ -302,7 +328,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     }
     if (t < bm) {
       const double gy = s.sval[2 * bn + t];
-      const double z = s.uz[g0 + c0 + t];
+      const double z = sc.uz[g0 + c0 + t];
       mx[0] = nanmax(mx[0], fabs(gy - z));
       mx[4] = nanmax(mx[4], fabs(gy));
       mx[5] = nanmax(mx[5], fabs(z));
@@ -390,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
   }
   const int n = p.n, m = p.m, D = p.D;
+  const int XS = xs_stride(p.Dpad, p.npad, p.mpad);  // doubles between the two copies of the iterate
   const int nc2 = p.Dpad >> 1;
   const int nc2p = (nc2 + 7) & ~7;  // rows of the re-tiled copy are padded to 8 pairs = 128 B
   // rows this CTA owns; L2/HBM tier: column pairs it streams per row (wc2), pair offset of its slice
@@ -440,24 +467,25 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in slot 0
   if (p.do_refresh) {
     double* v = p.vq;
-    for (int i = t; i < p.npad; i += kThreads) s.uy[i] = (i < n) ? __ldcg(v + i) : 0.0;
+    const Scratch sc = scratch(p, s, nullptr);  // (no iterate in shared memory yet)
+    for (int i = t; i < p.npad; i += kThreads) sc.uy[i] = (i < n) ? __ldcg(v + i) : 0.0;
     __syncthreads();
     const int per = (m + p.G - 1) / p.G;
     const int g0 = blockIdx.x * per;
     const int g1 = min(m, g0 + per);
     for (int row = g0 + warp; row < g1; row += kWarps) {
-      const double zs = warp_row_dot_mlp<8>(p.Gs + (size_t)row * p.npad, s.uy, p.npad, lane);
+      const double zs = warp_row_dot_mlp<8>(p.Gs + (size_t)row * p.npad, sc.uy, p.npad, lane);
       if (lane == 0) __stcg(v + n + row, zs);
     }
     grid_barrier(p.barrier, epoch, p.G, p.dbg);
   }
 
-  load_layer<RB>(p, s, layer, row0, nrows);
+  load_layer<RB>(p, s, layer, row0, nrows, nullptr);  // (scratch in the second copy, cleared below)
 
   // v_0 -> xs[0] (slot 0 holds the iterate between launches; refresh_z above is complete)
-  for (int i = t; i < p.Dpad; i += kThreads) {
+  for (int i = t; i < XS; i += kThreads) {
     s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
-    s.xs[p.Dpad + i] = 0.0;
+    s.xs[XS + i] = 0.0;
   }
   __syncthreads();
 
@@ -484,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 2); CQP_STAMP(p.dbg, i, 1); }  // v_{i-1} landed
       if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 10);
-      const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * p.Dpad);
+      const double2* x2 = reinterpret_cast<const double2*>(s.xs + (size_t)(b ^ 1) * XS);
       const double* Wrows = p.w_smem ? s.sW : (p.W + ((size_t)layer * D + row0) * p.Dpad);
       if (streaming) {
         // thread (pc = t & 127, rq = t >> 7): column pair pc of the chunk, rows 4 rq .. 4 rq + 3 of
@@ -548,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         // polls cannot succeed and would compete with the W prefetch for L2 bandwidth.
         mbar_wait(go, (i - 1) & 1, p.dbg, 9, i);
         if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);
-        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, t, nfetch, p.dbg, i);
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, t, nfetch, p.dbg, i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xready[b]);
       }
@@ -603,7 +631,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
       double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
       double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
-      const double* xprev = s.xs + (size_t)(b ^ 1) * p.Dpad;  // v_{i-1} (complete: the compute warps read it)
+      const double* xprev = s.xs + (size_t)(b ^ 1) * XS;  // v_{i-1} (complete: the compute warps read it)
+      // (one row per lane and trip: issuing three rows' loads together was measured 2-4 % SLOWER
+      // per iteration at the robot-sized configs: the first rows are published later)
       for (int r = lane; r < nrows; r += 32) {
         double x = 0.0;
 #pragma unroll
@@ -637,10 +667,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);  // (see launch_run)
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
       if (streaming)
-        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, kComputeThreads + lt, nfetch,
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, kComputeThreads + lt, nfetch,
                          p.dbg, i);
       else
-        fetch_iterate<8>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * p.Dpad, nc2, lt, nfetch, p.dbg, i);
+        fetch_iterate<8>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, lt, nfetch, p.dbg, i);
       __syncwarp();
       if (lt == 0) CQP_STAMP(p.dbg, i, 9);
       if (lane == 0) mbar_arrive(&xready[b]);
@@ -652,7 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     double nr[7];
-    residual_pass<RB>(p, s, s.xs + (size_t)(i & 1) * p.Dpad, false, epoch, nr);
+    const double* xcur = s.xs + (size_t)(i & 1) * XS;
+    residual_pass<RB>(p, s, xcur, false, epoch, nr);
     const double r_prim = nr[0], r_dual = nr[1];
     if (blockIdx.x == 0 && t == 0 && n_hist < p.cap) {
       p.hist_i[2 * n_hist] = i;
@@ -684,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
           p.trace[2 * n_trace + 1] = cand;
         }
         ++n_trace;
-        load_layer<RB>(p, s, layer, row0, nrows);
+        load_layer<RB>(p, s, layer, row0, nrows, xcur);
       }
     }
     if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
@@ -696,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // ---- epilogue (solver.cpp:90-99) ----
   if (t == 0) progress(p.dbg, 3, iters_done * 10 + 9);
   double nr[7];
-  const double* xfinal = s.xs + (size_t)(iters_done & 1) * p.Dpad;
+  const double* xfinal = s.xs + (size_t)(iters_done & 1) * XS;
   residual_pass<RB>(p, s, xfinal, true, epoch, nr);
   // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
   // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
@@ -712,11 +743,12 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     }
   }
   if (blockIdx.x == 0) {
-    mpc_extract_control(p, s.uy, t);
-    for (int i = t; i < n; i += kThreads) p.out_y[i] = s.uy[i];
+    const Scratch sc = scratch(p, s, xfinal);  // unscaled solution left by the final residual pass
+    mpc_extract_control(p, sc.uy, t);
+    for (int i = t; i < n; i += kThreads) p.out_y[i] = sc.uy[i];
     for (int i = t; i < m; i += kThreads) {
-      p.out_z[i] = s.uz[i];
-      p.out_lam[i] = s.ul[i];
+      p.out_z[i] = sc.uz[i];
+      p.out_lam[i] = sc.ul[i];
     }
     if (t == 0) {
       DevResultHead h;

@@ -18,6 +18,8 @@ words = (C.c_int * 256)()
 _lib.load().cqp_debug_words(s._h, words)
 st = np.frombuffer(bytes(words), dtype=np.int64)[32:32 + 64].reshape(4, 16)
 t0 = st[0][0]
+two = len(sys.argv) > 2 and sys.argv[2] == "two"   # -DCQP_TRACE_TWO build: rows = (CTA 0: it, it+1), (last CTA: it, it+1), ns
 for it in range(4):
     ev = sorted((int(st[it][k]), NAMES[k]) for k in NAMES if st[it][k] > 0)
-    print("iter", 100 + it, " ".join(f"{n}@{(t - t0) / 1965.0:.2f}" for t, n in ev))
+    label = (("cta0", "ctaLast")[it // 2] + f" iter {100 + it % 2}") if two else f"iter {100 + it}"
+    print(label, " ".join(f"{n}@{(t - t0) / (1000.0 if two else 1965.0):.2f}" for t, n in ev))
