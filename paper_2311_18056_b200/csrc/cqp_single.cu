@@ -113,6 +113,29 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch,
   __syncthreads();
 }
 
+// The same barrier in two halves, so that work which does not depend on the other CTAs can run
+// between the arrival and the wait.
+__device__ __forceinline__ void grid_barrier_arrive(unsigned* counter, unsigned& epoch, unsigned nblocks) {
+  __syncthreads();
+  epoch += nblocks;
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier_wait(unsigned* counter, unsigned epoch, int* dbg) {
+  if (threadIdx.x == 0) {
+    unsigned seen, spins = 0;
+    long long t0 = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+      if ((++spins & 0x3FF) == 0) {
+        if (t0 == 0) t0 = clock64();
+        else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 5, (int)epoch);
+      }
+    } while (seen < epoch);
+  }
+  __syncthreads();
+}
+
 template <int RB>
 struct Log2;
 template <> struct Log2<4> { static constexpr int v = 2; };
@@ -449,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   unsigned epoch = 0;
 
   int layer = p.state[0];
+  CQP_STAMP0(p.dbg, 0);  // (-DCQP_TRACE: prologue / epilogue timeline of CTA 0, tools/trace_tier1.py)
   if (blockIdx.x == 0 && t == 0) *p.barrier_next = 0u;  // counter of the NEXT launch (ping-pong)
 
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
@@ -477,10 +501,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       const double zs = warp_row_dot_mlp<8>(p.Gs + (size_t)row * p.npad, sc.uy, p.npad, lane);
       if (lane == 0) __stcg(v + n + row, zs);
     }
-    grid_barrier(p.barrier, epoch, p.G, p.dbg);
+    grid_barrier_arrive(p.barrier, epoch, p.G);  // (waited for below: the bias rows do not depend on z_s)
   }
 
+  CQP_STAMP0(p.dbg, 1);  // bounds + this CTA's rows of refresh_z done
   load_layer<RB>(p, s, layer, row0, nrows, nullptr);  // (scratch in the second copy, cleared below)
+  if (p.do_refresh) grid_barrier_wait(p.barrier, epoch, p.dbg);  // every CTA's rows of z_s are in slot 0
+  CQP_STAMP0(p.dbg, 2);  // bias rows done, refresh_z complete
 
   // v_0 -> xs[0] (slot 0 holds the iterate between launches; refresh_z above is complete)
   for (int i = t; i < XS; i += kThreads) {
@@ -495,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     p.trace[1] = layer;
   }
 
+  CQP_STAMP0(p.dbg, 3);  // v_0 in shared memory: iterations start
   bool converged = false;
   int iters_done = 0;
   int until_check = p.check_interval;
@@ -726,9 +754,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
 
   // ---- epilogue (solver.cpp:90-99) ----
   if (t == 0) progress(p.dbg, 3, iters_done * 10 + 9);
+  CQP_STAMP0(p.dbg, 4);  // iterations done
   double nr[7];
   const double* xfinal = s.xs + (size_t)(iters_done & 1) * XS;
   residual_pass<RB>(p, s, xfinal, true, epoch, nr);
+  CQP_STAMP0(p.dbg, 5);  // final residual pass done
   // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
   // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
   {
@@ -765,6 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       p.state[0] = layer;
     }
   }
+  CQP_STAMP0(p.dbg, 6);
 }
 
 // ---- small helper kernels ---------------------------------------------------------------

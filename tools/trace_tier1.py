@@ -13,6 +13,17 @@ s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=
 q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
 for _ in range(2):
     s.cold_start(); r = s.fixed_iters(120)
+if len(sys.argv) > 2 and sys.argv[2] == "step":
+    # prologue / epilogue stamps (slots 48..54, -DCQP_TRACE build) of one fused MPC step of k iterations
+    k = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    for _ in range(3):
+        r = s.mpc_step(q.g, q.c, q.d, k)
+    words = (C.c_int * 256)()
+    _lib.load().cqp_debug_words(s._h, words)
+    st = np.frombuffer(bytes(words), dtype=np.int64)[32 + 48:32 + 48 + 7]
+    names = ["entry", "bounds+refresh_z", "bias rows", "v0 loaded", "iterations", "final residual pass", "results written"]
+    print(which, "k", k, "kernel_us", r.kernel_us, " ".join(f"{nm}@{(int(t) - int(st[0])) / 1965.0:.2f}" for nm, t in zip(names, st)))
+    sys.exit(0)
 print(which, s.launch_info(), "kernel_us", r.kernel_us, "us/iter", r.kernel_us / 120)
 words = (C.c_int * 256)()
 _lib.load().cqp_debug_words(s._h, words)
