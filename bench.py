@@ -204,26 +204,18 @@ def measure_hbm_copy_peak():
     return 2 * 8 * n / (best * 1e-3) / 1e9
 
 
-def measure_l2_read_peak():
-    """Read rate of an L2-resident buffer (48 MB, read 40 times back to back by a reduction): the
-    ceiling of the single-QP streaming tier once its ladder level fits the 126 MB L2."""
-    import torch
-    a = torch.ones(6 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    for _ in range(3):
-        a.sum()
-    torch.cuda.synchronize()
-    best = 1e30
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(40):
-            a.sum()
-        e1.record(); torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
-    n = a.numel()
-    del a
-    torch.cuda.empty_cache()
-    return 40 * 8 * n / (best * 1e-3) / 1e9
+def measure_read_peaks(device: int):
+    """(HBM read GB/s, L2 read GB/s) with the library's own read kernel (cqp_measure_read_bandwidth):
+    a 2 GiB buffer read 3 times, and a 48 MB buffer (fits the 126 MB L2) read 60 times."""
+    import ctypes as C
+    from paper_2311_18056_b200 import _lib
+    L = _lib.load()
+    out = []
+    for nbytes, passes in ((2 << 30, 3), (48 << 20, 60)):
+        v = C.c_double()
+        rc = L.cqp_measure_read_bandwidth(device, nbytes, passes, C.byref(v))
+        out.append(v.value if rc == 0 else None)
+    return tuple(out)
 
 
 def single_qp_sweep(S, problems, repeats: int = 7):
@@ -413,7 +405,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         peaks = dict(peaks, hbm_gbs=hbm_measured)
         peak_src = "device copy measured in this run (MEASURED_PEAKS.json absent)"
     mpc_steps = guarded("mpc_steps", lambda: mpc_step_section(S, problems, peaks)) if extra else None
-    l2_read = guarded("l2_read_peak", measure_l2_read_peak) if extra else None
+    rd_peaks = guarded("read_peaks", lambda: measure_read_peaks(local_rank)) if extra else None
+    hbm_read, l2_read = rd_peaks if rd_peaks else (None, None)
 
     line = {
         "metric": METRIC, "value": value, "unit": "QP/s", "n_gpus": world, "steps": args.steps,
@@ -456,8 +449,9 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "frac": big["W_stream_GBs"] / l2_peak, "traffic": read_stream_traffic(),
             "kernel": "run_kernel<16, true> (persistent single-QP kernel, W through the cp.async.bulk ring)",
             "algorithmic": f"{big['W_bytes_per_iteration']:.0f} bytes of W per iteration (lambda rows streamed as rho*G only; dense 8*D^2 = {8 * big['D'] ** 2}) x {big['iters_per_step']} iterations per step / step kernel time (includes refresh_z, bias and epilogue residual passes)",
-            "peak_source": ("torch.sum over an L2-resident 48 MB buffer, 40 passes, measured in this run" if l2_read
+            "peak_source": ("cqp_measure_read_bandwidth: all SMs read an L2-resident 48 MB buffer 60 times (16-byte loads, 8 in flight per thread), measured in this run" if l2_read
                             else "fallback: ~6300 B/clk LTS cap x 1.965 GHz (B300_MICROARCH.md)"),
+            "hbm_read_gbs": hbm_read,
             "hbm_copy_gbs": peaks.get("hbm_gbs"), "frac_of_hbm_copy_rate": big["W_stream_frac_of_hbm_peak"],
             "traffic_source": "ncu dram__bytes_read + write per iteration (profiles/stream_traffic.json): DRAM supplies that much of the algorithmic bytes, L2 the rest",
             "note": "frac_of_hbm_copy_rate can exceed 1 because most of W is re-read from L2 every iteration; with the dense layer (133 MB, session 2) the same kernel was HBM-bound at 92 % of the copy rate"}

@@ -204,6 +204,12 @@ CQP_API int cqp_launch_info(const cqp_handle *h, int *ctas, int *rows_per_cta, i
  * and reports structured = 1. */
 CQP_API int cqp_layer_traffic(const cqp_handle *h, double *w_bytes_per_iteration, int *structured);
 
+/* Measurement helper for roofline denominators (bench.py): rate at which all SMs read a device
+ * buffer of `bytes` bytes `passes` times with 16-byte loads, 8 in flight per thread.  A buffer
+ * much larger than the 126 MB L2 gives the HBM read rate, one that fits it the L2 read rate. */
+CQP_API int cqp_measure_read_bandwidth(int device, unsigned long long bytes, int passes,
+                                       double *gb_per_s);
+
 /* Page-locked host memory for the caller's input / output buffers (cudaMallocHost / cudaFreeHost):
  * copies from and to pinned buffers run at full PCIe rate and asynchronously; pageable buffers
  * are staged by the driver.  Optional: every entry point accepts any host pointer. */

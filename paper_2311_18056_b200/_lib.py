@@ -56,7 +56,7 @@ EXPORTS = [
     "cqp_warm_start", "cqp_refresh_z", "cqp_solve", "cqp_fixed_iters", "cqp_mpc_step",
     "cqp_mpc_set_template", "cqp_mpc_step_x0",
     "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
-    "cqp_launch_info", "cqp_layer_traffic", "cqp_pinned_alloc", "cqp_pinned_free",
+    "cqp_launch_info", "cqp_layer_traffic", "cqp_measure_read_bandwidth", "cqp_pinned_alloc", "cqp_pinned_free",
     "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve", "cqp_batch_last_timing", "cqp_batch_last_profile", "cqp_batch_round_profile",
 ]
 
@@ -107,6 +107,7 @@ def load() -> C.CDLL:
     L.cqp_debug_words.argtypes = [C.c_void_p, c_int_p]
     L.cqp_launch_info.argtypes = [C.c_void_p, c_int_p, c_int_p, c_int_p, c_int_p]
     L.cqp_layer_traffic.argtypes = [C.c_void_p, c_double_p, c_int_p]
+    L.cqp_measure_read_bandwidth.argtypes = [C.c_int, C.c_ulonglong, C.c_int, c_double_p]
     L.cqp_pinned_alloc.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong]
     L.cqp_pinned_free.argtypes = [C.c_void_p]
     L.cqp_pinned_free.restype = None

@@ -169,6 +169,29 @@ int cold_start(cqp_handle* h) {
 
 using namespace cqp;
 
+// ---- measurement helper: read bandwidth of a device buffer -----------------------------------
+static __global__ void __launch_bounds__(512) read_bw_kernel(const double2* __restrict__ buf, size_t n2, int passes,
+                                                      double* __restrict__ sink) {
+  double acc = 0.0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int pass = 0; pass < passes; ++pass) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < n2; i += 8 * stride) {  // 8 independent 16-byte loads in flight per thread
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(buf + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y;
+    }
+    for (; i < n2; i += stride) {
+      const double2 v = __ldcg(buf + i);
+      acc += v.x + v.y;
+    }
+  }
+  if (acc == 123.456) *sink = acc;  // keeps the loads alive
+}
+
+
 extern "C" {
 
 void cqp_default_settings(cqp_settings* s) {
@@ -560,6 +583,39 @@ int cqp_launch_info(const cqp_handle* h, int* ctas, int* rows_per_cta, int* tier
   if (rows_per_cta) *rows_per_cta = h->R;
   if (tier) *tier = h->cluster ? 2 : (h->w_smem ? 0 : 1);
   if (smem_bytes) *smem_bytes = h->smem_bytes;
+  return CQP_OK;
+}
+
+int cqp_measure_read_bandwidth(int device, unsigned long long bytes, int passes, double* gb_per_s) {
+  if (!gb_per_s || bytes < 4096 || passes < 1) { set_error("measure_read_bandwidth: bad argument"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CQP_CUDA(cudaGetDeviceProperties(&prop, device));
+  double2* buf = nullptr;
+  double* sink = nullptr;
+  const size_t n2 = (size_t)bytes / sizeof(double2);
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&buf), n2 * sizeof(double2)));
+  CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&sink), sizeof(double)));
+  CQP_CUDA(cudaMemset(buf, 0, n2 * sizeof(double2)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int grid = prop.multiProcessorCount * 4;
+  read_bw_kernel<<<grid, 512>>>(buf, n2, 2, sink);  // warm-up (also brings an L2-sized buffer into L2)
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    read_bw_kernel<<<grid, 512>>>(buf, n2, passes, sink);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(buf); cudaFree(sink);
+  if (err != cudaSuccess) return cuda_fail(err, "read_bw_kernel");
+  *gb_per_s = (double)n2 * sizeof(double2) * passes / (best * 1e-3) / 1e9;
   return CQP_OK;
 }
 

@@ -70,6 +70,7 @@ struct RunParams {
   int sb_rows3;          // rows per super-block of the W stream in the lambda-row CTAs
   int nparts;            // per-row partial sums kept per parity: 16 (one per compute warp) or, for handles
                          // that always stream, 4
+  int cofetch;           // grid kernel, resident tier: the compute warps fetch the iterate along with the loaders
   int stage_doubles;     // doubles per ring stage (re-tiled stream: h->stage_doubles; row segments: kStageDoubles)
   int cw12, cw3;         // column pairs per ring stage (chunk width): a stage holds nv rows x cw pairs
                          // <= 32 KB, so super-blocks of fewer than 16 rows take wider chunks (one bulk

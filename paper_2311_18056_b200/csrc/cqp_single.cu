@@ -406,7 +406,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
 // ladder level fits one thread-block cluster's shared memory use cqp_cluster.cu instead.
 // STREAM selects the L2/HBM tier's code (W through the cp.async.bulk ring) at compile time, so the
 // shared-memory-resident tier keeps its registers.
-template <int RB, bool STREAM>
+template <int RB, bool STREAM, bool COFETCH = STREAM>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
@@ -429,8 +429,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if (t == 0) {
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
-    mbar_init(&xready[0], kLoaderWarps + (STREAM ? kComputeWarps : 0));
-    mbar_init(&xready[1], kLoaderWarps + (STREAM ? kComputeWarps : 0));
+    mbar_init(&xready[0], kLoaderWarps + (COFETCH ? kComputeWarps : 0));
+    mbar_init(&xready[1], kLoaderWarps + (COFETCH ? kComputeWarps : 0));
     mbar_init(go, 1);
     for (int k = 0; k < (STREAM ? NS : 0); ++k) {
       mbar_init(&wfull[k], 1);
@@ -529,7 +529,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   constexpr int shift = 5 - Log2<RB>::v;
   unsigned wstage = 0, wphase = 0;  // ring position of the next W chunk to consume (compute) / issue (streamer)
   const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
-  const int nfetch = streaming ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
+  constexpr bool cofetch = COFETCH;  // the compute warps fetch v_i together with the loaders
+  const int nfetch = cofetch ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
   for (int i = 1; i <= p.total_iters; ++i) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
     const int b = i & 1;
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 11);
       if (lane == 0) mbar_arrive(&full[b]);
       if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
-      if (streaming) {
+      if (cofetch) {
         // L2/HBM tier: large iterate, idle compute warps: they fetch v_i together with the loaders
         // (xs[b] held v_{i-2}, which every warp finished reading before any warp entered iteration i).
         // Like the loaders they start polling only once this CTA has published its own rows: earlier
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
       if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);  // (see launch_run)
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
-      if (streaming)
+      if (cofetch)
         fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, kComputeThreads + lt, nfetch,
                          p.dbg, i);
       else
@@ -940,19 +941,20 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
   dst[slice + (size_t)(sb * sbr) * pitch + (size_t)nv * (c * cwp) + (size_t)r * cw + pc] = val;
 }
 
-template <int RB, bool STREAM>
+template <int RB, bool STREAM, bool COFETCH>
 int launch_run_rb2(cqp_handle* h, RunParams& p) {
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, STREAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, STREAM, COFETCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->smem_bytes));
   void* args[] = {&p};
-  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, STREAM>, dim3(h->G), dim3(kThreads),
+  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, STREAM, COFETCH>, dim3(h->G), dim3(kThreads),
                                        args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
 }
 
 template <int RB>
 int launch_run_rb(cqp_handle* h, RunParams& p) {
-  return (!p.w_smem && p.stream_stages > 0) ? launch_run_rb2<RB, true>(h, p) : launch_run_rb2<RB, false>(h, p);
+  if (!p.w_smem && p.stream_stages > 0) return launch_run_rb2<RB, true, true>(h, p);
+  return p.cofetch ? launch_run_rb2<RB, false, true>(h, p) : launch_run_rb2<RB, false, false>(h, p);
 }
 
 }  // namespace
@@ -1168,6 +1170,10 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.sb_rows3 = h->structured ? stream_sb_rows(h->R3) : 1;
   p.cw12 = h->cw12; p.cw3 = h->cw3;  // (what prepare_streaming re-tiled Wt with)
   p.stage_doubles = p.Wt ? h->stage_doubles : kStageDoubles;
+  // resident tier: the compute warps, idle during the exchange, fetch v_i along with the loader warps
+  // (B200, 1000 iterations: D = 900 2576 -> 2468 us, D = 1500 3924 -> 3706 us); CQP_COFETCH=0 for A/B runs
+  p.cofetch = 1;
+  if (const char* e = std::getenv("CQP_COFETCH")) p.cofetch = std::atoi(e);
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;
