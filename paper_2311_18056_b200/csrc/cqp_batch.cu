@@ -1076,7 +1076,8 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
                               final_index, r_prim, r_dual, n_switches, device_ms, nullptr);
   // sub-batches: columns [off_k, off_k + B_k) go to lane k; small batches use one lane
   const int K = (int)b->lanes.size();
-  const int used = B < 512 ? 1 : K;
+  int used = B < 512 ? 1 : K;
+  while (used < K && (B + used - 1) / used > b->lanes[0]->capacity) ++used;  // (B <= capacity <= K * lane capacity)
   const int per = (B + used - 1) / used;
   const int n = b->n, m = b->m;
   CQP_CUDA(cudaSetDevice(b->h->device));

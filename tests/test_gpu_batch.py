@@ -135,6 +135,8 @@ def test_lanes_match_one_batch(G, oracle, P, monkeypatch):
         single = G.Solver(base.H, base.g, base.G, base.c, base.d)
         batch = G.BatchSolver(single, capacity=B)
         outs.append({k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in batch.solve(g, c, d).items()})
+        small = batch.solve(g[:, :500], c[:, :500], d[:, :500])     # < 512 columns: one lane if it has the capacity (not with 3)
+        assert np.array_equal(small["iterations"], outs[0]["iterations"][:500])
         small = batch.solve(g[:, :100], c[:, :100], d[:, :100])     # small batch on a multi-lane object: one lane
         assert np.array_equal(small["iterations"], outs[0]["iterations"][:100])
         assert rel_err(small["y"], outs[0]["y"][:, :100]) <= 1e-9

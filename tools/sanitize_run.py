@@ -20,7 +20,9 @@ if which in ("all", "cluster"):
     run("cluster-smem", problems.config2(6, 1), {"CQP_CLUSTER_MODE": "smem"})
 if which in ("all", "grid"):
     run("grid-resident", problems.config2(6, 1), {"CQP_FORCE_TIER": "0"})
-    run("grid-stream", problems.config2(6, 1), {"CQP_FORCE_TIER": "1"})
+    run("grid-stream", problems.config2(6, 1), {"CQP_FORCE_TIER": "1", "CQP_SINGLE_DENSE": "1"})
+    run("grid-stream-structured", problems.config2(6, 1), {"CQP_FORCE_TIER": "1", "CQP_FORCE_STRUCTURED": "1"})
+    run("grid-stream-structured-odd", problems.config2(7, 1), {"CQP_FORCE_TIER": "1", "CQP_FORCE_STRUCTURED": "1"})
 if which in ("all", "batch"):
     wl = problems.config2(6, 1); base = wl.base_problem()
     g, c, d, _ = problems.batch_instances(wl, 96)
@@ -28,3 +30,14 @@ if which in ("all", "batch"):
     b = S.BatchSolver(s, 96)
     out = b.solve(g, c, d)
     print("batch", out["iterations"][:8], flush=True)
+    b.close()
+    os.environ["CQP_BATCH_LANES"] = "2"           # two concurrent lanes (sub-batches on their own streams)
+    g, c, d, _ = problems.batch_instances(wl, 640)
+    b = S.BatchSolver(s, 640)
+    out = b.solve(g, c, d)
+    print("batch-lanes", out["iterations"][:8], out["launches"], flush=True)
+    b.close()
+    os.environ["CQP_BATCH_DENSE"] = "1"           # dense layer (A/B switch)
+    b = S.BatchSolver(s, 96)
+    out = b.solve(g[:, :96], c[:, :96], d[:, :96])
+    print("batch-dense", out["iterations"][:8], flush=True)
