@@ -477,3 +477,43 @@ def test_structured_stream_layer_matches_dense_and_oracle(G, oracle, monkeypatch
     assert struct.solution.iterations == dense.solution.iterations
     assert rel_err(struct.solution.y, dense.solution.y) <= 1e-9
     assert rel_err(struct.solution.lam, dense.solution.lam) <= 1e-9
+
+
+@pytest.mark.parametrize("shape", ["odd_n_odd_m", "even_n_odd_m"])
+def test_odd_dimensions_in_every_grid_mode(G, oracle, P, monkeypatch, shape):
+    """n and m whose separately padded scratch vectors [uy; uz; ul] need MORE room than the padded
+    iterate (npad + 2 mpad > Dpad): they alias the idle copy of the iterate in the grid kernel, so
+    the copies are spaced by max(Dpad, npad + 2 mpad).  Checked against the oracle in the resident
+    tier, the streamed tier with the dense and with the structured layer, and the cluster tier:
+    cold solve (14 residual passes), then fused MPC steps (refresh_z + bias + iterations)."""
+    import numpy as np
+    from paper_2311_18056_b200 import mpc
+    if shape == "odd_n_odd_m":
+        wl = P.make_mpc_workload(3, 6, 5, seed=2)                       # n = m = 15, D = 45
+    else:
+        lim = mpc.BoxLimits(np.full(2, -1.0), np.full(2, 1.0), np.full(5, -20.0), np.full(5, 20.0), x_rows=[0])
+        wl = P.make_mpc_workload(2, 5, 5, seed=2, limits=lim)           # n = 10, m = 15, D = 40
+    base = wl.base_problem()
+    assert (base.n + base.n % 2) + 2 * (base.m + base.m % 2) > (base.n + 2 * base.m + (base.n + 2 * base.m) % 2)
+    q = wl.problem_at(wl.x0(3.0))
+    q2 = wl.problem_at(wl.x0(2.0, seed=7))
+    envs = ({"CQP_FORCE_TIER": "0"}, {"CQP_FORCE_TIER": "1", "CQP_SINGLE_DENSE": "1"},
+            {"CQP_FORCE_TIER": "1", "CQP_FORCE_STRUCTURED": "1"}, {})
+    keys = ("CQP_FORCE_TIER", "CQP_SINGLE_DENSE", "CQP_FORCE_STRUCTURED")
+    for env in envs:
+        for k in keys:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        gs, os_ = make_pair(oracle, G, base)
+        for s in (gs, os_):
+            s.update_vectors(q.g, q.c, q.d); s.cold_start()
+        assert_report_parity(gs.solve(), os_.solve())
+        for _ in range(3):
+            os_.update_vectors(q2.g, q2.c, q2.d); os_.refresh_z(); ro = os_.fixed_iters(3)
+            rg = gs.mpc_step(q2.g, q2.c, q2.d, 3)
+            assert rg.solution.iterations == 3 and rel_err(rg.solution.y, ro.solution.y) <= 1e-9
+            assert rel_err(rg.solution.lam, ro.solution.lam) <= 1e-9 and rel_err(rg.solution.z, ro.solution.z) <= 1e-9
+        gs.close()
+    for k in keys:
+        monkeypatch.delenv(k, raising=False)
