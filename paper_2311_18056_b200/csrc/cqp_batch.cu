@@ -6,8 +6,8 @@
 //   * The iterates are the columns of S (D x B, each column contiguous); one batch iteration is
 //     the dense contraction  S <- clamp(W_k S + Bias_k, lo, hi)  evaluated with FP64 tensor
 //     cores (mma.sync m8n8k4 f64 = DMMA.8x8x4, the only FP64 tensor shape sm_100a has; tcgen05
-//     has no f64 kind).  128x128x16 CTA tiles, 8 warps of 64x32, operands staged in shared
-//     memory by a 4-stage cp.async pipeline in a 16-byte-chunk XOR swizzle (conflict-free 8-byte
+//     has no f64 kind).  64x64 / 64x32 / 32x32 x16 CTA tiles (by active-column count), operands
+//     staged in shared memory by a 4-stage cp.async pipeline in a 16-byte-chunk XOR swizzle (conflict-free 8-byte
 //     fragment loads), bias + clamp fused into the epilogue.
 //   * Every QP adapts rho on its own (parity demands it), so columns are bucketed by ladder
 //     index: a slot map lists, per 128-column tile, which columns it holds and which W_k it
@@ -19,6 +19,10 @@
 //     Bias = -[D_k; G D_k] G_s.  Converged columns leave the slot map, so they stop costing work.
 //   * No host round trip inside a round; the host only polls a pinned "active columns" word with
 //     a lag of two rounds to know when to stop enqueuing.
+//   * Structured layer: the lambda rows of W, [rho G, -diag(rho), I] (layers.cpp:159-161), only
+//     multiply y: their tiles run ceil(n / 16) k-tiles and start from fma(-rho_i, z_i, lambda_i)
+//     (GemmParams::split).  Batches of >= 1024 columns run as two concurrent lanes (sub-batches on
+//     their own streams, one host thread each), whose launches fill each other's wave tails.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

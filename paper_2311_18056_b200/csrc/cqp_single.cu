@@ -28,7 +28,7 @@
 //         iterations too (W does not depend on v);
 //       - 3 loader warps poll L2 for v_i into a double-buffered shared-memory copy: all loads in
 //         flight, every re-poll round re-issues ALL still-armed entries back to back (one L2 round
-//         trip per round); in tier 1 the otherwise idle compute warps fetch along.
+//         trip per round); the compute warps, idle during the exchange, fetch along.
 //     Hand-offs use parity-split mbarriers (full[2], xready[2], go, wfull[], wempty[]), so a role
 //     can run at most one phase ahead and arrivals of different iterations never mix.
 //   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
@@ -36,6 +36,12 @@
 //     max-norms exchanged through L2 behind one grid barrier), and every CTA takes the identical
 //     rho decision; a switch reloads the W slice and recomputes the bias rows
 //     b = -[D_k; G D_k] g_s it owns.
+//   * L2/HBM tier, structured layer: the lambda rows of W, [rho G, -diag(rho), I]
+//     (layers.cpp:159-161), are streamed as their first n columns only and the publisher adds the
+//     two diagonal terms; rows are partitioned by bytes (CTAs [0, G12) own R12 of the first n + m
+//     rows, the others R3 lambda rows).  The ring takes all the shared memory the vectors leave, as
+//     3 large stages whose chunk width follows the stage size (configure_launch).
+//   * The unscaled y / z / lambda of a residual pass alias the idle copy of the iterate (scratch()).
 //   * Nothing is launched per iteration; the result record is written straight into host-mapped
 //     memory, so the host sees one launch and one stream synchronisation per call.
 #include <algorithm>
