@@ -1038,11 +1038,15 @@ int configure_launch(cqp_handle* h) {
     const char* dense = std::getenv("CQP_SINGLE_DENSE");
     const int n = h->n, m = h->m, nm = n + m;
     if (stages >= 2 && !(dense && dense[0] == '1') && !std::getenv("CQP_NO_RETILE") && m >= 1 && n >= 2 && G >= 2) {
+      // a lambda row costs more than its bytes (many short rows: more ring stages per byte, more rows
+      // for the single publisher warp), so its CTAs get a little less than an equal share of bytes
+      double lambda_weight = 1.25;  // (B200: Atlas-sized 6.3 -> 5.3 us per iteration, quadruped-sized 11.2 -> 10.8; 1.1 .. 1.5 alike)
+      if (const char* e = std::getenv("CQP_LAMBDA_WEIGHT")) lambda_weight = std::atof(e);
       long long best = -1;
       int bestR12 = 0, bestR3 = 0;
       for (int g12 = 1; g12 < G; ++g12) {
         const int r12 = (nm + g12 - 1) / g12, r3 = (m + (G - g12) - 1) / (G - g12);
-        const long long cost = std::max((long long)r12 * D, (long long)r3 * n);
+        const long long cost = std::max((long long)r12 * D, (long long)(lambda_weight * r3 * n));
         if (best < 0 || cost < best) { best = cost; bestR12 = r12; bestR3 = r3; }
       }
       const int Rs = std::max(bestR12, bestR3);
@@ -1050,7 +1054,7 @@ int configure_launch(cqp_handle* h) {
       int stages_s = 0, stage_doubles_s = kStageDoubles;
       plan_ring(base_s, stages_s, stage_doubles_s);
       const bool force = std::getenv("CQP_FORCE_STRUCTURED") != nullptr;  // tests: also where it does not pay
-      if (stages_s >= 2 && (best < (long long)R * D || force)) {
+      if (stages_s >= 2 && (best < (long long)(lambda_weight * R * D) || force)) {
         h->structured = 1;
         h->R12 = bestR12; h->R3 = bestR3;
         h->G12 = (nm + bestR12 - 1) / bestR12;
