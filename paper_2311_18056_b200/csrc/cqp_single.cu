@@ -1184,6 +1184,10 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   // (B200, 1000 iterations: D = 900 2576 -> 2468 us, D = 1500 3924 -> 3706 us); CQP_COFETCH=0 for A/B runs
   p.cofetch = 1;
   if (const char* e = std::getenv("CQP_COFETCH")) p.cofetch = std::atoi(e);
+  // with 608 fetching threads the first poll of the resident tier is best issued at once (B200, 1000
+  // iterations: D = 900 2456 -> 2358 us, D = 1500 3701 -> 3667 us); the streamed tier keeps the pause
+  // (Atlas-sized 5.34 vs 5.55 us per iteration: early polls compete with the W stream)
+  if (p.w_smem && p.cofetch && !std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = 0;
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;
@@ -1191,6 +1195,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   // the ring then lives in the (unused) slice region
   if (total_iters < 4 && p.w_smem) {
     p.w_smem = 0;
+    if (!std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = 150;  // (streaming kernel: keeps the pause)
     int stages = h->wdoubles / kStageDoubles;
     if (stages > kMaxStages) stages = kMaxStages;
     p.stream_stages = stages >= 2 ? stages : 0;
