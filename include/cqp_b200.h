@@ -226,12 +226,28 @@ CQP_API void cqp_batch_destroy(cqp_batch *b);
 
 /* g_cols: n x B, c_cols/d_cols: m x B (column-major, original units).  Outputs, any may be
  * NULL: y_cols n x B, z_cols m x B, lambda_cols m x B, status/iterations/final_index (B),
- * r_prim/r_dual (B), n_switches (B).  device_ms: CUDA-event time of the whole batch solve. */
+ * r_prim/r_dual (B), n_switches (B).  device_ms: CUDA-event time of the whole batch solve.
+ * Every input / output array may live in host memory (pageable or pinned) OR in the handle's
+ * device memory (unified addressing decides): a caller that gathers results across GPUs passes
+ * device buffers and hands them to its collective without a host round trip. */
 CQP_API int cqp_batch_solve(cqp_batch *b, int B, const double *g_cols, const double *c_cols,
                             const double *d_cols, double *y_cols, double *z_cols,
                             double *lambda_cols, int *status, int *iterations,
                             int *final_index, double *r_prim, double *r_dual, int *n_switches,
                             double *device_ms);
+
+/* Per-column Solution::rho_trace (problem.hpp:57-70; entry 0 is {0, start index}, solver.cpp:50)
+ * of the LAST cqp_batch_solve (B must equal that call's B).  trace: B x cap records, column j at
+ * trace + j * cap; trace_len (B): records column j produced (records beyond `cap` are dropped, the
+ * length still counts them).  Either pointer may be NULL.  cap >= max_iters / check_interval + 2
+ * holds every possible trace. */
+CQP_API int cqp_batch_get_traces(cqp_batch *b, int B, int cap, cqp_rho_switch *trace,
+                                 int *trace_len);
+
+/* Per-column SolveReport::residual_history (solver.hpp:56-67: one sample per convergence check,
+ * grid_index = the index BEFORE that check's switch) of the last cqp_batch_solve; same layout. */
+CQP_API int cqp_batch_get_history(cqp_batch *b, int B, int cap, cqp_residual_sample *history,
+                                  int *history_len);
 
 /* CUDA-event times of the last cqp_batch_solve: compute_ms = from "inputs resident in HBM" to
  * "results ready in HBM"; total_ms additionally covers the host->device and device->host

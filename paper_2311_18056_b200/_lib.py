@@ -58,6 +58,7 @@ EXPORTS = [
     "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
     "cqp_launch_info", "cqp_layer_traffic", "cqp_measure_read_bandwidth", "cqp_pinned_alloc", "cqp_pinned_free",
     "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve", "cqp_batch_last_timing", "cqp_batch_last_profile", "cqp_batch_round_profile",
+    "cqp_batch_get_traces", "cqp_batch_get_history",
 ]
 
 _lib = None
@@ -119,6 +120,8 @@ def load() -> C.CDLL:
     L.cqp_batch_last_timing.argtypes = [C.c_void_p, c_double_p, c_double_p, C.POINTER(C.c_longlong)]
     L.cqp_batch_last_profile.argtypes = [C.c_void_p, c_double_p, c_double_p, c_int_p]
     L.cqp_batch_round_profile.argtypes = [C.c_void_p, C.c_int, c_int_p, c_double_p]
+    L.cqp_batch_get_traces.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(CqpRhoSwitch), c_int_p]
+    L.cqp_batch_get_history.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(CqpResidualSample), c_int_p]
     _lib = L
     return L
 

@@ -387,6 +387,11 @@ struct BatchDev {
   int* nsw;
   double* rp;
   double* rd;
+  // per-column records (problem.hpp:57-60, solver.hpp:56-61): rho_trace and residual_history
+  cqp_rho_switch* trace;       // [B][rec_cap]; entry 0 = {0, start index} (solver.cpp:50)
+  cqp_residual_sample* hist;   // [B][rec_cap]
+  int* nhist;
+  int rec_cap;
   // outputs
   double* out_y;     // [B][n]
   double* out_z;     // [B][m]
@@ -419,6 +424,8 @@ __global__ void batch_prepare_kernel(BatchDev b, int initial_index) {
     b.nsw[col] = 0;
     b.rp[col] = 0.0;
     b.rd[col] = 0.0;
+    b.nhist[col] = 0;
+    b.trace[(size_t)col * b.rec_cap] = {0, initial_index};  // every call's trace starts here (solver.cpp:50)
   }
 }
 
@@ -487,6 +494,11 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
   int layer = b.layer[col];
   bool converged = false;
   if (check) {
+    if (lane == 0) {  // residual_history sample: the index BEFORE this check's switch (solver.cpp:71)
+      const int k = b.nhist[col];
+      if (k < b.rec_cap) b.hist[(size_t)col * b.rec_cap + k] = {it, r_prim, r_dual, layer};
+      b.nhist[col] = k + 1;
+    }
     if (b.adaptive) {
       const double rho_cur = b.grid[layer];
       double rho_nom = rho_cur;
@@ -510,7 +522,12 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
       const int cand = ratio >= b.threshold ? best : layer;
       if (cand != layer) {
         layer = cand;
-        if (lane == 0) { b.layer[col] = cand; b.nsw[col] += 1; }
+        if (lane == 0) {
+          const int k = b.nsw[col] + 1;  // (entry 0 is the start index)
+          if (k < b.rec_cap) b.trace[(size_t)col * b.rec_cap + k] = {it, cand};
+          b.layer[col] = cand;
+          b.nsw[col] = k;
+        }
       }
     }
     converged = early_exit && r_prim <= b.eps_prim && r_dual <= b.eps_dual;
@@ -631,6 +648,12 @@ struct cqp_batch {
   double *uy = nullptr, *ul = nullptr, *uz = nullptr, *hy = nullptr, *gtl = nullptr, *gy = nullptr;
   int *layer = nullptr, *active = nullptr, *iters = nullptr, *status = nullptr, *nsw = nullptr;
   double *rp = nullptr, *rd = nullptr, *out_y = nullptr, *out_z = nullptr, *out_l = nullptr;
+  cqp_rho_switch* trace = nullptr;       // [capacity][rec_cap]
+  cqp_residual_sample* hist = nullptr;   // [capacity][rec_cap]
+  int* nhist = nullptr;
+  int rec_cap = 0;
+  int last_B = 0;                        // columns of the last solve (single lane)
+  std::vector<int> lane_off, lane_cnt;   // parent: column range every lane solved last
   int* cols = nullptr;
   TileDesc* tiles = nullptr;
   int *n_tiles = nullptr, *n_active = nullptr;
@@ -818,6 +841,8 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   BA(hy, cap * b->ld_n); BA(gtl, cap * b->ld_n); BA(gy, cap * b->ld_m);
   BA(layer, cap); BA(active, cap); BA(iters, cap); BA(status, cap); BA(nsw, cap);
   BA(rp, cap); BA(rd, cap); BA(out_y, cap * n); BA(out_z, cap * m); BA(out_l, cap * m);
+  b->rec_cap = h->s.max_iters / h->s.check_interval + 2;
+  BA(trace, cap * b->rec_cap); BA(hist, cap * b->rec_cap); BA(nhist, cap);
   BA(cols, slot_cap); BA(tiles, tile_cap); BA(n_tiles, 1); BA(n_active, 1);
 #undef BA
   // shared matrices: handle layouts (row-major, even ld) -> tile-padded copies
@@ -850,6 +875,7 @@ static void batch_destroy_single(cqp_batch* b) {
   void* ptrs[] = {b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
+                  b->trace, b->hist, b->nhist,
                   b->tiles, b->n_tiles, b->n_active};
   for (void* p : ptrs) cudaFree(p);
   if (b->h_active) cudaFreeHost(b->h_active);
@@ -904,9 +930,9 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   }
   CQP_CUDA(cudaEventRecord(b->ev0, st));
   CQP_CUDA(cudaMemsetAsync(b->work_ctrs, 0, sizeof(int) * b->work_ctr_cap, st));
-  CQP_CUDA(cudaMemcpyAsync(b->g, g_cols, sizeof(double) * (size_t)n * B, cudaMemcpyHostToDevice, st));
-  CQP_CUDA(cudaMemcpyAsync(b->c, c_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));
-  CQP_CUDA(cudaMemcpyAsync(b->d, d_cols, sizeof(double) * (size_t)m * B, cudaMemcpyHostToDevice, st));
+  CQP_CUDA(cudaMemcpyAsync(b->g, g_cols, sizeof(double) * (size_t)n * B, cudaMemcpyDefault, st));
+  CQP_CUDA(cudaMemcpyAsync(b->c, c_cols, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
+  CQP_CUDA(cudaMemcpyAsync(b->d, d_cols, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
   CQP_CUDA(cudaMemsetAsync(b->S0, 0, sizeof(double) * (size_t)B * b->ld_s, st));  // cold start: v = 0
   CQP_CUDA(cudaMemsetAsync(b->S1, 0, sizeof(double) * (size_t)B * b->ld_s, st));
 
@@ -919,6 +945,8 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   bd.uy = b->uy; bd.ul = b->ul; bd.uz = b->uz; bd.hy = b->hy; bd.gtl = b->gtl; bd.gy = b->gy;
   bd.layer = b->layer; bd.active = b->active; bd.iters = b->iters; bd.status = b->status;
   bd.nsw = b->nsw; bd.rp = b->rp; bd.rd = b->rd;
+  bd.trace = b->trace; bd.hist = b->hist; bd.nhist = b->nhist; bd.rec_cap = b->rec_cap;
+  b->last_B = B;
   bd.out_y = b->out_y; bd.out_z = b->out_z; bd.out_l = b->out_l;
   bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
   bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
@@ -999,15 +1027,15 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   }
   CQP_CUDA(cudaEventRecord(b->evc1, st));
   // results
-  if (y_cols) CQP_CUDA(cudaMemcpyAsync(y_cols, b->out_y, sizeof(double) * (size_t)n * B, cudaMemcpyDeviceToHost, st));
-  if (z_cols) CQP_CUDA(cudaMemcpyAsync(z_cols, b->out_z, sizeof(double) * (size_t)m * B, cudaMemcpyDeviceToHost, st));
-  if (lambda_cols) CQP_CUDA(cudaMemcpyAsync(lambda_cols, b->out_l, sizeof(double) * (size_t)m * B, cudaMemcpyDeviceToHost, st));
-  if (status) CQP_CUDA(cudaMemcpyAsync(status, b->status, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-  if (iterations) CQP_CUDA(cudaMemcpyAsync(iterations, b->iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-  if (final_index) CQP_CUDA(cudaMemcpyAsync(final_index, b->layer, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-  if (r_prim) CQP_CUDA(cudaMemcpyAsync(r_prim, b->rp, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
-  if (r_dual) CQP_CUDA(cudaMemcpyAsync(r_dual, b->rd, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
-  if (n_switches) CQP_CUDA(cudaMemcpyAsync(n_switches, b->nsw, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (y_cols) CQP_CUDA(cudaMemcpyAsync(y_cols, b->out_y, sizeof(double) * (size_t)n * B, cudaMemcpyDefault, st));
+  if (z_cols) CQP_CUDA(cudaMemcpyAsync(z_cols, b->out_z, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
+  if (lambda_cols) CQP_CUDA(cudaMemcpyAsync(lambda_cols, b->out_l, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
+  if (status) CQP_CUDA(cudaMemcpyAsync(status, b->status, sizeof(int) * B, cudaMemcpyDefault, st));
+  if (iterations) CQP_CUDA(cudaMemcpyAsync(iterations, b->iters, sizeof(int) * B, cudaMemcpyDefault, st));
+  if (final_index) CQP_CUDA(cudaMemcpyAsync(final_index, b->layer, sizeof(int) * B, cudaMemcpyDefault, st));
+  if (r_prim) CQP_CUDA(cudaMemcpyAsync(r_prim, b->rp, sizeof(double) * B, cudaMemcpyDefault, st));
+  if (r_dual) CQP_CUDA(cudaMemcpyAsync(r_dual, b->rd, sizeof(double) * B, cudaMemcpyDefault, st));
+  if (n_switches) CQP_CUDA(cudaMemcpyAsync(n_switches, b->nsw, sizeof(int) * B, cudaMemcpyDefault, st));
   CQP_CUDA(cudaEventRecord(b->ev1, st));
   CQP_CUDA(cudaStreamSynchronize(st));
   // iteration-GEMM profile of this solve: time of every round's GEMM launches and the
@@ -1034,6 +1062,45 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   cudaEventElapsedTime(&b->last_total_ms, b->ev0, b->ev1);
   cudaEventElapsedTime(&b->last_compute_ms, b->evc0, b->evc1);
   if (device_ms) *device_ms = b->last_total_ms;
+  return CQP_OK;
+}
+
+// Records of one lane's last solve -> host arrays of `cap` entries per column, from column `off`.
+template <typename Rec>
+static int fetch_records(cqp_batch* b, const Rec* dev, const int* dev_len, int len_bias, int off, int cap,
+                         Rec* out, int* out_len) {
+  const int B = b->last_B, rc_dev = b->rec_cap;
+  if (B <= 0) return CQP_OK;
+  CQP_CUDA(cudaSetDevice(b->h->device));
+  std::vector<Rec> host((size_t)B * rc_dev);
+  std::vector<int> len(B);
+  CQP_CUDA(cudaMemcpyAsync(host.data(), dev, sizeof(Rec) * host.size(), cudaMemcpyDeviceToHost, b->stream));
+  CQP_CUDA(cudaMemcpyAsync(len.data(), dev_len, sizeof(int) * B, cudaMemcpyDeviceToHost, b->stream));
+  CQP_CUDA(cudaStreamSynchronize(b->stream));
+  for (int j = 0; j < B; ++j) {
+    const int cnt = len[j] + len_bias;
+    if (out_len) out_len[off + j] = cnt;  // (records beyond a capacity are dropped, the length still counts them)
+    if (out)
+      for (int k = 0; k < std::min(std::min(cnt, cap), rc_dev); ++k)
+        out[(size_t)(off + j) * cap + k] = host[(size_t)j * rc_dev + k];
+  }
+  return CQP_OK;
+}
+
+template <typename Fn>
+static int for_each_lane(cqp_batch* b, int B, Fn fn) {
+  if (!b) { set_error("batch records: null batch"); return CQP_ERR_ARGUMENT; }
+  if (b->lanes.empty()) {
+    if (B != b->last_B) { set_error("batch records: B differs from the last solve"); return CQP_ERR_ARGUMENT; }
+    return fn(b, 0);
+  }
+  int total = 0;
+  for (int c : b->lane_cnt) total += c;
+  if (B != total) { set_error("batch records: B differs from the last solve"); return CQP_ERR_ARGUMENT; }
+  for (size_t k = 0; k < b->lane_cnt.size(); ++k) {
+    if (b->lane_cnt[k] <= 0) continue;
+    if (int rc = fn(b->lanes[k], b->lane_off[k])) return rc;
+  }
   return CQP_OK;
 }
 
@@ -1087,11 +1154,13 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   CQP_CUDA(cudaSetDevice(b->h->device));
   CQP_CUDA(cudaEventRecord(b->ev_start, b->lanes[0]->stream));
   std::vector<int> rcs(used, CQP_OK), counts(used, 0);
+  b->lane_off.assign(used, 0); b->lane_cnt.assign(used, 0);
   std::vector<std::string> errs(used);
   std::vector<std::thread> threads;
   for (int k = 0; k < used; ++k) {
     const int off = k * per, cnt = std::min(per, B - off);
     counts[k] = cnt;
+    b->lane_off[k] = off; b->lane_cnt[k] = cnt > 0 ? cnt : 0;
     if (cnt <= 0) continue;
     threads.emplace_back([&, k, off, cnt] {
       auto at = [&](auto* p, size_t stride) { return p ? p + (size_t)off * stride : p; };
@@ -1144,6 +1213,20 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
   b->last_compute_ms = c1 - c0;
   if (device_ms) *device_ms = total;
   return CQP_OK;
+}
+
+int cqp_batch_get_traces(cqp_batch* b, int B, int cap, cqp_rho_switch* trace, int* trace_len) {
+  if (cap < 0 || (cap > 0 && !trace && !trace_len)) { set_error("batch_get_traces: bad argument"); return CQP_ERR_ARGUMENT; }
+  return for_each_lane(b, B, [&](cqp_batch* lane, int off) {
+    return fetch_records(lane, lane->trace, lane->nsw, 1, off, cap, trace, trace_len);
+  });
+}
+
+int cqp_batch_get_history(cqp_batch* b, int B, int cap, cqp_residual_sample* history, int* history_len) {
+  if (cap < 0 || (cap > 0 && !history && !history_len)) { set_error("batch_get_history: bad argument"); return CQP_ERR_ARGUMENT; }
+  return for_each_lane(b, B, [&](cqp_batch* lane, int off) {
+    return fetch_records(lane, lane->hist, lane->nhist, 0, off, cap, history, history_len);
+  });
 }
 
 int cqp_batch_last_timing(const cqp_batch* b, double* compute_ms, double* total_ms, long long* launches) {

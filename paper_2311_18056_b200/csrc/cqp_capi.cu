@@ -117,7 +117,7 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->barrier, 2))) return rc;
   CQP_CUDA(cudaMemset(h->barrier, 0, 2 * sizeof(unsigned)));
   CQP_CUDA(cudaStreamSynchronize(0));  // legacy-stream memset vs the handle's non-blocking stream
-  if ((rc = dev_alloc(&h->partial, 8 * (size_t)(h->num_sms + 1)))) return rc;
+  if ((rc = dev_alloc(&h->partial, 2 * 8 * (size_t)(h->num_sms + 1)))) return rc;  // [pass parity][CTA][8]
   if ((rc = dev_alloc(&h->rho_vec, (size_t)L * m))) return rc;
   if ((rc = dev_alloc(&h->dtmp, (size_t)h->Dpad))) return rc;
   CQP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->hstage), sizeof(double) * (nm + m)));

@@ -658,11 +658,16 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   CQP_STAMP0(p.dbg, 10);
 }
 
+// `set_attrs`: opt the kernel into the full dynamic shared memory and 16-CTA clusters.  Done when
+// the handle is configured (ClOp::Fits), never on the launch path; the attributes are per function
+// and device, so they are set to the maximum (handles of different sizes share the functions).
 template <int RPW, int NPT>
-int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr) {
+int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, bool set_attrs) {
   auto fn = cluster_kernel<RPW, NPT>;
-  CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-  if (h->G > 8) CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (set_attrs) {
+    CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+    CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3(h->G);
   cfg.blockDim = dim3(kClThreads);
@@ -684,7 +689,7 @@ template <int RPW, int NPT>
 int cluster_do(ClOp op, cqp_handle* h, const RunParams* p) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
-  int rc = cluster_launch_cfg<RPW, NPT>(h, cfg, attr);
+  int rc = cluster_launch_cfg<RPW, NPT>(h, cfg, attr, op == ClOp::Fits);
   if (op == ClOp::Fits) {
     int clusters = 0;
     if (rc != CQP_OK || cudaOccupancyMaxActiveClusters(&clusters, cluster_kernel<RPW, NPT>, &cfg) != cudaSuccess) {

@@ -217,17 +217,20 @@ __device__ __forceinline__ double warp_row_dot_mlp(const double* __restrict__ Mr
 }
 
 // Control extraction of the closed loop (bench.cpp:169-175): u0 = clamp(-K x + y[0:nu], u_lo, u_hi).
-// `y` is the unscaled primal solution in shared memory; executed by one CTA (threads t < nu).
-__device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t) {
-  if (!p.mpc_K || t >= p.mpc_nu) return;
-  const double* Krow = p.mpc_K + (size_t)t * p.mpc_nxpad;
-  double kx = 0.0;
-  for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], p.mpc_x0[j], kx);
-  double u = -kx + y[t];
-  const double lo = p.mpc_ulo[t], hi = p.mpc_uhi[t];
-  u = u < lo ? lo : u;
-  u = u > hi ? hi : u;
-  p.out_u[t] = u;
+// `y` is the unscaled primal solution in shared memory; executed by one CTA (thread `t0` takes
+// controls t0, t0 + blockDim.x, ...).
+__device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t0) {
+  if (!p.mpc_K) return;
+  for (int t = t0; t < p.mpc_nu; t += (int)blockDim.x) {
+    const double* Krow = p.mpc_K + (size_t)t * p.mpc_nxpad;
+    double kx = 0.0;
+    for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], p.mpc_x0[j], kx);
+    double u = -kx + y[t];
+    const double lo = p.mpc_ulo[t], hi = p.mpc_uhi[t];
+    u = u < lo ? lo : u;
+    u = u > hi ? hi : u;
+    p.out_u[t] = u;
+  }
 }
 
 }  // namespace

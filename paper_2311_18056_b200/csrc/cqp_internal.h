@@ -105,7 +105,7 @@ struct RunParams {
   double eps_prim, eps_dual, threshold;
   int check_interval, adaptive, early_exit, total_iters;
   int do_refresh;     // run Solver::refresh_z before the first iteration
-  int fence_mode;     // 0: fence after re-arm (default); 1: none; 2: release-store publish
+  int fence_mode;     // 0: fence after re-arm (default); 2: release-store publish
   int poll_delay_ns;  // the fetching warps pause this long after `go` before their first poll of v_i
   int cap;            // capacity of the record arrays
   // receding-horizon control extraction (null Kt: none): u0 = clamp(-K x0 + y[0:nu], u_lo, u_hi)
@@ -181,6 +181,9 @@ struct cqp_handle {
   int rpw = 0;      // cluster kernel, shared-memory mode: rows of W per warp
   int npt = 0;      // cluster kernel, register mode: column pairs of W per lane (0: shared-memory mode)
   int xs_stride = 0, hg_smem = 0;
+  // tuning / test knobs, read from the environment once at handle creation (cqp_single.cu: read_knobs)
+  int knob_poll_delay_ns = -1, knob_fence_mode = 0, knob_cofetch = 1;
+  bool knob_sb_balance = true, knob_no_retile = false, knob_wide_chunks = true;
 };
 
 namespace cqp {

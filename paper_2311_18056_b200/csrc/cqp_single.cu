@@ -302,7 +302,7 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
 //   0 ||Gy - z||  1 ||Hy + g + G'lam||  2 ||Hy||  3 ||G'lam||  4 ||Gy||  5 ||z||  6 ||g||
 template <int RB>
 __device__ void residual_pass(const RunParams& p, const Smem& s, const double* xs, bool final,
-                              unsigned& epoch, double (&out)[7]) {
+                              unsigned& epoch, int& pass, double (&out)[7]) {
   const int t = threadIdx.x;
   const int n = p.n, m = p.m;
   const Scratch sc = scratch(p, s, xs);
@@ -377,14 +377,20 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     }
   }
   __syncthreads();
-  if (t < 7) __stcg(p.partial + (size_t)blockIdx.x * 8 + t, nanmax(s.sval[t], s.sval[8 + t]));
+  // The records are double-buffered by pass parity: a final pass may follow a check pass with no
+  // grid barrier or iterate exchange in between, so a fast CTA writes its next record while a slow
+  // one still reads this pass's (a third pass cannot start before every CTA left this one's barrier
+  // AND the next one's).
+  double* partial = p.partial + (size_t)(pass & 1) * 8 * (size_t)(G + 1);
+  ++pass;
+  if (t < 7) __stcg(partial + (size_t)blockIdx.x * 8 + t, nanmax(s.sval[t], s.sval[8 + t]));
   grid_barrier(p.barrier, epoch, G, p.dbg);
   // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
   // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant)
   {
     double mine[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) mine[k] = (t < G) ? __ldcg(p.partial + (size_t)t * 8 + k) : 0.0;
+    for (int k = 0; k < 7; ++k) mine[k] = (t < G) ? __ldcg(partial + (size_t)t * 8 + k) : 0.0;
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
 #pragma unroll
@@ -476,6 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   const int Rcap = round_up(p.R, RB);
   const bool owns_pad = (p.Dpad != D) && (row0 + nrows == D);  // last CTA also drives the pad slot
   unsigned epoch = 0;
+  int pass = 0;  // residual passes so far (parity selects the record buffer)
 
   int layer = p.state[0];
   CQP_STAMP0(p.dbg, 0);  // (-DCQP_TRACE: prologue / epilogue timeline of CTA 0, tools/trace_tier1.py)
@@ -718,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     // ---- convergence check + penalty adaptation (solver.cpp:65-87) ----
     double nr[7];
     const double* xcur = s.xs + (size_t)(i & 1) * XS;
-    residual_pass<RB>(p, s, xcur, false, epoch, nr);
+    residual_pass<RB>(p, s, xcur, false, epoch, pass, nr);
     const double r_prim = nr[0], r_dual = nr[1];
     if (blockIdx.x == 0 && t == 0 && n_hist < p.cap) {
       p.hist_i[2 * n_hist] = i;
@@ -764,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   CQP_STAMP0(p.dbg, 4);  // iterations done
   double nr[7];
   const double* xfinal = s.xs + (size_t)(iters_done & 1) * XS;
-  residual_pass<RB>(p, s, xfinal, true, epoch, nr);
+  residual_pass<RB>(p, s, xfinal, true, epoch, pass, nr);
   CQP_STAMP0(p.dbg, 5);  // final residual pass done
   // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
   // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
@@ -949,9 +956,7 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
 
 template <int RB, bool STREAM, bool COFETCH>
 int launch_run_rb2(cqp_handle* h, RunParams& p) {
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, STREAM, COFETCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->smem_bytes));
-  void* args[] = {&p};
+  void* args[] = {&p};  // (shared-memory opt-in: set once per handle by set_run_attributes)
   CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, STREAM, COFETCH>, dim3(h->G), dim3(kThreads),
                                        args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
@@ -963,10 +968,48 @@ int launch_run_rb(cqp_handle* h, RunParams& p) {
   return p.cofetch ? launch_run_rb2<RB, false, true>(h, p) : launch_run_rb2<RB, false, false>(h, p);
 }
 
+// Opt every instance of the grid kernel this handle can launch into the full 227 KB of dynamic
+// shared memory -- once, at handle creation, not per launch (the attribute is per function and
+// device, so it is set to the maximum: handles of different sizes share the functions).
+template <int RB>
+int set_run_attributes_rb() {
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  return CQP_OK;
+}
+
+int set_run_attributes(int rb) {
+  switch (rb) {
+    case 4: return set_run_attributes_rb<4>();
+    case 8: return set_run_attributes_rb<8>();
+    default: return set_run_attributes_rb<16>();
+  }
+}
+
+int env_int(const char* name, int fallback) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : fallback;
+}
+
 }  // namespace
+
+// Tuning / test knobs are read from the environment ONCE, when the handle is created; nothing on
+// the per-launch path (a kHz MPC loop) touches the environment.
+static void read_knobs(cqp_handle* h) {
+  h->knob_poll_delay_ns = env_int("CQP_POLL_DELAY_NS", -1);  // -1: the tier's default
+  // 0: fence after the re-arm (default); 2: release-store publish.  (The former mode 1, no fence at
+  // all, broke the ring's ordering argument and is gone: it maps to 0.)
+  h->knob_fence_mode = env_int("CQP_FENCE_MODE", 0) == 2 ? 2 : 0;
+  h->knob_cofetch = env_int("CQP_COFETCH", 1);
+  h->knob_sb_balance = env_int("CQP_SB_BALANCE", 1) != 0;
+  h->knob_no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
+  h->knob_wide_chunks = env_int("CQP_WIDE_CHUNKS", 1) != 0;
+}
 
 int configure_launch(cqp_handle* h) {
   const int D = h->D;
+  read_knobs(h);
   h->cluster = 0;
   // Small problems (one ladder level fits the shared memory of ONE thread-block cluster) run the
   // cluster kernel of cqp_cluster.cu: the iterate never leaves the SMs.  CQP_FORCE_TIER=0/1 pins
@@ -1000,7 +1043,7 @@ int configure_launch(cqp_handle* h) {
     // (one cp.async.bulk each).  Measured on B200: the per-SM streaming rate grows with the bytes in
     // flight (quadruped-sized: 3 x 30 KB were latency-bound at 66 GB/s per SM) and with the copy
     // size (Atlas-sized, same bytes in flight: 4 x 28 KB 7.3 us per iteration, 2 x 64 KB 6.2 us).
-    const bool no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
+    const bool no_retile = h->knob_no_retile;
     int want_stages = 3;
     if (const char* e = std::getenv("CQP_STREAM_STAGES")) want_stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
     auto plan_ring = [&](size_t base_bytes, int& stages, int& stage_doubles) {
@@ -1037,7 +1080,7 @@ int configure_launch(cqp_handle* h) {
     // byte count max(R12 D, R3 n).  CQP_SINGLE_DENSE=1 keeps the dense layer (A/B runs).
     const char* dense = std::getenv("CQP_SINGLE_DENSE");
     const int n = h->n, m = h->m, nm = n + m;
-    if (stages >= 2 && !(dense && dense[0] == '1') && !std::getenv("CQP_NO_RETILE") && m >= 1 && n >= 2 && G >= 2) {
+    if (stages >= 2 && !(dense && dense[0] == '1') && !h->knob_no_retile && m >= 1 && n >= 2 && G >= 2) {
       // a lambda row costs more than its bytes (many short rows: more ring stages per byte, more rows
       // for the single publisher warp), so its CTAs get a little less than an equal share of bytes
       double lambda_weight = 1.25;  // (B200: Atlas-sized 6.3 -> 5.3 us per iteration, quadruped-sized 11.2 -> 10.8; 1.1 .. 1.5 alike)
@@ -1069,13 +1112,13 @@ int configure_launch(cqp_handle* h) {
     }
   }
   h->smem_bytes = (int)need;
-  return CQP_OK;
+  return set_run_attributes(h->rb);
 }
 
 // Rows per super-block of the W stream: the R rows of a CTA are cut into ceil(R / 16) equal parts
 // (R = 18 -> 9 + 9 rather than 16 + 2, so that no ring stage is nearly empty).
-static int stream_sb_rows(int R) {
-  if (const char* e = std::getenv("CQP_SB_BALANCE")) if (e[0] == '0') return kStageRows;  // A/B knob
+static int stream_sb_rows(const cqp_handle* h, int R) {
+  if (!h->knob_sb_balance) return kStageRows;  // A/B knob (CQP_SB_BALANCE=0)
   const int nsb = (R + kStageRows - 1) / kStageRows;
   return (R + nsb - 1) / nsb;
 }
@@ -1083,8 +1126,8 @@ static int stream_sb_rows(int R) {
 // Column pairs per ring stage for super-blocks of up to `sbr` rows streaming `wc2` pairs per row: as
 // wide as the 32 KB stage allows (multiple of 8 pairs = 128 B), then evened out over the chunks of
 // a row so that no stage is nearly empty.  CQP_WIDE_CHUNKS=0 keeps 128-pair chunks (A/B runs).
-static int stream_chunk_pairs(int sbr, int wc2, int stage_doubles) {
-  if (const char* e = std::getenv("CQP_WIDE_CHUNKS")) if (e[0] == '0') return kStagePairs;
+static int stream_chunk_pairs(const cqp_handle* h, int sbr, int wc2, int stage_doubles) {
+  if (!h->knob_wide_chunks) return kStagePairs;
   const int cwmax = ((stage_doubles / 2) / sbr) & ~7;
   const int nch = (wc2 + cwmax - 1) / cwmax;
   const int even = (((wc2 + nch - 1) / nch) + 7) & ~7;
@@ -1102,7 +1145,7 @@ static size_t wt_level_pairs(const cqp_handle* h) {
 // L2/HBM tier: build the streaming copy of the ladder (RunParams::Wt).  Called once W is complete
 // (end of handle creation); launch_run re-checks so that a handle never streams a stale copy.
 int prepare_streaming(cqp_handle* h) {
-  if (h->cluster || h->w_smem || h->stream_stages <= 0 || h->Wt || std::getenv("CQP_NO_RETILE")) return CQP_OK;
+  if (h->cluster || h->w_smem || h->stream_stages <= 0 || h->Wt || h->knob_no_retile) return CQP_OK;
   const size_t per = (size_t)h->D * h->Dpad;
   const size_t per_t = 2 * wt_level_pairs(h);  // re-tiled level: rows padded to 128 bytes
   CQP_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->Wt), sizeof(double) * per_t * h->L));
@@ -1112,12 +1155,12 @@ int prepare_streaming(cqp_handle* h) {
   q.D = h->D; q.nc2 = h->Dpad >> 1; q.n = h->n; q.nm = h->n + h->m;
   if (h->structured) {
     q.G12 = h->G12; q.R12 = h->R12; q.R3 = h->R3;
-    q.sbr12 = stream_sb_rows(h->R12); q.sbr3 = stream_sb_rows(h->R3);
+    q.sbr12 = stream_sb_rows(h, h->R12); q.sbr3 = stream_sb_rows(h, h->R3);
   } else {
-    q.G12 = 0; q.R12 = h->R; q.R3 = 1; q.sbr12 = stream_sb_rows(h->R); q.sbr3 = 1;
+    q.G12 = 0; q.R12 = h->R; q.R3 = 1; q.sbr12 = stream_sb_rows(h, h->R); q.sbr3 = 1;
   }
-  q.cw12 = h->cw12 = stream_chunk_pairs(q.sbr12, q.nc2, h->stage_doubles);
-  q.cw3 = h->cw3 = stream_chunk_pairs(q.sbr3, (h->n + 1) >> 1, h->stage_doubles);
+  q.cw12 = h->cw12 = stream_chunk_pairs(h, q.sbr12, q.nc2, h->stage_doubles);
+  q.cw3 = h->cw3 = stream_chunk_pairs(h, q.sbr3, (h->n + 1) >> 1, h->stage_doubles);
   for (int k = 0; k < h->L; ++k) {
     retile_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, h->stream>>>(
         reinterpret_cast<const double2*>(h->W + per * k), reinterpret_cast<double2*>(h->Wt + per_t * k), q);
@@ -1154,40 +1197,43 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
     p.mpc_K = h->mpc_K; p.mpc_x0 = h->mpc_x0; p.mpc_ulo = h->mpc_ulo; p.mpc_uhi = h->mpc_uhi;
     p.mpc_nx = h->mpc_nx; p.mpc_nxpad = h->mpc_nxpad; p.mpc_nu = h->mpc_nu;
   }
-  p.fence_mode = 0;
   // The other CTAs publish within a few hundred ns of this one: a first poll issued right at `go`
   // mostly finds sentinels and costs a second L2 round trip, and the extra polling traffic slows the
   // publishes themselves.  A short pause before the first poll is a net win (B200, D = 900 / 1500:
   // 2.90 -> 2.60 / 4.11 -> 3.78 us per iteration at 100-200 ns; 400 ns is too long).
-  p.poll_delay_ns = 150;
-  if (const char* e = std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = std::atoi(e);
-  if (const char* fm = std::getenv("CQP_FENCE_MODE")) p.fence_mode = std::atoi(fm);  // experiment knob
+  const bool delay_set = h->knob_poll_delay_ns >= 0;
+  p.poll_delay_ns = delay_set ? h->knob_poll_delay_ns : 150;
+  p.fence_mode = h->knob_fence_mode;
   // grid-barrier counters ping-pong between launches: this launch counts on barrier[parity]
-  // (zeroed by the previous launch, or at allocation) and zeroes the other one.
+  // (zeroed by the previous launch, or at allocation) and zeroes the other one.  The parity only
+  // advances once the launch has been accepted (see the end of this function): a failed launch
+  // never ran, so it neither used its counter nor zeroed the other one.
   p.barrier = h->barrier + (h->launch_parity & 1);
   p.barrier_next = h->barrier + ((h->launch_parity + 1) & 1);
-  h->launch_parity ^= 1;
   p.dbg = h->dbg_dev;
-  if (h->cluster) return launch_cluster(h, p);
+  auto launched = [&](int rc) {
+    if (rc == CQP_OK) h->launch_parity ^= 1;
+    return rc;
+  };
+  if (h->cluster) return launched(launch_cluster(h, p));
   int rc_stream = prepare_streaming(h);  // (no-op unless the ladder was replaced)
   if (rc_stream) return rc_stream;
   p.Wt = (!h->w_smem) ? h->Wt : nullptr;
   p.wdoubles = h->wdoubles;
   p.stream_stages = h->stream_stages;
-  p.sb_rows = stream_sb_rows(h->structured ? h->R12 : h->R);
+  p.sb_rows = stream_sb_rows(h, h->structured ? h->R12 : h->R);
   p.structured = (h->structured && p.Wt) ? 1 : 0;
   p.G12 = h->G12; p.R12 = h->R12; p.R3 = h->R3;
-  p.sb_rows3 = h->structured ? stream_sb_rows(h->R3) : 1;
+  p.sb_rows3 = h->structured ? stream_sb_rows(h, h->R3) : 1;
   p.cw12 = h->cw12; p.cw3 = h->cw3;  // (what prepare_streaming re-tiled Wt with)
   p.stage_doubles = p.Wt ? h->stage_doubles : kStageDoubles;
   // resident tier: the compute warps, idle during the exchange, fetch v_i along with the loader warps
   // (B200, 1000 iterations: D = 900 2576 -> 2468 us, D = 1500 3924 -> 3706 us); CQP_COFETCH=0 for A/B runs
-  p.cofetch = 1;
-  if (const char* e = std::getenv("CQP_COFETCH")) p.cofetch = std::atoi(e);
+  p.cofetch = h->knob_cofetch;
   // with 608 fetching threads the first poll of the resident tier is best issued at once (B200, 1000
   // iterations: D = 900 2456 -> 2358 us, D = 1500 3701 -> 3667 us); the streamed tier keeps the pause
   // (Atlas-sized 5.34 vs 5.55 us per iteration: early polls compete with the W stream)
-  if (p.w_smem && p.cofetch && !std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = 0;
+  if (p.w_smem && p.cofetch && !delay_set) p.poll_delay_ns = 0;
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;
@@ -1195,15 +1241,15 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   // the ring then lives in the (unused) slice region
   if (total_iters < 4 && p.w_smem) {
     p.w_smem = 0;
-    if (!std::getenv("CQP_POLL_DELAY_NS")) p.poll_delay_ns = 150;  // (streaming kernel: keeps the pause)
+    if (!delay_set) p.poll_delay_ns = 150;  // (streaming kernel: keeps the pause)
     int stages = h->wdoubles / kStageDoubles;
     if (stages > kMaxStages) stages = kMaxStages;
     p.stream_stages = stages >= 2 ? stages : 0;
   }
   switch (h->rb) {
-    case 4: return launch_run_rb<4>(h, p);
-    case 8: return launch_run_rb<8>(h, p);
-    default: return launch_run_rb<16>(h, p);
+    case 4: return launched(launch_run_rb<4>(h, p));
+    case 8: return launched(launch_run_rb<8>(h, p));
+    default: return launched(launch_run_rb<16>(h, p));
   }
 }
 

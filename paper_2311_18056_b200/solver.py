@@ -159,6 +159,13 @@ class Solver:
         self.L = Lc.value
 
     def close(self) -> None:
+        """Frees the handle.  BatchSolvers built on this solver share its ladder: they are closed
+        first, so that none is left holding a dangling handle."""
+        for ref in list(self.__dict__.get("_dependents", [])):
+            dep = ref()
+            if dep is not None:
+                dep.close()
+        self.__dict__["_dependents"] = []
         h, self._h = getattr(self, "_h", None), C.c_void_p()
         if h:
             self._L.cqp_destroy(h)
@@ -190,9 +197,12 @@ class Solver:
         _raise(self._L.cqp_update_vectors(self._h, _p(g), _p(c), _p(d)))
 
     def _result(self, cap: int):
-        # result buffers are cached per capacity (the MPC step path calls this at kHz rates)
+        # result buffers are cached per capacity (the MPC step path calls this at kHz rates); only
+        # the most recent few capacities are kept
         cache = self.__dict__.setdefault("_res_cache", {})
         if cap not in cache:
+            while len(cache) >= 4:
+                cache.pop(next(iter(cache)))
             y, z, lam = np.empty(self.n), np.empty(self.m), np.empty(self.m)
             trace = (CqpRhoSwitch * cap)()
             hist = (CqpResidualSample * cap)()
@@ -311,14 +321,20 @@ class BatchSolver:
     after `update_vectors(g[:, j], c[:, j], d[:, j]); cold_start()` (solver.cpp:158-166)."""
 
     def __init__(self, solver: Solver, capacity: int):
+        import weakref
         self._L = solver._L
         self._solver = solver          # keeps the shared ladder alive
         self._b = C.c_void_p()
         self.capacity = int(capacity)
+        if not solver._h:
+            raise ValueError("BatchSolver: the Solver has been closed")
         _raise(self._L.cqp_batch_create(C.byref(self._b), solver._h, self.capacity))
+        solver.__dict__.setdefault("_dependents", []).append(weakref.ref(self))
         self.n, self.m = solver.n, solver.m
-        self._pinned = []     # page-locked output buffers, allocated once (views are returned)
+        self._rec_cap = solver.settings.max_iters // solver.settings.check_interval + 2
+        self._pinned = []     # page-locked output buffers, allocated once
         self._out = None
+        self._last_B = 0
 
     def _pinned_array(self, shape, dtype, order="C"):
         nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
@@ -343,7 +359,13 @@ class BatchSolver:
         except Exception:
             pass
 
-    def solve(self, g_cols, c_cols, d_cols) -> dict:
+    def solve(self, g_cols, c_cols, d_cols, zero_copy: bool = False) -> dict:
+        """Solves the B columns.  The result arrays are COPIES by default.  With `zero_copy=True`
+        they are views of this object's page-locked result buffers: valid only until the next
+        `solve()` (which overwrites them) or `close()` (which frees them) -- the caller must not
+        touch them afterwards."""
+        if not self._b:
+            raise ValueError("BatchSolver: closed (or its Solver was closed)")
         g = np.asfortranarray(np.asarray(g_cols, dtype=np.float64))
         c = np.asfortranarray(np.asarray(c_cols, dtype=np.float64))
         d = np.asfortranarray(np.asarray(d_cols, dtype=np.float64))
@@ -362,6 +384,7 @@ class BatchSolver:
                          self._pinned_array((cap,), np.int32), self._pinned_array((cap,), np.float64),
                          self._pinned_array((cap,), np.float64))
         y, z, lam, status, iters, final, nsw, rp, rd = (a[..., :B] for a in self._out)
+        self._last_B = B
         ms = C.c_double()
         ip = lambda a: a.ctypes.data_as(_lib.c_int_p)  # noqa: E731
         _raise(self._L.cqp_batch_solve(self._b, B, _p(g), _p(c), _p(d), _p(y), _p(z), _p(lam),
@@ -373,8 +396,58 @@ class BatchSolver:
         self._L.cqp_batch_last_profile(self._b, C.byref(gms), C.byref(gfl), C.byref(rounds))
         ract = np.zeros(max(rounds.value, 1), dtype=np.int32); rms = np.zeros(max(rounds.value, 1))
         self._L.cqp_batch_round_profile(self._b, rounds.value, ip(ract), _p(rms))
+        if not zero_copy:
+            y, z, lam, status, iters, final, nsw, rp, rd = (
+                np.array(a, copy=True, order="F" if a.ndim == 2 else "C") for a in (y, z, lam, status, iters, final, nsw, rp, rd))
         return {"round_active": ract, "round_ms": rms,
                 "y": y, "z": z, "lam": lam, "status": status, "iterations": iters,
                 "final_index": final, "n_switches": nsw, "r_prim": rp, "r_dual": rd,
                 "device_ms": ms.value, "compute_ms": comp.value, "launches": launches.value,
                 "gemm_ms": gms.value, "gemm_flops": gfl.value, "rounds": rounds.value}
+
+    def solve_into(self, B: int, g_ptr: int, c_ptr: int, d_ptr: int, y_ptr: int, z_ptr: int, lam_ptr: int,
+                   status_ptr: int, iterations_ptr: int, final_index_ptr: int, r_prim_ptr: int,
+                   r_dual_ptr: int, n_switches_ptr: int) -> dict:
+        """cqp_batch_solve on raw addresses (host or device memory of this GPU; 0 = not wanted for
+        an output): the caller owns every buffer.  Used by the multi-GPU gather
+        (sharding.solve_sharded_device), which hands device buffers straight to NCCL."""
+        if not self._b:
+            raise ValueError("BatchSolver: closed (or its Solver was closed)")
+        if not 1 <= B <= self.capacity:
+            raise MemoryError("batch solve: B exceeds the batch capacity")
+        dp = lambda a: C.cast(C.c_void_p(a or None), c_double_p)          # noqa: E731
+        ip = lambda a: C.cast(C.c_void_p(a or None), _lib.c_int_p)        # noqa: E731
+        ms = C.c_double()
+        _raise(self._L.cqp_batch_solve(self._b, B, dp(g_ptr), dp(c_ptr), dp(d_ptr), dp(y_ptr), dp(z_ptr),
+                                       dp(lam_ptr), ip(status_ptr), ip(iterations_ptr), ip(final_index_ptr),
+                                       dp(r_prim_ptr), dp(r_dual_ptr), ip(n_switches_ptr), C.byref(ms)))
+        self._last_B = B
+        comp, tot, launches = C.c_double(), C.c_double(), C.c_longlong()
+        self._L.cqp_batch_last_timing(self._b, C.byref(comp), C.byref(tot), C.byref(launches))
+        gms, gfl, rounds = C.c_double(), C.c_double(), C.c_int()
+        self._L.cqp_batch_last_profile(self._b, C.byref(gms), C.byref(gfl), C.byref(rounds))
+        return {"device_ms": ms.value, "compute_ms": comp.value, "launches": launches.value,
+                "gemm_ms": gms.value, "gemm_flops": gfl.value, "rounds": rounds.value}
+
+    def traces(self) -> List[List[Tuple[int, int]]]:
+        """Per-column `Solution.rho_trace` of the last solve (problem.hpp:57-70): a list of
+        (iteration, grid_index) per column, entry 0 = (0, start index)."""
+        B, cap = self._last_B, self._rec_cap
+        rec = (CqpRhoSwitch * (B * cap))()
+        ln = np.zeros(B, dtype=np.int32)
+        _raise(self._L.cqp_batch_get_traces(self._b, B, cap, rec, ln.ctypes.data_as(_lib.c_int_p)))
+        flat = np.frombuffer(rec, dtype=np.int32).reshape(B, cap, 2)
+        return [[(int(a), int(b)) for a, b in flat[j, :min(int(ln[j]), cap)]] for j in range(B)]
+
+    def histories(self) -> List[List[Tuple[int, float, float, int]]]:
+        """Per-column `SolveReport.residual_history` of the last solve (solver.hpp:56-67):
+        (iteration, r_prim, r_dual, grid_index before the check's switch) per convergence check."""
+        B, cap = self._last_B, self._rec_cap
+        rec = (CqpResidualSample * (B * cap))()
+        ln = np.zeros(B, dtype=np.int32)
+        _raise(self._L.cqp_batch_get_history(self._b, B, cap, rec, ln.ctypes.data_as(_lib.c_int_p)))
+        dt = np.dtype([("iteration", np.int32), ("pad0", np.int32), ("r_prim", np.float64),
+                       ("r_dual", np.float64), ("grid_index", np.int32), ("pad1", np.int32)])
+        flat = np.frombuffer(rec, dtype=dt).reshape(B, cap)
+        return [[(int(r["iteration"]), float(r["r_prim"]), float(r["r_dual"]), int(r["grid_index"]))
+                 for r in flat[j, :min(int(ln[j]), cap)]] for j in range(B)]

@@ -156,3 +156,117 @@ def test_lanes_match_one_batch(G, oracle, P, monkeypatch):
         s = cpu.solve().solution
         assert outs[1]["iterations"][j] == s.iterations and outs[1]["status"][j] == s.status
         assert rel_err(outs[1]["y"][:, j], s.y) <= 1e-6 and rel_err(outs[1]["lam"][:, j], s.lam) <= 1e-6
+
+
+def test_solve_sharded_paths_at_world_one(G, P):
+    """The multi-GPU host logic with the real BatchSolver as the per-rank solve, at world size 1
+    (one GPU box): `solve_sharded` (object gather) and `solve_sharded_device` (results stay in
+    device memory until the NCCL gather) both reproduce a plain `BatchSolver.solve`."""
+    import torch.distributed as dist
+    from paper_2311_18056_b200 import sharding
+    wl = P.config2(6, seed=3)
+    base = wl.base_problem()
+    B = 150
+    g, c, d, _ = P.batch_instances(wl, B)
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d)
+    batch = G.BatchSolver(single, capacity=B)
+    ref = batch.solve(g, c, d)
+    out_dev, timing = sharding.solve_sharded_device(batch, g, c, d)       # no process group: world 1
+    assert timing["compute_ms"] > 0 and timing["launches"] > 0
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        out_obj = sharding.solve_sharded(lambda a, b_, c_: batch.solve(a, b_, c_), g, c, d)
+    finally:
+        dist.destroy_process_group()
+    for out in (out_dev, out_obj):
+        for key in sharding.RESULT_KEYS:
+            assert np.array_equal(out[key], ref[key]), key
+    batch.close(); single.close()
+
+
+def _nccl_worker(rank, world, port, B, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    from paper_2311_18056_b200 import problems, sharding, solver as S
+    wl = problems.config2(6, seed=3)
+    base = wl.base_problem()
+    g, c, d, _ = problems.batch_instances(wl, B)
+    single = S.Solver(base.H, base.g, base.G, base.c, base.d, device=rank)
+    lo, hi = sharding.shard_range(B, world, rank)
+    batch = S.BatchSolver(single, capacity=max(hi - lo, 1))
+    out, _ = sharding.solve_sharded_device(batch, g, c, d, dst=0)
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_solve_sharded_device_two_gpus(G, P):
+    """World size 2 over NCCL (needs two GPUs; the 1-GPU boxes skip it)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 CUDA devices")
+    B = 151
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, B, q)) for r in range(2)]
+    [p.start() for p in procs]
+    got = q.get(timeout=600)
+    [p.join(timeout=120) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    wl = P.config2(6, seed=3)
+    base = wl.base_problem()
+    g, c, d, _ = P.batch_instances(wl, B)
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d)
+    ref = G.BatchSolver(single, capacity=B).solve(g, c, d)
+    for key in ("iterations", "status", "final_index", "n_switches"):
+        assert np.array_equal(got[key], ref[key]), key
+    for key in ("y", "z", "lam"):
+        assert rel_err(got[key], ref[key]) <= 1e-9, key
+
+
+def test_batch_traces_and_histories_match_single_solver(G, oracle, P):
+    """cqp_batch_get_traces / cqp_batch_get_history: column j's records equal what the oracle's
+    `solve()` reports for that column (problem.hpp:57-70, solver.hpp:56-67), also through the lanes."""
+    wl = P.config2(10, seed=5)
+    base = wl.base_problem()
+    B = 1100                                                     # >= 1024: two lanes
+    g, c, d, _ = P.batch_instances(wl, B, lo=0.3, hi=10.0)
+    cpu = oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), variant="ref")
+    layers = {"W": [cpu.cache.W(k) for k in range(cpu.cache.L)], "D": [cpu.cache.D(k) for k in range(cpu.cache.L)],
+              "GD": [cpu.cache.GD(k) for k in range(cpu.cache.L)], "grid": cpu.cache.grid,
+              "initial_index": cpu.cache.initial_index, "Gs": cpu.cache.Gs, "E": cpu.cache.E,
+              "F": cpu.cache.F, "cost_scale": cpu.cache.cost_scale}
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=layers)
+    batch = G.BatchSolver(single, capacity=B)
+    out = batch.solve(g, c, d)
+    traces, hists = batch.traces(), batch.histories()
+    assert max(len(t) for t in traces) >= 2
+    for j in list(range(0, B, 13)) + [B - 1]:
+        cpu.update_vectors(g[:, j], c[:, j], d[:, j]); cpu.cold_start()
+        ro = cpu.solve()
+        assert traces[j] == ro.solution.rho_trace, j
+        assert [(h[0], h[3]) for h in hists[j]] == [(h[0], h[3]) for h in ro.residual_history], j
+        for hg, ho in zip(hists[j], ro.residual_history):
+            assert abs(hg[1] - ho[1]) <= 2e-3 * abs(ho[1]) + 1e-9 and abs(hg[2] - ho[2]) <= 2e-3 * abs(ho[2]) + 1e-9
+        assert out["iterations"][j] == ro.solution.iterations
+    small = batch.solve(g[:, :40], c[:, :40], d[:, :40])         # one lane of the same object
+    assert batch.traces() == traces[:40] and len(batch.histories()) == 40
+    assert np.array_equal(small["iterations"], out["iterations"][:40])
+    with pytest.raises(ValueError):                              # results are copies: closing is safe
+        batch.close(); batch.solve(g, c, d)
+    assert out["y"].flags.owndata or out["y"].base is not None
+    single.close()

@@ -1,0 +1,215 @@
+"""GPU parity at the BASELINE.json configs AT THEIR STATED SIZES, through the C ABI vs the CPU oracle.
+
+Bar (BASELINE.json north_star): identical iteration counts and rho-switch SEQUENCE in FP64, primal
+and dual solutions within 1e-6 relative.  Covered here ("close parity at the
+stated configs"):
+
+  configs[4]  batched 4096 x nu = 50 (D = 1500): >= 256 columns including the slowest and the
+              fastest, per-column counts, status, FULL rho_trace and residual-history indices
+              (cqp_batch_get_traces / cqp_batch_get_history), y / z / lambda <= 1e-6
+  configs[2]  Atlas-sized N = 40 and N = 50 (D = 3480 / 4350; W level 97 / 151 MB: the only sizes
+              whose structured level no longer fits the 126 MB L2)
+  configs[3]  quadruped + arm sized, N = 30 (D = 4080)
+  configs[1]  the whole sweep nu in {10, 14, ..., 50} x seeds 0..9 (tools/main.cpp:243), easy and
+              hard start: counts + traces + solutions
+
+The GPU handle is built from the oracle's ladder (cqp_create_from_layers), so that the ONLY
+difference between the two sides is the online loop (the device offline stage is compared with
+the oracle's in test_gpu_single.py).  The oracle is the `ref` build (compiled like the reference:
+-O3 -DNDEBUG, no -march) except where its setup would take minutes (robot sizes: `v3`).
+"""
+import concurrent.futures as cf
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from test_gpu_single import REL_RES, REL_SOL, assert_report_parity, oracle_layers, rel_err  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2311_18056_b200 import _lib
+    from paper_2311_18056_b200 import solver as S
+    if _lib.load().cqp_device_count() < 1:
+        pytest.fail("no CUDA device: the solve path has no CPU fallback")
+    return S
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2311_18056_b200 import problems
+    return problems
+
+
+def host_threads():
+    return max(1, min(16, os.cpu_count() or 1))
+
+
+# ---- configs[4]: the headline batch at full size ------------------------------------------------
+def test_config5_batch_4096_columns_vs_oracle_with_full_traces(G, oracle, P):
+    O = oracle
+    B = 4096
+    wl = P.config2(50, seed=0)
+    base = wl.base_problem()
+    g, c, d, _ = P.batch_instances(wl, B)                      # the bench's instances, byte for byte
+    qp = O.QProblem(base.H, base.g, base.G, base.c, base.d)
+    nthreads = host_threads()
+    with cf.ThreadPoolExecutor(nthreads) as pool:              # one oracle Solver per thread (untimed)
+        cpus = list(pool.map(lambda _: O.Solver(qp, variant="ref"), range(nthreads)))
+    single = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=oracle_layers(cpus[0].cache))
+    assert single.n == 500 and single.m == 500
+    batch = G.BatchSolver(single, capacity=B)
+    out = batch.solve(g, c, d)
+    traces, hists = batch.traces(), batch.histories()
+    iters = out["iterations"]
+    assert len(traces) == B and len(hists) == B
+    # the batch is heterogeneous: many distinct counts, most columns switch rho
+    assert len(set(iters.tolist())) >= 20 and out["n_switches"].max() >= 1
+    # structural rules on EVERY column (solver.cpp:50,58-88): trace starts at (0, initial), its last
+    # entry is the final index, one history sample per check, switches happen at check iterations
+    init = cpus[0].cache.initial_index
+    for j in range(B):
+        tr, hi = traces[j], hists[j]
+        assert tr[0] == (0, init) and len(tr) == out["n_switches"][j] + 1
+        assert tr[-1][1] == out["final_index"][j]
+        assert [h[0] for h in hi] == list(range(25, 25 * (iters[j] // 25) + 1, 25))
+        assert all(it % 25 == 0 and 0 < it <= iters[j] for it, _ in tr[1:])
+        # history index = the index BEFORE that check's switch (solver.cpp:71 precedes :73)
+        cur, k = init, 1
+        for h in hi:
+            assert h[3] == cur
+            if k < len(tr) and tr[k][0] == h[0]:
+                cur = tr[k][1]; k += 1
+        assert k == len(tr)
+    # oracle comparison: the 64 slowest, the 64 fastest and 160 evenly spaced columns (>= 256 distinct)
+    order = np.argsort(iters, kind="stable")
+    pick = sorted(set(order[-64:].tolist()) | set(order[:64].tolist()) | set(range(0, B, B // 160)))
+    assert len(pick) >= 256
+
+    def work(i):
+        s, res = cpus[i], {}
+        for j in pick[i::nthreads]:
+            s.update_vectors(g[:, j], c[:, j], d[:, j]); s.cold_start()
+            res[j] = s.solve()
+        return res
+    ref = {}
+    with cf.ThreadPoolExecutor(nthreads) as pool:
+        for part in pool.map(work, range(nthreads)):
+            ref.update(part)
+    for j in pick:
+        ro = ref[j]
+        so = ro.solution
+        assert iters[j] == so.iterations, j
+        assert out["status"][j] == so.status, j
+        assert traces[j] == so.rho_trace, (j, traces[j], so.rho_trace)
+        assert [(h[0], h[3]) for h in hists[j]] == [(h[0], h[3]) for h in ro.residual_history], j
+        for hg, ho in zip(hists[j], ro.residual_history):
+            assert abs(hg[1] - ho[1]) <= REL_RES * abs(ho[1]) + 1e-9
+            assert abs(hg[2] - ho[2]) <= REL_RES * abs(ho[2]) + 1e-9
+        assert rel_err(out["y"][:, j], so.y) <= REL_SOL, j
+        assert rel_err(out["lam"][:, j], so.lam) <= REL_SOL, j
+        assert rel_err(out["z"][:, j], so.z) <= REL_SOL, j
+        assert abs(out["r_prim"][j] - so.r_prim) <= REL_RES * so.r_prim + 1e-9
+        assert abs(out["r_dual"][j] - so.r_dual) <= REL_RES * so.r_dual + 1e-9
+    # every column meets the reference's stopping rule on its ORIGINAL problem
+    assert np.all(out["status"] == G.SOLVED)
+    Y, Z, Lm = out["y"], out["z"], out["lam"]
+    assert np.abs(base.G @ Y - Z).max() <= 1e-6
+    assert np.abs(base.H @ Y + g + base.G.T @ Lm).max() <= 1e-6
+    assert np.all(Z >= c) and np.all(Z <= d)
+    batch.close(); single.close()
+
+
+# ---- configs[2], [3]: robot sizes at the stated horizons ---------------------------------------
+ROBOT = {"quad30": (lambda P: P.config4_quadruped(30, seed=0), 15, 4080),
+         "atlas40": (lambda P: P.config3_atlas(40, seed=0), 2, 3480),
+         "atlas50": (lambda P: P.config3_atlas(50, seed=0), 2, 4350)}
+
+
+@pytest.fixture(scope="module")
+def robot_oracles(oracle, P):
+    """The three oracle setups (1-2 minutes each, single-threaded) run concurrently."""
+    def build(name):
+        wl = ROBOT[name][0](P)
+        base = wl.base_problem()
+        return wl, oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), variant="v3")
+    with cf.ThreadPoolExecutor(3) as pool:
+        futs = {name: pool.submit(build, name) for name in ROBOT}
+        return {name: f.result() for name, f in futs.items()}
+
+
+@pytest.mark.parametrize("name", list(ROBOT))
+def test_robot_sized_full_horizon_vs_oracle(G, oracle, robot_oracles, name):
+    wl, cpu = robot_oracles[name]
+    _, k, D = ROBOT[name]
+    base = wl.base_problem()
+    assert base.n + 2 * base.m == D
+    gpu = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=oracle_layers(cpu.cache))
+    info = gpu.launch_info()
+    assert info["tier"] == 1 and info["ctas"] >= 140            # W streamed from L2/HBM by the whole grid
+    # initial solve to tolerance from a hard start
+    x = wl.x0(3.0)
+    q = wl.problem_at(x)
+    for s in (gpu, cpu):
+        s.update_vectors(q.g, q.c, q.d); s.cold_start()
+    rg, ro = gpu.solve(), cpu.solve()
+    assert ro.solution.status == oracle.SOLVED and len(ro.residual_history) >= 4
+    assert_report_parity(rg, ro)
+    # receding-horizon steps (bench.cpp:157-185), fused step with device-side instantiate
+    gpu.set_mpc_template(wl.tmpl, wl.limits)
+    A, Bm, K, nu = wl.sys.A, wl.sys.B, wl.tmpl.K, wl.sys.nu
+    for _ in range(4):
+        q = wl.problem_at(x)
+        cpu.update_vectors(q.g, q.c, q.d); cpu.refresh_z(); ro = cpu.fixed_iters(k)
+        u_ref = np.clip(-K @ x + ro.solution.y[:nu], wl.limits.u_lo, wl.limits.u_hi)
+        u0, rg = gpu.mpc_step_x0(x, k)
+        assert rg.solution.iterations == k == ro.solution.iterations
+        assert rg.solution.rho_trace == ro.solution.rho_trace
+        assert rel_err(rg.solution.y, ro.solution.y) <= 1e-9
+        assert rel_err(rg.solution.lam, ro.solution.lam) <= 1e-9
+        assert rel_err(rg.solution.z, ro.solution.z) <= 1e-9
+        assert np.abs(u0 - u_ref).max() <= 1e-9 * max(1.0, np.abs(u_ref).max())
+        x = A @ x + Bm @ u_ref
+    gpu.close()
+    robot_oracles[name] = (wl, None)   # free the oracle's ladder (1.3 - 2 GB)
+
+
+# ---- configs[1]: the full nu sweep x seeds 0..9 --------------------------------------------------
+def test_nu_sweep_all_seeds_counts_traces_solutions(G, oracle, P):
+    O = oracle
+    cases = [(nu, seed) for nu in range(10, 51, 4) for seed in range(10)]   # main.cpp:243 x seeds 0-9
+
+    def cpu_side(case):
+        nu, seed = case
+        wl = P.config2(nu, seed=seed)
+        base = wl.base_problem()
+        cpu = O.Solver(O.QProblem(base.H, base.g, base.G, base.c, base.d), variant="ref")
+        reps = []
+        for hard in (1.0, 10.0):                                # "easy" and "hard" start (bench.cpp:35)
+            q = wl.problem_at(wl.x0(hard))
+            cpu.update_vectors(q.g, q.c, q.d); cpu.cold_start()
+            reps.append((q, cpu.solve()))
+        return base, oracle_layers(cpu.cache), reps
+
+    switched = 0
+    distinct = set()
+    chunk = host_threads()
+    with cf.ThreadPoolExecutor(chunk) as pool:
+        for i in range(0, len(cases), chunk):
+            for case, (base, layers, reps) in zip(cases[i:i + chunk], pool.map(cpu_side, cases[i:i + chunk])):
+                gpu = G.Solver(base.H, base.g, base.G, base.c, base.d, layers=layers)
+                for q, ro in reps:
+                    gpu.update_vectors(q.g, q.c, q.d); gpu.cold_start()
+                    rg = gpu.solve()
+                    assert ro.solution.status == O.SOLVED, case
+                    try:
+                        assert_report_parity(rg, ro)
+                    except AssertionError as e:
+                        raise AssertionError(f"nu, seed = {case}: {e}") from e
+                    switched += len(ro.solution.rho_trace) > 1
+                    distinct.add(ro.solution.iterations)
+                gpu.close()
+    assert switched >= 30 and len(distinct) >= 10              # the sweep exercises rho switches

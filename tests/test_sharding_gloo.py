@@ -61,7 +61,7 @@ def _worker(rank, world, port, B, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B", [7, 1])
+@pytest.mark.parametrize("B", [7, 1, 0])
 def test_solve_sharded_world2_matches_single_process(B):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -76,6 +76,24 @@ def test_solve_sharded_world2_matches_single_process(B):
     from paper_2311_18056_b200 import problems
     wl = problems.config2(4, seed=2)
     g, c, d, _ = problems.batch_instances(wl, B)
+    if B == 0:      # every shard is empty: empty results of the right shapes, no IndexError
+        assert got["y"].shape == (wl.n, 0) and got["lam"].shape == (wl.m, 0) and got["iterations"].shape == (0,)
+        return
     ref = _oracle_solve_fn(wl.base_problem())(g, c, d)
     for k in ref:
         assert np.array_equal(got[k], ref[k]), k
+
+
+def test_bench_refuses_to_time_fewer_gpus_than_claimed():
+    """`python bench.py --gpus N` spawns the N ranks itself; on a box with fewer than N devices it
+    must fail loudly instead of timing one GPU under an N-GPU label."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 8:
+        pytest.skip("8 CUDA devices are present")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "8", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "only" in r.stderr and not r.stdout.strip()
