@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "cqp_internal.h"
+#include "cqp_device.cuh"
 
 namespace cqp {
 namespace {
@@ -80,6 +81,9 @@ struct GemmParams {
   // further one from this counter (zero at launch).  The next index is fetched while the current
   // item is being computed, so the atomic's latency never shows.
   int* work_ctr;
+  // 1: the columns of B and C are addressed by SLOT (the iterate S is stored in slot order, see
+  // cqp_batch_round.cuh); bias / bounds stay addressed by column through the slot map
+  int slot_major;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
     for (int i = 0; i < BCH; ++i) {
       const int ch = tid + i * T, r = ch >> 3, c = ch & 7;
       const int col = (ch < BN * 8) ? cols_s[r] : -1;
-      bsrc[i] = p.Bm + (size_t)(col < 0 ? 0 : col) * p.ldb + c * 2;
+      bsrc[i] = p.Bm + (size_t)(col < 0 ? 0 : (p.slot_major ? slot0 + r : col)) * p.ldb + c * 2;
       bdst[i] = r * BK + ((c ^ ((r & 3) << 1)) << 1);
       bbytes[i] = col < 0 ? 0 : 16;
     }
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(p.hi + (size_t)col * p.ld_lohi + row - p.n));
               }
             } else if (blk3 && row < p.M) {  // lambda row i: the diagonal blocks (3,2) = -rho, (3,3) = I
-              const double* v = p.Bm + (size_t)col * p.ldb;
+              const double* v = p.Bm + (size_t)(p.slot_major ? slot0 + warp_n * TN + ni * 8 + 2 * t4 + j : col) * p.ldb;
               const int i = row - p.nm;
               init = fma(p.negrho[(size_t)td.a_index * (p.M - p.nm) + i], v[p.n + i], v[row]);
             }
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
       for (int j = 0; j < 2; ++j) {
         const int col = cols_s[warp_n * TN + ni * 8 + 2 * t4 + j];
         if (col < 0) continue;
-        double* crow = p.C + (size_t)col * p.ldc;
+        double* crow = p.C + (size_t)(p.slot_major ? slot0 + warp_n * TN + ni * 8 + 2 * t4 + j : col) * p.ldc;
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
           const int row = row0 + warp_m * TM + mi * 8 + g;
@@ -329,6 +333,8 @@ __global__ void __launch_bounds__(WM * WN * 32 * KS, MINB) dmma_gemm_kernel(cons
     item = next_item_s;
   }
 }
+
+#include "cqp_batch_round.cuh"
 
 // dst[a][r][c] (rows_pad x ld_dst, zero padded) <- src[a][r][c] (rows x ld_src, first `cols`)
 __global__ void repad_kernel(const double* __restrict__ src, int rows, int cols, int ld_src,
@@ -401,6 +407,7 @@ struct BatchDev {
   TileDesc* tiles;   // [tile_cap]
   int* n_tiles;
   int* n_active;
+  int* slot_of;      // [B] column -> slot of its iterate in S (slot order)
   // settings
   double eps_prim, eps_dual, threshold;
   int adaptive, max_iters;
@@ -433,7 +440,7 @@ __global__ void batch_prepare_kernel(BatchDev b, int initial_index) {
 __global__ void batch_unscale_kernel(BatchDev b, const double* __restrict__ S) {
   const int col = blockIdx.x;
   if (!b.active[col]) return;
-  const double* v = S + (size_t)col * b.ld_s;
+  const double* v = S + (size_t)b.slot_of[col] * b.ld_s;
   for (int i = threadIdx.x; i < b.ld_n; i += blockDim.x)
     b.uy[(size_t)col * b.ld_n + i] = (i < b.n) ? b.E[i] * v[i] : 0.0;
   for (int i = threadIdx.x; i < b.ld_m; i += blockDim.x) {
@@ -447,7 +454,6 @@ __global__ void batch_unscale_kernel(BatchDev b, const double* __restrict__ S) {
   }
 }
 
-__device__ __forceinline__ double nanmax(double best, double a) { return (a > best || a != a) ? a : best; }
 __device__ __forceinline__ double warp_nanmax(double v) {
 #pragma unroll
   for (int w = 16; w >= 1; w >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, w));
@@ -598,6 +604,37 @@ __global__ void batch_regroup_kernel(BatchDev b) {
   if (tid == 0) { *b.n_tiles = n_tiles; *b.n_active = total_active_s; }
 }
 
+// Physical compaction of the iterate after a re-bucketing: slot s of `dst` <- the column the new
+// slot map puts there (from its old slot in `src`), zeros for a padding slot; then slot_of[col] = s.
+// One CTA per slot of the new map.
+__global__ void batch_permute_kernel(BatchDev b, const double* __restrict__ src, double* __restrict__ dst) {
+  const int s = blockIdx.x;
+  if (s >= (*b.n_tiles) * SLOT_TILE) return;
+  const int col = b.cols[s];
+  __shared__ int old_s;
+  if (threadIdx.x == 0) old_s = col >= 0 ? b.slot_of[col] : 0;
+  __syncthreads();
+  const double2* from = reinterpret_cast<const double2*>(src + (size_t)old_s * b.ld_s);
+  double2* to = reinterpret_cast<double2*>(dst + (size_t)s * b.ld_s);
+  for (int i = threadIdx.x; i < (b.ld_s >> 1); i += blockDim.x) to[i] = col >= 0 ? from[i] : make_double2(0.0, 0.0);
+  if (threadIdx.x == 0 && col >= 0) b.slot_of[col] = s;
+}
+
+// Debug (CQP_ROUND_VERIFY=1): first entry where the round kernel's iterate differs from the
+// legacy kernel's, over the slots of the current map.  out[0] = min linear index (slot * ld + row).
+__global__ void batch_compare_kernel(const double* __restrict__ a, const double* __restrict__ b, const int* n_tiles,
+                                     int ld, int D, unsigned long long* out) {
+  const int s = blockIdx.x;
+  if (s >= (*n_tiles) * SLOT_TILE) return;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    const double x = a[(size_t)s * ld + i], y = b[(size_t)s * ld + i];
+    if (__double_as_longlong(x) != __double_as_longlong(y)) {
+      atomicMin(out, (unsigned long long)s * ld + i);
+      atomicAdd(out + 1, 1ull);
+    }
+  }
+}
+
 }  // namespace
 }  // namespace cqp
 
@@ -657,6 +694,21 @@ struct cqp_batch {
   int* cols = nullptr;
   TileDesc* tiles = nullptr;
   int *n_tiles = nullptr, *n_active = nullptr;
+  int* slot_of = nullptr;   // [capacity] column -> slot of its iterate (S0 / S1 are in slot order)
+  int slot_cap = 0;         // slots of S0 / S1
+  // round kernel (cqp_batch_round.cuh): TMA descriptors of W (box rows 64 / 32) and of the two iterate
+  // buffers, the per-round counters {work, done[column tiles]}.  CQP_BATCH_LEGACY=1 keeps the
+  // one-launch-per-iteration cp.async kernel on the same slot-ordered iterate (A/B runs).
+  CUtensorMap mapA[2], mapS[2][2];  // [box: 0 = 64 rows, 1 = 32 rows], mapS[buffer][box]
+  int* round_ctrs = nullptr;
+  CUtensorMap* gmaps = nullptr;   // device copies: [box a][3] ... see round_run
+  int round_flags = 0;
+  int round_ctr_count = 0;
+  int round_grid[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int legacy = 0;
+  int verify = 0;                       // CQP_ROUND_VERIFY: run both kernels every round and compare
+  double* T[2] = {nullptr, nullptr};    // verify: the legacy kernel's copy of the iterate
+  unsigned long long* vres = nullptr;   // verify: {first mismatch index, count}
   int* h_active = nullptr;  // pinned, one word per round
   int h_active_cap = 0;
   // Lanes: a large batch is cut into independent sub-batches that run concurrently on their own
@@ -700,6 +752,54 @@ const GemmConfig kConfigs[kNumConfigs] = {
     {dmma_gemm_kernel<32, 32, 2, 2, 2, STAGES, 4>, 512, gemm_smem_bytes<32, 32>()},   // 4 k-split groups
     {dmma_gemm_kernel<32, 32, 2, 2, 3, STAGES, 2>, 256, gemm_smem_bytes<32, 32>()},   // 2 k-split groups
 };
+
+// Round kernel (cqp_batch_round.cuh) per tile configuration: same shapes as kConfigs (the unused
+// 128 x 128 entry maps to 64 x 64).
+using RoundKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const RoundParams);
+struct RoundConfig {
+  RoundKernel fn;
+  int threads;
+  int smem;
+  int box_a, box_s;  // index of the TMA descriptor: 0 = 64-row box, 1 = 32-row box
+};
+#define CQP_ROUND_CFG(BM, BN, ST, KS, MINB)                                                     \
+  { round_kernel<BM, BN, 2, 2, ST, KS, MINB>, (4 * KS + 1) * 32, round_smem_bytes<BM, BN, 2, 2, ST, KS>(), \
+    BM == 64 ? 0 : 1, BN == 64 ? 0 : 1 }
+const RoundConfig kRoundConfigs[kNumConfigs] = {
+    CQP_ROUND_CFG(64, 64, 4, 1, 3), CQP_ROUND_CFG(64, 64, 4, 1, 3), CQP_ROUND_CFG(64, 32, 4, 1, 4),
+    CQP_ROUND_CFG(32, 32, 4, 1, 6), CQP_ROUND_CFG(32, 32, 4, 4, 2), CQP_ROUND_CFG(32, 32, 4, 2, 3),
+};
+#undef CQP_ROUND_CFG
+
+// 2-D TMA descriptor of a row-major FP64 matrix [rows][ld] (K contiguous): box = 16 doubles (one
+// 128-byte swizzle span) x box_rows.
+int make_tensor_map(CUtensorMap* out, const double* base, size_t rows, int ld, int box_rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult st;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &st) != cudaSuccess || !fn) {
+      set_error("cuTensorMapEncodeTiled is not available from this driver");
+      return CQP_ERR_CUDA;
+    }
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return CQP_ERR_CUDA;
+  }
+  return CQP_OK;
+}
 
 // Tile shape for a round with (at most) `active` columns still iterating.
 int pick_config(const cqp_batch* b, int active) {
@@ -819,6 +919,18 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
       return fail(cuda_fail(cudaGetLastError(), "occupancy(dmma_gemm_kernel)"));
     b->grid_ctas[cfg] = occ * h->num_sms;
   }
+  for (int cfg = 0; cfg < kNumConfigs; ++cfg) {
+    const RoundConfig& rc = kRoundConfigs[cfg];
+    if (cudaFuncSetAttribute(rc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, rc.smem) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "cudaFuncSetAttribute(round_kernel)"));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rc.fn, rc.threads, rc.smem) != cudaSuccess || occ < 1)
+      return fail(cuda_fail(cudaGetLastError(), "occupancy(round_kernel)"));
+    b->round_grid[cfg] = occ * h->num_sms;
+  }
+  if (const char* e = std::getenv("CQP_BATCH_LEGACY")) b->legacy = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("CQP_ROUND_FLAGS")) b->round_flags = std::atoi(e);
+  if (const char* e = std::getenv("CQP_ROUND_VERIFY")) b->verify = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
   if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_DYNAMIC")) b->dynamic = std::atoi(e) ? 1 : 0;
@@ -834,7 +946,12 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   BA(Hb, (size_t)b->n_mpad * b->ld_n);
   BA(Gb, (size_t)b->m_mpad * b->ld_n);
   BA(Gtb, (size_t)b->n_mpad * b->ld_m);
-  BA(S0, cap * b->ld_s); BA(S1, cap * b->ld_s); BA(bias, cap * b->ld_nm);
+  b->slot_cap = (int)slot_cap;
+  BA(S0, slot_cap * b->ld_s); BA(S1, slot_cap * b->ld_s); BA(bias, cap * b->ld_nm);
+  BA(slot_of, cap);
+  if (b->verify) { BA(T[0], slot_cap * b->ld_s); BA(T[1], slot_cap * b->ld_s); BA(vres, 2); }
+  b->round_ctr_count = 1 + (int)(slot_cap / 32) + 8;
+  BA(round_ctrs, (size_t)b->round_ctr_count);
   BA(g, cap * n); BA(c, cap * m); BA(d, cap * m);
   BA(gs, cap * b->ld_n); BA(lo, cap * b->ld_m); BA(hi, cap * b->ld_m);
   BA(uy, cap * b->ld_n); BA(ul, cap * b->ld_m); BA(uz, cap * b->ld_m);
@@ -864,6 +981,25 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   if ((rc = repad(b, h->Gr, m, n, h->npad, 0, b->Gb, b->m_mpad, b->ld_n, 0, 1))) return fail(rc);
   if ((rc = repad(b, h->Gt, n, m, h->mpad, 0, b->Gtb, b->n_mpad, b->ld_m, 0, 1))) return fail(rc);
   if (cudaStreamSynchronize(b->stream) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "batch_create sync"));
+  for (int box = 0; box < 2; ++box) {
+    const int rows = box == 0 ? 64 : 32;
+    if ((rc = make_tensor_map(&b->mapA[box], b->Wb, (size_t)L * b->Dm_pad, b->ld_s, rows))) return fail(rc);
+    if ((rc = make_tensor_map(&b->mapS[0][box], b->S0, slot_cap, b->ld_s, rows))) return fail(rc);
+    if ((rc = make_tensor_map(&b->mapS[1][box], b->S1, slot_cap, b->ld_s, rows))) return fail(rc);
+  }
+  {
+    // device copies, indexed [box_a * 2 + box_s][3]
+    CUtensorMap host[12];
+    for (int ba = 0; ba < 2; ++ba)
+      for (int bs = 0; bs < 2; ++bs) {
+        host[(ba * 2 + bs) * 3 + 0] = b->mapA[ba];
+        host[(ba * 2 + bs) * 3 + 1] = b->mapS[0][bs];
+        host[(ba * 2 + bs) * 3 + 2] = b->mapS[1][bs];
+      }
+    if (cudaMalloc(reinterpret_cast<void**>(&b->gmaps), sizeof(host)) != cudaSuccess ||
+        cudaMemcpy(b->gmaps, host, sizeof(host), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "tensor map upload"));
+  }
   *out = b;
   return CQP_OK;
 }
@@ -872,7 +1008,7 @@ static void batch_destroy_single(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
                   b->trace, b->hist, b->nhist,
@@ -933,8 +1069,11 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   CQP_CUDA(cudaMemcpyAsync(b->g, g_cols, sizeof(double) * (size_t)n * B, cudaMemcpyDefault, st));
   CQP_CUDA(cudaMemcpyAsync(b->c, c_cols, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
   CQP_CUDA(cudaMemcpyAsync(b->d, d_cols, sizeof(double) * (size_t)m * B, cudaMemcpyDefault, st));
-  CQP_CUDA(cudaMemsetAsync(b->S0, 0, sizeof(double) * (size_t)B * b->ld_s, st));  // cold start: v = 0
-  CQP_CUDA(cudaMemsetAsync(b->S1, 0, sizeof(double) * (size_t)B * b->ld_s, st));
+  // cold start: v = 0 (S is kept in slot order; every slot the map can use starts at zero)
+  const size_t slots_used = (size_t)std::min(b->slot_cap, B + b->L * SLOT_TILE);
+  CQP_CUDA(cudaMemsetAsync(b->S0, 0, sizeof(double) * slots_used * b->ld_s, st));
+  CQP_CUDA(cudaMemsetAsync(b->S1, 0, sizeof(double) * slots_used * b->ld_s, st));
+  CQP_CUDA(cudaMemsetAsync(b->slot_of, 0, sizeof(int) * (size_t)B, st));
 
   BatchDev bd{};
   bd.n = n; bd.m = m; bd.D = b->D; bd.B = B;
@@ -949,6 +1088,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   b->last_B = B;
   bd.out_y = b->out_y; bd.out_z = b->out_z; bd.out_l = b->out_l;
   bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
+  bd.slot_of = b->slot_of;
   bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
   bd.adaptive = s.adaptive_rho; bd.max_iters = s.max_iters;
 
@@ -975,7 +1115,34 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     p.bias = b->bias; p.ld_bias = b->ld_nm; p.nm = nm; p.n = n;
     p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
     p.split = b->split; p.k_tiles3 = b->ld_n / BK; p.negrho = b->negrho;
+    p.slot_major = 1;
     return launch_gemm(b, p, cfg);
+  };
+  double* Sbuf[2] = {b->S0, b->S1};
+  // one persistent launch = `steps` ADMM layers of every active column (cqp_batch_round.cuh)
+  auto round_run = [&](int first, int steps, int cfg) {
+    const RoundConfig& rcfg = kRoundConfigs[cfg];
+    RoundParams p{};
+    p.n = n; p.m = m; p.nm = nm; p.D = b->D; p.M_pad = b->Dm_pad; p.split = b->split;
+    p.k_tiles = b->ld_s / BK; p.k_tiles3 = b->split ? b->ld_n / BK : b->ld_s / BK;
+    p.cols = b->cols; p.tiles = b->tiles; p.n_tiles = b->n_tiles;
+    p.bias = b->bias; p.ld_bias = b->ld_nm; p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
+    p.negrho = b->negrho;
+    p.S[0] = b->S0; p.S[1] = b->S1; p.ld_s = b->ld_s; p.first = first; p.n_iters = steps;
+    p.work = b->round_ctrs; p.done = b->round_ctrs + 1; p.dbg = h->dbg_dev;
+    p.flags = b->round_flags; p.gmaps = b->gmaps + (rcfg.box_a * 2 + rcfg.box_s) * 3;
+    CQP_CUDA(cudaMemsetAsync(b->round_ctrs, 0, sizeof(int) * (size_t)b->round_ctr_count, st));
+    rcfg.fn<<<b->round_grid[cfg], rcfg.threads, rcfg.smem, st>>>(b->mapA[rcfg.box_a], b->mapS[0][rcfg.box_s],
+                                                                 b->mapS[1][rcfg.box_s], p);
+    CQP_CUDA(cudaGetLastError());
+    b->last_launches += 1;
+    return (int)CQP_OK;
+  };
+  auto permute = [&](int from) {  // compact S[from] into S[from ^ 1] following the fresh slot map
+    batch_permute_kernel<<<(unsigned)slots_used, 128, 0, st>>>(bd, Sbuf[from], Sbuf[from ^ 1]);
+    CQP_CUDA(cudaGetLastError());
+    b->last_launches += 1;
+    return (int)CQP_OK;
   };
   auto gemm_plain = [&](const double* A, int M, int m_pad, int lda, const double* Bm, int ldb, double* C, int ldc, int cfg) {
     GemmParams p = base;
@@ -989,9 +1156,9 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   CQP_CUDA(cudaGetLastError());
   b->last_launches += 2;  // prepare, regroup
   if ((rc = gemm_bias(pick_config(b, B)))) return rc;
-
-  double* Sa = b->S0;
-  double* Sb = b->S1;
+  int cur = 0;  // Sbuf[cur] holds the iterate
+  if ((rc = permute(cur))) return rc;  // (all zeros: this only fills slot_of)
+  cur ^= 1;
   int it = 0, rounds_done = 0;
   for (int r = 0; r < rounds; ++r) {
     if (r >= 2) {  // stay at most two rounds ahead of the device; stop once every column is done
@@ -1002,16 +1169,69 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     // the host knows the active count with a lag of two rounds; it only decreases
     const int cfg = pick_config(b, r >= 2 ? b->h_active[r - 2] : B);
     CQP_CUDA(cudaEventRecord(b->it0[r], st));
-    for (int k = 0; k < steps; ++k) {
-      if ((rc = gemm_iter(Sa, Sb, cfg))) return rc;
-      std::swap(Sa, Sb);
+    if (b->legacy) {
+      for (int k = 0; k < steps; ++k) {
+        if ((rc = gemm_iter(Sbuf[cur], Sbuf[cur ^ 1], cfg))) return rc;
+        cur ^= 1;
+      }
+    } else {
+      if (b->verify) {
+        const size_t bytes = sizeof(double) * slots_used * b->ld_s;
+        CQP_CUDA(cudaMemcpyAsync(b->T[0], Sbuf[cur], bytes, cudaMemcpyDeviceToDevice, st));
+        CQP_CUDA(cudaMemcpyAsync(b->T[1], Sbuf[cur ^ 1], bytes, cudaMemcpyDeviceToDevice, st));
+        int tc = 0;
+        for (int k = 0; k < steps; ++k) {
+          if ((rc = gemm_iter(b->T[tc], b->T[tc ^ 1], cfg))) return rc;
+          tc ^= 1;
+        }
+        if ((rc = round_run(cur, steps, cfg))) return rc;
+        cur ^= steps & 1;
+        const unsigned long long init[2] = {~0ull, 0ull};
+        CQP_CUDA(cudaMemcpyAsync(b->vres, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        batch_compare_kernel<<<(unsigned)slots_used, 256, 0, st>>>(Sbuf[cur], b->T[tc], b->n_tiles, b->ld_s, b->D, b->vres);
+        unsigned long long got[2] = {0, 0};
+        int nt = 0;
+        CQP_CUDA(cudaMemcpyAsync(got, b->vres, sizeof(got), cudaMemcpyDeviceToHost, st));
+        CQP_CUDA(cudaMemcpyAsync(&nt, b->n_tiles, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CQP_CUDA(cudaStreamSynchronize(st));
+        if (got[1]) {
+          std::vector<int> hc((size_t)nt * SLOT_TILE);
+          std::vector<TileDesc> ht(nt);
+          cudaMemcpy(hc.data(), b->cols, sizeof(int) * hc.size(), cudaMemcpyDeviceToHost);
+          cudaMemcpy(ht.data(), b->tiles, sizeof(TileDesc) * nt, cudaMemcpyDeviceToHost);
+          std::vector<double> sa((size_t)hc.size() * b->ld_s), sb(sa.size());
+          cudaMemcpy(sa.data(), Sbuf[cur], sizeof(double) * sa.size(), cudaMemcpyDeviceToHost);
+          cudaMemcpy(sb.data(), b->T[tc], sizeof(double) * sb.size(), cudaMemcpyDeviceToHost);
+          std::fprintf(stderr, "[verify] round %d cfg %d steps %d: %llu entries differ; first slot %llu row %llu; tiles %d:", r, cfg,
+                       steps, got[1], got[0] / b->ld_s, got[0] % b->ld_s, nt);
+          for (int t = 0; t < nt; ++t) {
+            int real = 0;
+            for (int i = 0; i < SLOT_TILE; ++i) real += hc[(size_t)t * SLOT_TILE + i] >= 0;
+            std::fprintf(stderr, " [a%d:%d]", ht[t].a_index, real);
+          }
+          std::fprintf(stderr, "\n[verify]   differing (slot: rows lo-hi count):");
+          int shown = 0;
+          for (size_t sidx = 0; sidx < hc.size() && shown < 24; ++sidx) {
+            int lo = -1, hi = -1, cnt = 0;
+            for (int i = 0; i < b->D; ++i)
+              if (std::memcmp(&sa[sidx * b->ld_s + i], &sb[sidx * b->ld_s + i], 8) != 0) { if (lo < 0) lo = i; hi = i; ++cnt; }
+            if (cnt) { std::fprintf(stderr, " %zu(col %d): %d-%d %d;", sidx, hc[sidx], lo, hi, cnt); ++shown; }
+          }
+          std::fprintf(stderr, "\n");
+          // keep going from the legacy result so that later rounds are judged on their own
+          CQP_CUDA(cudaMemcpyAsync(Sbuf[cur], b->T[tc], bytes, cudaMemcpyDeviceToDevice, st));
+        }
+      } else {
+        if ((rc = round_run(cur, steps, cfg))) return rc;
+        cur ^= steps & 1;
+      }
     }
     CQP_CUDA(cudaEventRecord(b->it1[r], st));
     rounds_done = r + 1;
     it += steps;
     // NOTE: columns that stopped earlier keep their (stale) value in whichever buffer they were
     // last written to; they are never read again (results were captured when they stopped).
-    batch_unscale_kernel<<<B, 128, 0, st>>>(bd, Sa);
+    batch_unscale_kernel<<<B, 128, 0, st>>>(bd, Sbuf[cur]);
     CQP_CUDA(cudaGetLastError());
     b->last_launches += 3;  // unscale, decide, regroup
     if ((rc = gemm_plain(b->Hb, n, b->n_mpad, b->ld_n, b->uy, b->ld_n, b->hy, b->ld_n, cfg))) return rc;
@@ -1023,7 +1243,11 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     CQP_CUDA(cudaGetLastError());
     CQP_CUDA(cudaMemcpyAsync(&b->h_active[r], b->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CQP_CUDA(cudaEventRecord(b->round_events[r], st));
-    if (r + 1 < rounds && (rc = gemm_bias(cfg))) return rc;
+    if (r + 1 < rounds) {
+      if ((rc = permute(cur))) return rc;
+      cur ^= 1;
+      if ((rc = gemm_bias(cfg))) return rc;
+    }
   }
   CQP_CUDA(cudaEventRecord(b->evc1, st));
   // results

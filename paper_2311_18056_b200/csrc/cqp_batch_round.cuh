@@ -1,0 +1,343 @@
+// Batched path, iteration kernel: ONE persistent launch runs a whole check round (check_interval
+// ADMM layers, /root/reference/proj/src/solver.cpp:59-63 per column) of the batch.
+//
+// Included by cqp_batch.cu (inside namespace cqp { namespace { ... } }) after TileDesc / SLOT_TILE.
+//
+//   * Operands are staged by TMA: cp.async.bulk.tensor.2d (SASS UTMALDG) moves a BM x 16 tile of
+//     W_k and a BN x 16 tile of S into shared memory with the hardware 128-byte swizzle and
+//     completes on an mbarrier (complete_tx); a dedicated producer warp issues the copies, the
+//     consumer warps only wait on `full[stage]`, run DMMA.8x8x4 (mma.sync m8n8k4 f64: the FP64
+//     tensor shape of sm_100a; tcgen05 has no f64 kind) and release the stage through `empty[stage]`.
+//     No cp.async bookkeeping, no CTA-wide barrier in the K loop, and the producer runs ahead into
+//     the next work item, so there is no pipeline-fill bubble between tiles.
+//   * S is stored in SLOT order (physically compacted at every re-bucketing, batch_permute_kernel):
+//     the 128 columns of a slot tile are contiguous, which is what makes them one 2-D TMA box.
+//   * Fragment rows are permuted, g -> 2 (g & 3) | (g >> 2): the four rows a half-warp reads in one
+//     8-byte LDS then sit at row-in-8 = {0, 2, 4, 6} (or {1, 3, 5, 7}), and the XOR of the 128-byte
+//     swizzle (16-byte chunk ^ row-in-8) sends the two chunks {2 ks, 2 ks + 1} of those rows to eight
+//     distinct chunks = all 32 banks.  (With the identity mapping rows 0 and 1 collide.)  The C
+//     fragment is mapped back through the same permutation in the epilogue.
+//   * Dataflow across iterations: work item = (iteration, column tile, row tile), taken from one
+//     atomic counter in that order.  Item (i, c, *) reads column tile c of iteration i - 1, so the
+//     producer waits until done[c] has counted every row tile of iteration i - 1 (each consumer
+//     warp adds 1 after its stores, release at gpu scope; the producer's acquire + fence.proxy.async
+//     orders the generic-proxy stores before its async-proxy reads).  Columns of different tiles
+//     never wait for each other, so launches no longer end in a wave tail 25 times per round: the
+//     grid drains once, at the end of the round.  Items are handed out in index order, so the owner
+//     of the lowest unfinished item is always resident and never blocked: no deadlock whatever part
+//     of the grid the device keeps resident (two lanes can run their kernels concurrently).
+//   * KS > 1 (last rounds, a handful of columns): KS warp groups split the k steps of every k-tile
+//     and meet in shared memory; a tile's K loop is a latency chain, KS groups walk it KS steps at a
+//     time.
+#pragma once
+
+#include <cuda.h>
+
+struct RoundParams {
+  int n, m, nm, D;
+  int M_pad;        // padded rows of one ladder level in Wb
+  int split;        // padded row where the lambda block starts (0: dense layer)
+  int k_tiles, k_tiles3;
+  const int* cols;  // slot -> column (-1: padding slot)
+  const TileDesc* tiles;
+  const int* n_tiles;
+  const double* bias; int ld_bias;
+  const double* lo; const double* hi; int ld_lohi;
+  const double* negrho;  // [L][m]
+  double* S[2];     // iterate in slot order, [slot][ld_s]
+  int ld_s;
+  int first;        // S[first] holds the iterate when the round starts
+  int n_iters;
+  int* work;        // item counter (zero at launch)
+  int* done;        // [column tiles of BN slots] consumer-warp completions of this round (zero at launch)
+  int* dbg;
+  int flags;                  // debug switch (CQP_ROUND_FLAGS): 1 = TMA descriptors read from global memory
+  const CUtensorMap* gmaps;   // [3] copies of the descriptors in global memory: A, S0, S1
+};
+
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_barrier(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+constexpr int kRoundQ = 4;  // depth of the producer -> consumer item ring
+
+template <int BM, int BN, int WM, int WN, int ST, int KS>
+constexpr int round_smem_bytes() {
+  constexpr int MI = BM / WM / 8, NI = BN / WN / 8;
+  return 1024 /* alignment slack: the 128-byte swizzle wants 1024-byte aligned tiles */ + ST * (BM + BN) * 128 +
+         (KS > 1 ? (KS - 1) * WM * WN * 32 * MI * NI * 2 * 8 : 0) + 8 * (2 * ST + 2 * kRoundQ) + 4 * kRoundQ + 16;
+}
+
+template <int BM, int BN, int WM, int WN, int ST, int KS, int MINB>
+__global__ void __launch_bounds__((WM * WN * KS + 1) * 32, MINB)
+round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapS0,
+             const __grid_constant__ CUtensorMap mapS1, const RoundParams p) {
+  constexpr int NW = WM * WN;    // warps of one k-split group
+  constexpr int NCW = NW * KS;   // consumer warps; warp NCW is the producer
+  constexpr int TM = BM / WM, TN = BN / WN, MI = TM / 8, NI = TN / 8;
+  constexpr int SUB = SLOT_TILE / BN;
+  constexpr int A_BYTES = BM * 128, STAGE_BYTES = (BM + BN) * 128;
+  constexpr int PER = MI * NI * 2;
+  extern __shared__ unsigned char round_smem_raw[];
+  // (pointer arithmetic on the shared array, not an integer round trip: the compiler keeps the
+  // shared address space and emits LDS, not generic loads)
+  unsigned char* base = round_smem_raw + ((1024u - (smem_u32(round_smem_raw) & 1023u)) & 1023u);
+  double* red = reinterpret_cast<double*>(base + ST * STAGE_BYTES);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(red + (KS > 1 ? (KS - 1) * NW * 32 * PER : 0));
+  unsigned long long* empty = full + ST;
+  unsigned long long* sfull = empty + ST;
+  unsigned long long* sempty = sfull + kRoundQ;
+  int* item_s = reinterpret_cast<int*>(sempty + kRoundQ);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
+    for (int q = 0; q < kRoundQ; ++q) { mbar_init(&sfull[q], 1); mbar_init(&sempty[q], NCW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int m_tiles = p.M_pad / BM;
+  const int n_ct = __ldcg(p.n_tiles) * SUB;
+  const int per_iter = n_ct * m_tiles;
+  const int total = per_iter * p.n_iters;
+  int q = 0, qph = 0;
+  unsigned stage = 0, sph = 0;
+
+  if (warp == NCW) {
+    // ===== producer: item fetch, dependency wait, TMA issue =====
+    if (lane != 0) return;
+    for (;;) {
+      const int item = atomicAdd(p.work, 1);
+      // the consumers learn about the item only once its inputs are complete: they read S too (the
+      // diagonal terms of the lambda rows)
+      auto hand_over = [&](int value) {
+        mbar_wait(&sempty[q], qph ^ 1, p.dbg, 20, item);
+        item_s[q] = value;
+        mbar_arrive(&sfull[q]);
+        if (++q == kRoundQ) { q = 0; qph ^= 1; }
+      };
+      if (item >= total) { hand_over(-1); break; }
+      const int it = item / per_iter, r = item - it * per_iter;
+      const int ns = r / m_tiles, mt = r - ns * m_tiles;
+      const int nt = ns / SUB, sub = ns - nt * SUB;
+      TileDesc td;
+      td.slot0 = __ldcg(&p.tiles[nt].slot0);
+      td.a_index = __ldcg(&p.tiles[nt].a_index);
+      const int slot0 = td.slot0 + sub * BN;
+      const int m0 = mt * BM;
+      const bool blk3 = p.split > 0 && m0 >= p.split;
+      const int row0 = blk3 ? m0 - p.split + p.nm : m0;
+      const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
+      if (row0 >= row_end || __ldcg(p.cols + slot0) < 0) { hand_over(item); continue; }  // empty item: the consumers skip it too
+      if (it > 0) {
+        const int need = it * m_tiles * NW;
+        long long t0 = 0;
+        unsigned spins = 0;
+        while (ld_acquire_gpu(p.done + ns) < need) {
+          if ((++spins & 0x3FF) == 0) {
+            if (t0 == 0) t0 = clock64();
+            else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(p.dbg, 21, item);
+          }
+        }
+        fence_proxy_async();  // the generic-proxy stores just acquired, before the async-proxy reads below
+      }
+      hand_over(item);
+      const CUtensorMap* mapS = ((p.first ^ it) & 1) ? &mapS1 : &mapS0;
+      const CUtensorMap* mapAp = &mapA;
+      if (p.flags & 1) { mapAp = p.gmaps; mapS = p.gmaps + 1 + ((p.first ^ it) & 1); }
+      const int a_row = td.a_index * p.M_pad + m0;
+      const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
+      for (int kt = 0; kt < k_tiles; ++kt) {
+        mbar_wait(&empty[stage], (int)(sph ^ 1u), p.dbg, 22, item);
+        mbar_expect_tx(&full[stage], STAGE_BYTES);
+        const unsigned dst = smem_u32(base + stage * STAGE_BYTES);
+        tma_load_2d(dst, mapAp, kt * 16, a_row, smem_u32(&full[stage]));
+        tma_load_2d(dst + A_BYTES, mapS, kt * 16, slot0, smem_u32(&full[stage]));
+        if (++stage == (unsigned)ST) { stage = 0; sph ^= 1u; }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int g = lane >> 2, t4 = lane & 3;
+  const int kg = warp / NW, warp_in = warp - kg * NW;
+  const int warp_m = warp_in % WM, warp_n = warp_in / WM;
+  const int pg = ((g & 3) << 1) | (g >> 2);  // tile row-in-8 of fragment row g (see the header)
+  // tile column-in-8 of the C fragment's columns 2 t4, 2 t4 + 1
+  const int pc0 = (((2 * t4) & 3) << 1) | ((2 * t4) >> 2), pc1 = (((2 * t4 + 1) & 3) << 1) | ((2 * t4 + 1) >> 2);
+  for (;;) {
+    mbar_wait(&sfull[q], qph, p.dbg, 23, 0);
+    const int item = item_s[q];
+    __syncwarp();
+    if (item < 0) break;  // (the branch needs the loaded value: the slot is released only after the read returned)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sempty[q]);
+    if (++q == kRoundQ) { q = 0; qph ^= 1; }
+    const int it = item / per_iter, r = item - it * per_iter;
+    const int ns = r / m_tiles, mt = r - ns * m_tiles;
+    const int nt = ns / SUB, sub = ns - nt * SUB;
+    TileDesc td;
+      td.slot0 = __ldcg(&p.tiles[nt].slot0);
+      td.a_index = __ldcg(&p.tiles[nt].a_index);
+    const int slot0 = td.slot0 + sub * BN;
+    const int m0 = mt * BM;
+    const bool blk3 = p.split > 0 && m0 >= p.split;
+    const int row0 = blk3 ? m0 - p.split + p.nm : m0;
+    const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
+    if (!(row0 >= row_end || __ldcg(p.cols + slot0) < 0)) {
+      const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
+      const double* Sin = p.S[(p.first ^ it) & 1];
+      double* Sout = p.S[(p.first ^ it ^ 1) & 1];
+      // Accumulators start from the bias (rows < n + m) or from the two diagonal terms of a lambda row,
+      // -rho_i z_i + lambda_i (blocks (3,2), (3,3) of W, layers.cpp:159-161); the loads overlap the
+      // first stages.  S is read with ld.cg: these addresses are rewritten every other iteration.
+      double acc[MI][NI][2];
+      int colv[NI][2];
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int cs = slot0 + warp_n * TN + ni * 8 + (j ? pc1 : pc0);
+          const int col = __ldcg(p.cols + cs);
+          colv[ni][j] = col;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) {
+            const int row = row0 + warp_m * TM + mi * 8 + pg;
+            double init = 0.0;
+            if (col >= 0 && kg == 0) {
+              if (row < p.nm) {
+                init = __ldcg(p.bias + (size_t)col * p.ld_bias + row);
+              } else if (blk3 && row < p.D) {
+                const double* v = Sin + (size_t)cs * p.ld_s;
+                const int i = row - p.nm;
+                init = fma(p.negrho[(size_t)td.a_index * p.m + i], __ldcg(v + p.n + i), __ldcg(v + row));
+              }
+            }
+            acc[mi][ni][j] = init;
+          }
+        }
+      }
+      // Stage release discipline: a stage goes back to the TMA producer only once the DMMAs that consume
+      // its fragment loads have been ISSUED (an issued DMMA has its operands, so the loads have
+      // returned).  Program order alone does not give that: ptxas moves the arrive up, right behind
+      // the last (still in flight) LDS and ahead of the DMMAs (seen in SASS; the refill then raced with
+      // that load: wrong ni = last fragment).  So the arrive for k-tile kt sits behind the full-wait
+      // loop of k-tile kt + 1, and the last one behind the epilogue's fence / the reduction barrier.
+      int held = -1;
+      for (int kt = 0; kt < k_tiles; ++kt) {
+        mbar_wait(&full[stage], (int)sph, p.dbg, 24, item);
+        if (held >= 0 && lane == 0) mbar_arrive(&empty[held]);
+        const double* as = reinterpret_cast<const double*>(base + stage * STAGE_BYTES) + (warp_m * TM + pg) * 16;
+        const double* bs = reinterpret_cast<const double*>(base + stage * STAGE_BYTES + A_BYTES) + (warp_n * TN + pg) * 16;
+        double a[MI], b[NI];
+#pragma unroll
+        for (int ks0 = 0; ks0 < 4; ks0 += KS) {
+          const int ks = ks0 + kg;
+          const int e = ks * 4 + t4;
+          const int off = (((e >> 1) ^ pg) << 1) | (e & 1);
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) a[mi] = as[mi * 128 + off];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) b[ni] = bs[ni * 128 + off];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        held = (int)stage;
+        if (++stage == (unsigned)ST) { stage = 0; sph ^= 1u; }
+      }
+      if (KS > 1) {
+        // partial accumulators of groups 1 .. KS-1 meet in `red`; group 0 adds them in group order
+        named_barrier(1, NCW * 32);  // the previous item's readers of `red` are done
+        if (kg > 0) {
+          double* mine = red + ((size_t)(kg - 1) * (NW * 32) + warp_in * 32 + lane) * PER;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+              mine[(mi * NI + ni) * 2] = acc[mi][ni][0];
+              mine[(mi * NI + ni) * 2 + 1] = acc[mi][ni][1];
+            }
+        }
+        named_barrier(1, NCW * 32);
+        if (kg == 0) {
+#pragma unroll
+          for (int qq = 1; qq < KS; ++qq) {
+            const double* theirs = red + ((size_t)(qq - 1) * (NW * 32) + warp_in * 32 + lane) * PER;
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                acc[mi][ni][0] += theirs[(mi * NI + ni) * 2];
+                acc[mi][ni][1] += theirs[(mi * NI + ni) * 2 + 1];
+              }
+          }
+        }
+      }
+      if (kg == 0) {
+        // epilogue: clamp the z rows (solver.cpp:62), store in slot order.  Padding slots hold zeros
+        // and stay zero (no bias, W 0 = 0).
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int cs = slot0 + warp_n * TN + ni * 8 + (j ? pc1 : pc0);
+            const int col = colv[ni][j];
+            double* crow = Sout + (size_t)cs * p.ld_s;
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+              const int row = row0 + warp_m * TM + mi * 8 + pg;
+              if (row >= row_end) continue;
+              double v = acc[mi][ni][j];
+              if (col >= 0 && row >= p.n && row < p.nm) {
+                const double lo = __ldcg(p.lo + (size_t)col * p.ld_lohi + row - p.n);
+                const double hi = __ldcg(p.hi + (size_t)col * p.ld_lohi + row - p.n);
+                v = v < lo ? lo : v;
+                v = v > hi ? hi : v;
+              }
+              crow[row] = v;
+            }
+          }
+        }
+        // every thread makes ITS stores visible device-wide (and to the async proxy: other CTAs read
+        // them with TMA) before the warp's completion is counted
+        __threadfence();
+        fence_proxy_async();
+      }
+      // the item's last stage (see the release discipline above): behind the fence (group 0) or behind the
+      // reduction barrier, whose shared-memory stores carry the accumulators (groups > 0)
+      if (held >= 0 && lane == 0) mbar_arrive(&empty[held]);
+    }
+    // one completion per consumer warp of group 0 (empty items count too: the producer of the next
+    // iteration waits for m_tiles * NW of them per column tile)
+    if (kg == 0) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        red_release_gpu_add(p.done + ns, 1);
+      }
+    }
+  }
+}
