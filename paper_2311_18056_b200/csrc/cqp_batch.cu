@@ -408,6 +408,10 @@ struct BatchDev {
   int* n_tiles;
   int* n_active;
   int* slot_of;      // [B] column -> slot of its iterate in S (slot order)
+  // compact lists of the NON-EMPTY column tiles of 64 ([0]) and 32 ([1]) slots: {first slot, ladder
+  // index}; the round kernel enumerates these, so padding costs it nothing
+  TileDesc* ct[2];
+  int* n_ct;         // [2]
   // settings
   double eps_prim, eps_dual, threshold;
   int adaptive, max_iters;
@@ -602,6 +606,28 @@ __global__ void batch_regroup_kernel(BatchDev b) {
     __syncthreads();
   }
   if (tid == 0) { *b.n_tiles = n_tiles; *b.n_active = total_active_s; }
+  __syncthreads();
+  // non-empty column tiles (padding slots sit at the end of a bucket: a tile whose first slot is empty
+  // is empty); one warp per granularity, in slot order
+  if (warp < 2) {
+    const int bn = warp == 0 ? 64 : 32, sub = SLOT_TILE / bn;
+    int count = 0;
+    for (int base = 0; base < n_tiles * sub; base += 32) {
+      const int k = base + lane;
+      bool keep = false;
+      TileDesc td{0, 0};
+      if (k < n_tiles * sub) {
+        const TileDesc t128 = b.tiles[k / sub];
+        td.slot0 = t128.slot0 + (k % sub) * bn;
+        td.a_index = t128.a_index;
+        keep = b.cols[td.slot0] >= 0;
+      }
+      const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+      if (keep) b.ct[warp][count + __popc(ballot & ((1u << lane) - 1))] = td;
+      count += __popc(ballot);
+    }
+    if (lane == 0) b.n_ct[warp] = count;
+  }
 }
 
 // Physical compaction of the iterate after a re-bucketing: slot s of `dst` <- the column the new
@@ -656,13 +682,14 @@ struct cqp_batch {
   int* work_ctrs = nullptr;
   int work_ctr_cap = 0, work_ctr_next = 0;
   int dynamic = 0;
-  int grid_ctas[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // persistent grid per tile configuration
+  int grid_ctas[16] = {};  // persistent grid per tile configuration
   // active-column thresholds (see pick_config), calibrated on B200 at D = 1500 (profiles/,
   // CQP_BATCH_THRESHOLDS sweeps): 64x64 tiles with 3 CTAs/SM beat 128x128 at every batch size
   // (less wave quantisation, 12 warps/SM), 64x32 wins below ~3400 columns, 32x32 (6 CTAs/SM: more
   // warps to keep the tensor pipe fed when the grid no longer fills) below ~1400.
   int thr_big = 1 << 30, thr_mid = 3400, thr_small = 800;
   int force_cfg = -1;
+  std::vector<std::pair<int, int>> plan;  // CQP_BATCH_PLAN="cfg:min_active,...": first entry whose bound the active count reaches
   int small_cfg = 3;  // 32x32 tiles
   // below thr_tiny columns: 32x32 tiles with 4 k-split warp groups (cfg 4; cfg 5 has 2).  Measured
   // (B200, D = 1500): a round of <= 58 columns takes 0.62 instead of 0.72 ms; between 100 and 300
@@ -695,6 +722,8 @@ struct cqp_batch {
   TileDesc* tiles = nullptr;
   int *n_tiles = nullptr, *n_active = nullptr;
   int* slot_of = nullptr;   // [capacity] column -> slot of its iterate (S0 / S1 are in slot order)
+  TileDesc* ct[2] = {nullptr, nullptr};  // non-empty column tiles of 64 / 32 slots (BatchDev::ct)
+  int* n_ct = nullptr;
   int slot_cap = 0;         // slots of S0 / S1
   // round kernel (cqp_batch_round.cuh): TMA descriptors of W (box rows 64 / 32) and of the two iterate
   // buffers, the per-round counters {work, done[column tiles]}.  CQP_BATCH_LEGACY=1 keeps the
@@ -704,7 +733,7 @@ struct cqp_batch {
   CUtensorMap* gmaps = nullptr;   // device copies: [box a][3] ... see round_run
   int round_flags = 0;
   int round_ctr_count = 0;
-  int round_grid[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int round_grid[16] = {};
   int legacy = 0;
   int verify = 0;                       // CQP_ROUND_VERIFY: run both kernels every round and compare
   double* T[2] = {nullptr, nullptr};    // verify: the legacy kernel's copy of the iterate
@@ -742,7 +771,8 @@ struct GemmConfig {
   int threads;
   int smem;
 };
-constexpr int kNumConfigs = 6;
+constexpr int kNumConfigs = 10;
+static_assert(kNumConfigs <= 16, "grid_ctas / round_grid hold 16 configurations");
 const GemmConfig kConfigs[kNumConfigs] = {
     {dmma_gemm_kernel<128, 128, 2, 4, 1>, 256, gemm_smem_bytes<128, 128>()},
     {dmma_gemm_kernel<64, 64, 2, 2, 3>, 128, gemm_smem_bytes<64, 64>()},
@@ -751,6 +781,12 @@ const GemmConfig kConfigs[kNumConfigs] = {
     // deeper pipelines for the latency-bound last rounds (CQP_BATCH_FORCE_CFG / thresholds)
     {dmma_gemm_kernel<32, 32, 2, 2, 2, STAGES, 4>, 512, gemm_smem_bytes<32, 32>()},   // 4 k-split groups
     {dmma_gemm_kernel<32, 32, 2, 2, 3, STAGES, 2>, 256, gemm_smem_bytes<32, 32>()},   // 2 k-split groups
+    // 6 .. 9: same per-iteration kernels as 3, 5, 4, 2 (these indices differ in the ROUND kernel only:
+    // deeper TMA pipelines, see kRoundConfigs)
+    {dmma_gemm_kernel<32, 32, 2, 2, 6>, 128, gemm_smem_bytes<32, 32>()},
+    {dmma_gemm_kernel<32, 32, 2, 2, 3, STAGES, 2>, 256, gemm_smem_bytes<32, 32>()},
+    {dmma_gemm_kernel<32, 32, 2, 2, 2, STAGES, 4>, 512, gemm_smem_bytes<32, 32>()},
+    {dmma_gemm_kernel<64, 32, 2, 2, 4>, 128, gemm_smem_bytes<64, 32>()},
 };
 
 // Round kernel (cqp_batch_round.cuh) per tile configuration: same shapes as kConfigs (the unused
@@ -768,6 +804,10 @@ struct RoundConfig {
 const RoundConfig kRoundConfigs[kNumConfigs] = {
     CQP_ROUND_CFG(64, 64, 4, 1, 3), CQP_ROUND_CFG(64, 64, 4, 1, 3), CQP_ROUND_CFG(64, 32, 4, 1, 4),
     CQP_ROUND_CFG(32, 32, 4, 1, 6), CQP_ROUND_CFG(32, 32, 4, 4, 2), CQP_ROUND_CFG(32, 32, 4, 2, 3),
+    // deeper pipelines for rounds whose items no longer fill the SMs (an item's K loop is then bound by
+    // the TMA latency times k-tiles / stages in flight)
+    CQP_ROUND_CFG(32, 32, 8, 1, 3), CQP_ROUND_CFG(32, 32, 8, 2, 3), CQP_ROUND_CFG(32, 32, 10, 4, 2),
+    CQP_ROUND_CFG(64, 32, 6, 1, 3),
 };
 #undef CQP_ROUND_CFG
 
@@ -804,6 +844,8 @@ int make_tensor_map(CUtensorMap* out, const double* base, size_t rows, int ld, i
 // Tile shape for a round with (at most) `active` columns still iterating.
 int pick_config(const cqp_batch* b, int active) {
   if (b->force_cfg >= 0) return b->force_cfg;
+  for (const auto& step : b->plan)
+    if (active >= step.second) return step.first;
   if (active >= b->thr_big) return 0;
   if (active >= b->thr_mid) return 1;
   if (active >= b->thr_small) return 2;
@@ -933,6 +975,24 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   if (const char* e = std::getenv("CQP_ROUND_VERIFY")) b->verify = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_THRESHOLDS")) std::sscanf(e, "%d,%d,%d", &b->thr_big, &b->thr_mid, &b->thr_small);
   if (const char* e = std::getenv("CQP_BATCH_FORCE_CFG")) b->force_cfg = std::atoi(e);
+  if (!b->legacy && !std::getenv("CQP_BATCH_PLAN") && !std::getenv("CQP_BATCH_THRESHOLDS") && !std::getenv("CQP_BATCH_TINY") &&
+      !std::getenv("CQP_BATCH_SMALL_CFG")) {
+    // Round kernel, calibrated on B200 at D = 1500 (tools/ab_batch.py sweeps; ms per solve, same box):
+    // 4096 columns 242.7 with the per-iteration kernel's thresholds and 4-stage pipelines, 230.0 with
+    // this plan; 1024 columns 102.3 -> 88.3; 512: 78.0 -> 65.0; 256: 64.9 -> 56.5; 64: 50.7 -> 44.0.
+    // Below ~800 columns an iteration has fewer items than the SMs have CTA slots, an item's K loop is
+    // then bound by TMA latency x k-tiles / stages in flight: deeper pipelines (8 stages of 32 x 32,
+    // 6 of 64 x 32), and two k-split warp groups below 250 columns.
+    b->plan = {{1, 3400}, {2, 1600}, {9, 800}, {6, 250}, {7, 0}};
+  }
+  if (const char* e = std::getenv("CQP_BATCH_PLAN")) {
+    int cfg = 0, bound = 0, used = 0;
+    while (std::sscanf(e, "%d:%d%n", &cfg, &bound, &used) == 2) {
+      if (cfg >= 0 && cfg < kNumConfigs) b->plan.emplace_back(cfg, bound);
+      e += used;
+      if (*e == ',') ++e;
+    }
+  }
   if (const char* e = std::getenv("CQP_BATCH_DYNAMIC")) b->dynamic = std::atoi(e) ? 1 : 0;
   if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_TINY")) std::sscanf(e, "%d,%d", &b->tiny_cfg, &b->thr_tiny);
@@ -949,6 +1009,7 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   b->slot_cap = (int)slot_cap;
   BA(S0, slot_cap * b->ld_s); BA(S1, slot_cap * b->ld_s); BA(bias, cap * b->ld_nm);
   BA(slot_of, cap);
+  BA(ct[0], slot_cap / 64 + 1); BA(ct[1], slot_cap / 32 + 1); BA(n_ct, 2);
   if (b->verify) { BA(T[0], slot_cap * b->ld_s); BA(T[1], slot_cap * b->ld_s); BA(vres, 2); }
   b->round_ctr_count = 1 + (int)(slot_cap / 32) + 8;
   BA(round_ctrs, (size_t)b->round_ctr_count);
@@ -1008,7 +1069,7 @@ static void batch_destroy_single(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->ct[0], b->ct[1], b->n_ct, b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
                   b->trace, b->hist, b->nhist,
@@ -1089,6 +1150,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   bd.out_y = b->out_y; bd.out_z = b->out_z; bd.out_l = b->out_l;
   bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
   bd.slot_of = b->slot_of;
+  bd.ct[0] = b->ct[0]; bd.ct[1] = b->ct[1]; bd.n_ct = b->n_ct;
   bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
   bd.adaptive = s.adaptive_rho; bd.max_iters = s.max_iters;
 
@@ -1125,11 +1187,12 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     RoundParams p{};
     p.n = n; p.m = m; p.nm = nm; p.D = b->D; p.M_pad = b->Dm_pad; p.split = b->split;
     p.k_tiles = b->ld_s / BK; p.k_tiles3 = b->split ? b->ld_n / BK : b->ld_s / BK;
-    p.cols = b->cols; p.tiles = b->tiles; p.n_tiles = b->n_tiles;
+    p.cols = b->cols; p.tiles = b->ct[rcfg.box_s]; p.n_tiles = b->n_ct + rcfg.box_s;
     p.bias = b->bias; p.ld_bias = b->ld_nm; p.lo = b->lo; p.hi = b->hi; p.ld_lohi = b->ld_m;
     p.negrho = b->negrho;
     p.S[0] = b->S0; p.S[1] = b->S1; p.ld_s = b->ld_s; p.first = first; p.n_iters = steps;
     p.work = b->round_ctrs; p.done = b->round_ctrs + 1; p.dbg = h->dbg_dev;
+    p.num_sms = (b->round_flags & 2) ? 0 : h->num_sms;
     p.flags = b->round_flags; p.gmaps = b->gmaps + (rcfg.box_a * 2 + rcfg.box_s) * 3;
     CQP_CUDA(cudaMemsetAsync(b->round_ctrs, 0, sizeof(int) * (size_t)b->round_ctr_count, st));
     rcfg.fn<<<b->round_grid[cfg], rcfg.threads, rcfg.smem, st>>>(b->mapA[rcfg.box_a], b->mapS[0][rcfg.box_s],
@@ -1333,7 +1396,12 @@ extern "C" {
 int cqp_batch_create(cqp_batch** out, cqp_handle* h, int capacity) {
   if (!out || !h || capacity < 1) { set_error("batch_create: bad argument"); return CQP_ERR_ARGUMENT; }
   *out = nullptr;
-  int lanes = capacity >= 1024 ? 2 : 1;
+  // The round kernel keeps the SMs busy across iterations by itself (its grid drains once per round),
+  // so it runs as ONE lane; two lanes (sub-batches on their own streams filling each other's wave
+  // tails) only pay for the per-iteration kernel (CQP_BATCH_LEGACY=1).
+  int legacy = 0;
+  if (const char* e = std::getenv("CQP_BATCH_LEGACY")) legacy = std::atoi(e) ? 1 : 0;
+  int lanes = (legacy && capacity >= 1024) ? 2 : 1;
   if (const char* e = std::getenv("CQP_BATCH_LANES")) lanes = std::max(1, std::min(8, std::atoi(e)));
   if (lanes == 1) return batch_create_single(out, h, capacity);
   CQP_CUDA(cudaSetDevice(h->device));

@@ -39,7 +39,7 @@ struct RoundParams {
   int split;        // padded row where the lambda block starts (0: dense layer)
   int k_tiles, k_tiles3;
   const int* cols;  // slot -> column (-1: padding slot)
-  const TileDesc* tiles;
+  const TileDesc* tiles;  // the NON-EMPTY column tiles of BN slots: {first slot, ladder index} (BatchDev::ct)
   const int* n_tiles;
   const double* bias; int ld_bias;
   const double* lo; const double* hi; int ld_lohi;
@@ -51,6 +51,7 @@ struct RoundParams {
   int* work;        // item counter (zero at launch)
   int* done;        // [column tiles of BN slots] consumer-warp completions of this round (zero at launch)
   int* dbg;
+  int num_sms;                // CTAs beyond ceil(items per iteration / num_sms) * num_sms retire at once (see the kernel)
   int flags;                  // debug switch (CQP_ROUND_FLAGS): 1 = TMA descriptors read from global memory
   const CUtensorMap* gmaps;   // [3] copies of the descriptors in global memory: A, S0, S1
 };
@@ -94,7 +95,6 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   constexpr int NW = WM * WN;    // warps of one k-split group
   constexpr int NCW = NW * KS;   // consumer warps; warp NCW is the producer
   constexpr int TM = BM / WM, TN = BN / WN, MI = TM / 8, NI = TN / 8;
-  constexpr int SUB = SLOT_TILE / BN;
   constexpr int A_BYTES = BM * 128, STAGE_BYTES = (BM + BN) * 128;
   constexpr int PER = MI * NI * 2;
   extern __shared__ unsigned char round_smem_raw[];
@@ -109,6 +109,25 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   int* item_s = reinterpret_cast<int*>(sempty + kRoundQ);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m_tiles = p.M_pad / BM;
+  const int n_ct = __ldcg(p.n_tiles);
+  const int per_iter = n_ct * m_tiles;
+  const int total = per_iter * p.n_iters;
+  // row tiles that hold rows at all (the others are padding between the two parts of the structured
+  // layer and are skipped: they must not count as completions either, or the skipped tiles of LATER
+  // iterations, which nothing holds back, would release an iteration early)
+  int m_real = 0;
+  for (int mt = 0; mt < m_tiles; ++mt) {
+    const int m0 = mt * BM;
+    const bool blk3 = p.split > 0 && m0 >= p.split;
+    m_real += (blk3 ? m0 - p.split + p.nm : m0) < ((p.split > 0 && !blk3) ? p.nm : p.D) ? 1 : 0;
+  }
+  // Small rounds: no more CTAs than one iteration has items, rounded up to whole CTAs-per-SM layers.
+  // Surplus CTAs would only hold items of later iterations, and the items that ARE runnable would land
+  // on whatever CTAs happen to be free: several on one SM while other SMs idle (an item is bound by
+  // its SM's DMMA pipe: 12 us for a 32 x 32 tile at D = 1500).  With one layer per SM the runnable
+  // items spread evenly, as the block scheduler spreads a fresh launch.
+  if (p.num_sms > 0 && (int)blockIdx.x >= ((per_iter + p.num_sms - 1) / p.num_sms) * p.num_sms && blockIdx.x >= (unsigned)p.num_sms) return;
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
     for (int q = 0; q < kRoundQ; ++q) { mbar_init(&sfull[q], 1); mbar_init(&sempty[q], NCW); }
@@ -116,10 +135,6 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   }
   __syncthreads();
 
-  const int m_tiles = p.M_pad / BM;
-  const int n_ct = __ldcg(p.n_tiles) * SUB;
-  const int per_iter = n_ct * m_tiles;
-  const int total = per_iter * p.n_iters;
   int q = 0, qph = 0;
   unsigned stage = 0, sph = 0;
 
@@ -139,18 +154,17 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       if (item >= total) { hand_over(-1); break; }
       const int it = item / per_iter, r = item - it * per_iter;
       const int ns = r / m_tiles, mt = r - ns * m_tiles;
-      const int nt = ns / SUB, sub = ns - nt * SUB;
       TileDesc td;
-      td.slot0 = __ldcg(&p.tiles[nt].slot0);
-      td.a_index = __ldcg(&p.tiles[nt].a_index);
-      const int slot0 = td.slot0 + sub * BN;
+      td.slot0 = __ldcg(&p.tiles[ns].slot0);
+      td.a_index = __ldcg(&p.tiles[ns].a_index);
+      const int slot0 = td.slot0;
       const int m0 = mt * BM;
       const bool blk3 = p.split > 0 && m0 >= p.split;
       const int row0 = blk3 ? m0 - p.split + p.nm : m0;
       const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
-      if (row0 >= row_end || __ldcg(p.cols + slot0) < 0) { hand_over(item); continue; }  // empty item: the consumers skip it too
+      if (row0 >= row_end) { hand_over(item); continue; }  // row tile of padding only: the consumers skip it too
       if (it > 0) {
-        const int need = it * m_tiles * NW;
+        const int need = it * m_real * NW;
         long long t0 = 0;
         unsigned spins = 0;
         while (ld_acquire_gpu(p.done + ns) < need) {
@@ -196,16 +210,15 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
     if (++q == kRoundQ) { q = 0; qph ^= 1; }
     const int it = item / per_iter, r = item - it * per_iter;
     const int ns = r / m_tiles, mt = r - ns * m_tiles;
-    const int nt = ns / SUB, sub = ns - nt * SUB;
     TileDesc td;
-      td.slot0 = __ldcg(&p.tiles[nt].slot0);
-      td.a_index = __ldcg(&p.tiles[nt].a_index);
-    const int slot0 = td.slot0 + sub * BN;
+    td.slot0 = __ldcg(&p.tiles[ns].slot0);
+    td.a_index = __ldcg(&p.tiles[ns].a_index);
+    const int slot0 = td.slot0;
     const int m0 = mt * BM;
     const bool blk3 = p.split > 0 && m0 >= p.split;
     const int row0 = blk3 ? m0 - p.split + p.nm : m0;
     const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
-    if (!(row0 >= row_end || __ldcg(p.cols + slot0) < 0)) {
+    if (row0 < row_end) {
       const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
       const double* Sin = p.S[(p.first ^ it) & 1];
       double* Sout = p.S[(p.first ^ it ^ 1) & 1];
@@ -330,9 +343,9 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       // reduction barrier, whose shared-memory stores carry the accumulators (groups > 0)
       if (held >= 0 && lane == 0) mbar_arrive(&empty[held]);
     }
-    // one completion per consumer warp of group 0 (empty items count too: the producer of the next
-    // iteration waits for m_tiles * NW of them per column tile)
-    if (kg == 0) {
+    // one completion per consumer warp of group 0: the producer of the next iteration waits for
+    // m_real * NW of them per column tile
+    if (kg == 0 && row0 < row_end) {
       __syncwarp();
       if (lane == 0) {
         __threadfence();

@@ -1,10 +1,3 @@
-export AB_BRIEF=1 AB_REPS=1
-echo "### B=48 iters=400 cfg4 x2 / cfg5 vs legacy cfg4"
-AB_MAX_ITERS=400 timeout 900 python tools/ab_batch.py 48 "CQP_BATCH_LEGACY=1 CQP_BATCH_FORCE_CFG=4" "CQP_BATCH_FORCE_CFG=4" "CQP_BATCH_FORCE_CFG=4" "CQP_BATCH_FORCE_CFG=5" | grep -v "^{"
-echo "### 2 lanes B=4096 iters=100 cfg3 x6 cfg2 x2"
-AB_MAX_ITERS=100 timeout 900 python tools/ab_batch.py 4096 "CQP_BATCH_LEGACY=1 CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=2" "CQP_BATCH_FORCE_CFG=2" | grep -v "^{"
-echo "### full solve: legacy 2 lanes | new 2 lanes x2 | new 1 lane x2"
-timeout 900 python tools/ab_batch.py 4096 "CQP_BATCH_LEGACY=1" "" "" "CQP_BATCH_LANES=1" "CQP_BATCH_LANES=1"
-echo "### full solve B=512, B=64"
-timeout 900 python tools/ab_batch.py 512 "CQP_BATCH_LEGACY=1" "" ""
-timeout 900 python tools/ab_batch.py 64 "CQP_BATCH_LEGACY=1" "" ""
+export AB_BRIEF=1 AB_REPS=1 AB_NU=10
+echo "### nu=10 B=200 full solve"
+timeout 900 python tools/ab_batch.py 200 "CQP_BATCH_LEGACY=1" "" "CQP_BATCH_FORCE_CFG=3" "CQP_BATCH_FORCE_CFG=7" "CQP_BATCH_FORCE_CFG=4" | grep -E "^==|compute_ms|vs first"
