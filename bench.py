@@ -17,7 +17,8 @@ Run without torchrun, `--gpus N` spawns the N ranks itself.
   e2e    = QPs/s through the C-ABI call cqp_batch_solve with HOST buffers: host->device copy of
            (g, c, d), the solve, device->host copy of (y, z, lambda, status, ...) all inside the
            timed region
-  roofline = the iteration GEMM (dmma_gemm_kernel): EXECUTED flop per active column per iteration
+  roofline = the iteration kernel (round_kernel: one persistent launch per check round, TMA-staged
+           operands, FP64 DMMA): EXECUTED flop per active column per iteration
            (2 ((n+m) D + m n): the zero blocks (3,2), (3,3) of W are skipped, so less than the
            dense 2 D^2) / CUDA-event time of those launches, against the FP64 GEMM rate cuBLAS
            reaches on this GPU measured in the same run (MEASURED_PEAKS.json has no FP64 entry)
@@ -495,13 +496,14 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         "clocks": clocks,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
                      "frac": achieved / dgemm_peak, "traffic": traffic,
-                     "kernel": "dmma_gemm_kernel (iteration GEMM, FP64 DMMA.8x8x4)",
+                     "kernel": "round_kernel (persistent launch = one check round of 25 ADMM layers of every active column; operands staged by TMA cp.async.bulk.tensor, FP64 DMMA.8x8x4)",
+                     "frac_of_whole_step": (gemm_fl_all / world / (comp_ms_max * 1e-3) / 1e12 / dgemm_peak) if comp_ms_max else None,
                      "algorithmic": f"executed 2*((n+m)*D + m*n) + 4*m = {flop_col} flop per active column per iteration (the zero blocks (3,2), (3,3) of W are skipped; dense W would be 2*D^2 = {2 * D * D}); {gemm_fl_all:.4g} flop in {gemm_ms_max:.1f} ms over {args.steps} steps" + (f" on each of {world} GPUs (per-GPU rate)" if world > 1 else ""),
                      "dense_equivalent_tflops": dense_equiv,
                      "peak_source": "cuBLAS DGEMM 8192^3 via torch.matmul, best of 5, measured in this run (no FP64 entry in MEASURED_PEAKS.json)",
                      "peak_theoretical": f"148 SMs x 64 FP64 FMA/clk x 2 x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz = {148 * 64 * 2 * peaks.get('sm_max_mhz', 1965.0) * 1e-6:.1f} TFLOP/s",
                      "gemm_share_of_step": gemm_ms_max / comp_ms_max if comp_ms_max else None,
-                     "timing": "a batch of >= 1024 columns runs as two concurrent lanes (sub-batches on their own streams); the GEMM time is the length of the UNION of both lanes' GEMM phases (CUDA events on each lane's stream, common time base), so the other lane's small kernels that overlap a GEMM phase are inside it"},
+                     "timing": "achieved = executed flop of all round_kernel launches / the sum of their durations (CUDA events around every launch on the solve's stream); frac_of_whole_step divides the same flop by the whole device-timed step (check rounds, re-bucketing and setup included)"},
         "cpu_baseline": {"value": cpu_qps, "unit": "QP/s", "cores": cores, "kind": "port",
                          "sample": f"{sample} of the {BATCH} instances ({sample // cores} per core), one oracle Solver per thread (-O3 -DNDEBUG build = the reference's flags)",
                          "iteration_counts_match_gpu": parity_ok,

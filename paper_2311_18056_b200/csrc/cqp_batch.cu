@@ -3,26 +3,28 @@
 // calls (/root/reference/proj/src/solver.cpp:158-166 -> run_loop :43-105), one per column.
 //
 // Design:
-//   * The iterates are the columns of S (D x B, each column contiguous); one batch iteration is
-//     the dense contraction  S <- clamp(W_k S + Bias_k, lo, hi)  evaluated with FP64 tensor
-//     cores (mma.sync m8n8k4 f64 = DMMA.8x8x4, the only FP64 tensor shape sm_100a has; tcgen05
-//     has no f64 kind).  64x64 / 64x32 / 32x32 x16 CTA tiles (by active-column count), operands
-//     staged in shared memory by a 4-stage cp.async pipeline in a 16-byte-chunk XOR swizzle (conflict-free 8-byte
-//     fragment loads), bias + clamp fused into the epilogue.
-//   * Every QP adapts rho on its own (parity demands it), so columns are bucketed by ladder
-//     index: a slot map lists, per 128-column tile, which columns it holds and which W_k it
-//     multiplies (a grouped GEMM).  Tiles gather their columns through the map, so re-bucketing
-//     never moves S.
-//   * Every check_interval iterations: unscale, three more DMMA GEMMs (H Y, G' Lambda, G Y) on
-//     the active columns, a per-column reduction/decision kernel (residuals, rho rule, early
-//     exit, finalisation of converged columns), re-bucketing and the bias GEMM
+//   * The iterates are the columns of S (one column = D contiguous doubles), stored in SLOT order:
+//     every QP adapts rho on its own (parity demands it), so the active columns are bucketed by ladder
+//     index, every bucket padded to 128 slots, and S is physically compacted into that order at every
+//     re-bucketing (batch_permute_kernel: one copy per check round).  A column tile is then a
+//     contiguous 2-D box and multiplies ONE W_k: a grouped GEMM.
+//   * One persistent launch per check round (round_kernel, cqp_batch_round.cuh) runs all
+//     check_interval layers  S <- clamp(W_k S + Bias_k, lo, hi)  of the round: operands staged by TMA
+//     (cp.async.bulk.tensor.2d with the hardware 128-byte swizzle, completion on mbarriers, a producer
+//     warp), FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA.8x8x4, the only FP64 tensor shape of
+//     sm_100a; tcgen05 has no f64 kind), bias folded into the accumulator start, clamp fused into
+//     the epilogue, and dataflow dependencies between the iterations of a column tile instead of a
+//     launch per iteration.  The per-iteration cp.async kernel below (dmma_gemm_kernel) stays for the
+//     plain GEMMs of a check round and the offline stage, and as the A/B reference
+//     (CQP_BATCH_LEGACY=1; tests/test_gpu_batch.py::test_round_kernel_matches_per_iteration_kernel).
+//   * Every check_interval iterations: unscale, three DMMA GEMMs (H Y, G' Lambda, G Y) on the active
+//     columns, a per-column reduction/decision kernel (residuals, rho rule, early exit, finalisation
+//     of converged columns), re-bucketing + compaction and the bias GEMM
 //     Bias = -[D_k; G D_k] G_s.  Converged columns leave the slot map, so they stop costing work.
 //   * No host round trip inside a round; the host only polls a pinned "active columns" word with
-//     a lag of two rounds to know when to stop enqueuing.
+//     a lag of two rounds to know when to stop enqueuing and which tile shape the next round gets.
 //   * Structured layer: the lambda rows of W, [rho G, -diag(rho), I] (layers.cpp:159-161), only
-//     multiply y: their tiles run ceil(n / 16) k-tiles and start from fma(-rho_i, z_i, lambda_i)
-//     (GemmParams::split).  Batches of >= 1024 columns run as two concurrent lanes (sub-batches on
-//     their own streams, one host thread each), whose launches fill each other's wave tails.
+//     multiply y: their tiles run ceil(n / 16) k-tiles and start from fma(-rho_i, z_i, lambda_i).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

@@ -270,3 +270,49 @@ def test_batch_traces_and_histories_match_single_solver(G, oracle, P):
         batch.close(); batch.solve(g, c, d)
     assert out["y"].flags.owndata or out["y"].base is not None
     single.close()
+
+
+@pytest.mark.parametrize("nu,B", [(10, 200), (20, 333)])
+def test_round_kernel_matches_per_iteration_kernel(G, P, monkeypatch, nu, B):
+    """The persistent TMA round kernel (one launch per check round, dataflow dependencies between the
+    iterations of a column tile, cqp_batch_round.cuh) against the per-iteration cp.async kernel
+    (CQP_BATCH_LEGACY=1) on the same slot-ordered iterate, for EVERY tile configuration of the round
+    kernel.  The per-element summation order (k-tiles, then k-steps, ascending) is the same in both
+    kernels unless warp groups split k, so: bit-identical results for the plain configurations, and
+    counts / statuses / final indices / switch counts identical with values equal to rounding for
+    the k-split ones.  nu = 10 has n + m = 200: 32-row tiles leave a row tile of padding only between
+    the two parts of the structured layer (the skipped tile must not count as a completion)."""
+    wl = P.config2(nu, seed=5)
+    base = wl.base_problem()
+    g, c, d, _ = P.batch_instances(wl, B, lo=0.3, hi=10.0)
+
+    def run(env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        single = G.Solver(base.H, base.g, base.G, base.c, base.d)
+        batch = G.BatchSolver(single, capacity=B)
+        out = {k: np.array(v, copy=True) if isinstance(v, np.ndarray) else v for k, v in batch.solve(g, c, d).items()}
+        out["traces"] = batch.traces()
+        batch.close(); single.close()
+        for k in env:
+            monkeypatch.delenv(k, raising=False)
+        return out
+
+    ref = run({"CQP_BATCH_LEGACY": "1", "CQP_BATCH_FORCE_CFG": "3"})
+    assert len(set(ref["iterations"].tolist())) > 3 and ref["n_switches"].max() >= 1
+    assert ref["launches"] > 25 * ref["rounds"]                       # one launch per iteration
+    ksplit = {4, 5, 7, 8}
+    for cfg in range(1, 10):
+        out = run({"CQP_BATCH_FORCE_CFG": str(cfg)})
+        assert out["launches"] < 16 * out["rounds"], cfg              # one launch per ROUND
+        for key in ("iterations", "status", "final_index", "n_switches"):
+            assert np.array_equal(ref[key], out[key]), (cfg, key)
+        assert ref["traces"] == out["traces"], cfg
+        for key in ("y", "z", "lam"):
+            if cfg in ksplit:
+                assert rel_err(out[key], ref[key]) <= 1e-9, (cfg, key)
+            else:
+                assert np.array_equal(out[key], ref[key]), (cfg, key)
+    out = run({})                                                      # the default plan
+    for key in ("iterations", "status", "final_index", "n_switches"):
+        assert np.array_equal(ref[key], out[key]), key
