@@ -170,6 +170,24 @@ CQP_API int cqp_mpc_set_template(cqp_handle *h, int nx, int nu, const double *of
  * all on the device.  u0 (nu) and out may be NULL. */
 CQP_API int cqp_mpc_step_x0(cqp_handle *h, const double *x0, int k, double *u0, cqp_result *out);
 
+/* Resident control-step server for the closed loop of bench.cpp:157-185 (the reference calls
+ * instantiate / update_vectors / refresh_z / fixed_iters(k) once per control step; at kHz rates the
+ * GPU port of that loop is bound by launch and synchronisation overhead, not by the step itself).
+ * cqp_mpc_server_start launches ONE persistent kernel that keeps W_k, the scaling vectors and the
+ * residual rows on the SMs and serves steps from a host-mapped mailbox; while it is enabled,
+ * cqp_mpc_step_x0(h, x0, k, ...) posts x0 there and spins on the answer: no CUDA call per step, results
+ * bit-identical to the launch-per-step path.  The kernel leaves by itself when idle for
+ * idle_timeout_ms (<= 0: 100 ms) -- the next step restarts it -- and every other entry point of the
+ * handle retires it first, so the API keeps its meaning; it occupies the SMs it runs on (one 16-CTA
+ * cluster for small QPs, every SM otherwise) while it is resident.  nx <= 128. */
+CQP_API int cqp_mpc_server_start(cqp_handle *h, int k, double idle_timeout_ms);
+CQP_API int cqp_mpc_server_stop(cqp_handle *h);
+/* Last step served by the resident kernel: wall time inside cqp_mpc_step_x0 and the device-side
+ * duration (request seen -> answer written), both in microseconds.  With out == NULL the step
+ * returns u0 only and skips the final residual evaluation of solver.cpp:94-95 (its results would not
+ * be observable); the iterate and u0 are the same bits either way. */
+CQP_API int cqp_mpc_server_last_timing(const cqp_handle *h, double *wall_us, double *device_us);
+
 /* Solver::state() / layer_index(), solver.hpp:126-127: v (n+2m, cache space) and the index. */
 CQP_API int cqp_get_state(cqp_handle *h, double *v, int *layer_index);
 

@@ -1436,6 +1436,9 @@ int cqp_batch_solve(cqp_batch* b, int B, const double* g_cols, const double* c_c
                     double* r_dual, int* n_switches, double* device_ms) {
   if (!b || !g_cols || !c_cols || !d_cols) { set_error("batch_solve: null argument"); return CQP_ERR_ARGUMENT; }
   if (B < 1 || B > b->capacity) { set_error("batch_solve: B exceeds the batch capacity"); return CQP_ERR_CAPACITY; }
+  if (b->h->srv_running) {  // a resident MPC kernel owns the SMs: retire it first
+    if (int rc = server_stop(b->h)) return rc;
+  }
   if (b->lanes.empty())
     return batch_solve_single(b, B, g_cols, c_cols, d_cols, y_cols, z_cols, lambda_cols, status, iterations,
                               final_index, r_prim, r_dual, n_switches, device_ms, nullptr);

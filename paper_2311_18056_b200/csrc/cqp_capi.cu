@@ -1,6 +1,7 @@
 // C ABI of libcqp_b200.so (include/cqp_b200.h): handle management, uploads, result download.
 // Mirrors the reference's Solver lifecycle (/root/reference/proj/src/solver.cpp:180-218).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -158,6 +159,112 @@ int upload_vectors(cqp_handle* h, const double* g, const double* c, const double
   return CQP_OK;
 }
 
+// ---- resident MPC server (cqp_mpc_server_start) ------------------------------------------------
+// One persistent kernel keeps W (registers / shared memory), the scaling vectors and the residual
+// rows on the SMs and serves control steps from a host-mapped mailbox: the host writes x0 and a
+// request number, the kernel instantiates, refreshes z, iterates, extracts u0, writes the result
+// record (host-mapped) and answers with the request number.  No CUDA call on the per-step path.
+// The kernel leaves by itself when told to stop or when idle for srv_idle_ns (a crashed host never
+// leaves a spinning kernel behind); the next step relaunches it.
+int server_stop(cqp_handle* h) {
+  if (!h->srv_running) return CQP_OK;
+  reinterpret_cast<volatile unsigned long long*>(h->mb_host)[kMbStop] = 1ull;
+  const cudaError_t e = cudaStreamSynchronize(h->stream);
+  h->srv_running = false;
+  if (e != cudaSuccess) return cuda_fail(e, "mpc server kernel");
+  return CQP_OK;
+}
+
+static int server_launch_from(cqp_handle* h, int k, unsigned long long served) {
+  int rc = server_stop(h);
+  if (rc) return rc;
+  if (!h->mb_host) {
+    CQP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h->mb_host), sizeof(unsigned long long) * kMbWords, cudaHostAllocMapped));
+    CQP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->mb_dev), h->mb_host, 0));
+    std::memset(h->mb_host, 0, sizeof(unsigned long long) * kMbWords);
+    if ((rc = dev_alloc(&h->srv_seq, 1))) return rc;
+  }
+  if ((rc = ensure_result_capacity(h, k / h->s.check_interval + 2))) return rc;
+  volatile unsigned long long* mb = h->mb_host;
+  mb[kMbStop] = 0ull; mb[kMbExited] = 0ull;
+  if (served == h->srv_req) { mb[kMbReq] = served; mb[kMbResp] = served; }  // (else a request is pending: keep it)
+  CQP_CUDA(cudaMemcpyAsync(h->srv_seq, &served, sizeof(unsigned long long), cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaStreamSynchronize(h->stream));  // (pageable source)
+  h->srv_k = k;
+  h->srv_running = true;
+  h->mpc_extract = true;
+  h->vectors_device_only = true;
+  const unsigned long long newest = h->srv_req;
+  h->srv_req = served;  // (launch_run hands RunParams::served = srv_req to the kernel)
+  rc = launch_run(h, false, k, true);
+  h->srv_req = newest;
+  h->mpc_extract = false;
+  if (rc) { h->srv_running = false; return rc; }
+  return CQP_OK;
+}
+
+int server_launch(cqp_handle* h, int k) { return server_launch_from(h, k, h->srv_req); }
+
+// One control step through the resident kernel: post x0, wait for the answer, read the record.
+static int server_step(cqp_handle* h, const double* x0, int k, double* u0, cqp_result* out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  if (h->srv_running && h->srv_k != k && (rc = server_stop(h))) return rc;
+  if (h->srv_running && h->mb_host[kMbExited] != 0ull && (rc = server_stop(h))) return rc;  // idle timeout
+  if (!h->srv_running && (rc = server_launch(h, k))) return rc;
+  volatile unsigned long long* mb = h->mb_host;
+  std::memcpy(h->mb_host + kMbX0, x0, sizeof(double) * h->mpc_nx);
+  mb[kMbWantFull] = (out && (out->y || out->z || out->lambda)) ? 1ull : 0ull;
+  std::atomic_thread_fence(std::memory_order_release);
+  const unsigned long long seq = ++h->srv_req;
+  mb[kMbReq] = seq;
+  unsigned spins = 0;
+  while (mb[kMbResp] != seq) {
+    if ((++spins & 0x3FF) != 0) continue;
+    if (mb[kMbExited] != 0ull) {
+      // the kernel left its loop (idle timeout) around the time this request was posted
+      if ((rc = server_stop(h))) return rc;
+      if (mb[kMbResp] == seq) break;                        // it had answered before leaving
+      if ((rc = server_launch_from(h, k, seq - 1))) return rc;  // run it again: it finds the request
+    } else if ((spins & 0xFFFFF) == 0) {
+      const cudaError_t q = cudaStreamQuery(h->stream);
+      if (q != cudaErrorNotReady && mb[kMbResp] != seq && mb[kMbExited] == 0ull) {
+        // the kernel is gone without an answer and without the exit mark: a fault (watchdog trap)
+        h->srv_running = false;
+        const int* d = h->dbg_host;
+        set_error(std::string("mpc server kernel failed: ") + cudaGetErrorString(q) +
+                  (d && d[0] ? " (watchdog: where=" + std::to_string(d[1]) + " iter=" + std::to_string(d[2]) + ")" : std::string()));
+        return CQP_ERR_CUDA;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  h->srv_last_device_us = 1e-3 * (double)mb[kMbStepNs];
+  const unsigned char* base = static_cast<const unsigned char*>(h->hres);
+  const DevResultHead* head = reinterpret_cast<const DevResultHead*>(base);
+  const int cap = h->res_cap;
+  size_t off = sizeof(DevResultHead) + sizeof(int) * 4 * (size_t)cap + sizeof(double) * 2 * (size_t)cap;
+  const double* y = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->n;
+  const double* z = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  const double* lam = reinterpret_cast<const double*>(base + off); off += sizeof(double) * (size_t)h->m;
+  if (u0) std::memcpy(u0, base + off, sizeof(double) * (size_t)h->mpc_nu);
+  if (out) {
+    out->status = head->status; out->iterations = head->iterations;
+    out->r_prim = head->r_prim; out->r_dual = head->r_dual;
+    if (out->y) std::memcpy(out->y, y, sizeof(double) * h->n);
+    if (out->z) std::memcpy(out->z, z, sizeof(double) * h->m);
+    if (out->lambda) std::memcpy(out->lambda, lam, sizeof(double) * h->m);
+    out->rho_trace_len = head->n_trace; out->history_len = head->n_hist;
+    const int* trace = reinterpret_cast<const int*>(base + sizeof(DevResultHead));
+    if (out->rho_trace)
+      for (int i = 0; i < std::min(std::min(head->n_trace, out->rho_trace_cap), cap); ++i) out->rho_trace[i] = {trace[2 * i], trace[2 * i + 1]};
+    out->kernel_us = h->srv_last_device_us;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  h->srv_last_wall_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  return CQP_OK;
+}
+
 int cold_start(cqp_handle* h) {
   // ring invariant between launches: slot 0 = iterate (zero), slots 1..3 = sentinel (all ones)
   CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
@@ -280,9 +387,21 @@ int cqp_create_from_layers(cqp_handle** out, int n, int m, int L, const double* 
   return CQP_OK;
 }
 
+// Every entry point that touches the handle's state or stream first retires the resident MPC kernel
+// (it owns the SMs and the iterate while it runs).
+#define CQP_QUIESCE(h)                                  \
+  do {                                                  \
+    if ((h)->srv_running) {                             \
+      if (int rc__ = ::cqp::server_stop(h)) return rc__; \
+    }                                                   \
+  } while (0)
+
 void cqp_destroy(cqp_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  server_stop(h);
+  if (h->mb_host) cudaFreeHost(h->mb_host);
+  cudaFree(h->srv_seq);
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->W); cudaFree(h->Wt); cudaFree(h->Dk); cudaFree(h->H); cudaFree(h->Gr); cudaFree(h->Gt);
   cudaFree(h->Gs); cudaFree(h->E); cudaFree(h->F); cudaFree(h->dgrid); cudaFree(h->dlog_grid);
@@ -303,12 +422,14 @@ void cqp_destroy(cqp_handle* h) {
 int cqp_update_vectors(cqp_handle* h, const double* g, const double* c, const double* d) {
   if (!h || !g || !c || !d) { set_error("update_vectors: null argument"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   return upload_vectors(h, g, c, d);
 }
 
 int cqp_cold_start(cqp_handle* h) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   return cold_start(h);
 }
 
@@ -316,6 +437,7 @@ int cqp_warm_start(cqp_handle* h, const double* y, const double* lambda, int lay
   if (!h || !y || !lambda) { set_error("warm_start: null argument"); return CQP_ERR_ARGUMENT; }
   if (layer_index >= h->L) { set_error("warm_start: layer index out of range"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   const int n = h->n, m = h->m;
   CQP_CUDA(cudaStreamSynchronize(h->stream));  // hstage may still feed an update_vectors copy
   double* hs = h->hstage;
@@ -332,6 +454,7 @@ int cqp_warm_start(cqp_handle* h, const double* y, const double* lambda, int lay
 int cqp_refresh_z(cqp_handle* h) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   // Same device code as the fused step's prologue (run kernel, zero iterations), so that
   // update_vectors + refresh_z + fixed_iters(k) and cqp_mpc_step agree bit for bit.
   return launch_run(h, false, 0, true);
@@ -397,6 +520,7 @@ static int run_and_fetch(cqp_handle* h, bool early_exit, int total, bool refresh
 int cqp_solve(cqp_handle* h, cqp_result* out) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   return run_and_fetch(h, true, h->s.max_iters, false, out);
 }
 
@@ -404,6 +528,7 @@ int cqp_fixed_iters(cqp_handle* h, int k, cqp_result* out) {
   if (!h) return CQP_ERR_ARGUMENT;
   if (k < 1) { set_error("fixed_iters: k must be >= 1"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   return run_and_fetch(h, false, k, false, out);
 }
 
@@ -412,6 +537,7 @@ int cqp_mpc_step(cqp_handle* h, const double* g, const double* c, const double* 
   if (!h || !g || !c || !d) { set_error("mpc_step: null argument"); return CQP_ERR_ARGUMENT; }
   if (k < 1) { set_error("mpc_step: k must be >= 1"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   const auto t0 = std::chrono::steady_clock::now();  // wall_ms of a fused step includes the upload
   int rc = upload_vectors(h, g, c, d);
   if (rc) return rc;
@@ -427,6 +553,7 @@ int cqp_mpc_set_template(cqp_handle* h, int nx, int nu, const double* offset_g, 
   }
   if (nx < 1 || nu < 1 || nu > h->n) { set_error("mpc_set_template: bad dimensions"); return CQP_ERR_DIMENSION; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   CQP_CUDA(cudaStreamSynchronize(h->stream));
   const int n = h->n, m = h->m;
   cudaFree(h->mpc_og); cudaFree(h->mpc_oc); cudaFree(h->mpc_cb); cudaFree(h->mpc_db);
@@ -466,6 +593,7 @@ int cqp_mpc_step_x0(cqp_handle* h, const double* x0, int k, double* u0, cqp_resu
   if (!h->mpc_og) { set_error("mpc_step_x0: no template (call cqp_mpc_set_template first)"); return CQP_ERR_ARGUMENT; }
   if (k < 1) { set_error("mpc_step_x0: k must be >= 1"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  if (h->srv_enabled && h->mpc_nx <= kMaxInlineX0) return server_step(h, x0, k, u0, out);
   const auto t0 = std::chrono::steady_clock::now();
   int rc = launch_instantiate(h, x0);
   if (rc) return rc;
@@ -476,9 +604,35 @@ int cqp_mpc_step_x0(cqp_handle* h, const double* x0, int k, double* u0, cqp_resu
   return rc;
 }
 
+int cqp_mpc_server_start(cqp_handle* h, int k, double idle_timeout_ms) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  if (!h->mpc_og) { set_error("mpc_server_start: no template (call cqp_mpc_set_template first)"); return CQP_ERR_ARGUMENT; }
+  if (k < 1) { set_error("mpc_server_start: k must be >= 1"); return CQP_ERR_ARGUMENT; }
+  if (h->mpc_nx > kMaxInlineX0) { set_error("mpc_server_start: nx exceeds the mailbox (128 states)"); return CQP_ERR_CAPACITY; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  h->srv_idle_ns = (long long)((idle_timeout_ms > 0.0 ? idle_timeout_ms : 100.0) * 1e6);
+  h->srv_enabled = true;
+  return server_launch(h, k);
+}
+
+int cqp_mpc_server_last_timing(const cqp_handle* h, double* wall_us, double* device_us) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  if (wall_us) *wall_us = h->srv_last_wall_us;
+  if (device_us) *device_us = h->srv_last_device_us;
+  return CQP_OK;
+}
+
+int cqp_mpc_server_stop(cqp_handle* h) {
+  if (!h) return CQP_ERR_ARGUMENT;
+  CQP_CUDA(cudaSetDevice(h->device));
+  h->srv_enabled = false;
+  return server_stop(h);
+}
+
 int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
   if (!h) return CQP_ERR_ARGUMENT;
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   int st[1];
   CQP_CUDA(cudaMemcpyAsync(st, h->state, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
   CQP_CUDA(cudaStreamSynchronize(h->stream));
@@ -495,6 +649,7 @@ int cqp_get_layer(cqp_handle* h, int k, double* W, double* Dk, double* GDk, doub
                   double* rho_vec) {
   if (!h || k < 0 || k >= h->L) { set_error("get_layer: bad index"); return CQP_ERR_ARGUMENT; }
   CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
   const int n = h->n, m = h->m, D = h->D;
   const size_t nm = (size_t)n + m;
   double* scratch = nullptr;
@@ -534,6 +689,7 @@ int cqp_get_scaling(cqp_handle* h, double* E, double* F, double* cost_scale, dou
   const int n = h->n, m = h->m;
   if (h->vectors_device_only && (c_tilde || d_tilde)) {  // c, d came from the device-side instantiate
     CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
     h->c_host.resize(m); h->d_host.resize(m);
     CQP_CUDA(cudaMemcpyAsync(h->c_host.data(), h->c, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));
     CQP_CUDA(cudaMemcpyAsync(h->d_host.data(), h->d, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream));

@@ -195,10 +195,10 @@ __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& 
 // Makes layer k current: W slice -> shared memory, bias rows b = -[D_k; G D_k] g_s for the rows
 // this CTA owns, 0 on the lambda rows (layers.cpp:168-175).  s.uy is scratch for
 // g_s = cost_scale * E o g (layers.cpp:181).
-__device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int row0, int nrows) {
+__device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int row0, int nrows, bool copy_w = true) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   __syncthreads();
-  if (p.w_smem) {
+  if (p.w_smem && copy_w) {
     const double2* src = reinterpret_cast<const double2*>(p.W + ((size_t)k * p.D + row0) * p.Dpad);
     double2* dst = reinterpret_cast<double2*>(s.sW);
     const int count = nrows * (p.Dpad >> 1);
@@ -243,7 +243,7 @@ __device__ void cl_residual_pass(const RunParams& p, const ClSmem& s, const doub
     if (i < m) {
       z = xs[n + i] / s.sF[i];
       if (final) {  // solver.cpp:94  z = clamp(z, p.c, p.d) in original units
-        const double lo = p.c[i], hi = p.d[i];
+        const double lo = __ldcg(p.c + i), hi = __ldcg(p.d + i);  // (rewritten by every server step: not through L1)
         z = z < lo ? lo : z;
         z = z > hi ? hi : z;
       }
@@ -331,23 +331,12 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   const int n = p.n, m = p.m, D = p.D;
   const unsigned xbytes = 8u * (unsigned)D;
   CQP_STAMP0(p.dbg, 0);
-  if (t == 0) {
-    for (int k = 0; k < 4; ++k) mbar_init(&s.bars[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arm(&xready[0], xbytes);  // first use: v_2
-    mbar_arm(&xready[1], xbytes);  // first use: v_1
-    mbar_arm(&nbar[0], 7u * 8u * (unsigned)C);
-    mbar_arm(&nbar[1], 7u * 8u * (unsigned)C);
-  }
   // balanced row split: every CTA owns >= 1 row (D >= C), at most p.R = ceil(D / C)
   const int row0 = (int)(((long long)rank * D) / C);
   const int nrows = (int)(((long long)(rank + 1) * D) / C) - row0;
   int layer = p.state[0];
 
-  for (int i = t; i < p.npad; i += kClThreads) {
-    s.sE[i] = (i < n) ? p.E[i] : 1.0;
-    s.sg[i] = (i < n) ? p.g[i] : 0.0;
-  }
+  for (int i = t; i < p.npad; i += kClThreads) s.sE[i] = (i < n) ? p.E[i] : 1.0;
   for (int i = t; i < p.mpad; i += kClThreads) s.sF[i] = (i < m) ? p.F[i] : 1.0;
   const bool grid_smem = p.L <= 16;
   if (grid_smem && t < p.L) {
@@ -371,24 +360,6 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     copy_async(s.sG, p.Gr + (size_t)g0 * p.npad, cm * p.npad);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __syncthreads();
-  // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
-  // (layers.cpp:182-186, 223-226)
-  for (int r = t; r < nrows; r += kClThreads) {
-    const int row = row0 + r;
-    double lo = -INFINITY, hi = INFINITY;
-    if (row >= n && row < n + m) {
-      lo = s.sF[row - n] * p.c[row - n];
-      hi = s.sF[row - n] * p.d[row - n];
-    }
-    s.slo[r] = lo;
-    s.shi[r] = hi;
-  }
-  __syncthreads();
-  CQP_STAMP0(p.dbg, 1);
-  // (No cluster barrier here: nobody pushes into a peer before the barrier that follows the v_0
-  // load below, and that one also orders every peer's mbarrier initialisation before the pushes.)
-  CQP_STAMP0(p.dbg, 2);
 
   // ---- work split inside the CTA ----
   const int nc2 = p.Dpad >> 1;
@@ -427,6 +398,72 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
 
   load_registers(layer);  // (global loads into registers: their latency overlaps refresh_z and the bias rows)
 
+  // Resident MPC server (p.server): everything above is loaded ONCE; the loop below is one control
+  // step per request { x0 from the mailbox -> instantiate -> refresh_z -> total_iters layers -> final
+  // pass -> answer }.  W stays in registers / shared memory between steps.  A plain launch runs the
+  // body once.
+  unsigned long long served = p.served;
+  int resident_layer = -1;  // ladder level whose W slice is in shared memory (shared-memory mode)
+  // (two spare words of the barrier block: the kernel may not own static shared memory, its dynamic
+  // allocation is the full 227 KB)
+  unsigned long long& cmd_s = s.bars[4];
+  unsigned long long& want_full_s = s.bars[5];
+  for (;;) {
+  unsigned long long req = 0;
+  long long t_step = 0;
+  if (p.server) {
+    if (warp == 0) {
+      int want = 1;
+      const unsigned long long r = (rank == 0) ? server_fetch_request(p, served, lane, want)
+                                               : (lane == 0 ? server_wait_relay(p, served, want) : 0ull);
+      if (lane == 0) { cmd_s = r; want_full_s = (unsigned long long)want; }
+    }
+    __syncthreads();
+    req = cmd_s;
+    if (req == kSrvExit) break;
+    t_step = globaltimer_ns();
+    // mpc::instantiate (mpc.cpp:260-270): this CTA's share of the rows of [g; c; d]
+    const int rows = n + m, per = (rows + C - 1) / C;
+    const int r0 = (int)rank * per, r1 = min(rows, r0 + per);
+    for (int row = r0 + warp; row < r1; row += kClWarps)
+      instantiate_row(row, lane, p.mpc_og, p.mpc_oc, p.mpc_cb, p.mpc_db, p.mpc_x0, n, p.mpc_nx, p.mpc_nxpad, p.g_w, p.c_w, p.d_w);
+    __threadfence();
+  }
+  // (re-)initialise the mbarriers of this step: no peer pushes into this CTA between its final residual
+  // pass of the previous step and the cluster barrier below
+  if (t == 0) {
+    if (served != p.served) for (int k = 0; k < 4; ++k) mbar_inval(&s.bars[k]);  // (not the first step)
+    for (int k = 0; k < 4; ++k) mbar_init(&s.bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(&xready[0], xbytes);  // first use: v_2
+    mbar_arm(&xready[1], xbytes);  // first use: v_1
+    mbar_arm(&nbar[0], 7u * 8u * (unsigned)C);
+    mbar_arm(&nbar[1], 7u * 8u * (unsigned)C);
+  }
+  if (p.server) {
+    __syncthreads();
+    cluster_sync_all();  // every CTA's rows of g, c, d are visible
+  }
+  for (int i = t; i < p.npad; i += kClThreads) s.sg[i] = (i < n) ? __ldcg(p.g + i) : 0.0;
+  __syncthreads();
+  // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
+  // (layers.cpp:182-186, 223-226)
+  for (int r = t; r < nrows; r += kClThreads) {
+    const int row = row0 + r;
+    double lo = -INFINITY, hi = INFINITY;
+    if (row >= n && row < n + m) {
+      lo = s.sF[row - n] * __ldcg(p.c + row - n);
+      hi = s.sF[row - n] * __ldcg(p.d + row - n);
+    }
+    s.slo[r] = lo;
+    s.shi[r] = hi;
+  }
+  __syncthreads();
+  CQP_STAMP0(p.dbg, 1);
+  // (No cluster barrier here: nobody pushes into a peer before the barrier that follows the v_0
+  // load below, and that one also orders every peer's mbarrier initialisation before the pushes.)
+  CQP_STAMP0(p.dbg, 2);
+
   // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in p.vq (slot 0)
   if (p.do_refresh) {
     for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? __ldcg(p.vq + i) : 0.0;
@@ -443,7 +480,8 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   }
 
   CQP_STAMP0(p.dbg, 3);
-  cl_load_layer(p, s, layer, row0, nrows);
+  cl_load_layer(p, s, layer, row0, nrows, resident_layer != layer);  // (bias rows; the W slice only when it changed)
+  resident_layer = layer;
   CQP_STAMP0(p.dbg, 4);
 
   // v_0 -> xs[0]; pad slots of both copies stay zero for the whole launch
@@ -608,6 +646,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
         }
         ++n_trace;
         cl_load_layer(p, s, layer, row0, nrows);
+        resident_layer = layer;
         load_registers(layer);
       }
     }
@@ -623,20 +662,34 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   const int bf = iters_done & 1;
   if (iters_done >= 1 && have != iters_done)
     mbar_wait_cluster(&xready[bf], ((iters_done - 1) >> 1) & 1, p.dbg, 3, iters_done);
-  double nrm[7];
+  double nrm[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double* xfinal = s.xs + (size_t)bf * XS;
   CQP_STAMP0(p.dbg, 7);
-  cl_residual_pass(p, s, xfinal, true, pass++, rank, C, nrm);
+  // Server step whose caller takes only u0 (cqp_mpc_step_x0 with out == NULL): the report is not
+  // observable, so the final residual evaluation (solver.cpp:94-95) is skipped; iterate and u0 are
+  // the same bits.  Only the unscaled controls y[0:nu] are formed, for the extraction.
+  const bool fast = p.server && want_full_s == 0ull;
+  if (fast) {
+    __syncthreads();  // (every warp is past its wait for v_k)
+    if (rank == 0) {
+      for (int i = t; i < p.mpc_nu; i += kClThreads) s.uy[i] = s.sE[i] * xfinal[i];
+      __syncthreads();
+    }
+  } else {
+    cl_residual_pass(p, s, xfinal, true, pass++, rank, C, nrm);
+  }
   CQP_STAMP0(p.dbg, 8);
   // between-launch invariant: p.vq slot 0 = iterate (slots 1..3 keep the grid kernel's sentinel)
   for (int r = t; r < nrows; r += kClThreads) p.vq[row0 + r] = xfinal[row0 + r];
   if (rank == 0) {
     mpc_extract_control(p, s.uy, t);
     if (p.Dpad != D && t == 0) p.vq[D] = 0.0;
-    for (int i = t; i < n; i += kClThreads) p.out_y[i] = s.uy[i];
-    for (int i = t; i < m; i += kClThreads) {
-      p.out_z[i] = s.uz[i];
-      p.out_lam[i] = s.ul[i];
+    if (!p.server || want_full_s) {
+      for (int i = t; i < n; i += kClThreads) p.out_y[i] = s.uy[i];
+      for (int i = t; i < m; i += kClThreads) {
+        p.out_z[i] = s.uz[i];
+        p.out_lam[i] = s.ul[i];
+      }
     }
     if (t == 0) {
       DevResultHead h;
@@ -652,9 +705,27 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
       p.state[0] = layer;
     }
   }
+  if (!p.server) break;
+  // answer: the result record is host-mapped; every writer fences system-wide, then one thread
+  // publishes the request number.  The cluster barrier also keeps the next step's instantiate /
+  // relay from overwriting g, c, d, x0 while a peer still reads them.
+  __threadfence_system();
+  __syncthreads();
+  if (rank == 0 && t == 0) {
+    p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);
+    __threadfence_system();
+    p.mb[kMbResp] = req;
+  }
+  served = req;
+  cluster_sync_all();
+  }  // server loop
   __syncthreads();
   CQP_STAMP0(p.dbg, 9);
   cluster_sync_all();  // no CTA leaves while a peer could still address its shared memory
+  if (p.server && rank == 0 && t == 0) {
+    __threadfence_system();
+    p.mb[kMbExited] = 1ull;
+  }
   CQP_STAMP0(p.dbg, 10);
 }
 

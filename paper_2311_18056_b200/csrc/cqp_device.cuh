@@ -216,6 +216,90 @@ __device__ __forceinline__ double warp_row_dot_mlp(const double* __restrict__ Mr
   return v;
 }
 
+__device__ __forceinline__ void mbar_inval(unsigned long long* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One row of mpc::instantiate (mpc.cpp:260-270) by one warp: row < n: g[row] = offset_g[row, :] . x0;
+// else c / d [row - n] = base - offset_c[row - n, :] . x0.  The standalone kernel and the resident
+// server share this, so both produce the same bits.
+__device__ __forceinline__ void instantiate_row(int row, int lane, const double* __restrict__ og,
+                                                const double* __restrict__ oc, const double* __restrict__ cb,
+                                                const double* __restrict__ db, const double* x0, int n, int nx,
+                                                int nxpad, double* g, double* c, double* d, bool x0_in_global = true) {
+  const double* M = row < n ? og + (size_t)row * nxpad : oc + (size_t)(row - n) * nxpad;
+  double acc = 0.0;
+  for (int j = lane; j < nx; j += 32) acc = fma(M[j], x0_in_global ? __ldcg(x0 + j) : x0[j], acc);  // (x0 changes per server step: not through L1)
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+  if (lane == 0) {
+    if (row < n) {
+      g[row] = acc;
+    } else {
+      c[row - n] = cb[row - n] - acc;
+      d[row - n] = db[row - n] - acc;
+    }
+  }
+}
+
+// Resident MPC server, request side.  Warp 0 of the FIRST CTA polls the host-mapped mailbox; on a new
+// request it fetches x0 with all lanes at once (one PCIe round trip), stores it to the device copy and
+// republishes the request number in device memory for the other CTAs (release).  Returns the request
+// number, or kSrvExit when told to stop / idle for too long.  Call with the whole warp.
+__device__ __forceinline__ unsigned long long server_fetch_request(const RunParams& p, unsigned long long served, int lane,
+                                                                   int& want_full) {
+  unsigned long long seq = served;
+  if (lane == 0) {
+    const long long t0 = globaltimer_ns();
+    unsigned spins = 0;
+    for (;;) {
+      seq = p.mb[kMbReq];
+      if (seq != served) break;
+      if (p.mb[kMbStop] != 0ull) { seq = kSrvExit; break; }
+      if ((++spins & 0x3F) == 0 && globaltimer_ns() - t0 > p.idle_ns) { seq = kSrvExit; break; }
+    }
+  }
+  seq = __shfl_sync(0xffffffffu, seq, 0);
+  if (seq != kSrvExit) {
+    const volatile double* src = reinterpret_cast<const volatile double*>(p.mb + kMbX0);
+    double v[kMaxInlineX0 / 32];
+    const unsigned long long wf = (lane == 0) ? p.mb[kMbWantFull] : 0ull;  // (in flight together with x0)
+#pragma unroll
+    for (int u = 0; u < kMaxInlineX0 / 32; ++u) v[u] = (lane + 32 * u < p.mpc_nx) ? src[lane + 32 * u] : 0.0;
+    want_full = (int)__shfl_sync(0xffffffffu, wf, 0);
+#pragma unroll
+    for (int u = 0; u < kMaxInlineX0 / 32; ++u)
+      if (lane + 32 * u < p.mpc_nx) p.mpc_x0_w[lane + 32 * u] = v[u];
+    __threadfence();
+    __syncwarp();
+  }
+  // (the relay word carries "full report wanted" in bit 62: every CTA must take the same path)
+  if (lane == 0) st_release_gpu_u64(p.srv_seq, seq == kSrvExit ? seq : (seq | ((unsigned long long)(want_full != 0) << 62)));
+  return seq;
+}
+
+// The other CTAs: wait until the first CTA has republished a request newer than `served`.
+__device__ __forceinline__ unsigned long long server_wait_relay(const RunParams& p, unsigned long long served, int& want_full) {
+  unsigned long long w;
+  do { w = ld_acquire_gpu_u64(p.srv_seq); } while (w != kSrvExit && (w & ~(1ull << 62)) == served);
+  if (w == kSrvExit) return w;
+  want_full = (int)((w >> 62) & 1ull);
+  return w & ~(1ull << 62);
+}
+
 // Control extraction of the closed loop (bench.cpp:169-175): u0 = clamp(-K x + y[0:nu], u_lo, u_hi).
 // `y` is the unscaled primal solution in shared memory; executed by one CTA (thread `t0` takes
 // controls t0, t0 + blockDim.x, ...).
@@ -224,7 +308,7 @@ __device__ __forceinline__ void mpc_extract_control(const RunParams& p, const do
   for (int t = t0; t < p.mpc_nu; t += (int)blockDim.x) {
     const double* Krow = p.mpc_K + (size_t)t * p.mpc_nxpad;
     double kx = 0.0;
-    for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], p.mpc_x0[j], kx);
+    for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], __ldcg(p.mpc_x0 + j), kx);
     double u = -kx + y[t];
     const double lo = p.mpc_ulo[t], hi = p.mpc_uhi[t];
     u = u < lo ? lo : u;

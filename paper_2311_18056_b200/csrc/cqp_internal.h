@@ -26,6 +26,18 @@ constexpr int kMaxStages = 6;
 constexpr int kMaxInlineX0 = 128;  // x0 of an MPC step rides in the kernel parameters up to this size
 constexpr int kWarps = kThreads / 32;
 
+// Resident MPC server (cqp_mpc_server_start): the mailbox is host-mapped pinned memory, 64-bit words.
+// The host writes x0 then REQ; the kernel answers by writing the result record and then RESP = REQ.
+constexpr int kMbReq = 0;       // host -> device: sequence number of the newest request
+constexpr int kMbStop = 1;      // host -> device: non-zero = leave the loop
+constexpr int kMbResp = 2;      // device -> host: sequence number of the newest answered request
+constexpr int kMbExited = 3;    // device -> host: the kernel has left its loop (stop or idle timeout)
+constexpr int kMbStepNs = 4;    // device -> host: duration of the last step on the device (%globaltimer)
+constexpr int kMbWantFull = 5;  // host -> device: also write y, z, lambda (else only the head and u0)
+constexpr int kMbX0 = 8;        // x0 (kMaxInlineX0 doubles)
+constexpr int kMbWords = kMbX0 + kMaxInlineX0;
+constexpr unsigned long long kSrvExit = ~0ull;  // relay token: leave the loop
+
 inline int pad2(int x) { return (x + 1) & ~1; }
 
 void set_error(const std::string& msg);
@@ -115,6 +127,21 @@ struct RunParams {
   const double* mpc_uhi; // nu
   int mpc_nx, mpc_nxpad, mpc_nu;
   double* out_u;         // nu (in the result record)
+  // resident MPC server (server != 0): the kernel loops { wait for x0 in the mailbox; instantiate;
+  // refresh_z; total_iters iterations; final pass; answer } until told to stop or idle for idle_ns
+  int server;
+  volatile unsigned long long* mb;    // mailbox (kMb* words), host-mapped
+  unsigned long long served;          // newest request already answered when the kernel starts
+  unsigned long long* srv_seq;        // device relay: CTA 0 republishes the request number here
+  long long idle_ns;
+  const double* mpc_og;  // [n][nxpad] offset_g, [m][nxpad] offset_c, c_base, d_base (mpc.cpp:260-270)
+  const double* mpc_oc;
+  const double* mpc_cb;
+  const double* mpc_db;
+  double* mpc_x0_w;      // writable alias of mpc_x0 (the relay target)
+  double* g_w;           // writable aliases of g, c, d (the in-kernel instantiate)
+  double* c_w;
+  double* d_w;
   DevResultHead* head;
   int* trace;         // [cap][2]
   int* hist_i;        // [cap][2]  (iteration, grid index)
@@ -167,6 +194,15 @@ struct cqp_handle {
   double* hx0 = nullptr;                          // pinned staging of x0
   bool vectors_device_only = false;               // c/d were last set by the device-side instantiate
   bool mpc_extract = false;                       // the next launch also extracts the control
+  // resident MPC server
+  unsigned long long* mb_host = nullptr;          // mailbox, host-mapped (kMbWords words)
+  unsigned long long* mb_dev = nullptr;           // its device alias
+  unsigned long long* srv_seq = nullptr;          // device relay word
+  bool srv_enabled = false, srv_running = false;
+  int srv_k = 0;
+  long long srv_idle_ns = 0;
+  unsigned long long srv_req = 0;                 // sequence number of the newest request posted
+  double srv_last_wall_us = 0.0, srv_last_device_us = 0.0;  // last served step: C-ABI wall / device-side duration
   int* dbg_host = nullptr;  // host-mapped watchdog record (16 ints)
   int* dbg_dev = nullptr;
   // launch configuration
@@ -204,6 +240,8 @@ int launch_untranspose(cudaStream_t st, const double* src_rowmajor, int rows, in
                        double* dst_colmajor);
 int launch_bias(cqp_handle* h, int k, double* b_out);  // b_out: device, D doubles
 int launch_instantiate(cqp_handle* h, const double* x0_host);  // g, c, d <- template(x0) on the device
+int server_launch(cqp_handle* h, int k);   // start the resident MPC kernel for k iterations per step
+int server_stop(cqp_handle* h);            // leave the loop and wait for the kernel (no-op when not running)
 
 // cqp_batch.cu : dense DMMA GEMM with an identity slot map, used by the offline stage
 struct DenseGemm;

@@ -267,11 +267,12 @@ __device__ __forceinline__ Scratch scratch(const RunParams& p, const Smem& s, co
 // rows it owns: b = -[D_k; G D_k] g_s, 0 on the lambda rows (layers.cpp:168-175).
 // Uses s.uy as scratch for g_s = cost_scale * E o g (layers.cpp:181).
 template <int RB>
-__device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows, const double* cur) {
+__device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, int nrows, const double* cur,
+                           bool copy_w = true) {
   const int t = threadIdx.x;
   const Scratch sc = scratch(p, s, cur);
   __syncthreads();
-  if (p.w_smem) {
+  if (p.w_smem && copy_w) {
     const double2* src =
         reinterpret_cast<const double2*>(p.W + ((size_t)k * p.D + row0) * p.Dpad);
     double2* dst = reinterpret_cast<double2*>(s.sW);
@@ -279,7 +280,7 @@ __device__ void load_layer(const RunParams& p, const Smem& s, int k, int row0, i
     for (int i = t; i < count; i += kThreads) dst[i] = __ldg(src + i);
   }
   for (int i = t; i < p.npad; i += kThreads)
-    sc.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * p.g[i]) : 0.0;
+    sc.uy[i] = (i < p.n) ? p.cost_scale * (p.E[i] * __ldcg(p.g + i)) : 0.0;  // (g, c, d change per server step: not through L1)
   __syncthreads();
   const int nm = p.n + p.m;
   const double* DG = p.Dk + (size_t)k * nm * p.npad;  // [D_k; G D_k], (n+m) x npad
@@ -314,7 +315,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     if (i < m) {
       z = xs[n + i] / p.F[i];
       if (final) {  // solver.cpp:94  z = clamp(z, p.c, p.d) in original units
-        const double lo = p.c[i], hi = p.d[i];
+        const double lo = __ldcg(p.c + i), hi = __ldcg(p.d + i);
         z = z < lo ? lo : z;
         z = z > hi ? hi : z;
       }
@@ -348,7 +349,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     if (t < bn) {
       const int row = h0 + c0 + t;
       const double hy = s.sval[t], gtl = s.sval[bn + t];
-      const double gi = p.g[row];
+      const double gi = __ldcg(p.g + row);
       const double dual = (hy + gi) + gtl;  // (H y + g) + G' lambda
       mx[6] = nanmax(mx[6], fabs(gi));
       mx[1] = nanmax(mx[1], fabs(dual));
@@ -438,7 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // ring runs ahead of the compute warps, also across iterations (W does not depend on v).
   const int NS = STREAM ? p.stream_stages : 1;
   constexpr bool streaming = STREAM;
-  if (t == 0) {
+  auto init_barriers = [&](bool again) {  // thread 0; `again`: a later server step re-initialises them
+    if (again) {
+      mbar_inval(&full[0]); mbar_inval(&full[1]); mbar_inval(&xready[0]); mbar_inval(&xready[1]); mbar_inval(go);
+      for (int k = 0; k < (STREAM ? NS : 0); ++k) { mbar_inval(&wfull[k]); mbar_inval(&wempty[k]); }
+    }
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
     mbar_init(&xready[0], kLoaderWarps + (COFETCH ? kComputeWarps : 0));
@@ -449,7 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       mbar_init(&wempty[k], kComputeWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
-  }
+  };
+  if (t == 0) init_barriers(false);
   const int n = p.n, m = p.m, D = p.D;
   const int XS = xs_stride(p.Dpad, p.npad, p.mpad);  // doubles between the two copies of the iterate
   const int nc2 = p.Dpad >> 1;
@@ -488,14 +494,48 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   CQP_STAMP0(p.dbg, 0);  // (-DCQP_TRACE: prologue / epilogue timeline of CTA 0, tools/trace_tier1.py)
   if (blockIdx.x == 0 && t == 0) *p.barrier_next = 0u;  // counter of the NEXT launch (ping-pong)
 
+  // Resident MPC server (p.server): the loop below is one control step per request { x0 from the
+  // mailbox -> instantiate -> refresh_z -> total_iters layers -> final pass -> answer }; the W slice of
+  // the resident tier stays in shared memory between steps.  A plain launch runs the body once.
+  unsigned long long served = p.served;
+  int resident_layer = -1;
+  // (two spare words of the barrier block: the kernel may not own static shared memory, its dynamic
+  // allocation is the full 227 KB)
+  unsigned long long& cmd_s = s.bars[5];
+  unsigned long long& want_full_s = s.bars[6];
+  for (;;) {
+  unsigned long long req = 0;
+  long long t_step = 0;
+  if (p.server) {
+    if (warp == 0) {
+      int want = 1;
+      const unsigned long long r = (blockIdx.x == 0) ? server_fetch_request(p, served, lane, want)
+                                                     : (lane == 0 ? server_wait_relay(p, served, want) : 0ull);
+      if (lane == 0) { cmd_s = r; want_full_s = (unsigned long long)want; }
+    }
+    __syncthreads();
+    req = cmd_s;
+    if (req == kSrvExit) break;
+    t_step = globaltimer_ns();
+    if (t == 0 && served != p.served) init_barriers(true);  // (every role left them behind the last residual pass)
+    // mpc::instantiate (mpc.cpp:260-270): this CTA's share of the rows of [g; c; d]
+    const int rows = n + m, per = (rows + p.G - 1) / p.G;
+    const int r0 = (int)blockIdx.x * per, r1 = min(rows, r0 + per);
+    for (int row = r0 + warp; row < r1; row += kWarps)
+      instantiate_row(row, lane, p.mpc_og, p.mpc_oc, p.mpc_cb, p.mpc_db, p.mpc_x0, n, p.mpc_nx, p.mpc_nxpad, p.g_w, p.c_w, p.d_w);
+    __threadfence();
+    // every CTA's rows of g, c, d (and the previous step's iterate rows in slot 0) are visible
+    grid_barrier(p.barrier, epoch, p.G, p.dbg);
+  }
+
   // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
   // (layers.cpp:182-186, 223-226)
   for (int r = t; r < nrows; r += kThreads) {
     const int row = row0 + r;
     double lo = -INFINITY, hi = INFINITY;
     if (row >= n && row < n + m) {
-      lo = p.F[row - n] * p.c[row - n];
-      hi = p.F[row - n] * p.d[row - n];
+      lo = p.F[row - n] * __ldcg(p.c + row - n);
+      hi = p.F[row - n] * __ldcg(p.d + row - n);
     }
     s.slo[r] = lo;
     s.shi[r] = hi;
@@ -518,7 +558,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   }
 
   CQP_STAMP0(p.dbg, 1);  // bounds + this CTA's rows of refresh_z done
-  load_layer<RB>(p, s, layer, row0, nrows, nullptr);  // (scratch in the second copy, cleared below)
+  load_layer<RB>(p, s, layer, row0, nrows, nullptr, resident_layer != layer);  // (scratch in the second copy, cleared below)
+  resident_layer = layer;
   if (p.do_refresh) grid_barrier_wait(p.barrier, epoch, p.dbg);  // every CTA's rows of z_s are in slot 0
   CQP_STAMP0(p.dbg, 2);  // bias rows done, refresh_z complete
 
@@ -758,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         }
         ++n_trace;
         load_layer<RB>(p, s, layer, row0, nrows, xcur);
+        resident_layer = layer;
       }
     }
     if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
@@ -769,9 +811,24 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // ---- epilogue (solver.cpp:90-99) ----
   if (t == 0) progress(p.dbg, 3, iters_done * 10 + 9);
   CQP_STAMP0(p.dbg, 4);  // iterations done
-  double nr[7];
+  double nr[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double* xfinal = s.xs + (size_t)(iters_done & 1) * XS;
-  residual_pass<RB>(p, s, xfinal, true, epoch, pass, nr);
+  // Server step whose caller takes only u0 (cqp_mpc_step_x0 with out == NULL): the report is not
+  // observable, so the final residual evaluation (solver.cpp:94-95) is skipped; the iterate and u0
+  // are the same bits.  What remains of the pass is its grid barrier (every CTA has fetched v_k from the
+  // ring before the ring is reset below) and the unscaled controls y[0:nu] for the extraction.
+  const bool fast = p.server && want_full_s == 0ull;
+  if (fast) {
+    __syncthreads();
+    grid_barrier(p.barrier, epoch, p.G, p.dbg);
+    if (blockIdx.x == 0) {
+      const Scratch sc = scratch(p, s, xfinal);
+      for (int i = t; i < p.mpc_nu; i += kThreads) sc.uy[i] = p.E[i] * xfinal[i];
+      __syncthreads();
+    }
+  } else {
+    residual_pass<RB>(p, s, xfinal, true, epoch, pass, nr);
+  }
   CQP_STAMP0(p.dbg, 5);  // final residual pass done
   // Every CTA has read the final iterate (the pass ends behind a grid barrier): restore the
   // between-launch invariant  q[0] = iterate, q[1..3] = sentinel  for the rows this CTA owns.
@@ -789,10 +846,12 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if (blockIdx.x == 0) {
     const Scratch sc = scratch(p, s, xfinal);  // unscaled solution left by the final residual pass
     mpc_extract_control(p, sc.uy, t);
-    for (int i = t; i < n; i += kThreads) p.out_y[i] = sc.uy[i];
-    for (int i = t; i < m; i += kThreads) {
-      p.out_z[i] = sc.uz[i];
-      p.out_lam[i] = sc.ul[i];
+    if (!p.server || want_full_s) {
+      for (int i = t; i < n; i += kThreads) p.out_y[i] = sc.uy[i];
+      for (int i = t; i < m; i += kThreads) {
+        p.out_z[i] = sc.uz[i];
+        p.out_lam[i] = sc.ul[i];
+      }
     }
     if (t == 0) {
       DevResultHead h;
@@ -808,6 +867,22 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       *p.head = h;
       p.state[0] = layer;
     }
+  }
+  if (!p.server) break;
+  // answer: the result record is host-mapped; every writer fences system-wide, then one thread
+  // publishes the request number
+  __threadfence_system();
+  __syncthreads();
+  if (blockIdx.x == 0 && t == 0) {
+    p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);
+    __threadfence_system();
+    p.mb[kMbResp] = req;
+  }
+  served = req;
+  }  // server loop
+  if (p.server && blockIdx.x == 0 && t == 0) {
+    __threadfence_system();
+    p.mb[kMbExited] = 1ull;
   }
   CQP_STAMP0(p.dbg, 6);
 }
@@ -892,19 +967,7 @@ __global__ void instantiate_kernel(const double* __restrict__ og, const double* 
   if (INLINE && blockIdx.x == 0)  // keep a device copy for the control extraction of the run kernel
     for (int j = threadIdx.x; j < nx; j += blockDim.x) x0_dev[j] = xa.x[j];
   if (row >= n + m) return;
-  const double* M = row < n ? og + (size_t)row * nxpad : oc + (size_t)(row - n) * nxpad;
-  double acc = 0.0;
-  for (int j = lane; j < nx; j += 32) acc = fma(M[j], x0[j], acc);
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
-  if (lane == 0) {
-    if (row < n) {
-      g[row] = acc;
-    } else {
-      c[row - n] = cb[row - n] - acc;
-      d[row - n] = db[row - n] - acc;
-    }
-  }
+  instantiate_row(row, lane, og, oc, cb, db, x0, n, nx, nxpad, g, c, d, !INLINE);
 }
 
 // Row-major W_k ([D][Dpad]) -> the streaming layout of the L2/HBM tier (RunParams::Wt): inside the
@@ -1197,6 +1260,12 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
     p.mpc_K = h->mpc_K; p.mpc_x0 = h->mpc_x0; p.mpc_ulo = h->mpc_ulo; p.mpc_uhi = h->mpc_uhi;
     p.mpc_nx = h->mpc_nx; p.mpc_nxpad = h->mpc_nxpad; p.mpc_nu = h->mpc_nu;
   }
+  if (h->srv_running) {  // (set by server_launch around this call)
+    p.server = 1;
+    p.mb = h->mb_dev; p.served = h->srv_req; p.srv_seq = h->srv_seq; p.idle_ns = h->srv_idle_ns;
+    p.mpc_og = h->mpc_og; p.mpc_oc = h->mpc_oc; p.mpc_cb = h->mpc_cb; p.mpc_db = h->mpc_db;
+    p.mpc_x0_w = h->mpc_x0; p.g_w = h->g; p.c_w = h->c; p.d_w = h->d;
+  }
   // The other CTAs publish within a few hundred ns of this one: a first poll issued right at `go`
   // mostly finds sentinels and costs a second L2 round trip, and the extra polling traffic slows the
   // publishes themselves.  A short pause before the first poll is a net win (B200, D = 900 / 1500:
@@ -1239,7 +1308,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.rho_vec = h->rho_vec;
   // few iterations: copying the W slice into shared memory costs as much as streaming it once;
   // the ring then lives in the (unused) slice region
-  if (total_iters < 4 && p.w_smem) {
+  if (total_iters < 4 && p.w_smem && !p.server) {
     p.w_smem = 0;
     if (!delay_set) p.poll_delay_ns = 150;  // (streaming kernel: keeps the pause)
     int stages = h->wdoubles / kStageDoubles;

@@ -273,6 +273,29 @@ class Solver:
         _raise(self._L.cqp_mpc_step_x0(self._h, _p(x0), int(k), _p(u0), C.byref(res)))
         return u0, self._report(res, bufs)
 
+    def mpc_server_start(self, k: int, idle_timeout_ms: float = 100.0) -> None:
+        """Keep the solve kernel resident and serve `mpc_step_x0(x0, k)` from a host-mapped mailbox
+        (no CUDA call per control step; same results bit for bit).  Any other method of this Solver
+        retires the resident kernel first; it also leaves by itself after `idle_timeout_ms` without
+        a request and is restarted by the next step."""
+        if k < 1:
+            raise ValueError("mpc_server_start: k must be >= 1")
+        _raise(self._L.cqp_mpc_server_start(self._h, int(k), float(idle_timeout_ms)))
+
+    def mpc_server_stop(self) -> None:
+        _raise(self._L.cqp_mpc_server_stop(self._h))
+
+    def mpc_server_last_timing(self) -> Tuple[float, float]:
+        """(wall_us inside the C ABI call, device-side step duration in us) of the last served step."""
+        w, d = C.c_double(), C.c_double()
+        _raise(self._L.cqp_mpc_server_last_timing(self._h, C.byref(w), C.byref(d)))
+        return w.value, d.value
+
+    def mpc_step_x0_fast(self, x0: np.ndarray, k: int, u0: np.ndarray) -> None:
+        """`mpc_step_x0` without the report and without allocations (x0, u0: contiguous float64
+        arrays the caller keeps): what a control loop calls at kHz rates."""
+        _raise(self._L.cqp_mpc_step_x0(self._h, _p(x0), int(k), _p(u0), None))
+
     # ---- accessors, solver.hpp:123-127 ----
     @property
     def state(self) -> np.ndarray:
