@@ -326,6 +326,23 @@ def mpc_step_section(S, problems, peaks):
             u, rep = gs.mpc_step_x0(x, k)
             wall.append((time.perf_counter() - t1) * 1e6); ker.append(rep.kernel_us); cabi.append(rep.wall_ms * 1e3)
             x = A @ x + B @ u
+        # (a') the same closed loop served by the resident kernel (cqp_mpc_server_start): u0-only steps
+        # through the C ABI (no CUDA call per step), and steps that also return the report
+        x = wl.x0(1.0)
+        srv_c, srv_d, srv_cr = [], [], []
+        gs.cold_start(); gs.update_vectors(q.g, q.c, q.d); gs.solve()
+        gs.mpc_server_start(k)
+        u_buf = np.zeros(nu)
+        for t in range(200):
+            gs.mpc_step_x0_fast(np.ascontiguousarray(x), k, u_buf)
+            wsrv, dsrv = gs.mpc_server_last_timing()
+            srv_c.append(wsrv); srv_d.append(dsrv)
+            x = A @ x + B @ u_buf
+        for t in range(60):
+            u, rep = gs.mpc_step_x0(x, k)
+            srv_cr.append(rep.wall_ms * 1e3)
+            x = A @ x + B @ u
+        gs.mpc_server_stop()
         # (b) host-side instantiate (untimed), step uploads g, c, d (cqp_mpc_step)
         x = wl.x0(1.0)
         wall_gcd = []
@@ -345,6 +362,11 @@ def mpc_step_section(S, problems, peaks):
                     "step_wall_us_p50": w50, "step_kernel_us_p50": k50, "step_hz": 1e6 / w50,
                     "step_cabi_wall_us_p50": statistics.median(cabi[20:]),
                     "step_wall_us_p50_host_instantiate": statistics.median(wall_gcd[10:]),
+                    "server_step_cabi_wall_us_p50": statistics.median(srv_c[20:]),
+                    "server_step_device_us_p50": statistics.median(srv_d[20:]),
+                    "server_step_hz": 1e6 / statistics.median(srv_c[20:]),
+                    "server_step_with_report_cabi_wall_us_p50": statistics.median(srv_cr[10:]),
+                    "server_note": "resident kernel + host-mapped mailbox (cqp_mpc_server_start); u0-only steps skip the final residual pass whose results the caller does not take; bit-identical iterate and u0 (tests/test_gpu_mpc_server.py)",
                     "W_bytes_per_iteration": wbytes, "dense_W_bytes_per_iteration": 8.0 * D * D,
                     "W_stream_GBs": wbytes * k / (k50 * 1e-6) / 1e9,
                     "cold_solve_W_GBs": wbytes * r0.solution.iterations / (r0.kernel_us * 1e-6) / 1e9,

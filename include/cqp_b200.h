@@ -191,6 +191,11 @@ CQP_API int cqp_mpc_server_last_timing(const cqp_handle *h, double *wall_us, dou
 /* Solver::state() / layer_index(), solver.hpp:126-127: v (n+2m, cache space) and the index. */
 CQP_API int cqp_get_state(cqp_handle *h, double *v, int *layer_index);
 
+/* The inverse of cqp_get_state: the persistent iterate (cache space, n+2m) and the ladder index a
+ * free-standing solve(p, cache, s, warm) / fixed_iters(...) of solver.hpp:86-97 starts from or hands
+ * back (the host mirror saves and restores a Solver's iterate around those calls). */
+CQP_API int cqp_set_state(cqp_handle *h, const double *v, int layer_index);
+
 /* Solver::cache() read-back (solver.hpp:124) for one grid point; any pointer may be NULL.
  * W (n+2m)^2, Dk n*n, GDk m*n column-major; b (n+2m) for the CURRENT g; rho_vec (m). */
 CQP_API int cqp_get_layer(cqp_handle *h, int k, double *W, double *Dk, double *GDk, double *b,

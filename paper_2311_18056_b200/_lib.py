@@ -55,7 +55,7 @@ EXPORTS = [
     "cqp_create_from_layers", "cqp_destroy", "cqp_update_vectors", "cqp_cold_start",
     "cqp_warm_start", "cqp_refresh_z", "cqp_solve", "cqp_fixed_iters", "cqp_mpc_step",
     "cqp_mpc_set_template", "cqp_mpc_step_x0", "cqp_mpc_server_start", "cqp_mpc_server_stop", "cqp_mpc_server_last_timing",
-    "cqp_get_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
+    "cqp_get_state", "cqp_set_state", "cqp_get_layer", "cqp_get_scaling", "cqp_dims", "cqp_debug_words",
     "cqp_launch_info", "cqp_layer_traffic", "cqp_measure_read_bandwidth", "cqp_pinned_alloc", "cqp_pinned_free",
     "cqp_batch_create", "cqp_batch_destroy", "cqp_batch_solve", "cqp_batch_last_timing", "cqp_batch_last_profile", "cqp_batch_round_profile",
     "cqp_batch_get_traces", "cqp_batch_get_history",
@@ -104,6 +104,7 @@ def load() -> C.CDLL:
     L.cqp_mpc_server_stop.argtypes = [C.c_void_p]
     L.cqp_mpc_server_last_timing.argtypes = [C.c_void_p, c_double_p, c_double_p]
     L.cqp_get_state.argtypes = [C.c_void_p, c_double_p, c_int_p]
+    L.cqp_set_state.argtypes = [C.c_void_p, c_double_p, C.c_int]
     L.cqp_get_layer.argtypes = [C.c_void_p, C.c_int] + [c_double_p] * 5
     L.cqp_get_scaling.argtypes = [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p,
                                   c_int_p, c_double_p, c_double_p]

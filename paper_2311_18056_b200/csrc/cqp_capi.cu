@@ -645,6 +645,21 @@ int cqp_get_state(cqp_handle* h, double* v, int* layer_index) {
   return CQP_OK;
 }
 
+int cqp_set_state(cqp_handle* h, const double* v, int layer_index) {
+  if (!h || !v) { set_error("set_state: null argument"); return CQP_ERR_ARGUMENT; }
+  if (layer_index < 0 || layer_index >= h->L) { set_error("set_state: layer index out of range"); return CQP_ERR_ARGUMENT; }
+  CQP_CUDA(cudaSetDevice(h->device));
+  CQP_QUIESCE(h);
+  // ring invariant between launches: slot 0 = iterate, slots 1..3 = sentinel
+  CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemsetAsync(h->vq + h->Dpad, 0xFF, sizeof(double) * 3 * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->vq, v, sizeof(double) * (size_t)h->D, cudaMemcpyHostToDevice, h->stream));
+  int rc = launch_set_state(h, layer_index);
+  if (rc) return rc;
+  CQP_CUDA(cudaStreamSynchronize(h->stream));  // (v may be pageable)
+  return CQP_OK;
+}
+
 int cqp_get_layer(cqp_handle* h, int k, double* W, double* Dk, double* GDk, double* b,
                   double* rho_vec) {
   if (!h || k < 0 || k >= h->L) { set_error("get_layer: bad index"); return CQP_ERR_ARGUMENT; }

@@ -166,6 +166,103 @@ int main() {
     }
     CHECK_THROWS_AS(b.mpc_step(Vec{1.0}, 1, nullptr), std::invalid_argument);
   }
+  // Solver::cache() read-back (solver.hpp:124) against the 1-D layer of test_layers.cpp:191-207:
+  // H = 2, g = -2, G = 1, sigma = 0, rho = 1  =>  W = [[-1/3, 2/3, -1/3], [2/3, -1/3, 2/3], [1, -1, 1]], b = [2/3, 2/3, 0]
+  {
+    SolverSettings s;
+    s.sigma = 0.0;
+    s.equilibration.enabled = false;
+    s.grid_points = 7;                      // decade grid 1e-3 .. 1e3: index 3 is rho = 1 (test_layers.cpp:62-91)
+    Solver solver(box_1d(), s);
+    const LayerCache cache = solver.cache();
+    CHECK(cache.n() == 1 && cache.m() == 1 && cache.num_layers() == 7);
+    CHECK(cache.initial_index() == 2);
+    const std::vector<double> grid = cache.grid_values();
+    CHECK(grid.size() == 7 && grid[0] == 1e-3 && grid[6] == 1e3 && approx(grid[3], 1.0, 1e-15));
+    const Layer l = cache.layer(3);
+    const double W[3][3] = {{-1.0 / 3, 2.0 / 3, -1.0 / 3}, {2.0 / 3, -1.0 / 3, 2.0 / 3}, {1.0, -1.0, 1.0}};
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) CHECK(std::fabs(l.W(i, j) - W[i][j]) <= 1e-15);
+    CHECK(std::fabs(l.b[0] - 2.0 / 3) <= 1e-15 && std::fabs(l.b[1] - 2.0 / 3) <= 1e-15 && l.b[2] == 0.0);
+    CHECK(std::fabs(l.D(0, 0) - 1.0 / 3) <= 1e-15 && l.rho_vec[0] == grid[3] && l.rho_base == grid[3]);
+    const Scaling sc = cache.scaling();
+    CHECK(sc.E[0] == 1.0 && sc.F[0] == 1.0 && sc.cost_scale == 1.0);
+    const Vec ct = cache.c_tilde(), dt = cache.d_tilde();  // test_layers.cpp:223-245: [-inf; c; -inf], [+inf; d; +inf]
+    CHECK(ct[0] == -kInf && ct[1] == 0.0 && ct[2] == -kInf && dt[0] == kInf && dt[1] == 0.5 && dt[2] == kInf);
+  }
+  // free-standing solve / fixed_iters / warm_start on a cache (solver.hpp:81-97) == the Solver's own,
+  // bit for bit, and a Solver that shares the cache keeps its iterate and vectors
+  {
+    const SolverSettings s = tight_settings();
+    Solver solver(box_1d(), s);
+    const SolveReport own = solver.solve();
+    const Vec state_before = solver.state();
+    const int index_before = solver.layer_index();
+    const LayerCache cache = solver.cache();
+    const SolveReport free_cold = solve(box_1d(), cache, s);
+    CHECK(free_cold.solution.status == SolveStatus::Solved);
+    CHECK(free_cold.solution.iterations == own.solution.iterations);
+    CHECK(free_cold.solution.y[0] == own.solution.y[0] && free_cold.solution.lambda[0] == own.solution.lambda[0]);
+    CHECK(free_cold.solution.rho_trace.size() == own.solution.rho_trace.size());
+    // another problem on the same ladder (same H, G; other vectors), warm-started from the first solution
+    QProblem q = box_1d();
+    q.g = Vec{-1.5}; q.d = Vec{0.4};
+    const SolveReport free_warm = solve(q, cache, s, &own.solution);
+    Solver ref(q, s);
+    ref.warm_start(own.solution);
+    const SolveReport ref_warm = ref.solve();
+    CHECK(free_warm.solution.iterations == ref_warm.solution.iterations);
+    CHECK(free_warm.solution.y[0] == ref_warm.solution.y[0] && free_warm.solution.lambda[0] == ref_warm.solution.lambda[0]);
+    CHECK(approx(free_warm.solution.y[0], 0.4, 1e-6));
+    const SolveReport fi = fixed_iters(q, cache, s, 50);
+    Solver ref2(q, s);
+    const SolveReport fi_ref = ref2.fixed_iters(50);
+    CHECK(fi.solution.iterations == 50 && fi.solution.y[0] == fi_ref.solution.y[0] && fi.residual_history.size() == 2);
+    CHECK_THROWS_AS(fixed_iters(q, cache, s, 0), std::invalid_argument);
+    // dims mismatch: a status, not an exception (solver.cpp:161)
+    QProblem bad;
+    bad.H = Mat{{1.0, 0.0}, {0.0, 1.0}}; bad.g = Vec{0.0, 0.0}; bad.G = Mat{{1.0, 0.0}}; bad.c = Vec{0.0}; bad.d = Vec{1.0};
+    CHECK(solve(bad, cache, s).solution.status == SolveStatus::Invalid);
+    // the Solver that shares the cache is where it was
+    const Vec state_after = solver.state();
+    CHECK(solver.layer_index() == index_before);
+    for (Index i = 0; i < state_after.size(); ++i) CHECK(state_after[i] == state_before[i]);
+    const SolveReport again = solver.fixed_iters(25);       // continues from its own iterate, own vectors
+    Solver twin(box_1d(), s);
+    twin.solve();
+    const SolveReport twin_again = twin.fixed_iters(25);
+    CHECK(again.solution.y[0] == twin_again.solution.y[0] && again.solution.lambda[0] == twin_again.solution.lambda[0]);
+    // warm_start(prev, cache): the mapped iterate [y / E; G_s y_s; cost_scale lambda / F] and the last index
+    const std::pair<Vec, int> ws = warm_start(own.solution, cache);
+    CHECK(ws.second == own.solution.rho_trace.back().grid_index);
+    ref.warm_start(own.solution);
+    const Vec ref_state = ref.state();
+    for (Index i = 0; i < ref_state.size(); ++i) CHECK(ws.first[i] == ref_state[i]);
+  }
+  // precompute_all + BatchSolver: column j == solve(p_j, cache, s)
+  {
+    const SolverSettings s = tight_settings();
+    const LayerCache cache = precompute_all(box_1d(), s);
+    const int B = 5;
+    Mat g(1, B), c(1, B), d(1, B);
+    for (int j = 0; j < B; ++j) { g(0, j) = -2.0 + 0.3 * j; c(0, j) = 0.0; d(0, j) = 0.5 + 0.1 * j; }
+    BatchSolver batch(cache, 8);
+    const BatchSolver::Result r = batch.solve(g, c, d);
+    for (int j = 0; j < B; ++j) {
+      QProblem q = box_1d();
+      q.g = Vec{g(0, j)}; q.c = Vec{c(0, j)}; q.d = Vec{d(0, j)};
+      const SolveReport one = solve(q, cache, s);
+      CHECK(r.status[static_cast<size_t>(j)] == one.solution.status);
+      CHECK(r.iterations[static_cast<size_t>(j)] == one.solution.iterations);
+      CHECK(approx(r.y(0, j), one.solution.y[0], 1e-9) || std::fabs(r.y(0, j) - one.solution.y[0]) <= 1e-12);
+      CHECK(r.rho_trace[static_cast<size_t>(j)].size() == one.solution.rho_trace.size());
+      for (size_t i = 0; i < one.solution.rho_trace.size() && i < r.rho_trace[static_cast<size_t>(j)].size(); ++i) {
+        CHECK(r.rho_trace[static_cast<size_t>(j)][i].iteration == one.solution.rho_trace[i].iteration);
+        CHECK(r.rho_trace[static_cast<size_t>(j)][i].grid_index == one.solution.rho_trace[i].grid_index);
+      }
+    }
+    CHECK_THROWS_AS(batch.solve(Mat(2, 1), c, d), std::invalid_argument);
+  }
   if (failures == 0) std::printf("ALL C++ HOST-MIRROR CHECKS PASSED\n");
   return failures == 0 ? 0 : 1;
 }
