@@ -463,7 +463,9 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     flop_col = 2 * ((n + m) * D + m * n) + 4 * m     # executed per active column per iteration
     dense_equiv = achieved * (2 * D * D) / flop_col   # what a dense-W kernel would need for the same solves
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "dmma_gemm_traffic.json")
+    # (ncu --set full on two full-batch round_kernel launches, tools/summarize_profiles.py: dram read + write
+    # bytes per LAUNCH = per check round of 25 layers over 4096 columns)
+    prof = os.path.join(ROOT, "profiles", "round_kernel_traffic.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")

@@ -57,67 +57,170 @@ __global__ void kkt_and_t_kernel(const double* __restrict__ H, const double* __r
   T[at] = s - M[at];
 }
 
-// ---- Cholesky + inverse (LLT, then solve(I)) -------------------------------------------------
-// Column j of the factor: l_jj = sqrt(a_jj), a_ij /= l_jj.  A non-positive pivot is recorded
-// (first one wins) and replaced by 1 so that the remaining kernels stay finite.
-__global__ void chol_scale_kernel(double* __restrict__ A, int ld, int n, int j, int* fail) {
-  __shared__ double l;
-  if (threadIdx.x == 0) {
-    double a = A[j + (size_t)j * ld];
-    if (!(a > 0.0)) {
-      atomicCAS(fail, 0, j + 1);
-      a = 1.0;
-    }
-    l = sqrt(a);
-    A[j + (size_t)j * ld] = l;
+// ---- Cholesky + inverse (LLT, then solve(I)), blocked ---------------------------------------
+// Block size 64: per block column one diagonal-block kernel (one CTA, the block in shared memory),
+// one panel / row-block solve (a thread per row or column, its 64 unknowns in registers) and one
+// tiled rank-64 update of everything behind it: ~7 n / 64 launches per ladder level instead of 4 n
+// (n = 870: 98 instead of 3480), and the update runs as 64 x 64 x 64 shared-memory tiles instead of
+// rank-1 sweeps over the whole trailing matrix.  Same algorithm as before and as the reference
+// (layers.cpp:126-130: LLT, then forward and backward substitution on the identity); only the
+// summation order inside a block differs.
+constexpr int kNB = 64;
+
+// Diagonal block A[j0 : j0+nb, j0 : j0+nb] -> its Cholesky factor, in place.  A non-positive pivot is
+// recorded (first one wins, 1-based global column) and replaced by 1 so that the rest stays finite.
+__global__ void __launch_bounds__(256) chol_diag_kernel(double* __restrict__ A, int ld, int j0, int nb, int* fail) {
+  __shared__ double S[kNB][kNB + 1];
+  const int t = threadIdx.x;
+  for (int e = t; e < nb * nb; e += 256) {
+    const int r = e % nb, c = e / nb;
+    S[r][c] = (r >= c) ? A[(j0 + r) + (size_t)(j0 + c) * ld] : 0.0;
   }
   __syncthreads();
-  for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + (size_t)j * ld] /= l;
-}
-
-// Trailing update of the lower triangle: a_ic -= l_ij l_cj for i >= c > j.
-__global__ void chol_update_kernel(double* __restrict__ A, int ld, int n, int j) {
-  if (blockIdx.y > blockIdx.x) return;  // tile strictly above the diagonal
-  const int i = j + 1 + blockIdx.x * 32 + threadIdx.x;
-  const int c0 = j + 1 + blockIdx.y * 32;
-  if (i >= n) return;
-  const double li = A[i + (size_t)j * ld];
-  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
-    const int c = c0 + cc;
-    if (c < n && c <= i) A[i + (size_t)c * ld] -= li * A[c + (size_t)j * ld];
+  for (int j = 0; j < nb; ++j) {
+    if (t == 0) {
+      double a = S[j][j];
+      if (!(a > 0.0)) {
+        atomicCAS(fail, 0, j0 + j + 1);
+        a = 1.0;
+      }
+      S[j][j] = sqrt(a);
+    }
+    __syncthreads();
+    const double l = S[j][j];
+    for (int r = j + 1 + t; r < nb; r += 256) S[r][j] /= l;
+    __syncthreads();
+    const int rem = nb - j - 1;
+    for (int e = t; e < rem * rem; e += 256) {
+      const int r = j + 1 + e % rem, c = j + 1 + e / rem;
+      if (r >= c) S[r][c] -= S[r][j] * S[c][j];
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < nb * nb; e += 256) {
+    const int r = e % nb, c = e / nb;
+    if (r >= c) A[(j0 + r) + (size_t)(j0 + c) * ld] = S[r][c];
   }
 }
 
-// row k of Y /= l_kk   (columns [0, ncols))
-__global__ void tri_scale_row_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
-                                     int k, int ncols) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < ncols) Y[k + (size_t)c * ld] /= L[k + (size_t)k * ld];
-}
-
-// forward substitution step k (L Y = I): y_ic -= l_ik y_kc for i > k, c <= k
-__global__ void fwd_update_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
-                                  int n, int k) {
-  const int i = k + 1 + blockIdx.x * 32 + threadIdx.x;
-  const int c0 = blockIdx.y * 32;
+// Panel below the diagonal block: row i of A[i, j0 : j0+nb] <- row i . L11^-T (one thread per row).
+__global__ void __launch_bounds__(128) chol_panel_kernel(double* __restrict__ A, int ld, int n, int j0, int nb) {
+  __shared__ double L[kNB][kNB + 1];
+  for (int e = threadIdx.x; e < nb * nb; e += 128) {
+    const int r = e % nb, c = e / nb;
+    L[r][c] = (r >= c) ? A[(j0 + r) + (size_t)(j0 + c) * ld] : 0.0;
+  }
+  __syncthreads();
+  const int i = j0 + nb + blockIdx.x * 128 + threadIdx.x;
   if (i >= n) return;
-  const double lik = L[i + (size_t)k * ld];
-  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
-    const int c = c0 + cc;
-    if (c <= k) Y[i + (size_t)c * ld] -= lik * Y[k + (size_t)c * ld];
+  double x[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    if (c < nb) {
+      double v = A[i + (size_t)(j0 + c) * ld];
+#pragma unroll
+      for (int k = 0; k < kNB; ++k)
+        if (k < c) v -= x[k] * L[c][k];
+      x[c] = v / L[c][c];
+      A[i + (size_t)(j0 + c) * ld] = x[c];
+    }
   }
 }
 
-// backward substitution step k (L' X = Y, in place): y_ic -= l_ki x_kc for i < k, all c
-__global__ void bwd_update_kernel(const double* __restrict__ L, double* __restrict__ Y, int ld,
-                                  int n, int k) {
-  const int i = blockIdx.x * 32 + threadIdx.x;
-  const int c0 = blockIdx.y * 32;
-  if (i >= k) return;
-  const double lki = L[k + (size_t)i * ld];
-  for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
-    const int c = c0 + cc;
-    if (c < n) Y[i + (size_t)c * ld] -= lki * Y[k + (size_t)c * ld];
+// C[i, c] -= sum_{q < nb} P(i, q) Q(q, c)  over rows [i0, i1) and columns [c0, c1), 64 x 64 tiles:
+//   P(i, q) = PT ? Pm[(p0 + q) + i ld] : Pm[i + (p0 + q) ld]     (PT: the factor read transposed)
+//   Q(q, c) = QT ? Qm[c + (p0 + q) ld] : Qm[(p0 + q) + c ld]
+//   LOWER: only entries with i >= c (the trailing update of the Cholesky factor)
+template <bool PT, bool QT, bool LOWER>
+__global__ void __launch_bounds__(256) tile_update_kernel(double* __restrict__ C, const double* __restrict__ Pm,
+                                                          const double* __restrict__ Qm, int ld, int i0, int i1, int c0,
+                                                          int c1, int p0, int nb) {
+  const int ti = i0 + blockIdx.x * 64, tc = c0 + blockIdx.y * 64;
+  if (LOWER && tc > ti + 63) return;  // tile strictly above the diagonal
+  constexpr int KH = 32;              // q is walked in halves: two 32 x 65 tiles fit the static 48 KB
+  __shared__ double Ps[KH][65];       // [q][row]
+  __shared__ double Qs[KH][65];       // [q][col]
+  const int t = threadIdx.x;
+  const int tr = (t & 15) * 4, tcol = (t >> 4) * 4;
+  double acc[4][4] = {};
+  for (int qh = 0; qh < nb; qh += KH) {
+    const int nq = min(KH, nb - qh);
+    for (int e = t; e < 64 * nq; e += 256) {
+      int r, q;
+      if (PT) { q = e % nq; r = e / nq; } else { r = e % 64; q = e / 64; }
+      const int i = ti + r;
+      Ps[q][r] = (i < i1) ? (PT ? Pm[(p0 + qh + q) + (size_t)i * ld] : Pm[i + (size_t)(p0 + qh + q) * ld]) : 0.0;
+    }
+    for (int e = t; e < 64 * nq; e += 256) {
+      int cc, q;
+      if (QT) { cc = e % 64; q = e / 64; } else { q = e % nq; cc = e / nq; }
+      const int c = tc + cc;
+      Qs[q][cc] = (c < c1) ? (QT ? Qm[c + (size_t)(p0 + qh + q) * ld] : Qm[(p0 + qh + q) + (size_t)c * ld]) : 0.0;
+    }
+    __syncthreads();
+    for (int q = 0; q < nq; ++q) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { a[u] = Ps[q][tr + u]; b[u] = Qs[q][tcol + u]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int c = tc + tcol + v;
+    if (c >= c1) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = ti + tr + u;
+      if (i < i1 && (!LOWER || i >= c)) C[i + (size_t)c * ld] -= acc[u][v];
+    }
+  }
+}
+
+// Row block k0 of the forward substitution L Y = I:  Y[k0 : k0+nb, c] <- L11^-1 Y[k0 : k0+nb, c] for the
+// columns c < ncols (a thread per column).  BWD: the backward substitution L' X = Y (L11^-T instead).
+template <bool BWD>
+__global__ void __launch_bounds__(128) tri_block_solve_kernel(const double* __restrict__ Lm, double* __restrict__ Y, int ld,
+                                                              int k0, int nb, int ncols) {
+  __shared__ double L[kNB][kNB + 1];
+  for (int e = threadIdx.x; e < nb * nb; e += 128) {
+    const int r = e % nb, c = e / nb;
+    L[r][c] = (r >= c) ? Lm[(k0 + r) + (size_t)(k0 + c) * ld] : 0.0;
+  }
+  __syncthreads();
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  if (c >= ncols) return;
+  double* y = Y + (size_t)c * ld + k0;
+  double x[kNB];
+  if (!BWD) {
+#pragma unroll
+    for (int r = 0; r < kNB; ++r) {
+      if (r < nb) {
+        double v = y[r];
+#pragma unroll
+        for (int q = 0; q < kNB; ++q)
+          if (q < r) v -= L[r][q] * x[q];
+        x[r] = v / L[r][r];
+        y[r] = x[r];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < kNB; ++rr) {
+      const int r = kNB - 1 - rr;
+      if (r < nb) {
+        double v = y[r];
+#pragma unroll
+        for (int q = 0; q < kNB; ++q)
+          if (q > r && q < nb) v -= L[q][r] * x[q];
+        x[r] = v / L[r][r];
+        y[r] = x[r];
+      }
+    }
   }
 }
 
@@ -315,12 +418,13 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
   // In-place lower Cholesky of the n x n matrix A (leading dimension ld_n); fail flag on device.
   auto cholesky = [&](double* A, cudaStream_t st) -> int {
     CQP_CUDA(cudaMemsetAsync(dfail, 0, sizeof(int), st));
-    for (int j = 0; j < n; ++j) {
-      chol_scale_kernel<<<1, 256, 0, st>>>(A, ld_n, n, j, dfail);
-      const int rem = n - j - 1;
+    for (int j0 = 0; j0 < n; j0 += kNB) {
+      const int nb = std::min(kNB, n - j0), rem = n - j0 - nb;
+      chol_diag_kernel<<<1, 256, 0, st>>>(A, ld_n, j0, nb, dfail);
       if (rem > 0) {
-        const int tiles = (rem + 31) / 32;
-        chol_update_kernel<<<dim3(tiles, tiles), dim3(32, 8), 0, st>>>(A, ld_n, n, j);
+        chol_panel_kernel<<<(rem + 127) / 128, 128, 0, st>>>(A, ld_n, n, j0, nb);
+        const int tiles = (rem + 63) / 64;
+        tile_update_kernel<false, true, true><<<dim3(tiles, tiles), 256, 0, st>>>(A, A, A, ld_n, j0 + nb, n, j0 + nb, n, j0, nb);
       }
     }
     CQP_CUDA(cudaGetLastError());
@@ -419,16 +523,21 @@ extern "C" int cqp_create(cqp_handle** out, int n, int m, const double* H, const
     // D = kkt^-1: Cholesky, then L Y = I and L' D = Y (layers.cpp:126-130)
     TRY(cholesky(dKkt, st));
     set_identity_kernel<<<blocks_for((size_t)n * n), 256, 0, st>>>(dY, ld_n, n);
-    for (int kk = 0; kk < n; ++kk) {
-      tri_scale_row_kernel<<<(kk + 1 + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, kk, kk + 1);
-      const int rem = n - kk - 1;
+    // L Y = I, block row by block row: only the columns c < k0 + nb of row block k0 are non-zero
+    for (int k0 = 0; k0 < n; k0 += kNB) {
+      const int nb = std::min(kNB, n - k0), ncols = k0 + nb, rem = n - k0 - nb;
+      tri_block_solve_kernel<false><<<(ncols + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, k0, nb, ncols);
       if (rem > 0)
-        fwd_update_kernel<<<dim3((rem + 31) / 32, (kk + 1 + 31) / 32), dim3(32, 8), 0, st>>>(dKkt, dY, ld_n, n, kk);
+        tile_update_kernel<false, false, false><<<dim3((rem + 63) / 64, (ncols + 63) / 64), 256, 0, st>>>(
+            dY, dKkt, dY, ld_n, k0 + nb, n, 0, ncols, k0, nb);
     }
-    for (int kk = n - 1; kk >= 0; --kk) {
-      tri_scale_row_kernel<<<(n + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, kk, n);
-      if (kk > 0)
-        bwd_update_kernel<<<dim3((kk + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, st>>>(dKkt, dY, ld_n, n, kk);
+    // L' D = Y, from the last block row up
+    for (int k0 = (n - 1) / kNB * kNB; k0 >= 0; k0 -= kNB) {
+      const int nb = std::min(kNB, n - k0);
+      tri_block_solve_kernel<true><<<(n + 127) / 128, 128, 0, st>>>(dKkt, dY, ld_n, k0, nb, n);
+      if (k0 > 0)
+        tile_update_kernel<true, false, false><<<dim3((k0 + 63) / 64, (n + 63) / 64), 256, 0, st>>>(
+            dY, dKkt, dY, ld_n, 0, k0, 0, n, k0, nb);
     }
     mirror_lower_kernel<<<blocks_for((size_t)n * n), 256, 0, st>>>(dY, ld_n, n);  // dY = D
     TRY(read_fail(st, &info));

@@ -143,7 +143,7 @@ def test_dense_qp_parity_with_device_offline_stage(G, oracle, n, seeds):
             assert np.abs(lay["D"] - os_.cache.D(k)).max() <= tol * max(1.0, np.abs(os_.cache.D(k)).max())
             assert np.array_equal(lay["rho_vec"], os_.cache.rho_vec(k))
             assert np.abs(lay["b"] - os_.cache.b(k)).max() <= tol * max(1.0, np.abs(os_.cache.b(k)).max())
-        # Two FP64 offline stages (cuSOLVER potrf/potri here, the oracle's Cholesky there) differ
+        # Two FP64 offline stages (the blocked device Cholesky + substitution of cqp_setup.cu here, the oracle's there) differ
         # by ~cond(KKT)*eps in W (up to 1e-10 at these sizes); the x1e3 equality penalties
         # amplify that into the 1e-7 digits of the residual SAMPLES near convergence.  Counts,
         # traces and solutions must still agree.

@@ -89,6 +89,16 @@ def main():
         traffic = sum(to_bytes(r["dram__bytes_read.sum"]) + to_bytes(r["dram__bytes_write.sum"]) for r in recs) / len(recs)
         json.dump({"dram_bytes_per_launch": traffic, "captures": len(recs), "source": f"{TAG}_ncu_summary.json"},
                   open(os.path.join(OUT, "dmma_gemm_traffic.json"), "w"), indent=1)
+    # per-launch DRAM traffic of the batched round kernel (one launch = one check round of 25 layers)
+    rk = prefix + "prof_round.ncu-rep"
+    if rk in summary and summary[rk]:
+        def to_bytes2(s):
+            v, unit = s.split()[0].replace(",", ""), s.split()[1] if len(s.split()) > 1 else "byte"
+            return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+        recs = summary[rk]
+        traffic = sum(to_bytes2(r["dram__bytes_read.sum"]) + to_bytes2(r["dram__bytes_write.sum"]) for r in recs) / len(recs)
+        json.dump({"dram_bytes_per_launch": traffic, "captures": len(recs), "launch": "round_kernel, 4096-column rounds (25 layers each)",
+                   "source": f"{TAG}_ncu_summary.json"}, open(os.path.join(OUT, "round_kernel_traffic.json"), "w"), indent=1)
     # DRAM bytes per iteration of the streamed single-QP tier (tools/profile_tier1.py runs
     # fixed_iters(100)), for bench.py's roofline_single_qp_stream.traffic
     t1 = prefix + "prof_tier1.ncu-rep"
