@@ -414,6 +414,12 @@ struct BatchDev {
   // index}; the round kernel enumerates these, so padding costs it nothing
   TileDesc* ct[2];
   int* n_ct;         // [2]
+  // second slot map: only the columns whose bias rows are stale (first round: all; later: the columns
+  // that switched their ladder level at the last check) -- the bias GEMM runs on this one
+  int* bias_dirty;   // [B]
+  int* cols2;
+  TileDesc* tiles2;
+  int* n_tiles2;
   // settings
   double eps_prim, eps_dual, threshold;
   int adaptive, max_iters;
@@ -438,6 +444,7 @@ __global__ void batch_prepare_kernel(BatchDev b, int initial_index) {
     b.rp[col] = 0.0;
     b.rd[col] = 0.0;
     b.nhist[col] = 0;
+    b.bias_dirty[col] = 1;
     b.trace[(size_t)col * b.rec_cap] = {0, initial_index};  // every call's trace starts here (solver.cpp:50)
   }
 }
@@ -539,6 +546,7 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
           if (k < b.rec_cap) b.trace[(size_t)col * b.rec_cap + k] = {it, cand};
           b.layer[col] = cand;
           b.nsw[col] = k;
+          b.bias_dirty[col] = 1;  // Bias = -[D_k; G D_k] g_s follows the level (layers.cpp:168-175)
         }
       }
     }
@@ -567,6 +575,114 @@ __global__ void batch_decide_kernel(BatchDev b, int it, int check, int early_exi
 // Rebuild the slot map: active columns bucketed by ladder index, every bucket padded to a
 // multiple of 128 with -1 slots, one TileDesc per 128 slots.  Single CTA, deterministic (stable
 // in the column index).
+// Fast path (L <= 16, the default ladder has 13 levels): a counting sort in one pass.  Thread t owns
+// the contiguous columns [t cpt, (t + 1) cpt); per-thread per-level counts, one exclusive scan per
+// level over the threads, then every thread scatters its columns in order (stable in the column
+// index, hence deterministic).  Builds both maps (all active columns / the bias-stale ones).
+constexpr int kRegroupThreads = 256, kRegroupMaxL = 16;
+__global__ void __launch_bounds__(kRegroupThreads) batch_regroup_fast_kernel(BatchDev b) {
+  __shared__ int cnt[2][kRegroupMaxL][kRegroupThreads];
+  __shared__ int tot[2][kRegroupMaxL], base[2][kRegroupMaxL], ntile[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cpt = (b.B + kRegroupThreads - 1) / kRegroupThreads;
+  const int c0 = tid * cpt, c1 = min(b.B, c0 + cpt);
+  for (int k = 0; k < b.L; ++k) { cnt[0][k][tid] = 0; cnt[1][k][tid] = 0; }
+  for (int col = c0; col < c1; ++col) {
+    if (!b.active[col]) continue;
+    const int k = b.layer[col];
+    cnt[0][k][tid] += 1;
+    if (b.bias_dirty[col]) cnt[1][k][tid] += 1;
+  }
+  __syncthreads();
+  // exclusive scan over the threads, one (map, level) row per warp at a time
+  for (int row = warp; row < 2 * b.L; row += kRegroupThreads / 32) {
+    int* v = cnt[row / b.L][row % b.L];
+    int carry = 0;
+    for (int i0 = 0; i0 < kRegroupThreads; i0 += 32) {
+      const int x = v[i0 + lane];
+      int incl = x;
+#pragma unroll
+      for (int w = 1; w < 32; w <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, w);
+        if (lane >= w) incl += y;
+      }
+      v[i0 + lane] = carry + incl - x;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) tot[row / b.L][row % b.L] = carry;
+  }
+  __syncthreads();
+  if (tid < 2) {  // bucket bases (every bucket padded to 128 slots) and tile counts of the two maps
+    int slot = 0, tiles = 0;
+    for (int k = 0; k < b.L; ++k) {
+      base[tid][k] = slot;
+      const int padded = (tot[tid][k] + SLOT_TILE - 1) / SLOT_TILE * SLOT_TILE;
+      slot += padded;
+      tiles += padded / SLOT_TILE;
+    }
+    ntile[tid] = tiles;
+  }
+  __syncthreads();
+  for (int col = c0; col < c1; ++col) {
+    if (!b.active[col]) continue;
+    const int k = b.layer[col];
+    b.cols[base[0][k] + cnt[0][k][tid]++] = col;
+    if (b.bias_dirty[col]) {
+      b.cols2[base[1][k] + cnt[1][k][tid]++] = col;
+      b.bias_dirty[col] = 0;
+    }
+  }
+  for (int map = 0; map < 2; ++map) {
+    int* cols = map ? b.cols2 : b.cols;
+    TileDesc* tiles = map ? b.tiles2 : b.tiles;
+    int t0 = 0;
+    for (int k = 0; k < b.L; ++k) {
+      const int count = tot[map][k], padded = (count + SLOT_TILE - 1) / SLOT_TILE * SLOT_TILE;
+      for (int i = count + tid; i < padded; i += kRegroupThreads) cols[base[map][k] + i] = -1;
+      for (int t = tid; t < padded / SLOT_TILE; t += kRegroupThreads) tiles[t0 + t] = {base[map][k] + t * SLOT_TILE, k};
+      t0 += padded / SLOT_TILE;
+    }
+  }
+  if (tid == 0) {
+    int total = 0;
+    for (int k = 0; k < b.L; ++k) total += tot[0][k];
+    *b.n_tiles = ntile[0];
+    *b.n_tiles2 = ntile[1];
+    *b.n_active = total;
+  }
+  __syncthreads();
+  // non-empty column tiles of the full map (padding slots sit at the end of a bucket: a tile whose first
+  // slot is empty is empty); one warp per granularity, in slot order
+  if (warp < 2) {
+    const int n_tiles = ntile[0];
+    const int bn = warp == 0 ? 64 : 32, sub = SLOT_TILE / bn;
+    int count = 0;
+    for (int k0 = 0; k0 < n_tiles * sub; k0 += 32) {
+      const int k = k0 + lane;
+      bool keep = false;
+      TileDesc td{0, 0};
+      if (k < n_tiles * sub) {
+        // (tile k / sub: recompute instead of re-reading b.tiles, which other threads just wrote)
+        int t = k / sub, lvl = 0, tb = 0;
+        for (; lvl < b.L; ++lvl) {
+          const int nt = (tot[0][lvl] + SLOT_TILE - 1) / SLOT_TILE;
+          if (t < tb + nt) break;
+          tb += nt;
+        }
+        td.slot0 = base[0][lvl] + (t - tb) * SLOT_TILE + (k % sub) * bn;
+        td.a_index = lvl;
+        keep = (td.slot0 - base[0][lvl]) < tot[0][lvl];
+      }
+      const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+      if (keep) b.ct[warp][count + __popc(ballot & ((1u << lane) - 1))] = td;
+      count += __popc(ballot);
+    }
+    if (lane == 0) b.n_ct[warp] = count;
+  }
+}
+
+// General path (any L): one compaction pass per ladder level.  Builds the full map only; the bias map
+// aliases it (every active column gets its bias rows recomputed).
 __global__ void batch_regroup_kernel(BatchDev b) {
   __shared__ int warp_sums[32];
   __shared__ int base_s, slot_base_s, total_active_s;
@@ -726,6 +842,10 @@ struct cqp_batch {
   int* slot_of = nullptr;   // [capacity] column -> slot of its iterate (S0 / S1 are in slot order)
   TileDesc* ct[2] = {nullptr, nullptr};  // non-empty column tiles of 64 / 32 slots (BatchDev::ct)
   int* n_ct = nullptr;
+  int* bias_dirty = nullptr;             // second slot map: the bias-stale columns (BatchDev::cols2)
+  int* cols2 = nullptr;
+  TileDesc* tiles2 = nullptr;
+  int* n_tiles2 = nullptr;
   int slot_cap = 0;         // slots of S0 / S1
   // round kernel (cqp_batch_round.cuh): TMA descriptors of W (box rows 64 / 32) and of the two iterate
   // buffers, the per-round counters {work, done[column tiles]}.  CQP_BATCH_LEGACY=1 keeps the
@@ -1012,6 +1132,7 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   BA(S0, slot_cap * b->ld_s); BA(S1, slot_cap * b->ld_s); BA(bias, cap * b->ld_nm);
   BA(slot_of, cap);
   BA(ct[0], slot_cap / 64 + 1); BA(ct[1], slot_cap / 32 + 1); BA(n_ct, 2);
+  BA(bias_dirty, cap); BA(cols2, slot_cap); BA(tiles2, tile_cap); BA(n_tiles2, 1);
   if (b->verify) { BA(T[0], slot_cap * b->ld_s); BA(T[1], slot_cap * b->ld_s); BA(vres, 2); }
   b->round_ctr_count = 1 + (int)(slot_cap / 32) + 8;
   BA(round_ctrs, (size_t)b->round_ctr_count);
@@ -1071,7 +1192,7 @@ static void batch_destroy_single(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->ct[0], b->ct[1], b->n_ct, b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->bias_dirty, b->cols2, b->tiles2, b->n_tiles2, b->ct[0], b->ct[1], b->n_ct, b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
                   b->trace, b->hist, b->nhist,
@@ -1153,6 +1274,10 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   bd.cols = b->cols; bd.tiles = b->tiles; bd.n_tiles = b->n_tiles; bd.n_active = b->n_active;
   bd.slot_of = b->slot_of;
   bd.ct[0] = b->ct[0]; bd.ct[1] = b->ct[1]; bd.n_ct = b->n_ct;
+  const bool fast_regroup = b->L <= kRegroupMaxL;
+  bd.bias_dirty = b->bias_dirty;
+  bd.cols2 = fast_regroup ? b->cols2 : b->cols; bd.tiles2 = fast_regroup ? b->tiles2 : b->tiles;
+  bd.n_tiles2 = fast_regroup ? b->n_tiles2 : b->n_tiles;
   bd.eps_prim = s.eps_prim; bd.eps_dual = s.eps_dual; bd.threshold = s.rho_switch_threshold;
   bd.adaptive = s.adaptive_rho; bd.max_iters = s.max_iters;
 
@@ -1166,6 +1291,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   base.alpha = 1.0;
   auto gemm_bias = [&](int cfg) {  // Bias = -[D_k; G D_k] g_s  (layers.cpp:168-175), per bucket
     GemmParams p = base;
+    p.cols = bd.cols2; p.tiles = bd.tiles2; p.n_tiles = bd.n_tiles2;  // only the columns whose level changed
     p.A = b->DGb; p.a_stride = (size_t)b->nm_mpad * b->ld_n; p.lda = b->ld_n; p.M = nm;
     p.M_pad = b->nm_mpad; p.k_tiles = b->ld_n / BK;
     p.Bm = b->gs; p.ldb = b->ld_n; p.C = b->bias; p.ldc = b->ld_nm; p.alpha = -1.0; p.mode = 0;
@@ -1217,7 +1343,11 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   };
 
   int rc;
-  batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
+  auto regroup = [&]() {
+    if (fast_regroup) batch_regroup_fast_kernel<<<1, kRegroupThreads, 0, st>>>(bd);
+    else batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
+  };
+  regroup();
   CQP_CUDA(cudaGetLastError());
   b->last_launches += 2;  // prepare, regroup
   if ((rc = gemm_bias(pick_config(b, B)))) return rc;
@@ -1304,7 +1434,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     if ((rc = gemm_plain(b->Gb, m, b->m_mpad, b->ld_n, b->uy, b->ld_n, b->gy, b->ld_m, cfg))) return rc;
     batch_decide_kernel<<<(B + 7) / 8, 256, 0, st>>>(bd, it, r < full_rounds ? 1 : 0, 1);
     CQP_CUDA(cudaGetLastError());
-    batch_regroup_kernel<<<1, 1024, 0, st>>>(bd);
+    regroup();
     CQP_CUDA(cudaGetLastError());
     CQP_CUDA(cudaMemcpyAsync(&b->h_active[r], b->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     CQP_CUDA(cudaEventRecord(b->round_events[r], st));

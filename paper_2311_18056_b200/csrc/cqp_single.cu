@@ -419,7 +419,10 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
 // ladder level fits one thread-block cluster's shared memory use cqp_cluster.cu instead.
 // STREAM selects the L2/HBM tier's code (W through the cp.async.bulk ring) at compile time, so the
 // shared-memory-resident tier keeps its registers.
-template <int RB, bool STREAM, bool COFETCH = STREAM>
+// SERVER: the resident MPC control-step loop (cqp_mpc_server_start) is its own instantiation, so that
+// the plain launches keep their code (wrapping the body in the request loop cost the streamed tier 17 %
+// per iteration: 11.0 -> 12.9 us at D = 4080, same registers, worse schedule).
+template <int RB, bool STREAM, bool COFETCH = STREAM, bool SERVER = false>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   CQP_STAMP0(p.dbg, 0);  // (-DCQP_TRACE: prologue / epilogue timeline of CTA 0, tools/trace_tier1.py)
   if (blockIdx.x == 0 && t == 0) *p.barrier_next = 0u;  // counter of the NEXT launch (ping-pong)
 
-  // Resident MPC server (p.server): the loop below is one control step per request { x0 from the
+  // Resident MPC server (SERVER): the loop below is one control step per request { x0 from the
   // mailbox -> instantiate -> refresh_z -> total_iters layers -> final pass -> answer }; the W slice of
   // the resident tier stays in shared memory between steps.  A plain launch runs the body once.
   unsigned long long served = p.served;
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   for (;;) {
   unsigned long long req = 0;
   long long t_step = 0;
-  if (p.server) {
+  if constexpr (SERVER) {
     if (warp == 0) {
       int want = 1;
       const unsigned long long r = (blockIdx.x == 0) ? server_fetch_request(p, served, lane, want)
@@ -817,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // observable, so the final residual evaluation (solver.cpp:94-95) is skipped; the iterate and u0
   // are the same bits.  What remains of the pass is its grid barrier (every CTA has fetched v_k from the
   // ring before the ring is reset below) and the unscaled controls y[0:nu] for the extraction.
-  const bool fast = p.server && want_full_s == 0ull;
+  const bool fast = SERVER && want_full_s == 0ull;
   if (fast) {
     __syncthreads();
     grid_barrier(p.barrier, epoch, p.G, p.dbg);
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if (blockIdx.x == 0) {
     const Scratch sc = scratch(p, s, xfinal);  // unscaled solution left by the final residual pass
     mpc_extract_control(p, sc.uy, t);
-    if (!p.server || want_full_s) {
+    if (!SERVER || want_full_s) {
       for (int i = t; i < n; i += kThreads) p.out_y[i] = sc.uy[i];
       for (int i = t; i < m; i += kThreads) {
         p.out_z[i] = sc.uz[i];
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       p.state[0] = layer;
     }
   }
-  if (!p.server) break;
+  if constexpr (!SERVER) break;
   // answer: the result record is host-mapped; every writer fences system-wide, then one thread
   // publishes the request number
   __threadfence_system();
@@ -880,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   }
   served = req;
   }  // server loop
-  if (p.server && blockIdx.x == 0 && t == 0) {
+  if (SERVER && blockIdx.x == 0 && t == 0) {
     __threadfence_system();
     p.mb[kMbExited] = 1ull;
   }
@@ -1020,8 +1023,8 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
 template <int RB, bool STREAM, bool COFETCH>
 int launch_run_rb2(cqp_handle* h, RunParams& p) {
   void* args[] = {&p};  // (shared-memory opt-in: set once per handle by set_run_attributes)
-  CQP_CUDA(cudaLaunchCooperativeKernel((const void*)run_kernel<RB, STREAM, COFETCH>, dim3(h->G), dim3(kThreads),
-                                       args, (size_t)h->smem_bytes, h->stream));
+  const void* fn = p.server ? (const void*)run_kernel<RB, STREAM, COFETCH, true> : (const void*)run_kernel<RB, STREAM, COFETCH, false>;
+  CQP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->G), dim3(kThreads), args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
 }
 
@@ -1039,6 +1042,9 @@ int set_run_attributes_rb() {
   CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
   CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
   CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
   return CQP_OK;
 }
 
