@@ -5,9 +5,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2311_18056_b200 import problems, solver as S, _lib
 NAMES = {0: "cmp:start", 1: "cmp:v landed", 10: "cmp15:v landed", 2: "cmp:done", 11: "cmp15:done", 4: "pub:start",
-         5: "pub:full", 6: "pub:published", 7: "pub:rearmed", 8: "ldr:go", 9: "ldr:fetched"}
+         5: "pub:full", 6: "pub:published", 7: "pub:rearmed", 8: "ldr:go", 9: "ldr:fetched",
+         3: "cmp:dot done", 12: "cmp:row ready", 13: "cmp:rearm ok"}
 which = sys.argv[1] if len(sys.argv) > 1 else "quad"
-wl = problems.config4_quadruped(30, 0) if which == "quad" else problems.config3_atlas(30, 0)
+if which == "quad":
+    wl = problems.config4_quadruped(30, 0)
+elif which == "atlas":
+    wl = problems.config3_atlas(30, 0)
+else:
+    wl = problems.config2(int(which[2:]), 0)   # "nu30": the resident tier at D = 900
 base = wl.base_problem()
 s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
 q = wl.problem_at(wl.x0(1.0)); s.update_vectors(q.g, q.c, q.d)
