@@ -69,6 +69,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // One warp: M[row, :] . x with M row-major in global memory (read through L1/L2), x in shared
 // memory, pad entries of both zero.  Fixed order: lane l takes column pairs l, l + 32, ...
+template <bool LDG = true>
 __device__ __forceinline__ double warp_row_dot(const double* __restrict__ Mrow, const double* __restrict__ x,
                                                int ncols_pad, int lane) {
   const double2* m2 = reinterpret_cast<const double2*>(Mrow);
@@ -77,7 +78,7 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ Mrow, 
   double a0 = 0.0, a1 = 0.0;
   int c2 = lane;
   for (; c2 + 32 < nc2; c2 += 64) {
-    const double2 w0 = __ldg(m2 + c2), w1 = __ldg(m2 + c2 + 32);
+    const double2 w0 = LDG ? __ldg(m2 + c2) : m2[c2], w1 = LDG ? __ldg(m2 + c2 + 32) : m2[c2 + 32];
     const double2 x0 = x2[c2], x1 = x2[c2 + 32];
     a0 = fma(w0.x, x0.x, a0);
     a0 = fma(w0.y, x0.y, a0);
@@ -85,7 +86,7 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ Mrow, 
     a1 = fma(w1.y, x1.y, a1);
   }
   if (c2 < nc2) {
-    const double2 w0 = __ldg(m2 + c2);
+    const double2 w0 = LDG ? __ldg(m2 + c2) : m2[c2];
     const double2 x0 = x2[c2];
     a0 = fma(w0.x, x0.x, a0);
     a0 = fma(w0.y, x0.y, a0);
@@ -153,7 +154,8 @@ struct ClSmem {
   double* wmax;   // kClWarps * 8   per-warp partial maxima
   double* cmax;   // 8              this CTA's maxima / the cluster-wide result
   double* norms;  // 2 * 16 * 8     per-CTA maxima of a residual pass, by pass parity (peers write here)
-  unsigned long long* bars;  // xready[2], nbar[2]
+  unsigned long long* bars;  // xready[2], nbar[2], (server: request word, report flag), cbar, gbar
+  double* sx0;    // 2 + kMaxInlineX0   resident server: {request number, report flag, x0} pushed by CTA 0
 };
 
 // Shared-memory doubles: `wrows` rows of W (0 in register mode), the iterate copies, and the
@@ -162,7 +164,8 @@ __host__ __device__ inline size_t cl_smem_doubles(int R, int wrows, int Dpad, in
                                                   int hg_rows_n, int hg_rows_m) {
   const int Rp = (R + 1) & ~1;
   return (size_t)wrows * Dpad + 2 * (size_t)xs_stride + 3 * (size_t)npad + 3 * (size_t)mpad + 3 * (size_t)Rp +
-         (size_t)hg_rows_n * (npad + mpad) + (size_t)hg_rows_m * npad + 32 + kClWarps * 8 + 8 + 2 * 16 * 8 + 8;
+         (size_t)hg_rows_n * (npad + mpad) + (size_t)hg_rows_m * npad + 32 + kClWarps * 8 + 8 + 2 * 16 * 8 + 8 +
+         2 + kMaxInlineX0;
 }
 
 __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& p) {
@@ -189,13 +192,16 @@ __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& 
   s.cmax = s.wmax + kClWarps * 8;
   s.norms = s.cmax + 8;
   s.bars = reinterpret_cast<unsigned long long*>(s.norms + 2 * 16 * 8);
+  s.sx0 = reinterpret_cast<double*>(s.bars + 8);
   return s;
 }
 
 // Makes layer k current: W slice -> shared memory, bias rows b = -[D_k; G D_k] g_s for the rows
 // this CTA owns, 0 on the lambda rows (layers.cpp:168-175).  s.uy is scratch for
 // g_s = cost_scale * E o g (layers.cpp:181).
-__device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int row0, int nrows, bool copy_w = true) {
+// `dg_cache` (resident server): this CTA's rows of [D_k; G D_k] for level k, in shared memory.
+__device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int row0, int nrows, bool copy_w = true,
+                              const double* dg_cache = nullptr) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   __syncthreads();
   if (p.w_smem && copy_w) {
@@ -220,7 +226,8 @@ __device__ void cl_load_layer(const RunParams& p, const ClSmem& s, int k, int ro
   for (int r = warp; r < nrows; r += kClWarps) {
     const int row = row0 + r;
     double bias = 0.0;
-    if (row < nm) bias = -warp_row_dot(DG + (size_t)row * p.npad, s.uy, p.npad, lane);
+    if (row < nm) bias = dg_cache ? -warp_row_dot<false>(dg_cache + (size_t)r * p.npad, s.uy, p.npad, lane)
+                                  : -warp_row_dot(DG + (size_t)row * p.npad, s.uy, p.npad, lane);
     if (lane == 0) s.sb[r] = bias;
   }
   __syncthreads();
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
 
   for (int i = t; i < p.npad; i += kClThreads) s.sE[i] = (i < n) ? p.E[i] : 1.0;
   for (int i = t; i < p.mpad; i += kClThreads) s.sF[i] = (i < m) ? p.F[i] : 1.0;
+  for (int i = n + t; i < p.npad; i += kClThreads) s.sg[i] = 0.0;  // (pad entries; the resident server never rewrites them)
   const bool grid_smem = p.L <= 16;
   if (grid_smem && t < p.L) {
     s.sgrid[t] = p.grid[t];
@@ -402,70 +410,87 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   // step per request { x0 from the mailbox -> instantiate -> refresh_z -> total_iters layers -> final
   // pass -> answer }.  W stays in registers / shared memory between steps.  A plain launch runs the
   // body once.
+  // Resident server, shared-memory caches of what a step reads besides W (srv_cache: when they fit): this
+  // CTA's rows of the bias operator [D_k; G D_k] of the current level, of offset_g / offset_c, c_base,
+  // d_base, and (CTA 0) K, u_lo, u_hi.  From L2 each of these reads is a dependent 0.7 us round trip.
+  double* const c_dg = s.sx0 + 2 + kMaxInlineX0;                 // [R][npad]
+  const int perg = (n + C - 1) / C;
+  double* const c_og = c_dg + (size_t)p.R * p.npad;                // [perg][nxpad]  g rows [rank perg, ...)
+  double* const c_oc = c_og + (size_t)perg * p.mpc_nxpad;          // [R][nxpad]     the z rows this CTA owns
+  double* const c_cb = c_oc + (size_t)p.R * p.mpc_nxpad;           // [R]
+  double* const c_db = c_cb + p.R;                                 // [R]
+  double* const c_K = c_db + p.R;                                  // [nu][nxpad]
+  double* const c_ul = c_K + (size_t)p.mpc_nu * p.mpc_nxpad;       // [nu]
+  double* const c_uh = c_ul + p.mpc_nu;                            // [nu]
+  const bool cached = p.server && p.srv_cache;
+  const int zlo = max(row0, n) - n, zhi = max(zlo, min(row0 + nrows, n + m) - n);  // z rows of this CTA: [zlo, zhi)
+  int cached_dg_layer = -1;
+  auto cache_dg = [&](int k) {  // (all threads; callers synchronise afterwards)
+    const double* DG = p.Dk + (size_t)k * (n + m) * p.npad;
+    for (int e = t; e < nrows * p.npad; e += kClThreads) {
+      const int r = e / p.npad, cidx = e - r * p.npad;
+      c_dg[e] = (row0 + r < n + m) ? __ldg(DG + (size_t)(row0 + r) * p.npad + cidx) : 0.0;
+    }
+    cached_dg_layer = k;
+  };
+  if (cached) {
+    cache_dg(layer);
+    const int ga = (int)rank * perg, gb = min(n, ga + perg);
+    for (int e = t; e < max(0, gb - ga) * p.mpc_nxpad; e += kClThreads) c_og[e] = p.mpc_og[(size_t)ga * p.mpc_nxpad + e];
+    for (int e = t; e < (zhi - zlo) * p.mpc_nxpad; e += kClThreads) c_oc[e] = p.mpc_oc[(size_t)zlo * p.mpc_nxpad + e];
+    for (int e = t; e < zhi - zlo; e += kClThreads) { c_cb[e] = p.mpc_cb[zlo + e]; c_db[e] = p.mpc_db[zlo + e]; }
+    if (rank == 0) {
+      for (int e = t; e < p.mpc_nu * p.mpc_nxpad; e += kClThreads) c_K[e] = p.mpc_K[e];
+      for (int e = t; e < p.mpc_nu; e += kClThreads) { c_ul[e] = p.mpc_ulo[e]; c_uh[e] = p.mpc_uhi[e]; }
+    }
+    __syncthreads();
+  }
   unsigned long long served = p.served;
   int resident_layer = -1;  // ladder level whose W slice is in shared memory (shared-memory mode)
   // (two spare words of the barrier block: the kernel may not own static shared memory, its dynamic
   // allocation is the full 227 KB)
   unsigned long long& cmd_s = s.bars[4];
   unsigned long long& want_full_s = s.bars[5];
-  for (;;) {
-  unsigned long long req = 0;
-  long long t_step = 0;
-  if (p.server) {
-    if (warp == 0) {
-      int want = 1;
-      const unsigned long long r = (rank == 0) ? server_fetch_request(p, served, lane, want)
-                                               : (lane == 0 ? server_wait_relay(p, served, want) : 0ull);
-      if (lane == 0) { cmd_s = r; want_full_s = (unsigned long long)want; }
+  unsigned long long* cbar = s.bars + 6;  // resident server: the request has landed in s.sx0
+  unsigned long long* gbar = s.bars + 7;  // resident server: g is complete in s.sg
+  // The pieces of a step's prologue.  A plain launch runs them in the reference's order; the resident
+  // server moves everything that does not depend on the request (barriers, refresh_z, v_0) in FRONT of the
+  // wait for it, so that it overlaps the host's turnaround instead of sitting on the step's critical path.
+  bool first_step = true;
+  auto init_barriers = [&]() {  // no peer pushes into this CTA between its final residual pass of the previous
+    if (t == 0) {               // step and the next cluster barrier
+      if (!first_step) {
+        for (int k = 0; k < 4; ++k) mbar_inval(&s.bars[k]);
+        mbar_inval(cbar); mbar_inval(gbar);
+      }
+      for (int k = 0; k < 4; ++k) mbar_init(&s.bars[k], 1);
+      mbar_init(cbar, 1); mbar_init(gbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(&xready[0], xbytes);  // first use: v_2
+      mbar_arm(&xready[1], xbytes);  // first use: v_1
+      mbar_arm(&nbar[0], 7u * 8u * (unsigned)C);
+      mbar_arm(&nbar[1], 7u * 8u * (unsigned)C);
+      if (p.server) {
+        mbar_arm(cbar, 8u * (unsigned)(2 + p.mpc_nx));  // the request: {number, report flag, x0} from CTA 0
+        mbar_arm(gbar, 8u * (unsigned)n);               // g = offset_g x0: every CTA pushes its rows to every CTA
+      }
+    }
+  };
+  auto step_vectors = [&]() {  // g and the clamp bounds of the rows this CTA owns (layers.cpp:182-186, 223-226)
+    for (int i = t; i < p.npad; i += kClThreads) s.sg[i] = (i < n) ? __ldcg(p.g + i) : 0.0;
+    for (int r = t; r < nrows; r += kClThreads) {
+      const int row = row0 + r;
+      double lo = -INFINITY, hi = INFINITY;  // c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
+      if (row >= n && row < n + m) {
+        lo = s.sF[row - n] * __ldcg(p.c + row - n);
+        hi = s.sF[row - n] * __ldcg(p.d + row - n);
+      }
+      s.slo[r] = lo;
+      s.shi[r] = hi;
     }
     __syncthreads();
-    req = cmd_s;
-    if (req == kSrvExit) break;
-    t_step = globaltimer_ns();
-    // mpc::instantiate (mpc.cpp:260-270): this CTA's share of the rows of [g; c; d]
-    const int rows = n + m, per = (rows + C - 1) / C;
-    const int r0 = (int)rank * per, r1 = min(rows, r0 + per);
-    for (int row = r0 + warp; row < r1; row += kClWarps)
-      instantiate_row(row, lane, p.mpc_og, p.mpc_oc, p.mpc_cb, p.mpc_db, p.mpc_x0, n, p.mpc_nx, p.mpc_nxpad, p.g_w, p.c_w, p.d_w);
-    __threadfence();
-  }
-  // (re-)initialise the mbarriers of this step: no peer pushes into this CTA between its final residual
-  // pass of the previous step and the cluster barrier below
-  if (t == 0) {
-    if (served != p.served) for (int k = 0; k < 4; ++k) mbar_inval(&s.bars[k]);  // (not the first step)
-    for (int k = 0; k < 4; ++k) mbar_init(&s.bars[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arm(&xready[0], xbytes);  // first use: v_2
-    mbar_arm(&xready[1], xbytes);  // first use: v_1
-    mbar_arm(&nbar[0], 7u * 8u * (unsigned)C);
-    mbar_arm(&nbar[1], 7u * 8u * (unsigned)C);
-  }
-  if (p.server) {
-    __syncthreads();
-    cluster_sync_all();  // every CTA's rows of g, c, d are visible
-  }
-  for (int i = t; i < p.npad; i += kClThreads) s.sg[i] = (i < n) ? __ldcg(p.g + i) : 0.0;
-  __syncthreads();
-  // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
-  // (layers.cpp:182-186, 223-226)
-  for (int r = t; r < nrows; r += kClThreads) {
-    const int row = row0 + r;
-    double lo = -INFINITY, hi = INFINITY;
-    if (row >= n && row < n + m) {
-      lo = s.sF[row - n] * __ldcg(p.c + row - n);
-      hi = s.sF[row - n] * __ldcg(p.d + row - n);
-    }
-    s.slo[r] = lo;
-    s.shi[r] = hi;
-  }
-  __syncthreads();
-  CQP_STAMP0(p.dbg, 1);
-  // (No cluster barrier here: nobody pushes into a peer before the barrier that follows the v_0
-  // load below, and that one also orders every peer's mbarrier initialisation before the pushes.)
-  CQP_STAMP0(p.dbg, 2);
-
-  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in p.vq (slot 0)
-  if (p.do_refresh) {
+  };
+  auto refresh_z = [&]() {  // Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in p.vq (slot 0)
     for (int i = t; i < p.npad; i += kClThreads) s.uy[i] = (i < n) ? __ldcg(p.vq + i) : 0.0;
     __syncthreads();
     const int per = (m + C - 1) / C;
@@ -477,20 +502,106 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
     __syncthreads();
     cluster_sync_all();  // release/acquire at cluster scope: the peers' rows of z_s are visible
+  };
+  auto load_v0 = [&]() {  // v_0 -> xs[0]; pad slots of both copies stay zero for the whole step
+    for (int i = t; i < XS; i += kClThreads) {
+      s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
+      s.xs[XS + i] = 0.0;
+    }
+    __syncthreads();
+    cluster_sync_all();  // peers write into xs[1] as soon as they finish iteration 1 (and: every peer's
+                         // mbarrier initialisation is ordered before the pushes)
+  };
+  for (;;) {
+  unsigned long long req = 0;
+  long long t_step = 0;
+  if (p.server) {
+    // before the request: everything of the step that only needs the previous step's result
+    init_barriers();
+    refresh_z();
+    load_v0();
+    // The request.  Warp 0 of CTA 0 polls the host-mapped mailbox, then pushes {number, report flag, x0}
+    // into every CTA's shared memory with st.async (completion counted on the receiver's cbar): no L2
+    // relay, and x0 is where instantiate needs it.
+    if (rank == 0 && warp == 0) {
+      int want = 1;
+      double* stage = s.norms;  // (2 * 16 * 8 doubles, idle between residual passes)
+      const unsigned long long r = server_fetch_request(p, served, lane, want, stage);  // (x0 -> stage[2 ...] and the device copy)
+      if (lane == 0) {
+        stage[0] = __longlong_as_double((long long)r);
+        stage[1] = (double)want;
+      }
+      __syncwarp();
+      const int words = 2 + p.mpc_nx;
+      for (int idx = lane; idx < words * C; idx += 32) {
+        const int peer_c = idx % C, word = idx / C;
+        st_async_f64(map_to_cta(smem_u32(s.sx0 + word), (unsigned)peer_c), stage[word], map_to_cta(smem_u32(cbar), (unsigned)peer_c));
+      }
+    }
+    mbar_wait_cluster(cbar, 0, p.dbg, 7, 0);
+    req = (unsigned long long)__double_as_longlong(s.sx0[0]);
+    if (t == 0) { cmd_s = req; want_full_s = (unsigned long long)(s.sx0[1] != 0.0); }
+    __syncthreads();
+    if (req == kSrvExit) break;
+    t_step = globaltimer_ns();
+    // mpc::instantiate (mpc.cpp:260-270).  g rows: this CTA's share, pushed to every CTA's s.sg (gbar);
+    // c, d rows: exactly the z rows this CTA owns in the iterate, so the clamp bounds need no exchange.
+    // All of g, c, d also go to global memory (the report's final clamp and later plain calls read them).
+    {
+      const double* x0s = s.sx0 + 2;
+      const int ga = (int)rank * perg, gb = min(n, ga + perg);
+      for (int row = ga + warp; row < gb; row += kClWarps) {
+        const double* M = cached ? c_og + (size_t)(row - ga) * p.mpc_nxpad : p.mpc_og + (size_t)row * p.mpc_nxpad;
+        double acc = 0.0;
+        for (int j = lane; j < p.mpc_nx; j += 32) acc = fma(M[j], x0s[j], acc);
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+        if (lane < C) st_async_f64(map_to_cta(smem_u32(s.sg + row), (unsigned)lane), acc, map_to_cta(smem_u32(gbar), (unsigned)lane));
+        if (lane == 0) p.g_w[row] = acc;
+      }
+      for (int j = zlo + warp; j < zhi; j += kClWarps) {
+        const double* M = cached ? c_oc + (size_t)(j - zlo) * p.mpc_nxpad : p.mpc_oc + (size_t)j * p.mpc_nxpad;
+        double acc = 0.0;
+        for (int q = lane; q < p.mpc_nx; q += 32) acc = fma(M[q], x0s[q], acc);
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+        if (lane == 0) {
+          const double cj = (cached ? c_cb[j - zlo] : p.mpc_cb[j]) - acc, dj = (cached ? c_db[j - zlo] : p.mpc_db[j]) - acc;
+          p.c_w[j] = cj;
+          p.d_w[j] = dj;
+          s.slo[n + j - row0] = s.sF[j] * cj;   // c~, d~ of this row (layers.cpp:182-186)
+          s.shi[n + j - row0] = s.sF[j] * dj;
+        }
+      }
+      for (int r = t; r < nrows; r += kClThreads)
+        if (row0 + r < n || row0 + r >= n + m) { s.slo[r] = -INFINITY; s.shi[r] = INFINITY; }
+    }
+#ifdef CQP_SRV_TRACE
+#define SRV_STAMP(k) do { if (p.server && rank == 0 && t == 0) p.mb[kMbX0 + 100 + (k)] = (unsigned long long)(globaltimer_ns() - t_step); } while (0)
+#else
+#define SRV_STAMP(k) do {} while (0)
+#endif
+    SRV_STAMP(0);  // instantiate rows pushed
+    mbar_wait_cluster(gbar, 0, p.dbg, 8, 0);
+    __syncthreads();
+    SRV_STAMP(1);  // g complete
+    CQP_STAMP0(p.dbg, 3);
+    if (cached && cached_dg_layer != layer) { cache_dg(layer); __syncthreads(); }
+    cl_load_layer(p, s, layer, row0, nrows, resident_layer != layer, cached ? c_dg : nullptr);  // (bias rows; W only when it changed)
+    resident_layer = layer;
+    SRV_STAMP(2);  // bias rows done
+  } else {
+    init_barriers();
+    step_vectors();
+    CQP_STAMP0(p.dbg, 1);
+    if (p.do_refresh) refresh_z();
+    CQP_STAMP0(p.dbg, 3);
+    cl_load_layer(p, s, layer, row0, nrows, resident_layer != layer);  // (bias rows; the W slice only when it changed)
+    resident_layer = layer;
+    CQP_STAMP0(p.dbg, 4);
+    load_v0();
   }
-
-  CQP_STAMP0(p.dbg, 3);
-  cl_load_layer(p, s, layer, row0, nrows, resident_layer != layer);  // (bias rows; the W slice only when it changed)
-  resident_layer = layer;
-  CQP_STAMP0(p.dbg, 4);
-
-  // v_0 -> xs[0]; pad slots of both copies stay zero for the whole launch
-  for (int i = t; i < XS; i += kClThreads) {
-    s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
-    s.xs[XS + i] = 0.0;
-  }
-  __syncthreads();
-  cluster_sync_all();  // peers write into xs[1] as soon as they finish iteration 1
+  first_step = false;
   CQP_STAMP0(p.dbg, 5);
 
   int n_trace = 1, n_hist = 0, pass = 0;
@@ -645,7 +756,8 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
           p.trace[2 * n_trace + 1] = cand;
         }
         ++n_trace;
-        cl_load_layer(p, s, layer, row0, nrows);
+        if (cached) { __syncthreads(); cache_dg(layer); __syncthreads(); }
+        cl_load_layer(p, s, layer, row0, nrows, true, cached ? c_dg : nullptr);
         resident_layer = layer;
         load_registers(layer);
       }
@@ -658,6 +770,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   }
 
   // ---- epilogue (solver.cpp:90-99) ----
+  SRV_STAMP(3);  // iterations issued
   CQP_STAMP0(p.dbg, 6);
   const int bf = iters_done & 1;
   if (iters_done >= 1 && have != iters_done)
@@ -676,13 +789,33 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
       __syncthreads();
     }
   } else {
+    if (p.server) {  // the final clamp reads every CTA's rows of c, d from global memory
+      __threadfence();
+      __syncthreads();
+      cluster_sync_all();
+    }
     cl_residual_pass(p, s, xfinal, true, pass++, rank, C, nrm);
   }
   CQP_STAMP0(p.dbg, 8);
   // between-launch invariant: p.vq slot 0 = iterate (slots 1..3 keep the grid kernel's sentinel)
   for (int r = t; r < nrows; r += kClThreads) p.vq[row0 + r] = xfinal[row0 + r];
   if (rank == 0) {
-    mpc_extract_control(p, s.uy, t);
+    if (cached) {
+      // u0 = clamp(-K x0 + y[0:nu], u_lo, u_hi) (bench.cpp:169-175) from the shared-memory copies of K and
+      // x0; same operation order as mpc_extract_control
+      const double* x0s = s.sx0 + 2;
+      for (int c = t; c < p.mpc_nu; c += kClThreads) {
+        const double* Krow = c_K + (size_t)c * p.mpc_nxpad;
+        double kx = 0.0;
+        for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], x0s[j], kx);
+        double u = -kx + s.uy[c];
+        u = u < c_ul[c] ? c_ul[c] : u;
+        u = u > c_uh[c] ? c_uh[c] : u;
+        p.out_u[c] = u;
+      }
+    } else {
+      mpc_extract_control(p, s.uy, t, p.server ? s.sx0 + 2 : nullptr);
+    }
     if (p.Dpad != D && t == 0) p.vq[D] = 0.0;
     if (!p.server || want_full_s) {
       for (int i = t; i < n; i += kClThreads) p.out_y[i] = s.uy[i];
@@ -691,7 +824,8 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
         p.out_lam[i] = s.ul[i];
       }
     }
-    if (t == 0) {
+    if (t == 0 && fast) p.state[0] = layer;  // (u0-only step: the host does not read the record's head)
+    if (t == 0 && !fast) {
       DevResultHead h;
       h.r_prim = nrm[0];
       h.r_dual = nrm[1];
@@ -706,16 +840,16 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
   }
   if (!p.server) break;
+  SRV_STAMP(4);  // results written
   // answer: the result record is host-mapped; every writer fences system-wide, then one thread
   // publishes the request number.  The cluster barrier also keeps the next step's instantiate /
   // relay from overwriting g, c, d, x0 while a peer still reads them.
-  __threadfence_system();
-  __syncthreads();
-  if (rank == 0 && t == 0) {
-    p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);
-    __threadfence_system();
-    p.mb[kMbResp] = req;
-  }
+  // (a u0-only step wrote nu <= 32 words from warp 0 of CTA 0: only that warp fences)
+  if (rank == 0 && t == 0) p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);  // (up to the fence)
+  if (!fast || (rank == 0 && warp == 0)) __threadfence_system();
+  if (!fast) __syncthreads(); else __syncwarp();
+  SRV_STAMP(5);  // system fence done
+  if (rank == 0 && t == 0) p.mb[kMbResp] = req;
   served = req;
   cluster_sync_all();
   }  // server loop
@@ -733,7 +867,7 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
 // the handle is configured (ClOp::Fits), never on the launch path; the attributes are per function
 // and device, so they are set to the maximum (handles of different sizes share the functions).
 template <int RPW, int NPT>
-int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, bool set_attrs) {
+int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, bool set_attrs, size_t extra_smem = 0) {
   auto fn = cluster_kernel<RPW, NPT>;
   if (set_attrs) {
     CQP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
@@ -742,7 +876,7 @@ int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribu
   cfg = cudaLaunchConfig_t{};
   cfg.gridDim = dim3(h->G);
   cfg.blockDim = dim3(kClThreads);
-  cfg.dynamicSmemBytes = (size_t)h->smem_bytes;
+  cfg.dynamicSmemBytes = (size_t)h->smem_bytes + extra_smem;
   cfg.stream = h->stream;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)h->G;
@@ -755,12 +889,20 @@ int cluster_launch_cfg(cqp_handle* h, cudaLaunchConfig_t& cfg, cudaLaunchAttribu
 
 enum class ClOp { Launch, Fits };
 
+// Shared memory of the resident server's caches (see the kernel): rows of the bias operator, of the MPC
+// template and of K, for one CTA.
+size_t server_cache_bytes(const cqp_handle* h) {
+  const size_t R = (size_t)h->R, perg = (size_t)(h->n + h->G - 1) / h->G, nxp = (size_t)h->mpc_nxpad, nu = (size_t)h->mpc_nu;
+  return sizeof(double) * (R * h->npad + perg * nxp + R * nxp + 2 * R + nu * nxp + 2 * nu);
+}
+
 // Launch, or ask whether the device schedules one cluster of h->G CTAs with h->smem_bytes each.
 template <int RPW, int NPT>
 int cluster_do(ClOp op, cqp_handle* h, const RunParams* p) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
-  int rc = cluster_launch_cfg<RPW, NPT>(h, cfg, attr, op == ClOp::Fits);
+  const size_t extra = (op == ClOp::Launch && p && p->server && p->srv_cache) ? server_cache_bytes(h) : 0;
+  int rc = cluster_launch_cfg<RPW, NPT>(h, cfg, attr, op == ClOp::Fits, extra);
   if (op == ClOp::Fits) {
     int clusters = 0;
     if (rc != CQP_OK || cudaOccupancyMaxActiveClusters(&clusters, cluster_kernel<RPW, NPT>, &cfg) != cudaSuccess) {
@@ -842,6 +984,7 @@ int launch_cluster(cqp_handle* h, const RunParams& p0) {
   p.w_smem = h->w_smem;
   p.xs_stride = h->xs_stride;
   p.hg_smem = h->hg_smem;
+  p.srv_cache = (p.server && (size_t)h->smem_bytes + server_cache_bytes(h) <= (size_t)kMaxSmemBytes) ? 1 : 0;
   return cluster_dispatch(ClOp::Launch, h, &p);
 }
 

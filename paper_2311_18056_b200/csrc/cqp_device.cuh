@@ -259,8 +259,11 @@ __device__ __forceinline__ void instantiate_row(int row, int lane, const double*
 // request it fetches x0 with all lanes at once (one PCIe round trip), stores it to the device copy and
 // republishes the request number in device memory for the other CTAs (release).  Returns the request
 // number, or kSrvExit when told to stop / idle for too long.  Call with the whole warp.
+// `stage` (shared memory, optional): x0 is also left at stage[2 ...] for a caller that forwards the request
+// itself (the cluster kernel pushes it through distributed shared memory); the device-memory relay and
+// its fence are then skipped.
 __device__ __forceinline__ unsigned long long server_fetch_request(const RunParams& p, unsigned long long served, int lane,
-                                                                   int& want_full) {
+                                                                   int& want_full, double* stage = nullptr) {
   unsigned long long seq = served;
   if (lane == 0) {
     const long long t0 = globaltimer_ns();
@@ -282,12 +285,15 @@ __device__ __forceinline__ unsigned long long server_fetch_request(const RunPara
     want_full = (int)__shfl_sync(0xffffffffu, wf, 0);
 #pragma unroll
     for (int u = 0; u < kMaxInlineX0 / 32; ++u)
-      if (lane + 32 * u < p.mpc_nx) p.mpc_x0_w[lane + 32 * u] = v[u];
-    __threadfence();
+      if (lane + 32 * u < p.mpc_nx) {
+        p.mpc_x0_w[lane + 32 * u] = v[u];
+        if (stage) stage[2 + lane + 32 * u] = v[u];
+      }
+    if (!stage) __threadfence();
     __syncwarp();
   }
   // (the relay word carries "full report wanted" in bit 62: every CTA must take the same path)
-  if (lane == 0) st_release_gpu_u64(p.srv_seq, seq == kSrvExit ? seq : (seq | ((unsigned long long)(want_full != 0) << 62)));
+  if (lane == 0 && !stage) st_release_gpu_u64(p.srv_seq, seq == kSrvExit ? seq : (seq | ((unsigned long long)(want_full != 0) << 62)));
   return seq;
 }
 
@@ -303,12 +309,12 @@ __device__ __forceinline__ unsigned long long server_wait_relay(const RunParams&
 // Control extraction of the closed loop (bench.cpp:169-175): u0 = clamp(-K x + y[0:nu], u_lo, u_hi).
 // `y` is the unscaled primal solution in shared memory; executed by one CTA (thread `t0` takes
 // controls t0, t0 + blockDim.x, ...).
-__device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t0) {
+__device__ __forceinline__ void mpc_extract_control(const RunParams& p, const double* y, int t0, const double* x0_smem = nullptr) {
   if (!p.mpc_K) return;
   for (int t = t0; t < p.mpc_nu; t += (int)blockDim.x) {
     const double* Krow = p.mpc_K + (size_t)t * p.mpc_nxpad;
     double kx = 0.0;
-    for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], __ldcg(p.mpc_x0 + j), kx);
+    for (int j = 0; j < p.mpc_nx; ++j) kx = fma(Krow[j], x0_smem ? x0_smem[j] : __ldcg(p.mpc_x0 + j), kx);
     double u = -kx + y[t];
     const double lo = p.mpc_ulo[t], hi = p.mpc_uhi[t];
     u = u < lo ? lo : u;

@@ -130,6 +130,7 @@ struct RunParams {
   // resident MPC server (server != 0): the kernel loops { wait for x0 in the mailbox; instantiate;
   // refresh_z; total_iters iterations; final pass; answer } until told to stop or idle for idle_ns
   int server;
+  int srv_cache;                      // cluster kernel: template / bias-operator rows cached in shared memory
   volatile unsigned long long* mb;    // mailbox (kMb* words), host-mapped
   unsigned long long served;          // newest request already answered when the kernel starts
   unsigned long long* srv_seq;        // device relay: CTA 0 republishes the request number here

@@ -874,13 +874,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   if constexpr (!SERVER) break;
   // answer: the result record is host-mapped; every writer fences system-wide, then one thread
   // publishes the request number
-  __threadfence_system();
+  if (blockIdx.x == 0 && t == 0) p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);  // (up to the fence)
+  if (blockIdx.x == 0) __threadfence_system();  // (only CTA 0 writes the record)
   __syncthreads();
-  if (blockIdx.x == 0 && t == 0) {
-    p.mb[kMbStepNs] = (unsigned long long)(globaltimer_ns() - t_step);
-    __threadfence_system();
-    p.mb[kMbResp] = req;
-  }
+  if (blockIdx.x == 0 && t == 0) p.mb[kMbResp] = req;
   served = req;
   }  // server loop
   if (SERVER && blockIdx.x == 0 && t == 0) {

@@ -1,15 +1,21 @@
-for sl in 0 200 500 800 1200; do for nu in 30 50; do CQP_IDLE_SLEEP_NS=$sl python - <<PY
-import sys, os; sys.path.insert(0,'.')
-from paper_2311_18056_b200 import problems, solver as S
-wl = problems.config2($nu, 0); base = wl.base_problem()
-s = S.Solver(base.H, base.g, base.G, base.c, base.d, S.SolverSettings(max_iters=100000))
-q = wl.problem_at(wl.x0(10.0)); s.update_vectors(q.g, q.c, q.d)
-ts = {}
-for k in (1000, 4000):
-    v = []
-    for _ in range(3):
-        s.cold_start(); v.append(s.fixed_iters(k).kernel_us)
-    ts[k] = sorted(v)[1]
-print("sleep", $sl, "nu", $nu, "D", 3*base.n, "us/iter %.3f" % ((ts[4000]-ts[1000])/3000), flush=True)
+export CQP_B200_LIB=$PWD/build/trace/libcqp_b200.so
+python - <<'PY'
+import sys, ctypes as C, numpy as np
+sys.path.insert(0, '.')
+from paper_2311_18056_b200 import problems, solver as S, _lib
+wl = problems.config1(seed=0); base = wl.base_problem()
+gpu = S.Solver(base.H, base.g, base.G, base.c, base.d); gpu.set_mpc_template(wl.tmpl, wl.limits)
+q = wl.problem_at(wl.x0(1.0)); gpu.update_vectors(q.g, q.c, q.d); gpu.cold_start(); gpu.solve()
+gpu.mpc_server_start(1)
+x = np.ascontiguousarray(wl.x0(1.0)); u0 = np.zeros(wl.sys.nu)
+A, B = wl.sys.A, wl.sys.B
+# find mailbox: not exposed; read stamps through a debug hook: the stamps live in the host-mapped mailbox -> expose via ctypes on the handle? use cqp_mpc_server_last_timing only
+for t in range(200):
+    gpu.mpc_step_x0_fast(x, 1, u0); x = np.ascontiguousarray(A @ x + B @ u0)
+print("timing", gpu.mpc_server_last_timing())
+lib = _lib.load()
+buf = (C.c_ulonglong * 8)()
+lib.cqp_debug_server_stamps.argtypes = [C.c_void_p, C.POINTER(C.c_ulonglong)]
+lib.cqp_debug_server_stamps(gpu._h, buf)
+print("stamps ns: pushed, g complete, bias, iterations, results, sysfence:", list(buf)[:6])
 PY
-done; done
