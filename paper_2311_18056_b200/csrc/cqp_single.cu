@@ -506,46 +506,21 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   // allocation is the full 227 KB)
   unsigned long long& cmd_s = s.bars[5];
   unsigned long long& want_full_s = s.bars[6];
-  for (;;) {
-  unsigned long long req = 0;
-  long long t_step = 0;
-  if constexpr (SERVER) {
-    if (warp == 0) {
-      int want = 1;
-      const unsigned long long r = (blockIdx.x == 0) ? server_fetch_request(p, served, lane, want)
-                                                     : (lane == 0 ? server_wait_relay(p, served, want) : 0ull);
-      if (lane == 0) { cmd_s = r; want_full_s = (unsigned long long)want; }
+  // The pieces of a step's prologue.  A plain launch runs them in the reference's order; the resident
+  // server runs everything that does not depend on the request (refresh_z, v_0) BEFORE it waits for it.
+  auto step_bounds = [&]() {  // c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf] (layers.cpp:182-186, 223-226)
+    for (int r = t; r < nrows; r += kThreads) {
+      const int row = row0 + r;
+      double lo = -INFINITY, hi = INFINITY;
+      if (row >= n && row < n + m) {
+        lo = p.F[row - n] * __ldcg(p.c + row - n);
+        hi = p.F[row - n] * __ldcg(p.d + row - n);
+      }
+      s.slo[r] = lo;
+      s.shi[r] = hi;
     }
-    __syncthreads();
-    req = cmd_s;
-    if (req == kSrvExit) break;
-    t_step = globaltimer_ns();
-    if (t == 0 && served != p.served) init_barriers(true);  // (every role left them behind the last residual pass)
-    // mpc::instantiate (mpc.cpp:260-270): this CTA's share of the rows of [g; c; d]
-    const int rows = n + m, per = (rows + p.G - 1) / p.G;
-    const int r0 = (int)blockIdx.x * per, r1 = min(rows, r0 + per);
-    for (int row = r0 + warp; row < r1; row += kWarps)
-      instantiate_row(row, lane, p.mpc_og, p.mpc_oc, p.mpc_cb, p.mpc_db, p.mpc_x0, n, p.mpc_nx, p.mpc_nxpad, p.g_w, p.c_w, p.d_w);
-    __threadfence();
-    // every CTA's rows of g, c, d (and the previous step's iterate rows in slot 0) are visible
-    grid_barrier(p.barrier, epoch, p.G, p.dbg);
-  }
-
-  // clamp bounds of the rows this CTA owns: c~ = [-inf; F o c; -inf], d~ = [+inf; F o d; +inf]
-  // (layers.cpp:182-186, 223-226)
-  for (int r = t; r < nrows; r += kThreads) {
-    const int row = row0 + r;
-    double lo = -INFINITY, hi = INFINITY;
-    if (row >= n && row < n + m) {
-      lo = p.F[row - n] * __ldcg(p.c + row - n);
-      hi = p.F[row - n] * __ldcg(p.d + row - n);
-    }
-    s.slo[r] = lo;
-    s.shi[r] = hi;
-  }
-
-  // optional Solver::refresh_z (solver.cpp:197-200): z_s <- G_s y_s, in place in slot 0
-  if (p.do_refresh) {
+  };
+  auto refresh_rows = [&]() {  // Solver::refresh_z (solver.cpp:197-200): this CTA's rows of z_s <- G_s y_s, in slot 0
     double* v = p.vq;
     const Scratch sc = scratch(p, s, nullptr);  // (no iterate in shared memory yet)
     for (int i = t; i < p.npad; i += kThreads) sc.uy[i] = (i < n) ? __ldcg(v + i) : 0.0;
@@ -557,21 +532,59 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       const double zs = warp_row_dot_mlp<8>(p.Gs + (size_t)row * p.npad, sc.uy, p.npad, lane);
       if (lane == 0) __stcg(v + n + row, zs);
     }
-    grid_barrier_arrive(p.barrier, epoch, p.G);  // (waited for below: the bias rows do not depend on z_s)
+  };
+  auto load_v0 = [&]() {  // v_0 -> xs[0] (slot 0 holds the iterate between launches / steps)
+    for (int i = t; i < XS; i += kThreads) {
+      s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
+      s.xs[XS + i] = 0.0;
+    }
+    __syncthreads();
+  };
+  for (;;) {
+  unsigned long long req = 0;
+  long long t_step = 0;
+  if constexpr (SERVER) {
+    // before the request: what only needs the previous step's result
+    if (served != p.served) {
+      grid_barrier(p.barrier, epoch, p.G, p.dbg);  // every CTA's rows of the last iterate are in slot 0
+      if (t == 0) init_barriers(true);              // (every role left them behind the last pass)
+    }
+    refresh_rows();
+    grid_barrier(p.barrier, epoch, p.G, p.dbg);    // every CTA's rows of z_s are in slot 0
+    load_v0();
+    if (warp == 0) {
+      int want = 1;
+      const unsigned long long r = (blockIdx.x == 0) ? server_fetch_request(p, served, lane, want)
+                                                     : (lane == 0 ? server_wait_relay(p, served, want) : 0ull);
+      if (lane == 0) { cmd_s = r; want_full_s = (unsigned long long)want; }
+    }
+    __syncthreads();
+    req = cmd_s;
+    if (req == kSrvExit) break;
+    t_step = globaltimer_ns();
+    // mpc::instantiate (mpc.cpp:260-270): this CTA's share of the rows of [g; c; d]
+    const int rows = n + m, per = (rows + p.G - 1) / p.G;
+    const int r0 = (int)blockIdx.x * per, r1 = min(rows, r0 + per);
+    for (int row = r0 + warp; row < r1; row += kWarps)
+      instantiate_row(row, lane, p.mpc_og, p.mpc_oc, p.mpc_cb, p.mpc_db, p.mpc_x0, n, p.mpc_nx, p.mpc_nxpad, p.g_w, p.c_w, p.d_w);
+    __threadfence();
+    grid_barrier(p.barrier, epoch, p.G, p.dbg);    // every CTA's rows of g, c, d are visible
+    step_bounds();
+    load_layer<RB>(p, s, layer, row0, nrows, nullptr, resident_layer != layer);  // (bias rows; scratch in the second copy)
+    resident_layer = layer;
+  } else {
+    step_bounds();
+    if (p.do_refresh) {
+      refresh_rows();
+      grid_barrier_arrive(p.barrier, epoch, p.G);  // (waited for below: the bias rows do not depend on z_s)
+    }
+    CQP_STAMP0(p.dbg, 1);  // bounds + this CTA's rows of refresh_z done
+    load_layer<RB>(p, s, layer, row0, nrows, nullptr, resident_layer != layer);  // (scratch in the second copy, cleared below)
+    resident_layer = layer;
+    if (p.do_refresh) grid_barrier_wait(p.barrier, epoch, p.dbg);  // every CTA's rows of z_s are in slot 0
+    CQP_STAMP0(p.dbg, 2);  // bias rows done, refresh_z complete
+    load_v0();
   }
-
-  CQP_STAMP0(p.dbg, 1);  // bounds + this CTA's rows of refresh_z done
-  load_layer<RB>(p, s, layer, row0, nrows, nullptr, resident_layer != layer);  // (scratch in the second copy, cleared below)
-  resident_layer = layer;
-  if (p.do_refresh) grid_barrier_wait(p.barrier, epoch, p.dbg);  // every CTA's rows of z_s are in slot 0
-  CQP_STAMP0(p.dbg, 2);  // bias rows done, refresh_z complete
-
-  // v_0 -> xs[0] (slot 0 holds the iterate between launches; refresh_z above is complete)
-  for (int i = t; i < XS; i += kThreads) {
-    s.xs[i] = (i < D) ? __ldcg(p.vq + i) : 0.0;
-    s.xs[XS + i] = 0.0;
-  }
-  __syncthreads();
 
   int n_trace = 1, n_hist = 0;
   if (blockIdx.x == 0 && t == 0) {
