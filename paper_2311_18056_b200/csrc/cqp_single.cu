@@ -1322,15 +1322,10 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;
-  // few iterations: copying the W slice into shared memory costs as much as streaming it once;
-  // the ring then lives in the (unused) slice region
-  if (total_iters < 4 && p.w_smem && !p.server) {
-    p.w_smem = 0;
-    if (!delay_set) p.poll_delay_ns = 150;  // (streaming kernel: keeps the pause)
-    int stages = h->wdoubles / kStageDoubles;
-    if (stages > kMaxStages) stages = kMaxStages;
-    p.stream_stages = stages >= 2 ? stages : 0;
-  }
+  // (A launch of very few iterations could stream W once instead of copying the slice into shared
+  // memory first, at about the same cost -- but the streamed code adds a row's products up in another
+  // order, so the bits of fixed_iters(k) would depend on how the iterations are split over launches and
+  // the resident server would not reproduce a launch per step.  The order is a property of the handle.)
   switch (h->rb) {
     case 4: return launched(launch_run_rb<4>(h, p));
     case 8: return launched(launch_run_rb<8>(h, p));

@@ -119,3 +119,19 @@ def test_server_mid_size_streamed_tier(G, P):
     got = closed_loop(gs, wl, 2, 12, use_server=True)
     same(ref, got)
     gs.close()
+
+
+@pytest.mark.parametrize("nu,k", [(40, 1), (50, 2)])
+def test_server_resident_tier_large_slices(G, P, nu, k):
+    """Resident tier with 9..11 rows per CTA (16-row blocks; D = 1200 / 1500): server == launch per
+    step.  (A launch of k < 4 iterations used to stream W instead of holding it in shared memory, which
+    adds a row's products up in another order: the two paths then differed in the last bits.)"""
+    wl = P.config2(nu, seed=0)
+    base = wl.base_problem()
+    gs = G.Solver(base.H, base.g, base.G, base.c, base.d)
+    assert gs.launch_info()["tier"] == 0 and gs.launch_info()["rows_per_cta"] > 8
+    gs.set_mpc_template(wl.tmpl, wl.limits)
+    ref = closed_loop(gs, wl, k, 25, use_server=False, fast=True)
+    got = closed_loop(gs, wl, k, 25, use_server=True, fast=True)
+    same(ref, got)
+    gs.close()

@@ -237,6 +237,26 @@ def test_fixed_iters_composes_and_history(G, oracle):
     assert [h[0] for h in rep.residual_history] == [25, 50, 75, 100]
 
 
+@pytest.mark.parametrize("nu", [30, 40, 50])
+def test_iteration_split_is_bitwise_neutral_at_mpc_sizes(G, P, nu):
+    """fixed_iters(1) + fixed_iters(2) + fixed_iters(5) == fixed_iters(8) bit for bit at the sizes of the
+    nu sweep (resident tier, 7..11 rows per CTA): the summation order of a layer is a property of the
+    handle, not of how many iterations one launch runs."""
+    wl = P.config2(nu, seed=1)
+    base = wl.base_problem()
+    gs = G.Solver(base.H, base.g, base.G, base.c, base.d, G.SolverSettings(adaptive_rho=False))
+    q = wl.problem_at(wl.x0(1.0))
+    gs.update_vectors(q.g, q.c, q.d)
+    gs.cold_start()
+    for k in (1, 2, 5):
+        gs.fixed_iters(k)
+    split = gs.state.copy()
+    gs.cold_start()
+    gs.fixed_iters(8)
+    assert np.array_equal(gs.state, split)
+    gs.close()
+
+
 def test_rho_trace_structure_and_persistent_index(G, oracle):
     # tests/test_solver.cpp:390-401 + semantics 2/6 of SURVEY.md section 8(a)
     p = oracle.gen_random_dense_qp(16, 14)
