@@ -29,6 +29,20 @@ __device__ __noinline__ void watchdog_fire(int* d, int where, int iter) {
     d[4] = (int)threadIdx.x;
     __threadfence_system();
   }
+#ifdef CQP_DEBUG_PROGRESS
+  // debug builds: the first 47 threads that time out leave a record each, and the trap waits a while
+  // so that the others get there (tools/deadlock_probe.py)
+  if (d) {
+    const int idx = atomicAdd(d + 5, 1);
+    if (idx < 47) {
+      volatile int* r = d + 64 + 4 * idx;
+      r[0] = where; r[1] = iter; r[2] = (int)blockIdx.x; r[3] = (int)threadIdx.x;
+      __threadfence_system();
+    }
+    const long long t0 = clock64();
+    while (clock64() - t0 < 40000000ll) {}
+  }
+#endif
   __trap();
 }
 

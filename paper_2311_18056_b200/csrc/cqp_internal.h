@@ -82,7 +82,9 @@ struct RunParams {
   int sb_rows3;          // rows per super-block of the W stream in the lambda-row CTAs
   int nparts;            // per-row partial sums kept per parity: 16 (one per compute warp) or, for handles
                          // that always stream, 4
-  int cofetch;           // grid kernel, resident tier: the compute warps fetch the iterate along with the loaders
+  int cofetch;           // grid kernel: 1: the compute warps fetch the iterate along with the loaders; 2 (resident
+                         // tier): direct fetch, every compute thread polls for its own column pairs (run_kernel)
+  int wreg;              // direct fetch: column pairs of W per compute thread kept in registers (0: shared memory)
   int stage_doubles;     // doubles per ring stage (re-tiled stream: h->stage_doubles; row segments: kStageDoubles)
   int cw12, cw3;         // column pairs per ring stage (chunk width): a stage holds nv rows x cw pairs
                          // <= 32 KB, so super-blocks of fewer than 16 rows take wider chunks (one bulk
@@ -212,6 +214,7 @@ struct cqp_handle {
   int cw12 = 128, cw3 = 128;                      // tier 1: chunk widths Wt was re-tiled with
   int stage_doubles = 4096;                       // tier 1: doubles per ring stage of the re-tiled stream
   int nparts = 16;                                // per-row partial sums per parity (RunParams::nparts)
+  int fetch = 1;                                  // resident tier: RunParams::cofetch (0 loaders, 1 cofetch, 2 direct)
   int stream_stages = 0;  // tier 1: stages of the W streaming ring that fit the shared memory
   int wdoubles = 0;       // shared-memory doubles reserved for W (resident slice or ring)
   int cluster = 0;  // 1: single thread-block cluster with DSMEM exchange (small problems)
@@ -219,7 +222,7 @@ struct cqp_handle {
   int npt = 0;      // cluster kernel, register mode: column pairs of W per lane (0: shared-memory mode)
   int xs_stride = 0, hg_smem = 0;
   // tuning / test knobs, read from the environment once at handle creation (cqp_single.cu: read_knobs)
-  int knob_poll_delay_ns = -1, knob_fence_mode = 0, knob_cofetch = 1;
+  int knob_poll_delay_ns = -1, knob_fence_mode = 0, knob_cofetch = 2, knob_wreg = 1;
   bool knob_sb_balance = true, knob_no_retile = false, knob_wide_chunks = true;
 };
 

@@ -101,6 +101,44 @@ __device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int n
   }
 }
 
+// Direct fetch (resident tier): compute thread `t` polls ring slot `q` for its own column pairs
+// c2 = t + u * kComputeThreads of v_i, keeps them in registers (xv) and leaves a copy in shared memory
+// (xs) for the residual passes.  All its loads are in flight together; only armed entries are re-polled.
+template <int U>
+__device__ __forceinline__ void fetch_own(const double* q, double* xs, int nc2, int t, double2 (&xv)[U], int* dbg,
+                                          int iter) {
+  double2* xs2 = reinterpret_cast<double2*>(xs);
+  unsigned pending = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int c2 = t + u * kComputeThreads;
+    if (c2 < nc2) {
+      xv[u] = load_pair(q + 2 * c2);
+      pending |= 1u << u;
+    }
+  }
+  long long t0 = 0;
+  unsigned spins = 0;
+  while (pending) {
+    unsigned again = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if ((pending >> u) & 1u) {
+        if (is_sentinel(xv[u].x) || is_sentinel(xv[u].y)) again |= 1u << u;
+        else xs2[t + u * kComputeThreads] = xv[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((again >> u) & 1u) xv[u] = load_pair(q + 2 * (t + u * kComputeThreads));
+    pending = again;
+    if (pending && (++spins & 0x3FF) == 0) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 100 + t, iter);
+    }
+  }
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks, int* dbg) {
   __syncthreads();
   epoch += nblocks;
@@ -422,8 +460,20 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
 // SERVER: the resident MPC control-step loop (cqp_mpc_server_start) is its own instantiation, so that
 // the plain launches keep their code (wrapping the body in the request loop cost the streamed tier 17 %
 // per iteration: 11.0 -> 12.9 us at D = 4080, same registers, worse schedule).
-template <int RB, bool STREAM, bool COFETCH = STREAM, bool SERVER = false>
+// FETCH: who brings v_i into the CTA.  0: the loader warps; 1: loaders + the compute warps (cofetch);
+// 2 (resident tier only, "direct"): every compute thread polls the ring for ITS OWN column pairs of v_i
+// and keeps them in registers -- a thread multiplies only those columns, so the iterate needs no
+// shared-memory staging, no loader warps and no xready hand-off inside the loop (a copy still goes to
+// shared memory for the residual passes).  WREG > 0: the thread also keeps its WREG column pairs of the
+// CTA's RB rows of W_k in registers (reloaded at a rho switch), so a layer reads nothing from shared
+// memory but the partial sums.  Same products, same summation order: the bits do not depend on FETCH / WREG.
+template <int RB, bool STREAM, int FETCH = (STREAM ? 1 : 0), bool SERVER = false, int WREG = 0>
 __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
+  static_assert(!(STREAM && FETCH == 2), "direct fetch is for the shared-memory-resident tier");
+  static_assert(WREG == 0 || FETCH == 2, "register-resident W needs the direct fetch");
+  constexpr bool COFETCH = FETCH == 1;
+  constexpr bool DIRECT = FETCH == 2;
+  constexpr int XU = 2;  // direct fetch: column pairs per compute thread (nc2 <= XU * kComputeThreads)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem s = carve<RB>(smem_raw, p);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -449,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     }
     mbar_init(&full[0], kComputeWarps);
     mbar_init(&full[1], kComputeWarps);
-    mbar_init(&xready[0], kLoaderWarps + (COFETCH ? kComputeWarps : 0));
+    mbar_init(&xready[0], kLoaderWarps + (COFETCH ? kComputeWarps : 0));  // (unused by the direct fetch)
     mbar_init(&xready[1], kLoaderWarps + (COFETCH ? kComputeWarps : 0));
     mbar_init(go, 1);
     for (int k = 0; k < (STREAM ? NS : 0); ++k) {
@@ -601,12 +651,82 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   const int npart = streaming ? 4 : kComputeWarps;  // per-row partials the publisher adds up
   constexpr bool cofetch = COFETCH;  // the compute warps fetch v_i together with the loaders
   const int nfetch = cofetch ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
+  // direct fetch: this thread's column pairs of the current iterate, and (WREG) of the CTA's rows of W_k
+  double2 xv[XU];
+  double2 wreg[WREG > 0 ? RB : 1][WREG > 0 ? WREG : 1];
+  auto load_wreg = [&]() {  // (after load_layer: the slice of the active level is in shared memory)
+    if constexpr (WREG > 0) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+#pragma unroll
+        for (int u = 0; u < WREG; ++u) {
+          const int c2 = t + u * kComputeThreads;
+          wreg[r][u] = (compute && r < nrows && c2 < nc2)
+                           ? reinterpret_cast<const double2*>(s.sW + (size_t)r * p.Dpad)[c2]
+                           : make_double2(0.0, 0.0);
+        }
+      }
+    }
+  };
+  if constexpr (DIRECT) {
+    if (compute) {
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int c2 = t + u * kComputeThreads;
+        xv[u] = c2 < nc2 ? reinterpret_cast<const double2*>(s.xs)[c2] : make_double2(0.0, 0.0);
+      }
+    }
+    load_wreg();
+  }
   for (int i = 1; i <= p.total_iters; ++i) {
     // ---- one fused layer: v <- clamp(W v + b, c~, d~)  (solver.cpp:59-63) ----
     const int b = i & 1;
     const int par = ((i - 1) >> 1) & 1;  // phase parity of the k-th use of a [2]-split barrier
     double* part = s.spart + (size_t)b * p.nparts * Rcap;
-    if (compute) {
+    if (DIRECT && compute) {
+      if constexpr (DIRECT) {
+        if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 1); CQP_STAMP(p.dbg, i, 1); }  // v_{i-1} in registers
+        if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 10);
+        double acc[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+        if constexpr (WREG > 0) {
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+#pragma unroll
+            for (int u = 0; u < WREG; ++u) {
+              acc[r] = fma(wreg[r][u].x, xv[u].x, acc[r]);
+              acc[r] = fma(wreg[r][u].y, xv[u].y, acc[r]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < XU; ++u) {
+            const int c2 = t + u * kComputeThreads;
+            if (c2 < nc2) fma_rows<RB>(s.sW, p.Dpad, nrows, c2, xv[u], acc);
+          }
+        }
+        if (lane == 0 && warp == 0) CQP_STAMP(p.dbg, i, 3);
+        const double total = warp_butterfly<RB>(acc, lane);
+        if ((lane & ((1 << shift) - 1)) == 0) part[warp * Rcap + (lane >> shift)] = total;
+        __syncwarp();
+        if (lane == 0 && warp == 0) CQP_STAMP(p.dbg, i, 2);
+        if (lane == 0 && warp == 15) CQP_STAMP(p.dbg, i, 11);
+        if (lane == 0) mbar_arrive(&full[b]);
+        if (lane == 0 && warp == 0) progress(p.dbg, 0, i * 10 + 3);
+        // The wait for this CTA's own publish keeps the compute warps of a CTA within one iteration of each
+        // other (a warp whose threads own no column pair has nothing to poll for: without the wait it runs
+        // ahead and arrives on `full` twice in one phase -- seen as a hang).  Polls issued while the
+        // publishes are in flight cannot complete and slow every CTA's publishes down (they hit the very
+        // L2 lines the publishes go to): hence the pause (launch_run).
+        mbar_wait(go, (i - 1) & 1, p.dbg, 9, i);
+        if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);
+        // v_i: this thread's own column pairs, straight from the ring into registers (+ a copy in xs[b]
+        // for the residual passes: xs[b] held v_{i-2}, which nobody reads inside the loop)
+        fetch_own<XU>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, t, xv, p.dbg, i);
+        if (lane == 0 && warp == 0) CQP_STAMP(p.dbg, i, 0);  // v_i landed (this warp's pairs)
+      }
+    } else if (compute) {
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 1); CQP_STAMP(p.dbg, i, 0); }
       if (i > 1) mbar_wait(&xready[b ^ 1], ((i - 2) >> 1) & 1, p.dbg, 1, i);
       if (lane == 0 && warp == 0) { progress(p.dbg, 0, i * 10 + 2); CQP_STAMP(p.dbg, i, 1); }  // v_{i-1} landed
@@ -760,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
       if (p.fence_mode == 0) __threadfence();
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 3); CQP_STAMP(p.dbg, i, 7); }
-    } else if (loader) {
+    } else if (loader && !DIRECT) {
       if (lt == 0) progress(p.dbg, 2, i * 10 + 1);
       mbar_wait(go, (i - 1) & 1, p.dbg, 3, i);
       if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);  // (see launch_run)
@@ -816,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         ++n_trace;
         load_layer<RB>(p, s, layer, row0, nrows, xcur);
         resident_layer = layer;
+        load_wreg();
       }
     }
     if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
@@ -1030,18 +1151,27 @@ __global__ void retile_kernel(const double2* __restrict__ src, double2* __restri
   dst[slice + (size_t)(sb * sbr) * pitch + (size_t)nv * (c * cwp) + (size_t)r * cw + pc] = val;
 }
 
-template <int RB, bool STREAM, bool COFETCH>
+template <int RB, bool STREAM, int FETCH, int WREG = 0>
 int launch_run_rb2(cqp_handle* h, RunParams& p) {
   void* args[] = {&p};  // (shared-memory opt-in: set once per handle by set_run_attributes)
-  const void* fn = p.server ? (const void*)run_kernel<RB, STREAM, COFETCH, true> : (const void*)run_kernel<RB, STREAM, COFETCH, false>;
+  const void* fn = p.server ? (const void*)run_kernel<RB, STREAM, FETCH, true, WREG> : (const void*)run_kernel<RB, STREAM, FETCH, false, WREG>;
   CQP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->G), dim3(kThreads), args, (size_t)h->smem_bytes, h->stream));
   return CQP_OK;
 }
 
+// Register-resident W (direct fetch): instantiated where RB rows x WREG column pairs (4 registers each)
+// leave the kernel inside its 96-register budget.
+template <int RB> constexpr int kMaxWreg = RB == 4 ? 2 : (RB == 8 ? 1 : 0);
+
 template <int RB>
 int launch_run_rb(cqp_handle* h, RunParams& p) {
-  if (!p.w_smem && p.stream_stages > 0) return launch_run_rb2<RB, true, true>(h, p);
-  return p.cofetch ? launch_run_rb2<RB, false, true>(h, p) : launch_run_rb2<RB, false, false>(h, p);
+  if (!p.w_smem && p.stream_stages > 0) return launch_run_rb2<RB, true, 1>(h, p);
+  if (p.cofetch == 2) {
+    if constexpr (kMaxWreg<RB> >= 2) if (p.wreg == 2) return launch_run_rb2<RB, false, 2, 2>(h, p);
+    if constexpr (kMaxWreg<RB> >= 1) if (p.wreg == 1) return launch_run_rb2<RB, false, 2, 1>(h, p);
+    return launch_run_rb2<RB, false, 2>(h, p);
+  }
+  return p.cofetch ? launch_run_rb2<RB, false, 1>(h, p) : launch_run_rb2<RB, false, 0>(h, p);
 }
 
 // Opt every instance of the grid kernel this handle can launch into the full 227 KB of dynamic
@@ -1049,12 +1179,22 @@ int launch_run_rb(cqp_handle* h, RunParams& p) {
 // device, so it is set to the maximum: handles of different sizes share the functions).
 template <int RB>
 int set_run_attributes_rb() {
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
-  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  CQP_CUDA(cudaFuncSetAttribute(run_kernel<RB, false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes));
+  if constexpr (kMaxWreg<RB> >= 1) {
+    CQP_CUDA((cudaFuncSetAttribute(run_kernel<RB, false, 2, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)));
+    CQP_CUDA((cudaFuncSetAttribute(run_kernel<RB, false, 2, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)));
+  }
+  if constexpr (kMaxWreg<RB> >= 2) {
+    CQP_CUDA((cudaFuncSetAttribute(run_kernel<RB, false, 2, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)));
+    CQP_CUDA((cudaFuncSetAttribute(run_kernel<RB, false, 2, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemBytes)));
+  }
   return CQP_OK;
 }
 
@@ -1080,7 +1220,8 @@ static void read_knobs(cqp_handle* h) {
   // 0: fence after the re-arm (default); 2: release-store publish.  (The former mode 1, no fence at
   // all, broke the ring's ordering argument and is gone: it maps to 0.)
   h->knob_fence_mode = env_int("CQP_FENCE_MODE", 0) == 2 ? 2 : 0;
-  h->knob_cofetch = env_int("CQP_COFETCH", 1);
+  h->knob_cofetch = env_int("CQP_COFETCH", 2);  // 0: loader warps only; 1: + compute warps; 2: direct fetch (resident tier)
+  h->knob_wreg = env_int("CQP_WREG", 1);
   h->knob_sb_balance = env_int("CQP_SB_BALANCE", 1) != 0;
   h->knob_no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
   h->knob_wide_chunks = env_int("CQP_WIDE_CHUNKS", 1) != 0;
@@ -1111,6 +1252,10 @@ int configure_launch(cqp_handle* h) {
   size_t need = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, (size_t)h->wdoubles) * sizeof(double);
   h->w_smem = need <= (size_t)kMaxSmemBytes ? 1 : 0;
   if (force_tier && force_tier[0] == '1') h->w_smem = 0;  // test hook: stream W from L2/HBM
+  // Resident tier, direct fetch (run_kernel, FETCH == 2): needs every row of the CTA in one row block and at
+  // most two column pairs per compute thread.
+  h->fetch = h->knob_cofetch ? 1 : 0;
+  if (h->w_smem && h->knob_cofetch == 2 && R <= h->rb && (h->Dpad >> 1) <= 2 * kComputeThreads) h->fetch = 2;
   if (!h->w_smem) {
     // L2/HBM tier: give the rest of the shared memory to the W streaming ring
     const size_t base = smem_doubles(R, h->rb, h->Dpad, h->npad, h->mpad, 0) * sizeof(double);
@@ -1314,11 +1459,23 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.stage_doubles = p.Wt ? h->stage_doubles : kStageDoubles;
   // resident tier: the compute warps, idle during the exchange, fetch v_i along with the loader warps
   // (B200, 1000 iterations: D = 900 2576 -> 2468 us, D = 1500 3924 -> 3706 us); CQP_COFETCH=0 for A/B runs
-  p.cofetch = h->knob_cofetch;
+  p.cofetch = h->w_smem ? h->fetch : 1;
+  // direct fetch: the W slice lives in registers too where it fits (see run_kernel)
+  p.wreg = 0;
+  if (p.cofetch == 2 && h->knob_wreg != 0) {
+    const int u = ((h->Dpad >> 1) + kComputeThreads - 1) / kComputeThreads;
+    const int maxw = h->rb == 4 ? 2 : (h->rb == 8 ? 1 : 0);
+    if (u <= maxw) p.wreg = u;
+  }
   // with 608 fetching threads the first poll of the resident tier is best issued at once (B200, 1000
   // iterations: D = 900 2456 -> 2358 us, D = 1500 3701 -> 3667 us); the streamed tier keeps the pause
   // (Atlas-sized 5.34 vs 5.55 us per iteration: early polls compete with the W stream)
   if (p.w_smem && p.cofetch && !delay_set) p.poll_delay_ns = 0;
+  // direct fetch: a first poll that finds sentinels costs far more than a short pause (B200, us per
+  // iteration at D = 660 / 900 / 1140 / 1260 / 1500: no pause 3.13 / 2.84 / 2.00 / 4.85 / 3.50, 100 ns
+  // 2.66 / 1.79 / 2.08 / 3.12 / 2.83, 200 ns 2.14 / 1.79 / 2.11 / 2.91 / 2.88, 400 ns 2.09 / 1.85 / 2.35 / 2.93 / 3.14;
+  // loaders + compute warps fetching into shared memory: 2.24 / 2.32 / 2.50 / 3.56 / 3.66)
+  if (p.w_smem && p.cofetch == 2 && !delay_set) p.poll_delay_ns = 200;
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;

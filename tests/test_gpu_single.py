@@ -499,6 +499,46 @@ def test_structured_stream_layer_matches_dense_and_oracle(G, oracle, monkeypatch
     assert rel_err(struct.solution.lam, dense.solution.lam) <= 1e-9
 
 
+@pytest.mark.parametrize("nu", [22, 30, 42])
+def test_resident_tier_fetch_modes_are_bit_identical(G, oracle, P, monkeypatch, nu):
+    """The shared-memory-resident tier can bring the iterate into a CTA three ways (CQP_COFETCH=0: loader
+    warps, 1: loaders + compute warps, 2 = default: every compute thread polls for its own column pairs
+    and keeps them -- and, where they fit, its columns of W_k -- in registers).  Same products, same
+    summation order: the iterate after a fixed number of layers, a full solve with rho switches (which
+    reload the register copy of W_k) and fused MPC steps are the same bits; the default also matches the
+    oracle.  nu = 22 / 30: W_k in registers (4 / 8 rows per CTA); nu = 42: two column pairs per thread,
+    W_k in shared memory."""
+    wl = P.config2(nu, seed=1)
+    base = wl.base_problem()
+    q = wl.problem_at(wl.x0(10.0))
+    q2 = wl.problem_at(wl.x0(3.0, seed=5))
+    outs = []
+    os_ = oracle.Solver(oracle.QProblem(base.H, base.g, base.G, base.c, base.d), oracle.SolverSettings(), variant="ref")
+    layers = oracle_layers(os_.cache)
+    for mode in ("2", "1", "0", "2w"):
+        monkeypatch.setenv("CQP_COFETCH", mode[0])
+        monkeypatch.setenv("CQP_WREG", "0" if mode.endswith("w") else "1")
+        s = G.Solver(base.H, base.g, base.G, base.c, base.d, G.SolverSettings(), layers=layers)
+        assert s.launch_info()["tier"] == 0
+        s.update_vectors(q.g, q.c, q.d); s.cold_start()
+        r = s.solve()
+        s.cold_start(); s.fixed_iters(60)
+        v60 = s.state.copy()
+        steps = [s.mpc_step(q2.g, q2.c, q2.d, 2).solution.y.copy() for _ in range(3)]
+        outs.append((r, v60, steps))
+        s.close()
+    monkeypatch.delenv("CQP_COFETCH", raising=False)
+    monkeypatch.delenv("CQP_WREG", raising=False)
+    r0, v0, st0 = outs[0]
+    for r, v, st in outs[1:]:
+        assert r.solution.iterations == r0.solution.iterations and r.solution.rho_trace == r0.solution.rho_trace
+        assert np.array_equal(r.solution.y, r0.solution.y) and np.array_equal(r.solution.lam, r0.solution.lam)
+        assert np.array_equal(v, v0)
+        assert all(np.array_equal(a, b) for a, b in zip(st, st0))
+    os_.update_vectors(q.g, q.c, q.d); os_.cold_start()
+    assert_report_parity(r0, os_.solve())
+
+
 @pytest.mark.parametrize("shape", ["odd_n_odd_m", "even_n_odd_m"])
 def test_odd_dimensions_in_every_grid_mode(G, oracle, P, monkeypatch, shape):
     """n and m whose separately padded scratch vectors [uy; uz; ul] need MORE room than the padded
