@@ -113,7 +113,8 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->g, nm + m))) return rc;
   h->c = h->g + n;
   h->d = h->c + m;
-  if ((rc = dev_alloc(&h->vq, 4 * (size_t)h->Dpad))) return rc;
+  h->ring_ld = (h->Dpad + 15) / 16 * 16;  // ring slots start on their own 128-byte L2 lines
+  if ((rc = dev_alloc(&h->vq, 4 * (size_t)h->ring_ld))) return rc;
   if ((rc = dev_alloc(&h->state, 2))) return rc;
   if ((rc = dev_alloc(&h->barrier, 2))) return rc;
   CQP_CUDA(cudaMemset(h->barrier, 0, 2 * sizeof(unsigned)));
@@ -268,7 +269,7 @@ static int server_step(cqp_handle* h, const double* x0, int k, double* u0, cqp_r
 int cold_start(cqp_handle* h) {
   // ring invariant between launches: slot 0 = iterate (zero), slots 1..3 = sentinel (all ones)
   CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
-  CQP_CUDA(cudaMemsetAsync(h->vq + h->Dpad, 0xFF, sizeof(double) * 3 * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemsetAsync(h->vq + h->ring_ld, 0xFF, sizeof(double) * 3 * (size_t)h->ring_ld, h->stream));
   return launch_set_state(h, h->initial_index);
 }
 
@@ -652,7 +653,7 @@ int cqp_set_state(cqp_handle* h, const double* v, int layer_index) {
   CQP_QUIESCE(h);
   // ring invariant between launches: slot 0 = iterate, slots 1..3 = sentinel
   CQP_CUDA(cudaMemsetAsync(h->vq, 0, sizeof(double) * (size_t)h->Dpad, h->stream));
-  CQP_CUDA(cudaMemsetAsync(h->vq + h->Dpad, 0xFF, sizeof(double) * 3 * (size_t)h->Dpad, h->stream));
+  CQP_CUDA(cudaMemsetAsync(h->vq + h->ring_ld, 0xFF, sizeof(double) * 3 * (size_t)h->ring_ld, h->stream));
   CQP_CUDA(cudaMemcpyAsync(h->vq, v, sizeof(double) * (size_t)h->D, cudaMemcpyHostToDevice, h->stream));
   int rc = launch_set_state(h, layer_index);
   if (rc) return rc;

@@ -110,7 +110,8 @@ struct RunParams {
   const double* g;   // n unscaled
   const double* c;   // m unscaled
   const double* d;   // m unscaled
-  double* vq;        // [4][Dpad] iterate ring; between launches slot 0 = iterate, 1..3 = sentinel
+  double* vq;        // [4][ring_ld] iterate ring; between launches slot 0 = iterate, 1..3 = sentinel
+  int ring_ld;       // doubles between two slots of the ring (Dpad rounded up: slots do not share L2 lines)
   int* state;        // [0] layer index
   unsigned* barrier;       // grid barrier counter of this launch (zero on entry)
   unsigned* barrier_next;  // counter of the next launch, zeroed by this one
@@ -119,6 +120,7 @@ struct RunParams {
   double eps_prim, eps_dual, threshold;
   int check_interval, adaptive, early_exit, total_iters;
   int do_refresh;     // run Solver::refresh_z before the first iteration
+  int gate_cycles, gate_adapt, gate_up, gate_down, gate_max;  // direct fetch: the publisher's poll gate (run_kernel)
   int fence_mode;     // 0: fence after re-arm (default); 2: release-store publish
   int poll_delay_ns;  // the fetching warps pause this long after `go` before their first poll of v_i
   int cap;            // capacity of the record arrays
@@ -173,7 +175,8 @@ struct cqp_handle {
   double *H = nullptr, *Gr = nullptr, *Gt = nullptr, *Gs = nullptr;
   double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;
   double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
-  double* vq = nullptr;  // [4][Dpad] iterate ring (see RunParams::vq)
+  double* vq = nullptr;  // [4][ring_ld] iterate ring (see RunParams::vq)
+  int ring_ld = 0;
   int* state = nullptr;
   unsigned* barrier = nullptr;  // [2] ping-pong grid-barrier counters
   int launch_parity = 0;
@@ -223,6 +226,7 @@ struct cqp_handle {
   int xs_stride = 0, hg_smem = 0;
   // tuning / test knobs, read from the environment once at handle creation (cqp_single.cu: read_knobs)
   int knob_poll_delay_ns = -1, knob_fence_mode = 0, knob_cofetch = 2, knob_wreg = 1;
+  int knob_gate[5] = {100, 1, 16, 4, 300};
   bool knob_sb_balance = true, knob_no_retile = false, knob_wide_chunks = true;
 };
 

@@ -105,7 +105,7 @@ __device__ __forceinline__ void fetch_iterate(const double* q, double* xs, int n
 // c2 = t + u * kComputeThreads of v_i, keeps them in registers (xv) and leaves a copy in shared memory
 // (xs) for the residual passes.  All its loads are in flight together; only armed entries are re-polled.
 template <int U>
-__device__ __forceinline__ void fetch_own(const double* q, double* xs, int nc2, int t, double2 (&xv)[U], int* dbg,
+__device__ __forceinline__ bool fetch_own(const double* q, double* xs, int nc2, int t, double2 (&xv)[U], int* dbg,
                                           int iter) {
   double2* xs2 = reinterpret_cast<double2*>(xs);
   unsigned pending = 0;
@@ -119,6 +119,7 @@ __device__ __forceinline__ void fetch_own(const double* q, double* xs, int nc2, 
   }
   long long t0 = 0;
   unsigned spins = 0;
+  bool repolled = false;
   while (pending) {
     unsigned again = 0;
 #pragma unroll
@@ -132,11 +133,13 @@ __device__ __forceinline__ void fetch_own(const double* q, double* xs, int nc2, 
     for (int u = 0; u < U; ++u)
       if ((again >> u) & 1u) xv[u] = load_pair(q + 2 * (t + u * kComputeThreads));
     pending = again;
+    if (pending) repolled = true;
     if (pending && (++spins & 0x3FF) == 0) {
       if (t0 == 0) t0 = clock64();
       else if (clock64() - t0 > kSpinLimitCycles) watchdog_fire(dbg, 100 + t, iter);
     }
   }
+  return repolled;
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch, unsigned nblocks, int* dbg) {
@@ -652,6 +655,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
   constexpr bool cofetch = COFETCH;  // the compute warps fetch v_i together with the loaders
   const int nfetch = cofetch ? kComputeThreads + kLoaderThreads : kLoaderThreads;  // threads that fetch v_i
   // direct fetch: this thread's column pairs of the current iterate, and (WREG) of the CTA's rows of W_k
+  unsigned* early_polls = reinterpret_cast<unsigned*>(&s.bars[7]);  // direct fetch: first polls that came back armed
+  int gate = p.gate_cycles;                                          // ... and the publisher's gate (cycles)
+  if (DIRECT && t == 0) *early_polls = 0u;
   double2 xv[XU];
   double2 wreg[WREG > 0 ? RB : 1][WREG > 0 ? WREG : 1];
   auto load_wreg = [&]() {  // (after load_layer: the slice of the active level is in shared memory)
@@ -723,7 +729,12 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);
         // v_i: this thread's own column pairs, straight from the ring into registers (+ a copy in xs[b]
         // for the residual passes: xs[b] held v_{i-2}, which nobody reads inside the loop)
-        fetch_own<XU>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, t, xv, p.dbg, i);
+        const bool repolled = fetch_own<XU>(p.vq + (size_t)(i & 3) * p.ring_ld, s.xs + (size_t)b * XS, nc2, t, xv, p.dbg, i);
+        // The vote reconverges the warp behind the polling loop -- without it the lanes whose pairs landed
+        // first run the next layer's products on their own, and the layer time follows the arrival pattern
+        // (same problem in another handle, i.e. at other addresses: 1.72 or 2.2 - 3.2 us per iteration,
+        // tools/ab_instances.py) -- and feeds the publisher's gate: this warp's first poll came back armed.
+        if (__any_sync(0xffffffffu, repolled) && lane == 0) atomicAdd(early_polls, 1u);
         if (lane == 0 && warp == 0) CQP_STAMP(p.dbg, i, 0);  // v_i landed (this warp's pairs)
       }
     } else if (compute) {
@@ -795,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         // polls cannot succeed and would compete with the W prefetch for L2 bandwidth.
         mbar_wait(go, (i - 1) & 1, p.dbg, 9, i);
         if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);
-        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, t, nfetch, p.dbg, i);
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.ring_ld, s.xs + (size_t)b * XS, nc2, t, nfetch, p.dbg, i);
         __syncwarp();
         if (lane == 0) mbar_arrive(&xready[b]);
       }
@@ -848,8 +859,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       }
       mbar_wait(&full[b], par, p.dbg, 2, i);
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 2); CQP_STAMP(p.dbg, i, 5); }
-      double* qout = p.vq + (size_t)(i & 3) * p.Dpad;
-      double* qclr = p.vq + (size_t)((i + 2) & 3) * p.Dpad;
+      double* qout = p.vq + (size_t)(i & 3) * p.ring_ld;
+      double* qclr = p.vq + (size_t)((i + 2) & 3) * p.ring_ld;
       const double* xprev = s.xs + (size_t)(b ^ 1) * XS;  // v_{i-1} (complete: the compute warps read it)
       // (one row per lane and trip: issuing three rows' loads together was measured 2-4 % SLOWER
       // per iteration at the robot-sized configs: the first rows are published later)
@@ -870,14 +881,33 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (owns_pad && lane == 0) publish(qout + D, 0.0);
       __syncwarp();
       if (lane == 0) CQP_STAMP(p.dbg, i, 6);
-      if (lane == 0) mbar_arrive(go);
       // re-arm this CTA's rows of the slot that will carry v_{i+2}; every reader of its old
       // content (v_{i-2}) finished before any v_{i-1} row was published, and all of v_{i-1} has
       // been consumed by this CTA.  The fence orders the re-arm before the next iteration's
-      // publish (off the compute warps' critical path).
+      // publish (off the compute warps' critical path).  The re-arm stores are issued BEFORE the
+      // fetching warps are released (B200, direct fetch, D = 900: 1.86 -> 1.75 us per iteration).
       const double sentinel = __longlong_as_double((long long)kSentinel);
       for (int r = lane; r < nrows; r += 32) publish(qclr + row0 + r, sentinel);
       if (owns_pad && lane == 0) publish(qclr + D, sentinel);
+      if constexpr (DIRECT) {
+        // Gate of the direct fetch.  A first poll that arrives before the last CTA's rows costs a second L2
+        // round trip (everybody waits for the slowest CTA); one that arrives late costs only its lateness
+        // (measured: a fixed gate of g cycles adds exactly g cycles per iteration).  How long after its own
+        // publish a CTA should start polling depends on where it sits in the skew of the grid, so every CTA
+        // steers its own gate: the compute warps count the first polls that came back armed, and the publisher
+        // releases them a little later after an iteration that had some, a little earlier after one without
+        // (B200, D = 600 ... 1020: 1.72 - 1.81 us per iteration, fixed 120 cycles: 1.77 - 1.86).
+        const unsigned early = *reinterpret_cast<volatile unsigned*>(early_polls);
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<volatile unsigned*>(early_polls) = 0u;  // (the compute warps are parked on `go`)
+        if (p.gate_adapt) gate = early ? min(gate + p.gate_up, p.gate_max) : max(gate - p.gate_down, 0);
+        if (gate > 0) {
+          const long long t0 = clock64();
+          while (clock64() - t0 < gate) {}
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(go);
       if (p.fence_mode == 0) __threadfence();
       if (lane == 0) { progress(p.dbg, 1, i * 10 + 3); CQP_STAMP(p.dbg, i, 7); }
     } else if (loader && !DIRECT) {
@@ -886,10 +916,10 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       if (p.poll_delay_ns > 0) __nanosleep(p.poll_delay_ns);  // (see launch_run)
       if (lt == 0) { progress(p.dbg, 2, i * 10 + 2); CQP_STAMP(p.dbg, i, 8); }
       if (cofetch)
-        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, kComputeThreads + lt, nfetch,
+        fetch_iterate<4>(p.vq + (size_t)(i & 3) * p.ring_ld, s.xs + (size_t)b * XS, nc2, kComputeThreads + lt, nfetch,
                          p.dbg, i);
       else
-        fetch_iterate<8>(p.vq + (size_t)(i & 3) * p.Dpad, s.xs + (size_t)b * XS, nc2, lt, nfetch, p.dbg, i);
+        fetch_iterate<8>(p.vq + (size_t)(i & 3) * p.ring_ld, s.xs + (size_t)b * XS, nc2, lt, nfetch, p.dbg, i);
       __syncwarp();
       if (lt == 0) CQP_STAMP(p.dbg, i, 9);
       if (lane == 0) mbar_arrive(&xready[b]);
@@ -975,9 +1005,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     for (int r = t; r < count; r += kThreads) {
       const int row = row0 + r;
       p.vq[row] = (row < D) ? xfinal[row] : 0.0;
-      p.vq[(size_t)p.Dpad + row] = sentinel;
-      p.vq[2 * (size_t)p.Dpad + row] = sentinel;
-      p.vq[3 * (size_t)p.Dpad + row] = sentinel;
+      p.vq[(size_t)p.ring_ld + row] = sentinel;
+      p.vq[2 * (size_t)p.ring_ld + row] = sentinel;
+      p.vq[3 * (size_t)p.ring_ld + row] = sentinel;
     }
   }
   if (blockIdx.x == 0) {
@@ -1222,6 +1252,9 @@ static void read_knobs(cqp_handle* h) {
   h->knob_fence_mode = env_int("CQP_FENCE_MODE", 0) == 2 ? 2 : 0;
   h->knob_cofetch = env_int("CQP_COFETCH", 2);  // 0: loader warps only; 1: + compute warps; 2: direct fetch (resident tier)
   h->knob_wreg = env_int("CQP_WREG", 1);
+  // direct fetch, the publisher's gate: "initial cycles, adapt (0/1), step up, step down, maximum"
+  if (const char* e = std::getenv("CQP_GATE"))
+    std::sscanf(e, "%d,%d,%d,%d,%d", &h->knob_gate[0], &h->knob_gate[1], &h->knob_gate[2], &h->knob_gate[3], &h->knob_gate[4]);
   h->knob_sb_balance = env_int("CQP_SB_BALANCE", 1) != 0;
   h->knob_no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
   h->knob_wide_chunks = env_int("CQP_WIDE_CHUNKS", 1) != 0;
@@ -1236,7 +1269,14 @@ int configure_launch(cqp_handle* h) {
   // the all-SM grid kernel (tests, A/B measurements).
   const char* force_tier = std::getenv("CQP_FORCE_TIER");
   const bool force_grid = force_tier && (force_tier[0] == '0' || force_tier[0] == '1');
-  if (!force_grid && configure_cluster(h) == CQP_OK && h->cluster) return CQP_OK;
+  if (!force_grid && configure_cluster(h) == CQP_OK && h->cluster) {
+    // Where the cluster kernel would have to keep W_k in shared memory (more than 32 rows per CTA: D > 512)
+    // the all-SM grid with the direct fetch is faster (B200, D = 540: 2.29 vs 1.57 us per iteration; D = 420,
+    // register mode: 1.51 vs 1.88).  The test hooks that pin a cluster shape keep the cluster kernel.
+    const bool pinned = std::getenv("CQP_CLUSTER_SIZE") || std::getenv("CQP_CLUSTER_MODE") ||
+                        (force_tier && force_tier[0] == '2');
+    if (h->npt > 0 || pinned || h->knob_cofetch != 2) return CQP_OK;
+  }
   h->cluster = 0;
   h->structured = 0;
   h->nparts = kComputeWarps;
@@ -1402,7 +1442,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.E = h->E; p.F = h->F; p.cost_scale = h->cost_scale;
   p.grid = h->dgrid; p.log_grid = h->dlog_grid;
   p.g = h->g; p.c = h->c; p.d = h->d;
-  p.vq = h->vq; p.state = h->state; p.partial = h->partial;
+  p.vq = h->vq; p.ring_ld = h->ring_ld; p.state = h->state; p.partial = h->partial;
   p.eps_prim = h->s.eps_prim; p.eps_dual = h->s.eps_dual; p.threshold = h->s.rho_switch_threshold;
   p.check_interval = h->s.check_interval; p.adaptive = h->s.adaptive_rho;
   p.early_exit = early_exit ? 1 : 0; p.total_iters = total_iters; p.do_refresh = do_refresh ? 1 : 0;
@@ -1471,11 +1511,13 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   // iterations: D = 900 2456 -> 2358 us, D = 1500 3701 -> 3667 us); the streamed tier keeps the pause
   // (Atlas-sized 5.34 vs 5.55 us per iteration: early polls compete with the W stream)
   if (p.w_smem && p.cofetch && !delay_set) p.poll_delay_ns = 0;
-  // direct fetch: a first poll that finds sentinels costs far more than a short pause (B200, us per
-  // iteration at D = 660 / 900 / 1140 / 1260 / 1500: no pause 3.13 / 2.84 / 2.00 / 4.85 / 3.50, 100 ns
-  // 2.66 / 1.79 / 2.08 / 3.12 / 2.83, 200 ns 2.14 / 1.79 / 2.11 / 2.91 / 2.88, 400 ns 2.09 / 1.85 / 2.35 / 2.93 / 3.14;
-  // loaders + compute warps fetching into shared memory: 2.24 / 2.32 / 2.50 / 3.56 / 3.66)
-  if (p.w_smem && p.cofetch == 2 && !delay_set) p.poll_delay_ns = 200;
+  // Direct fetch: no pause on the fetching side (__nanosleep is no instrument for this: it sleeps 44 / 113 /
+  // 241 / 497 / 1005 ns for requests of <= 50 / 100 / 150-200 / 300-400 / 600-1000 ns, tools/nanosleep_bench.cu);
+  // the publisher gates the first poll instead (run_kernel).
+  if (p.w_smem && p.cofetch == 2 && !delay_set) p.poll_delay_ns = 0;
+  p.gate_cycles = h->knob_gate[0]; p.gate_adapt = h->knob_gate[1]; p.gate_up = h->knob_gate[2];
+  p.gate_down = h->knob_gate[3]; p.gate_max = h->knob_gate[4];
+
   p.nparts = h->nparts;
   p.wt_level_pairs = wt_level_pairs(h);
   p.rho_vec = h->rho_vec;

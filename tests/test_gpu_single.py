@@ -150,11 +150,13 @@ def test_dense_qp_parity_with_device_offline_stage(G, oracle, n, seeds):
         assert_report_parity(gs.solve(), os_.solve(), res_rel=0.5, res_abs=1e-7)
 
 
-def test_cluster_kernel_layouts(G, oracle, P):
-    """The cluster tier picks its layout from D: register mode with NPT = 2..16 column pairs per
+def test_cluster_kernel_layouts(G, oracle, P, monkeypatch):
+    """(CQP_FORCE_TIER=2 keeps the cluster kernel above D = 512, where the default is the all-SM grid.)
+    The cluster tier picks its layout from D: register mode with NPT = 2..16 column pairs per
     lane (D <= 512), shared-memory mode with 1-4 rows per warp above, residual rows cached in shared
     memory or read through L2 when they do not fit.  One parity solve per layout, odd D included."""
     cases = [("dense", 35), ("dense", 90), ("dense", 130), ("dense", 200), ("mpc", 21)]
+    monkeypatch.setenv("CQP_FORCE_TIER", "2")
     for kind, size in cases:
         if kind == "dense":
             p = oracle.gen_random_dense_qp(size, 7)
