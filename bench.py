@@ -506,6 +506,26 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     rd_peaks = guarded("read_peaks", lambda: measure_read_peaks(local_rank)) if extra else None
     hbm_read, l2_read = rd_peaks if rd_peaks else (None, None)
 
+    def small_batch_section(cols=512, reps=3):
+        """The per-GPU share of the batch at N = 8 (512 columns), solved alone on this GPU: the small-batch
+        regime that strong scaling runs into (device-resident timing, same accounting as `roofline`)."""
+        sb = S.BatchSolver(single, capacity=cols)
+        pin2 = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, :cols].T)).pin_memory().numpy().T  # noqa: E731
+        g2, c2, d2 = pin2(g), pin2(c), pin2(d)
+        sb.solve(g2, c2, d2, zero_copy=True)
+        ms = gms = gfl = 0.0
+        for _ in range(reps):
+            o = sb.solve(g2, c2, d2, zero_copy=True)
+            ms += o["compute_ms"]; gms += o["gemm_ms"]; gfl += o["gemm_flops"]
+        its = float(np.mean(o["iterations"]))
+        sb.close()
+        return {"columns": cols, "steps": reps, "ms_per_step": ms / reps, "value": cols * reps / (ms * 1e-3), "unit": "QP/s",
+                "mean_iterations": its, "round_kernel_tflops": gfl / (gms * 1e-3) / 1e12, "frac": gfl / (gms * 1e-3) / 1e12 / dgemm_peak,
+                "frac_of_whole_step": gfl / (ms * 1e-3) / 1e12 / dgemm_peak,
+                "note": "columns 0..511 of the same batch; what one of 8 GPUs solves under strong scaling"}
+
+    batched_small = guarded("batched_small", small_batch_section) if extra else None
+
     line = {
         "metric": METRIC, "value": value, "unit": "QP/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": comp_ms_max / args.steps, "higher_is_better": True,
@@ -551,6 +571,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
                 "kernel": "run_kernel<16, true> at D = 4350 (W level 151 MB dense, structured 118 MB)",
                 "algorithmic": f"{r50['W_bytes_per_iteration']:.0f} bytes of W per iteration x {r50['initial_solve_iterations']} iterations of the cold solve / its kernel time",
                 "peak_source": peak_src}
+    if batched_small is not None:
+        line["batched_512_columns"] = batched_small
     if single_qp is not None:
         line["single_qp"] = single_qp
     if mpc_steps is not None:
