@@ -31,6 +31,12 @@
 //         trip per round); the compute warps, idle during the exchange, fetch along.
 //     Hand-offs use parity-split mbarriers (full[2], xready[2], go, wfull[], wempty[]), so a role
 //     can run at most one phase ahead and arrivals of different iterations never mix.
+//   * Shared-memory-resident tier, default ("direct fetch", run_kernel<.., FETCH = 2, .., WREG>): a compute
+//     thread multiplies the same column pairs of every row, so it polls the ring for ITS OWN pairs of
+//     v_i and keeps them -- and, where they fit, its columns of W_k -- in registers: no loader warps, no
+//     shared-memory staging and no xready hand-off in the loop.  The publisher gates the first poll
+//     (a per-CTA adaptive spin in front of `go`), and a warp vote reconverges the warp behind the
+//     polling loop.  Same products, same summation order as the staged fetch: bit-identical.
 //   * Every check_interval iterations the whole grid evaluates the residuals on the unscaled
 //     problem (H y, G' lambda, G y as independent warp-per-row dots spread over the CTAs, seven
 //     max-norms exchanged through L2 behind one grid barrier), and every CTA takes the identical
