@@ -109,7 +109,7 @@ int handle_alloc(cqp_handle** out, int n, int m, int L, const cqp_settings& s, i
   if ((rc = dev_alloc(&h->E, (size_t)n))) return rc;
   if ((rc = dev_alloc(&h->F, (size_t)m))) return rc;
   if ((rc = dev_alloc(&h->dgrid, (size_t)L))) return rc;
-  if ((rc = dev_alloc(&h->dlog_grid, (size_t)L))) return rc;
+  if ((rc = dev_alloc(&h->dlog_grid, 2 * (size_t)L))) return rc;  // log10(grid), then the bounds between neighbours
   if ((rc = dev_alloc(&h->g, nm + m))) return rc;
   h->c = h->g + n;
   h->d = h->c + m;
@@ -137,10 +137,16 @@ int upload_small(cqp_handle* h, const double* grid, const double* E, const doubl
   h->grid.assign(grid, grid + h->L);
   h->E_host.assign(E, E + h->n);
   h->F_host.assign(F, F + h->m);
-  std::vector<double> lg(h->L);
+  std::vector<double> lg(2 * (size_t)h->L, 0.0);
   for (int k = 0; k < h->L; ++k) lg[k] = std::log10(grid[k]);
+  // bounds between neighbours for nearest_grid_index_fast (cqp_device.cuh); only for an ascending grid
+  h->grid_bounds = true;
+  for (int k = 0; k + 1 < h->L; ++k) {
+    if (!(grid[k] > 0.0) || !(grid[k + 1] > grid[k])) h->grid_bounds = false;
+    lg[h->L + k] = std::sqrt(grid[k] * grid[k + 1]);
+  }
   CQP_CUDA(cudaMemcpyAsync(h->dgrid, grid, sizeof(double) * h->L, cudaMemcpyHostToDevice, h->stream));
-  CQP_CUDA(cudaMemcpyAsync(h->dlog_grid, lg.data(), sizeof(double) * h->L, cudaMemcpyHostToDevice, h->stream));
+  CQP_CUDA(cudaMemcpyAsync(h->dlog_grid, lg.data(), sizeof(double) * 2 * h->L, cudaMemcpyHostToDevice, h->stream));
   CQP_CUDA(cudaMemcpyAsync(h->E, E, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   CQP_CUDA(cudaMemcpyAsync(h->F, F, sizeof(double) * h->m, cudaMemcpyHostToDevice, h->stream));
   CQP_CUDA(cudaStreamSynchronize(h->stream));  // lg is a local

@@ -150,7 +150,7 @@ struct ClSmem {
   double* sb;     // Rp  bias rows
   double* slo;    // Rp
   double* shi;    // Rp
-  double* sgrid;  // 2 * 16   grid values, then log10(grid) (L <= 16; else read from global)
+  double* sgrid;  // 3 * 16   grid values, log10(grid), bounds between neighbours (L <= 16; else read from global)
   double* wmax;   // kClWarps * 8   per-warp partial maxima
   double* cmax;   // 8              this CTA's maxima / the cluster-wide result
   double* norms;  // 2 * 16 * 8     per-CTA maxima of a residual pass, by pass parity (peers write here)
@@ -164,7 +164,7 @@ __host__ __device__ inline size_t cl_smem_doubles(int R, int wrows, int Dpad, in
                                                   int hg_rows_n, int hg_rows_m) {
   const int Rp = (R + 1) & ~1;
   return (size_t)wrows * Dpad + 2 * (size_t)xs_stride + 3 * (size_t)npad + 3 * (size_t)mpad + 3 * (size_t)Rp +
-         (size_t)hg_rows_n * (npad + mpad) + (size_t)hg_rows_m * npad + 32 + kClWarps * 8 + 8 + 2 * 16 * 8 + 8 +
+         (size_t)hg_rows_n * (npad + mpad) + (size_t)hg_rows_m * npad + 48 + kClWarps * 8 + 8 + 2 * 16 * 8 + 8 +
          2 + kMaxInlineX0;
 }
 
@@ -188,7 +188,7 @@ __device__ __forceinline__ ClSmem cl_carve(unsigned char* raw, const RunParams& 
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sgrid = s.shi + Rp;
-  s.wmax = s.sgrid + 32;
+  s.wmax = s.sgrid + 48;
   s.cmax = s.wmax + kClWarps * 8;
   s.norms = s.cmax + 8;
   s.bars = reinterpret_cast<unsigned long long*>(s.norms + 2 * 16 * 8);
@@ -350,9 +350,11 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
   if (grid_smem && t < p.L) {
     s.sgrid[t] = p.grid[t];
     s.sgrid[16 + t] = p.log_grid[t];
+    s.sgrid[32 + t] = p.grid_bound ? p.grid_bound[t] : 0.0;
   }
   const double* grid_v = grid_smem ? s.sgrid : p.grid;
   const double* grid_log = grid_smem ? s.sgrid + 16 : p.log_grid;
+  const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sgrid + 32 : p.grid_bound) : nullptr;
   if (p.hg_smem) {  // the rows of H, G', G this CTA needs at every residual check
     const int pern = (n + C - 1) / C, perm = (m + C - 1) / C;
     const int h0 = (int)rank * pern, g0 = (int)rank * perm;
@@ -734,21 +736,28 @@ __global__ void __launch_bounds__(kClThreads, 1) cluster_kernel(const RunParams 
     }
     ++n_hist;
     if (p.adaptive) {
-      const double rho_cur = grid_v[layer];
-      double rho_nom = rho_cur;
-      if (!(r_prim == 0.0 || r_dual == 0.0)) {
-        const double g_norm = nrm[6];
-        double num = nrm[2] < nrm[3] ? nrm[3] : nrm[2];  // std::max({hy, gtl, ||g||, 1e-4})
-        num = num < g_norm ? g_norm : num;
-        num = num < 1e-4 ? 1e-4 : num;
-        double den = nrm[4] < nrm[5] ? nrm[5] : nrm[4];  // std::max({gy, ||z||, 1e-4})
-        den = den < 1e-4 ? 1e-4 : den;
-        rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+      // one thread evaluates the rule (FP64 sqrt, divisions, log10, the scan of the grid) and hands the
+      // result to the others: 512 threads doing it took about a third of the check step
+      int* cand_s = reinterpret_cast<int*>(s.cmax + 7);
+      if (t == 0) {
+        const double rho_cur = grid_v[layer];
+        double rho_nom = rho_cur;
+        if (!(r_prim == 0.0 || r_dual == 0.0)) {
+          const double g_norm = nrm[6];
+          double num = nrm[2] < nrm[3] ? nrm[3] : nrm[2];  // std::max({hy, gtl, ||g||, 1e-4})
+          num = num < g_norm ? g_norm : num;
+          num = num < 1e-4 ? 1e-4 : num;
+          double den = nrm[4] < nrm[5] ? nrm[5] : nrm[4];  // std::max({gy, ||z||, 1e-4})
+          den = den < 1e-4 ? 1e-4 : den;
+          rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+        }
+        const int cand_near = nearest_grid_index_fast(grid_log, grid_bnd, p.L, rho_nom);
+        const double qa = rho_nom / rho_cur, qb = rho_cur / rho_nom;
+        const double ratio = qa < qb ? qb : qa;
+        *cand_s = ratio >= p.threshold ? cand_near : layer;
       }
-      const int cand_near = nearest_grid_index(grid_log, p.L, rho_nom);
-      const double qa = rho_nom / rho_cur, qb = rho_cur / rho_nom;
-      const double ratio = qa < qb ? qb : qa;
-      const int cand = ratio >= p.threshold ? cand_near : layer;
+      __syncthreads();
+      const int cand = *cand_s;
       if (cand != layer) {
         layer = cand;
         if (rank == 0 && t == 0 && n_trace < p.cap) {

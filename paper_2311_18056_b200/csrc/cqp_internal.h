@@ -107,6 +107,7 @@ struct RunParams {
   double cost_scale;
   const double* grid;      // L
   const double* log_grid;  // L  (log10 of the grid values, computed on the host)
+  const double* grid_bound;  // L - 1 bounds between neighbouring grid values (nearest_grid_index_fast), or null
   const double* g;   // n unscaled
   const double* c;   // m unscaled
   const double* d;   // m unscaled
@@ -173,7 +174,8 @@ struct cqp_handle {
   double *W = nullptr, *Dk = nullptr;  // Dk: [L][n+m][npad] = [D_k; G D_k]
   double* Wt = nullptr;                // tier 1 only: W re-tiled for contiguous streaming (built lazily)
   double *H = nullptr, *Gr = nullptr, *Gt = nullptr, *Gs = nullptr;
-  double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;
+  double *E = nullptr, *F = nullptr, *dgrid = nullptr, *dlog_grid = nullptr;  // dlog_grid: [log10(grid) (L); bounds (L)]
+  bool grid_bounds = false;  // the grid is ascending: dlog_grid + L holds the bounds between neighbours
   double *g = nullptr, *c = nullptr, *d = nullptr;  // one allocation [g; c; d] (unscaled)
   double* vq = nullptr;  // [4][ring_ld] iterate ring (see RunParams::vq)
   int ring_ld = 0;
@@ -227,6 +229,7 @@ struct cqp_handle {
   // tuning / test knobs, read from the environment once at handle creation (cqp_single.cu: read_knobs)
   int knob_poll_delay_ns = -1, knob_fence_mode = 0, knob_cofetch = 2, knob_wreg = 1;
   int knob_gate[5] = {100, 1, 16, 4, 300};
+  bool knob_exact_log = false;
   bool knob_sb_balance = true, knob_no_retile = false, knob_wide_chunks = true;
 };
 

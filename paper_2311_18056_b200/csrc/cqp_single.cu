@@ -249,6 +249,7 @@ struct Smem {
   double* slo;   // Rp
   double* shi;   // Rp
   double* sval;  // 128 + Rp scratch
+  double* sgrid; // 48  the penalty grid, its log10 and the bounds between neighbours (the rho rule reads them at every check)
   unsigned long long* bars;  // full[2], xready[2], go, (pad), wfull[kMaxStages], wempty[kMaxStages]
 };
 
@@ -274,7 +275,7 @@ __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
   return wdoubles + 2 * (size_t)xs_stride(Dpad, npad, mpad) + kWarps * 16 +
-         2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
+         2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 48 + 8 + 2 * kMaxStages;
 }
 
 template <int RB>
@@ -291,7 +292,8 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
-  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128 + Rp);  // 8 + 2 kMaxStages words
+  s.sgrid = s.sval + 128 + Rp;  // 3 x 16: grid, log10(grid), bounds between neighbours (L <= 16)
+  s.bars = reinterpret_cast<unsigned long long*>(s.sgrid + 48);  // 8 + 2 kMaxStages words
   return s;
 }
 
@@ -354,7 +356,9 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
   const int t = threadIdx.x;
   const int n = p.n, m = p.m;
   const Scratch sc = scratch(p, s, xs);
+  CQP_STAMPR(p.dbg, pass, 0);  // entered (thread 0: the compute warps' last poll has landed)
   __syncthreads();
+  CQP_STAMPR(p.dbg, pass, 1);  // every warp of the CTA is here
   // unscale (layers.hpp:57-59)
   for (int i = t; i < p.npad; i += kThreads) sc.uy[i] = (i < n) ? p.E[i] * xs[i] : 0.0;
   for (int i = t; i < p.mpad; i += kThreads) {
@@ -372,6 +376,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     sc.ul[i] = l;
   }
   __syncthreads();
+  CQP_STAMPR(p.dbg, pass, 2);  // unscaled
 
   double mx[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const int G = p.G;
@@ -412,6 +417,7 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
     }
     __syncthreads();
   }
+  CQP_STAMPR(p.dbg, pass, 3);  // row dots done
   // the threads t < 40 hold values: warps 0 and 1 reduce them, then two lanes meet in shared memory
   if (warp < 2) {
 #pragma unroll
@@ -430,36 +436,37 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
   // one still reads this pass's (a third pass cannot start before every CTA left this one's barrier
   // AND the next one's).
   double* partial = p.partial + (size_t)(pass & 1) * 8 * (size_t)(G + 1);
+  CQP_STAMPR(p.dbg, pass, 4);  // CTA maxima ready
   ++pass;
   if (t < 7) __stcg(partial + (size_t)blockIdx.x * 8 + t, nanmax(s.sval[t], s.sval[8 + t]));
   grid_barrier(p.barrier, epoch, G, p.dbg);
-  // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
-  // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant)
+  CQP_STAMPR(p.dbg, pass - 1, 5);  // grid barrier passed
+  // all-CTA max of the seven norms: warp k takes norm k, a lane the records lane, lane + 32, ... (all loads
+  // in flight together), then one shuffle tree (max is exact, so the order is irrelevant)
   {
-    double mine[7];
-#pragma unroll
-    for (int k = 0; k < 7; ++k) mine[k] = (t < G) ? __ldcg(partial + (size_t)t * 8 + k) : 0.0;
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-#pragma unroll
-      for (int w = 16; w >= 1; w >>= 1) mine[k] = nanmax(mine[k], __shfl_xor_sync(0xffffffffu, mine[k], w));
-    }
     const int lane_ = t & 31, warp_ = t >> 5;
-    if (lane_ == 0) {
-#pragma unroll
-      for (int k = 0; k < 7; ++k) s.sred[warp_ * 8 + k] = mine[k];
-    }
-    __syncthreads();
-    if (t < 7) {
+    if (warp_ < 7) {
       double best = 0.0;
-      for (int w = 0; w < kWarps; ++w) best = nanmax(best, s.sred[w * 8 + t]);
-      s.sval[t] = best;
+      for (int base = lane_; base < G; base += 32 * 5) {
+        double v[5];
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          const int idx = base + 32 * u;
+          v[u] = idx < G ? __ldcg(partial + (size_t)idx * 8 + warp_) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 5; ++u) best = nanmax(best, v[u]);
+      }
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) best = nanmax(best, __shfl_xor_sync(0xffffffffu, best, w));
+      if (lane_ == 0) s.sval[warp_] = best;
     }
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 7; ++k) out[k] = s.sval[k];
   __syncthreads();
+  CQP_STAMPR(p.dbg, pass - 1, 6);  // all-CTA maxima known
 }
 
 // All-SM grid, iterate exchanged through the L2 ring (cooperative launch).  Small problems whose
@@ -518,6 +525,15 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
   };
   if (t == 0) init_barriers(false);
+  const bool grid_smem = p.L <= 16;
+  if (grid_smem && t < p.L) {  // (visible to thread 0's first decision behind many CTA barriers)
+    s.sgrid[t] = p.grid[t];
+    s.sgrid[16 + t] = p.log_grid[t];
+    s.sgrid[32 + t] = p.grid_bound ? p.grid_bound[t] : 0.0;
+  }
+  const double* grid_v = grid_smem ? s.sgrid : p.grid;
+  const double* grid_log = grid_smem ? s.sgrid + 16 : p.log_grid;
+  const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sgrid + 32 : p.grid_bound) : nullptr;
   const int n = p.n, m = p.m, D = p.D;
   const int XS = xs_stride(p.Dpad, p.npad, p.mpad);  // doubles between the two copies of the iterate
   const int nc2 = p.Dpad >> 1;
@@ -948,21 +964,29 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     }
     ++n_hist;
     if (p.adaptive) {
-      const double rho_cur = p.grid[layer];
-      double rho_nom = rho_cur;
-      if (!(r_prim == 0.0 || r_dual == 0.0)) {
-        const double g_norm = nr[6];
-        double num = nr[2] < nr[3] ? nr[3] : nr[2];  // std::max({hy, gtl, ||g||, 1e-4})
-        num = num < g_norm ? g_norm : num;
-        num = num < 1e-4 ? 1e-4 : num;
-        double den = nr[4] < nr[5] ? nr[5] : nr[4];  // std::max({gy, ||z||, 1e-4})
-        den = den < 1e-4 ? 1e-4 : den;
-        rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+      // the rule is evaluated by ONE thread per CTA (sqrt, two divisions, log10 and the scan of the grid in
+      // FP64: all 640 threads doing it cost 1.8 us per check) and handed to the others through shared memory;
+      // every CTA still takes the identical decision from identical data
+      int* cand_s = reinterpret_cast<int*>(s.sval + 16);
+      if (t == 0) {
+        const double rho_cur = grid_v[layer];
+        double rho_nom = rho_cur;
+        if (!(r_prim == 0.0 || r_dual == 0.0)) {
+          const double g_norm = nr[6];
+          double num = nr[2] < nr[3] ? nr[3] : nr[2];  // std::max({hy, gtl, ||g||, 1e-4})
+          num = num < g_norm ? g_norm : num;
+          num = num < 1e-4 ? 1e-4 : num;
+          double den = nr[4] < nr[5] ? nr[5] : nr[4];  // std::max({gy, ||z||, 1e-4})
+          den = den < 1e-4 ? 1e-4 : den;
+          rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+        }
+        const int cand_near = nearest_grid_index_fast(grid_log, grid_bnd, p.L, rho_nom);
+        const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
+        const double ratio = a < b ? b : a;
+        *cand_s = ratio >= p.threshold ? cand_near : layer;
       }
-      const int cand_near = nearest_grid_index(p.log_grid, p.L, rho_nom);
-      const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
-      const double ratio = a < b ? b : a;
-      const int cand = ratio >= p.threshold ? cand_near : layer;
+      __syncthreads();
+      const int cand = *cand_s;
       if (cand != layer) {
         layer = cand;
         if (blockIdx.x == 0 && t == 0 && n_trace < p.cap) {
@@ -975,6 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         load_wreg();
       }
     }
+    CQP_STAMPR(p.dbg, pass - 1, 7);  // decision taken (layer switch included)
     if (p.early_exit && r_prim <= p.eps_prim && r_dual <= p.eps_dual) {
       converged = true;
       break;
@@ -1261,6 +1286,7 @@ static void read_knobs(cqp_handle* h) {
   // direct fetch, the publisher's gate: "initial cycles, adapt (0/1), step up, step down, maximum"
   if (const char* e = std::getenv("CQP_GATE"))
     std::sscanf(e, "%d,%d,%d,%d,%d", &h->knob_gate[0], &h->knob_gate[1], &h->knob_gate[2], &h->knob_gate[3], &h->knob_gate[4]);
+  h->knob_exact_log = env_int("CQP_EXACT_LOG", 0) != 0;  // A/B: always take log10 in the rho rule
   h->knob_sb_balance = env_int("CQP_SB_BALANCE", 1) != 0;
   h->knob_no_retile = std::getenv("CQP_NO_RETILE") != nullptr;
   h->knob_wide_chunks = env_int("CQP_WIDE_CHUNKS", 1) != 0;
@@ -1447,6 +1473,7 @@ int launch_run(cqp_handle* h, bool early_exit, int total_iters, bool do_refresh)
   p.W = h->W; p.Dk = h->Dk; p.H = h->H; p.Gr = h->Gr; p.Gt = h->Gt; p.Gs = h->Gs;
   p.E = h->E; p.F = h->F; p.cost_scale = h->cost_scale;
   p.grid = h->dgrid; p.log_grid = h->dlog_grid;
+  p.grid_bound = (h->grid_bounds && !h->knob_exact_log) ? h->dlog_grid + h->L : nullptr;
   p.g = h->g; p.c = h->c; p.d = h->d;
   p.vq = h->vq; p.ring_ld = h->ring_ld; p.state = h->state; p.partial = h->partial;
   p.eps_prim = h->s.eps_prim; p.eps_dual = h->s.eps_dual; p.threshold = h->s.rho_switch_threshold;

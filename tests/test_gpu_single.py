@@ -501,6 +501,39 @@ def test_structured_stream_layer_matches_dense_and_oracle(G, oracle, monkeypatch
     assert rel_err(struct.solution.lam, dense.solution.lam) <= 1e-9
 
 
+def test_rho_rule_without_log10_takes_the_same_decisions(G, oracle, P, monkeypatch):
+    """nearest_grid_index (layers.cpp:38-50) compares |log10(grid[k]) - log10(rho)|.  The kernels count the
+    bounds sqrt(grid[k] grid[k+1]) below rho instead and fall back to the log10 comparison within 1e-9 of a
+    bound or for a rho that is not a positive finite number; CQP_EXACT_LOG=1 always takes log10.  Same
+    rho_trace, iteration count and bits on the rho-switching dense family and an MPC problem, in the
+    cluster tier and on the all-SM grid."""
+    cases = [(oracle.gen_random_dense_qp(120, seed), None) for seed in (1, 3)]      # 4 -> 2, 4 -> 1 at iteration 75
+    for seed in range(4):                                                          # 4 -> 5 (-> 6) at 50 ... 550
+        wl = P.config2(10, seed=seed)
+        cases.append((wl.base_problem(), wl.problem_at(wl.x0(10.0))))
+    switches = 0
+    for tier in (None, "0"):
+        for prob, q in cases:
+            reps = []
+            for exact in ("0", "1"):
+                monkeypatch.setenv("CQP_EXACT_LOG", exact)
+                if tier is not None:
+                    monkeypatch.setenv("CQP_FORCE_TIER", tier)
+                s = G.Solver(prob.H, prob.g, prob.G, prob.c, prob.d)
+                if q is not None:
+                    s.update_vectors(q.g, q.c, q.d)
+                s.cold_start()
+                reps.append(s.solve())
+                s.close()
+            a, b = reps
+            assert a.solution.iterations == b.solution.iterations and a.solution.rho_trace == b.solution.rho_trace
+            assert np.array_equal(a.solution.y, b.solution.y) and np.array_equal(a.solution.lam, b.solution.lam)
+            switches += len(a.solution.rho_trace) - 1
+    monkeypatch.delenv("CQP_EXACT_LOG", raising=False)
+    monkeypatch.delenv("CQP_FORCE_TIER", raising=False)
+    assert switches >= 12
+
+
 @pytest.mark.parametrize("nu", [22, 30, 42])
 def test_resident_tier_fetch_modes_are_bit_identical(G, oracle, P, monkeypatch, nu):
     """The shared-memory-resident tier can bring the iterate into a CTA three ways (CQP_COFETCH=0: loader

@@ -31,6 +31,14 @@ if len(sys.argv) > 2 and sys.argv[2] == "step":
     print(which, "k", k, "kernel_us", r.kernel_us, " ".join(f"{nm}@{(int(t) - int(st[0])) / 1965.0:.2f}" for nm, t in zip(names, st)))
     sys.exit(0)
 print(which, s.launch_info(), "kernel_us", r.kernel_us, "us/iter", r.kernel_us / 120)
+if len(sys.argv) > 2 and sys.argv[2] == "check":
+    # stamps of the third residual pass of the launch (iteration 75), thread 0 of CTA 0
+    words = (C.c_int * 256)()
+    _lib.load().cqp_debug_words(s._h, words)
+    st = np.frombuffer(bytes(words), dtype=np.int64)[32 + 64:32 + 64 + 8]
+    names = ["entered", "CTA assembled", "unscaled", "row dots", "CTA maxima", "grid barrier", "all-CTA maxima", "decision"]
+    print("check pass:", " ".join(f"{nm}@{(int(t) - int(st[0])) / 1965.0:.2f}" for nm, t in zip(names, st)))
+    sys.exit(0)
 words = (C.c_int * 256)()
 _lib.load().cqp_debug_words(s._h, words)
 st = np.frombuffer(bytes(words), dtype=np.int64)[32:32 + 64].reshape(4, 16)
