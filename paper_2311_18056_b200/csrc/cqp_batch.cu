@@ -852,6 +852,10 @@ struct cqp_batch {
   // one-launch-per-iteration cp.async kernel on the same slot-ordered iterate (A/B runs).
   CUtensorMap mapA[2], mapS[2][2];  // [box: 0 = 64 rows, 1 = 32 rows], mapS[buffer][box]
   int* round_ctrs = nullptr;
+  double* kx_part = nullptr;  // partial tiles of the K split over CTAs (RoundParams::part)
+  int kx_cnt_off = 0;         // offset of its arrival counters inside round_ctrs
+  // rounds with at most kx_thr active columns split every tile's K loop over kx CTAs (CQP_BATCH_KX=kx,thr)
+  int kx = 3, kx_thr = 350;
   CUtensorMap* gmaps = nullptr;   // device copies: [box a][3] ... see round_run
   int round_flags = 0;
   int round_ctr_count = 0;
@@ -894,6 +898,7 @@ struct GemmConfig {
   int smem;
 };
 constexpr int kNumConfigs = 10;
+constexpr int kKxMaxTiles = 16;  // column tiles a round may have for its K loops to be split over CTAs
 static_assert(kNumConfigs <= 16, "grid_ctas / round_grid hold 16 configurations");
 const GemmConfig kConfigs[kNumConfigs] = {
     {dmma_gemm_kernel<128, 128, 2, 4, 1>, 256, gemm_smem_bytes<128, 128>()},
@@ -1105,7 +1110,11 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
     // Below ~800 columns an iteration has fewer items than the SMs have CTA slots, an item's K loop is
     // then bound by TMA latency x k-tiles / stages in flight: deeper pipelines (8 stages of 32 x 32,
     // 6 of 64 x 32), and two k-split warp groups below 250 columns.
-    b->plan = {{1, 3400}, {2, 1600}, {9, 800}, {6, 250}, {7, 0}};
+    // With the K loops of the small rounds split over 3 CTAs (kx, kx_thr: rounds of at most 350 columns) the
+    // plain 32 x 32 configuration serves all of them (one B200, ms per solve of 512 / 4096 columns: no split
+    // 64.3 / 225.8; split below 96 columns 57.2 / 221.7, below 350: 52.8 / 219.9; and without the in-CTA
+    // k-split groups below 250 columns: 49.9 / 218.6).
+    b->plan = {{1, 3400}, {2, 1600}, {9, 800}, {6, 0}};
   }
   if (const char* e = std::getenv("CQP_BATCH_PLAN")) {
     int cfg = 0, bound = 0, used = 0;
@@ -1116,6 +1125,8 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
     }
   }
   if (const char* e = std::getenv("CQP_BATCH_DYNAMIC")) b->dynamic = std::atoi(e) ? 1 : 0;
+  if (const char* e = std::getenv("CQP_BATCH_KX")) std::sscanf(e, "%d,%d", &b->kx, &b->kx_thr);
+  b->kx = std::max(1, std::min(4, b->kx));
   if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_TINY")) std::sscanf(e, "%d,%d", &b->tiny_cfg, &b->thr_tiny);
   int rc;
@@ -1135,7 +1146,10 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   BA(bias_dirty, cap); BA(cols2, slot_cap); BA(tiles2, tile_cap); BA(n_tiles2, 1);
   if (b->verify) { BA(T[0], slot_cap * b->ld_s); BA(T[1], slot_cap * b->ld_s); BA(vres, 2); }
   b->round_ctr_count = 1 + (int)(slot_cap / 32) + 8;
+  b->kx_cnt_off = b->round_ctr_count;                       // per-tile arrival counters of the K split
+  b->round_ctr_count += kKxMaxTiles * (b->Dm_pad / 32) * 4;
   BA(round_ctrs, (size_t)b->round_ctr_count);
+  BA(kx_part, (size_t)kKxMaxTiles * b->Dm_pad * 4 * 32);    // [tiles][row tiles][<= 4 splits][32 x 32]
   BA(g, cap * n); BA(c, cap * m); BA(d, cap * m);
   BA(gs, cap * b->ld_n); BA(lo, cap * b->ld_m); BA(hi, cap * b->ld_m);
   BA(uy, cap * b->ld_n); BA(ul, cap * b->ld_m); BA(uz, cap * b->ld_m);
@@ -1192,7 +1206,7 @@ static void batch_destroy_single(cqp_batch* b) {
   if (!b) return;
   if (b->h) cudaSetDevice(b->h->device);
   if (b->stream) cudaStreamSynchronize(b->stream);
-  void* ptrs[] = {b->bias_dirty, b->cols2, b->tiles2, b->n_tiles2, b->ct[0], b->ct[1], b->n_ct, b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
+  void* ptrs[] = {b->bias_dirty, b->cols2, b->tiles2, b->n_tiles2, b->ct[0], b->ct[1], b->n_ct, b->T[0], b->T[1], b->vres, b->gmaps, b->slot_of, b->round_ctrs, b->kx_part, b->work_ctrs, b->negrho, b->Wb, b->DGb, b->Hb, b->Gb, b->Gtb, b->S0, b->S1, b->bias, b->g, b->c, b->d, b->gs,
                   b->lo, b->hi, b->uy, b->ul, b->uz, b->hy, b->gtl, b->gy, b->layer, b->active,
                   b->iters, b->status, b->nsw, b->rp, b->rd, b->out_y, b->out_z, b->out_l, b->cols,
                   b->trace, b->hist, b->nhist,
@@ -1310,6 +1324,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
   };
   double* Sbuf[2] = {b->S0, b->S1};
   // one persistent launch = `steps` ADMM layers of every active column (cqp_batch_round.cuh)
+  int kx_for_round = 1;
   auto round_run = [&](int first, int steps, int cfg) {
     const RoundConfig& rcfg = kRoundConfigs[cfg];
     RoundParams p{};
@@ -1322,6 +1337,9 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     p.work = b->round_ctrs; p.done = b->round_ctrs + 1; p.dbg = h->dbg_dev;
     p.num_sms = (b->round_flags & 2) ? 0 : h->num_sms;
     p.flags = b->round_flags; p.gmaps = b->gmaps + (rcfg.box_a * 2 + rcfg.box_s) * 3;
+    // K split over CTAs in the small rounds (32 x 32 tiles only: that is what `part` is sized for)
+    p.kx = (rcfg.box_a == 1 && rcfg.box_s == 1 && kx_for_round > 1) ? kx_for_round : 1;
+    p.kx_max_tiles = kKxMaxTiles; p.part = b->kx_part; p.tile_cnt = b->round_ctrs + b->kx_cnt_off;
     CQP_CUDA(cudaMemsetAsync(b->round_ctrs, 0, sizeof(int) * (size_t)b->round_ctr_count, st));
     rcfg.fn<<<b->round_grid[cfg], rcfg.threads, rcfg.smem, st>>>(b->mapA[rcfg.box_a], b->mapS[0][rcfg.box_s],
                                                                  b->mapS[1][rcfg.box_s], p);
@@ -1363,6 +1381,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     const int steps = (r < full_rounds) ? interval : rem;
     // the host knows the active count with a lag of two rounds; it only decreases
     const int cfg = pick_config(b, r >= 2 ? b->h_active[r - 2] : B);
+    kx_for_round = ((r >= 2 ? b->h_active[r - 2] : B) <= b->kx_thr) ? b->kx : 1;
     CQP_CUDA(cudaEventRecord(b->it0[r], st));
     if (b->legacy) {
       for (int k = 0; k < steps; ++k) {

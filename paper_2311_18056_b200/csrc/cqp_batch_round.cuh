@@ -52,6 +52,13 @@ struct RoundParams {
   int* done;        // [column tiles of BN slots] consumer-warp completions of this round (zero at launch)
   int* dbg;
   int num_sms;                // CTAs beyond ceil(items per iteration / num_sms) * num_sms retire at once (see the kernel)
+  // Small rounds: the K loop of every (column tile, row tile) is split over `kx` work items (= CTAs on
+  // different SMs); the splits leave their partial accumulators in `part`, and the LAST one to arrive (a
+  // counter per tile and consumer warp in `tile_cnt`, zero at launch) adds them up in split order, so the sum
+  // does not depend on who arrives when.  Used while the round has at most kx_max_tiles column tiles.
+  int kx, kx_max_tiles;
+  double* part;               // [kx_max_tiles * m_tiles][kx][BM * BN]
+  int* tile_cnt;              // [kx_max_tiles * m_tiles][consumer warps of group 0]
   int flags;                  // debug switch (CQP_ROUND_FLAGS): 1 = TMA descriptors read from global memory
   const CUtensorMap* gmaps;   // [3] copies of the descriptors in global memory: A, S0, S1
 };
@@ -111,7 +118,9 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m_tiles = p.M_pad / BM;
   const int n_ct = __ldcg(p.n_tiles);
-  const int per_iter = n_ct * m_tiles;
+  const int KX = (p.kx > 1 && n_ct <= p.kx_max_tiles) ? p.kx : 1;  // (the same value in every CTA)
+  const int per_tile_col = m_tiles * KX;
+  const int per_iter = n_ct * per_tile_col;
   const int total = per_iter * p.n_iters;
   // row tiles that hold rows at all (the others are padding between the two parts of the structured
   // layer and are skipped: they must not count as completions either, or the skipped tiles of LATER
@@ -153,7 +162,8 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       };
       if (item >= total) { hand_over(-1); break; }
       const int it = item / per_iter, r = item - it * per_iter;
-      const int ns = r / m_tiles, mt = r - ns * m_tiles;
+      const int ns = r / per_tile_col, r2 = r - ns * per_tile_col;
+      const int mt = r2 / KX, kx = r2 - mt * KX;
       TileDesc td;
       td.slot0 = __ldcg(&p.tiles[ns].slot0);
       td.a_index = __ldcg(&p.tiles[ns].a_index);
@@ -181,7 +191,9 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       if (p.flags & 1) { mapAp = p.gmaps; mapS = p.gmaps + 1 + ((p.first ^ it) & 1); }
       const int a_row = td.a_index * p.M_pad + m0;
       const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
-      for (int kt = 0; kt < k_tiles; ++kt) {
+      const int kt_per = (k_tiles + KX - 1) / KX;
+      const int kt0 = kx * kt_per, kt1 = min(k_tiles, kt0 + kt_per);  // this split's k-tiles
+      for (int kt = kt0; kt < kt1; ++kt) {
         mbar_wait(&empty[stage], (int)(sph ^ 1u), p.dbg, 22, item);
         mbar_expect_tx(&full[stage], STAGE_BYTES);
         const unsigned dst = smem_u32(base + stage * STAGE_BYTES);
@@ -209,7 +221,8 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
     if (lane == 0) mbar_arrive(&sempty[q]);
     if (++q == kRoundQ) { q = 0; qph ^= 1; }
     const int it = item / per_iter, r = item - it * per_iter;
-    const int ns = r / m_tiles, mt = r - ns * m_tiles;
+    const int ns = r / per_tile_col, r2 = r - ns * per_tile_col;
+    const int mt = r2 / KX, kx = r2 - mt * KX;
     TileDesc td;
     td.slot0 = __ldcg(&p.tiles[ns].slot0);
     td.a_index = __ldcg(&p.tiles[ns].a_index);
@@ -218,8 +231,12 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
     const bool blk3 = p.split > 0 && m0 >= p.split;
     const int row0 = blk3 ? m0 - p.split + p.nm : m0;
     const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
+    bool finalize = true;  // this warp writes the tile (always, unless the K loop is split over CTAs)
     if (row0 < row_end) {
-      const int k_tiles = blk3 ? p.k_tiles3 : p.k_tiles;
+      const int k_tiles_all = blk3 ? p.k_tiles3 : p.k_tiles;
+      const int kt_per = (k_tiles_all + KX - 1) / KX;
+      const int kt0 = kx * kt_per;
+      const int k_tiles = max(0, min(k_tiles_all, kt0 + kt_per) - kt0);  // this split's k-tiles
       const double* Sin = p.S[(p.first ^ it) & 1];
       double* Sout = p.S[(p.first ^ it ^ 1) & 1];
       // Accumulators start from the bias (rows < n + m) or from the two diagonal terms of a lambda row,
@@ -238,7 +255,7 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
           for (int mi = 0; mi < MI; ++mi) {
             const int row = row0 + warp_m * TM + mi * 8 + pg;
             double init = 0.0;
-            if (col >= 0 && kg == 0) {
+            if (col >= 0 && kg == 0 && kx == 0) {
               if (row < p.nm) {
                 init = __ldcg(p.bias + (size_t)col * p.ld_bias + row);
               } else if (blk3 && row < p.D) {
@@ -309,7 +326,41 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
           }
         }
       }
-      if (kg == 0) {
+      if (KX > 1 && kg == 0) {
+        // K split over CTAs: leave this split's partial tile in global memory; the last split to arrive
+        // (per consumer warp) adds all of them up in split order and goes on to the epilogue
+        const size_t tile = (size_t)ns * m_tiles + mt;
+        double* mine = p.part + ((tile * KX + kx) * NW + warp_in) * (32 * PER) + lane;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            __stcg(mine + ((mi * NI + ni) * 2) * 32, acc[mi][ni][0]);
+            __stcg(mine + ((mi * NI + ni) * 2 + 1) * 32, acc[mi][ni][1]);
+          }
+        __threadfence();
+        __syncwarp();
+        int old = 0;
+        if (lane == 0) old = atomicAdd(p.tile_cnt + tile * NW + warp_in, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        finalize = ((old + 1) % KX) == 0;  // (KX arrivals per iteration; iterations of a column tile do not overlap)
+        if (finalize) {
+          __threadfence();
+          for (int q2 = 0; q2 < KX; ++q2) {
+            const double* theirs = p.part + ((tile * KX + q2) * NW + warp_in) * (32 * PER) + lane;
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                const double v0 = __ldcg(theirs + ((mi * NI + ni) * 2) * 32);
+                const double v1 = __ldcg(theirs + ((mi * NI + ni) * 2 + 1) * 32);
+                acc[mi][ni][0] = q2 == 0 ? v0 : acc[mi][ni][0] + v0;
+                acc[mi][ni][1] = q2 == 0 ? v1 : acc[mi][ni][1] + v1;
+              }
+          }
+        }
+      }
+      if (kg == 0 && finalize) {
         // epilogue: clamp the z rows (solver.cpp:62), store in slot order.  Padding slots hold zeros
         // and stay zero (no bias, W 0 = 0).
 #pragma unroll
@@ -345,7 +396,7 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
     }
     // one completion per consumer warp of group 0: the producer of the next iteration waits for
     // m_real * NW of them per column tile
-    if (kg == 0 && row0 < row_end) {
+    if (kg == 0 && row0 < row_end && finalize) {
       __syncwarp();
       if (lane == 0) {
         __threadfence();

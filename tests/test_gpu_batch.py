@@ -303,7 +303,8 @@ def test_round_kernel_matches_per_iteration_kernel(G, P, monkeypatch, nu, B):
     assert ref["launches"] > 25 * ref["rounds"]                       # one launch per iteration
     ksplit = {4, 5, 7, 8}
     for cfg in range(1, 10):
-        out = run({"CQP_BATCH_FORCE_CFG": str(cfg)})
+        # (CQP_BATCH_KX=1,0: no K split over CTAs, which adds a tile's products up in another order)
+        out = run({"CQP_BATCH_FORCE_CFG": str(cfg), "CQP_BATCH_KX": "1,0"})
         assert out["launches"] < 16 * out["rounds"], cfg              # one launch per ROUND
         for key in ("iterations", "status", "final_index", "n_switches"):
             assert np.array_equal(ref[key], out[key]), (cfg, key)
@@ -313,6 +314,18 @@ def test_round_kernel_matches_per_iteration_kernel(G, P, monkeypatch, nu, B):
                 assert rel_err(out[key], ref[key]) <= 1e-9, (cfg, key)
             else:
                 assert np.array_equal(out[key], ref[key]), (cfg, key)
+    # K loops split over 2, 3, 4 CTAs in EVERY round (threshold above B): the last split to arrive adds the
+    # partial tiles up in split order, so the result does not depend on the arrival order: two runs agree bit
+    # for bit, and with the unsplit kernel to rounding
+    for kx in ("2", "3", "4"):
+        a = run({"CQP_BATCH_FORCE_CFG": "6", "CQP_BATCH_KX": kx + ",100000"})
+        b = run({"CQP_BATCH_FORCE_CFG": "6", "CQP_BATCH_KX": kx + ",100000"})
+        for key in ("iterations", "status", "final_index", "n_switches"):
+            assert np.array_equal(ref[key], a[key]), (kx, key)
+        assert ref["traces"] == a["traces"], kx
+        for key in ("y", "z", "lam"):
+            assert rel_err(a[key], ref[key]) <= 1e-9, (kx, key)
+            assert np.array_equal(a[key], b[key]), (kx, key)
     out = run({})                                                      # the default plan
     for key in ("iterations", "status", "final_index", "n_switches"):
         assert np.array_equal(ref[key], out[key]), key
