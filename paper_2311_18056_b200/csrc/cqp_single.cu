@@ -243,13 +243,13 @@ struct Smem {
   double* xs;    // 2 * XS     iterate (cache space), double buffered by iteration parity; XS = xs_stride()
                  // The unscaled y / z / lambda of a residual pass (and the g_s scratch of load_layer)
                  // live in whichever of the two buffers does NOT hold the current iterate: see scratch().
-  double* sred;  // kWarps * 16          (all-CTA reduction of the residual norms)
+  double* sred;  // kWarps * 16          (resident tier: 3 x 16 words: the penalty grid, its log10 and the bounds
+                 //                        between neighbours, which the rho rule reads at every check)
   double* spart; // 2 * kComputeWarps * Rcap   per-warp partials of the hot loop, by parity
   double* sb;    // Rp  bias rows
   double* slo;   // Rp
   double* shi;   // Rp
   double* sval;  // 128 + Rp scratch
-  double* sgrid; // 48  the penalty grid, its log10 and the bounds between neighbours (the rho rule reads them at every check)
   unsigned long long* bars;  // full[2], xready[2], go, (pad), wfull[kMaxStages], wempty[kMaxStages]
 };
 
@@ -275,7 +275,7 @@ __host__ __device__ inline size_t smem_doubles(int R, int rb, int Dpad, int npad
   const int Rp = (R + 1) & ~1;
   const int Rcap = round_up(R, rb);
   return wdoubles + 2 * (size_t)xs_stride(Dpad, npad, mpad) + kWarps * 16 +
-         2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 48 + 8 + 2 * kMaxStages;
+         2 * (size_t)nparts * Rcap + 4 * (size_t)Rp + 128 + 8 + 2 * kMaxStages;
 }
 
 template <int RB>
@@ -292,8 +292,7 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, const RunParams& p) {
   s.slo = s.sb + Rp;
   s.shi = s.slo + Rp;
   s.sval = s.shi + Rp;
-  s.sgrid = s.sval + 128 + Rp;  // 3 x 16: grid, log10(grid), bounds between neighbours (L <= 16)
-  s.bars = reinterpret_cast<unsigned long long*>(s.sgrid + 48);  // 8 + 2 kMaxStages words
+  s.bars = reinterpret_cast<unsigned long long*>(s.sval + 128 + Rp);  // 8 + 2 kMaxStages words
   return s;
 }
 
@@ -525,15 +524,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
   };
   if (t == 0) init_barriers(false);
-  const bool grid_smem = p.L <= 16;
-  if (grid_smem && t < p.L) {  // (visible to thread 0's first decision behind many CTA barriers)
-    s.sgrid[t] = p.grid[t];
-    s.sgrid[16 + t] = p.log_grid[t];
-    s.sgrid[32 + t] = p.grid_bound ? p.grid_bound[t] : 0.0;
+  if constexpr (!STREAM) {  // (the streamed instantiation reads the grid from global memory: see the rho rule below)
+    if (p.L <= 16 && t < p.L) {  // (visible to thread 0's first decision behind many CTA barriers)
+      s.sred[t] = p.grid[t];
+      s.sred[16 + t] = p.log_grid[t];
+      s.sred[32 + t] = p.grid_bound ? p.grid_bound[t] : 0.0;
+    }
   }
-  const double* grid_v = grid_smem ? s.sgrid : p.grid;
-  const double* grid_log = grid_smem ? s.sgrid + 16 : p.log_grid;
-  const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sgrid + 32 : p.grid_bound) : nullptr;
   const int n = p.n, m = p.m, D = p.D;
   const int XS = xs_stride(p.Dpad, p.npad, p.mpad);  // doubles between the two copies of the iterate
   const int nc2 = p.Dpad >> 1;
@@ -967,8 +964,17 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
       // the rule is evaluated by ONE thread per CTA (sqrt, two divisions, log10 and the scan of the grid in
       // FP64: all 640 threads doing it cost 1.8 us per check) and handed to the others through shared memory;
       // every CTA still takes the identical decision from identical data
+      // (STREAM: the streamed instantiation keeps the all-thread evaluation -- its layer loop lost 5-9 % to the
+      // code motion the single-thread version brought with it, far more than the check gains there)
       int* cand_s = reinterpret_cast<int*>(s.sval + 16);
-      if (t == 0) {
+      int cand_stream = layer;
+      if (STREAM || t == 0) {
+        // (the three pointers are formed here, not at kernel entry: six registers held through the layer
+        // loop were enough to make the streamed instantiation spill and to slow its iteration by 3-7 %)
+        const bool grid_smem = !STREAM && p.L <= 16;
+        const double* grid_v = grid_smem ? s.sred : p.grid;
+        const double* grid_log = grid_smem ? s.sred + 16 : p.log_grid;
+        const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sred + 32 : p.grid_bound) : nullptr;
         const double rho_cur = grid_v[layer];
         double rho_nom = rho_cur;
         if (!(r_prim == 0.0 || r_dual == 0.0)) {
@@ -983,10 +989,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
         const int cand_near = nearest_grid_index_fast(grid_log, grid_bnd, p.L, rho_nom);
         const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
         const double ratio = a < b ? b : a;
-        *cand_s = ratio >= p.threshold ? cand_near : layer;
+        if (!STREAM) *cand_s = ratio >= p.threshold ? cand_near : layer;
+        else cand_stream = ratio >= p.threshold ? cand_near : layer;
       }
-      __syncthreads();
-      const int cand = *cand_s;
+      if (!STREAM) __syncthreads();
+      const int cand = STREAM ? cand_stream : *cand_s;
       if (cand != layer) {
         layer = cand;
         if (blockIdx.x == 0 && t == 0 && n_trace < p.cap) {
