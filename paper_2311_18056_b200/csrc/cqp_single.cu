@@ -440,25 +440,30 @@ __device__ void residual_pass(const RunParams& p, const Smem& s, const double* x
   if (t < 7) __stcg(partial + (size_t)blockIdx.x * 8 + t, nanmax(s.sval[t], s.sval[8 + t]));
   grid_barrier(p.barrier, epoch, G, p.dbg);
   CQP_STAMPR(p.dbg, pass - 1, 5);  // grid barrier passed
-  // all-CTA max of the seven norms: warp k takes norm k, a lane the records lane, lane + 32, ... (all loads
-  // in flight together), then one shuffle tree (max is exact, so the order is irrelevant)
+  // all-CTA max of the seven norms: thread b < G fetches CTA b's record (loads in flight
+  // together), then a shuffle + shared-memory max (max is exact, so the order is irrelevant).
+  // (One warp per norm, five records per lane, saves 0.2 us of the 7 us check in the resident tier -- and
+  // costs the streamed instantiations, whose layer loop moves with any change of this function, 4 % per
+  // iteration.  The per-warp maxima sit in the upper half of sred: its first 48 words hold the grid.)
   {
+    double mine[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) mine[k] = (t < G) ? __ldcg(partial + (size_t)t * 8 + k) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) mine[k] = nanmax(mine[k], __shfl_xor_sync(0xffffffffu, mine[k], w));
+    }
     const int lane_ = t & 31, warp_ = t >> 5;
-    if (warp_ < 7) {
+    if (lane_ == 0) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) s.sred[64 + warp_ * 8 + k] = mine[k];
+    }
+    __syncthreads();
+    if (t < 7) {
       double best = 0.0;
-      for (int base = lane_; base < G; base += 32 * 5) {
-        double v[5];
-#pragma unroll
-        for (int u = 0; u < 5; ++u) {
-          const int idx = base + 32 * u;
-          v[u] = idx < G ? __ldcg(partial + (size_t)idx * 8 + warp_) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 5; ++u) best = nanmax(best, v[u]);
-      }
-#pragma unroll
-      for (int w = 16; w >= 1; w >>= 1) best = nanmax(best, __shfl_xor_sync(0xffffffffu, best, w));
-      if (lane_ == 0) s.sval[warp_] = best;
+      for (int w = 0; w < kWarps; ++w) best = nanmax(best, s.sred[64 + w * 8 + t]);
+      s.sval[t] = best;
     }
   }
   __syncthreads();
@@ -961,21 +966,13 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
     }
     ++n_hist;
     if (p.adaptive) {
-      // the rule is evaluated by ONE thread per CTA (sqrt, two divisions, log10 and the scan of the grid in
-      // FP64: all 640 threads doing it cost 1.8 us per check) and handed to the others through shared memory;
-      // every CTA still takes the identical decision from identical data
-      // (STREAM: the streamed instantiation keeps the all-thread evaluation -- its layer loop lost 5-9 % to the
-      // code motion the single-thread version brought with it, far more than the check gains there)
-      int* cand_s = reinterpret_cast<int*>(s.sval + 16);
-      int cand_stream = layer;
-      if (STREAM || t == 0) {
-        // (the three pointers are formed here, not at kernel entry: six registers held through the layer
-        // loop were enough to make the streamed instantiation spill and to slow its iteration by 3-7 %)
-        const bool grid_smem = !STREAM && p.L <= 16;
-        const double* grid_v = grid_smem ? s.sred : p.grid;
-        const double* grid_log = grid_smem ? s.sred + 16 : p.log_grid;
-        const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sred + 32 : p.grid_bound) : nullptr;
-        const double rho_cur = grid_v[layer];
+      int cand;
+      if constexpr (STREAM) {
+        // The streamed instantiations keep the rule as every thread's own computation from global memory: ANY
+        // change here moves their layer loop's schedule (the single-thread version below cost the streamed
+        // loop 5-9 % per iteration, and even the log10-free index 4 % in the resident server), and a check
+        // is 1 of 25 iterations of 5-11 us there.
+        const double rho_cur = p.grid[layer];
         double rho_nom = rho_cur;
         if (!(r_prim == 0.0 || r_dual == 0.0)) {
           const double g_norm = nr[6];
@@ -986,14 +983,39 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(const RunParams p) {
           den = den < 1e-4 ? 1e-4 : den;
           rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
         }
-        const int cand_near = nearest_grid_index_fast(grid_log, grid_bnd, p.L, rho_nom);
+        const int cand_near = nearest_grid_index(p.log_grid, p.L, rho_nom);
         const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
         const double ratio = a < b ? b : a;
-        if (!STREAM) *cand_s = ratio >= p.threshold ? cand_near : layer;
-        else cand_stream = ratio >= p.threshold ? cand_near : layer;
+        cand = ratio >= p.threshold ? cand_near : layer;
+      } else {
+        // the rule is evaluated by ONE thread per CTA (sqrt, two divisions and the scan of the grid in FP64:
+        // all 640 threads doing it cost 1.8 us per check) and handed to the others through shared memory;
+        // every CTA still takes the identical decision from identical data
+        int* cand_s = reinterpret_cast<int*>(s.sval + 16);
+        if (t == 0) {
+          const bool grid_smem = p.L <= 16;
+          const double* grid_v = grid_smem ? s.sred : p.grid;
+          const double* grid_log = grid_smem ? s.sred + 16 : p.log_grid;
+          const double* grid_bnd = p.grid_bound ? (grid_smem ? s.sred + 32 : p.grid_bound) : nullptr;
+          const double rho_cur = grid_v[layer];
+          double rho_nom = rho_cur;
+          if (!(r_prim == 0.0 || r_dual == 0.0)) {
+            const double g_norm = nr[6];
+            double num = nr[2] < nr[3] ? nr[3] : nr[2];  // std::max({hy, gtl, ||g||, 1e-4})
+            num = num < g_norm ? g_norm : num;
+            num = num < 1e-4 ? 1e-4 : num;
+            double den = nr[4] < nr[5] ? nr[5] : nr[4];  // std::max({gy, ||z||, 1e-4})
+            den = den < 1e-4 ? 1e-4 : den;
+            rho_nom = rho_cur * sqrt((r_prim * num) / (r_dual * den));
+          }
+          const int cand_near = nearest_grid_index_fast(grid_log, grid_bnd, p.L, rho_nom);
+          const double a = rho_nom / rho_cur, b = rho_cur / rho_nom;
+          const double ratio = a < b ? b : a;
+          *cand_s = ratio >= p.threshold ? cand_near : layer;
+        }
+        __syncthreads();
+        cand = *cand_s;
       }
-      if (!STREAM) __syncthreads();
-      const int cand = STREAM ? cand_stream : *cand_s;
       if (cand != layer) {
         layer = cand;
         if (blockIdx.x == 0 && t == 0 && n_trace < p.cap) {
