@@ -19,7 +19,10 @@ if which in ("all", "cluster"):
     run("cluster-reg", problems.config2(6, 1))                       # D = 180: register mode
     run("cluster-smem", problems.config2(6, 1), {"CQP_CLUSTER_MODE": "smem"})
 if which in ("all", "grid"):
-    run("grid-resident", problems.config2(6, 1), {"CQP_FORCE_TIER": "0"})
+    run("grid-resident", problems.config2(6, 1), {"CQP_FORCE_TIER": "0"})                      # direct fetch, W in registers
+    run("grid-resident-wsmem", problems.config2(6, 1), {"CQP_FORCE_TIER": "0", "CQP_WREG": "0"})  # direct fetch, W in shared memory
+    run("grid-resident-staged", problems.config2(6, 1), {"CQP_FORCE_TIER": "0", "CQP_COFETCH": "1"})
+    run("grid-resident-540", problems.config2(18, 1), k=30)                                       # D = 540: the default grid size class
     run("grid-stream", problems.config2(6, 1), {"CQP_FORCE_TIER": "1", "CQP_SINGLE_DENSE": "1"})
     run("grid-stream-structured", problems.config2(6, 1), {"CQP_FORCE_TIER": "1", "CQP_FORCE_STRUCTURED": "1"})
     run("grid-stream-structured-odd", problems.config2(7, 1), {"CQP_FORCE_TIER": "1", "CQP_FORCE_STRUCTURED": "1"})
@@ -31,6 +34,12 @@ if which in ("all", "batch"):
     out = b.solve(g, c, d)
     print("batch", out["iterations"][:8], flush=True)
     b.close()
+    os.environ["CQP_BATCH_KX"] = "1,0"             # no K split over CTAs
+    b = S.BatchSolver(s, 96)
+    out = b.solve(g, c, d)
+    print("batch-nosplit", out["iterations"][:8], flush=True)
+    b.close()
+    os.environ.pop("CQP_BATCH_KX")
     os.environ["CQP_BATCH_LANES"] = "2"           # two concurrent lanes (sub-batches on their own streams)
     g, c, d, _ = problems.batch_instances(wl, 640)
     b = S.BatchSolver(s, 640)
