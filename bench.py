@@ -101,7 +101,7 @@ class ClockSampler:
 
 
 def make_workload(first: int = 0):
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     wl = problems.config2(NU, seed=0)
     g, c, d, _ = problems.batch_instances(wl, BATCH, first=first)
     return wl, g, c, d
@@ -382,7 +382,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    from paper_2311_18056_b200 import problems, sharding, solver as S
+    from workloads import problems
+    from paper_2311_18056_b200 import sharding, solver as S
 
     wl, g, c, d = make_workload(0)                       # every rank builds the same global batch
     base = wl.base_problem()

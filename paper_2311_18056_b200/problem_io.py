@@ -17,10 +17,29 @@ from __future__ import annotations
 import json
 import math
 import sys
+from dataclasses import dataclass
 
 import numpy as np
 
-from .problems import DenseQP
+
+@dataclass
+class DenseQP:
+    """QProblem of the reference (/root/reference/proj/include/clampqp/problem.hpp:31-40): min 1/2 y'Hy + g'y
+    subject to c <= Gy <= d, dense, column-major on the device side."""
+    H: np.ndarray
+    g: np.ndarray
+    G: np.ndarray
+    c: np.ndarray
+    d: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.H.shape[0]
+
+    @property
+    def m(self) -> int:
+        return self.G.shape[0]
+
 
 INF_THRESHOLD = 1e30  # problem.cpp:25
 

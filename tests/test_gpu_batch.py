@@ -17,7 +17,7 @@ def G():
 
 @pytest.fixture(scope="module")
 def P():
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     return problems
 
 
@@ -195,7 +195,8 @@ def _nccl_worker(rank, world, port, B, q):
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
-    from paper_2311_18056_b200 import problems, sharding, solver as S
+    from workloads import problems
+    from paper_2311_18056_b200 import sharding, solver as S
     wl = problems.config2(6, seed=3)
     base = wl.base_problem()
     g, c, d, _ = problems.batch_instances(wl, B)

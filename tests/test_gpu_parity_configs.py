@@ -40,7 +40,7 @@ def G():
 
 @pytest.fixture(scope="module")
 def P():
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     return problems
 
 

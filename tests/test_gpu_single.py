@@ -25,7 +25,7 @@ def G():
 
 @pytest.fixture(scope="module")
 def P():
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     return problems
 
 
@@ -582,7 +582,7 @@ def test_odd_dimensions_in_every_grid_mode(G, oracle, P, monkeypatch, shape):
     tier, the streamed tier with the dense and with the structured layer, and the cluster tier:
     cold solve (14 residual passes), then fused MPC steps (refresh_z + bias + iterations)."""
     import numpy as np
-    from paper_2311_18056_b200 import mpc
+    from workloads import mpc
     if shape == "odd_n_odd_m":
         wl = P.make_mpc_workload(3, 6, 5, seed=2)                       # n = m = 15, D = 45
     else:

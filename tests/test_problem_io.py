@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2311_18056_b200 import problem_io as IO
-from paper_2311_18056_b200 import problems
+from workloads import problems
 
 
 def box_1d():

@@ -48,7 +48,7 @@ def _worker(rank, world, port, B, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     from paper_2311_18056_b200.sharding import solve_sharded
     wl = problems.config2(4, seed=2)
     g, c, d, _ = problems.batch_instances(wl, B)
@@ -73,7 +73,7 @@ def test_solve_sharded_world2_matches_single_process(B):
     got = q.get(timeout=180)
     [p.join(timeout=60) for p in procs]
     assert all(p.exitcode == 0 for p in procs)
-    from paper_2311_18056_b200 import problems
+    from workloads import problems
     wl = problems.config2(4, seed=2)
     g, c, d, _ = problems.batch_instances(wl, B)
     if B == 0:      # every shard is empty: empty results of the right shapes, no IndexError

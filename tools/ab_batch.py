@@ -10,7 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 if len(sys.argv) > 1 and sys.argv[1] == "--child":
-    from paper_2311_18056_b200 import problems, solver as S
+    from workloads import problems
+    from paper_2311_18056_b200 import solver as S
     B, nu, out_path, reps = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], int(sys.argv[5])
     wl = problems.config2(nu, 0); base = wl.base_problem()
     g, c, d, _ = problems.batch_instances(wl, B)

@@ -2,7 +2,8 @@
 device buffers sit at different addresses): per-iteration time of each."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 nu = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 wl = problems.config2(nu, 0)

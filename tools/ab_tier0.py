@@ -4,7 +4,8 @@ iterate after 1000 iterations so that runs under different knobs can be compared
 import hashlib, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 
 nus = [int(a) for a in sys.argv[1:]] or [22, 30, 38, 50]
 tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("CQP_") and k != "CQP_B200_LIB")

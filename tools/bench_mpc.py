@@ -13,7 +13,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
-from paper_2311_18056_b200 import problems, solver as S  # noqa: E402
+from workloads import problems  # noqa: E402
+from paper_2311_18056_b200 import solver as S  # noqa: E402
 
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["config1", "atlas30", "quad30"]

@@ -5,7 +5,8 @@ import json, os, statistics, sys, time
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2311_18056_b200 import problems, solver as S  # noqa: E402
+from workloads import problems  # noqa: E402
+from paper_2311_18056_b200 import solver as S  # noqa: E402
 
 CASES = {
     "config1": (lambda: problems.config1(seed=0), 1),

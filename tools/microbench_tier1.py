@@ -2,7 +2,8 @@
 usage: microbench_tier1.py [atlas:N | quad:N ...]   (default atlas:30 quad:30)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 specs = sys.argv[1:] or ["atlas:30", "quad:30"]
 for spec in specs:
     kind, N = spec.split(":"); N = int(N)

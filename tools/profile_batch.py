@@ -1,7 +1,8 @@
 """Scratch (GPU box): one batched solve (B columns, nu=50) for ncu captures."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 wl = problems.config2(50, 0); base = wl.base_problem()
 g, c, d, _ = problems.batch_instances(wl, B)

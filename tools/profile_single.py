@@ -1,7 +1,8 @@
 """Scratch (GPU box): one single-QP solve at nu=50 (D=1500) for ncu captures."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 nu = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 wl = problems.config2(nu, 0); base = wl.base_problem()
 s = S.Solver(base.H, base.g, base.G, base.c, base.d)

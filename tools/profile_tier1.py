@@ -1,7 +1,8 @@
 """Scratch (GPU box): one solve at the quadruped-sized config (D = 4080, L2/HBM tier) for ncu captures."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 wl = problems.config4_quadruped(30, 0) if (len(sys.argv) < 2 or sys.argv[1] == "quad") else problems.config3_atlas(30, 0)
 base = wl.base_problem()
 s = S.Solver(base.H, base.g, base.G, base.c, base.d)

@@ -2,7 +2,8 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-from paper_2311_18056_b200 import problems, solver as S
+from workloads import problems
+from paper_2311_18056_b200 import solver as S
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 def run(tag, wl, env=None, k=60):
     for kk, v in (env or {}).items(): os.environ[kk] = v

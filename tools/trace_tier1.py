@@ -3,7 +3,8 @@
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-from paper_2311_18056_b200 import problems, solver as S, _lib
+from workloads import problems
+from paper_2311_18056_b200 import solver as S, _lib
 NAMES = {0: "cmp:v_i landed", 1: "cmp:v landed", 10: "cmp15:v landed", 2: "cmp:done", 11: "cmp15:done", 4: "pub:start",
          5: "pub:full", 6: "pub:published", 7: "pub:rearmed", 8: "ldr:go", 9: "ldr:fetched",
          3: "cmp:dot done", 12: "cmp:row ready", 13: "cmp:rearm ok"}

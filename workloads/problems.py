@@ -19,27 +19,12 @@ from typing import Optional
 
 import numpy as np
 
+from paper_2311_18056_b200.problem_io import DenseQP  # noqa: F401  (re-exported: problems.DenseQP)
+
 from . import mpc
 from .rng import Rng
 
 X0_STREAM = 0x9E3779B97F4A7C15
-
-
-@dataclass
-class DenseQP:
-    H: np.ndarray
-    g: np.ndarray
-    G: np.ndarray
-    c: np.ndarray
-    d: np.ndarray
-
-    @property
-    def n(self) -> int:
-        return self.H.shape[0]
-
-    @property
-    def m(self) -> int:
-        return self.G.shape[0]
 
 
 def gen_random_dense_qp(n: int, seed: int) -> DenseQP:
