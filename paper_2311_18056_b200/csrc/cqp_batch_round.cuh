@@ -32,6 +32,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <type_traits>
 
 struct RoundParams {
   int n, m, nm, D;
@@ -59,7 +60,7 @@ struct RoundParams {
   int kx, kx_max_tiles;
   double* part;               // [kx_max_tiles * m_tiles][kx][BM * BN]
   int* tile_cnt;              // [kx_max_tiles * m_tiles][consumer warps of group 0]
-  int flags;                  // debug switch (CQP_ROUND_FLAGS): 1 = TMA descriptors read from global memory
+  int flags;                  // debug switches (CQP_ROUND_FLAGS): 1 = TMA descriptors read from global memory, 2 = padding groups are not skipped
   const CUtensorMap* gmaps;   // [3] copies of the descriptors in global memory: A, S0, S1
 };
 
@@ -274,30 +275,54 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       // the last (still in flight) LDS and ahead of the DMMAs (seen in SASS; the refill then raced with
       // that load: wrong ni = last fragment).  So the arrive for k-tile kt sits behind the full-wait
       // loop of k-tile kt + 1, and the last one behind the epilogue's fence / the reduction barrier.
-      int held = -1;
-      for (int kt = 0; kt < k_tiles; ++kt) {
-        mbar_wait(&full[stage], (int)sph, p.dbg, 24, item);
-        if (held >= 0 && lane == 0) mbar_arrive(&empty[held]);
-        const double* as = reinterpret_cast<const double*>(base + stage * STAGE_BYTES) + (warp_m * TM + pg) * 16;
-        const double* bs = reinterpret_cast<const double*>(base + stage * STAGE_BYTES + A_BYTES) + (warp_n * TN + pg) * 16;
-        double a[MI], b[NI];
+      // Partially filled column tiles (the last tile of every ladder level; in the late rounds every tile):
+      // a group of 8 slots that holds padding only gets no fragment loads and no DMMAs.  Its accumulators
+      // stay at their initial 0, which is what W 0 adds up to, and the columns that are there see the same
+      // products in the same order: bit-identical, and the SM's DMMA pipe (what bounds an item) is busy for
+      // the occupied groups only.  The stage waits and releases are kept, so the pipeline protocol is the same.
+      // (The 32 x 32 configurations only: they serve the rounds below 800 columns, where the partial tiles
+      // are a visible share; the large tiles keep their schedule.)
+      constexpr bool SKIP = (BM == 32 && BN == 32);
+      unsigned act = (1u << NI) - 1u;
+      if (SKIP && !(p.flags & 2)) {  // (CQP_ROUND_FLAGS=2: A/B switch, no skipping)
+        act = 0;
 #pragma unroll
-        for (int ks0 = 0; ks0 < 4; ks0 += KS) {
-          const int ks = ks0 + kg;
-          const int e = ks * 4 + t4;
-          const int off = (((e >> 1) ^ pg) << 1) | (e & 1);
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi) a[mi] = as[mi * 128 + off];
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) b[ni] = bs[ni * 128 + off];
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-        }
-        held = (int)stage;
-        if (++stage == (unsigned)ST) { stage = 0; sph ^= 1u; }
+        for (int ni = 0; ni < NI; ++ni)
+          act |= __any_sync(0xffffffffu, colv[ni][0] >= 0 || colv[ni][1] >= 0) ? (1u << ni) : 0u;
       }
+      int held = -1;
+      auto k_loop = [&](auto guard) {
+        constexpr bool GUARD = decltype(guard)::value;
+        for (int kt = 0; kt < k_tiles; ++kt) {
+          mbar_wait(&full[stage], (int)sph, p.dbg, 24, item);
+          if (held >= 0 && lane == 0) mbar_arrive(&empty[held]);
+          if (!GUARD || act != 0) {
+            const double* as = reinterpret_cast<const double*>(base + stage * STAGE_BYTES) + (warp_m * TM + pg) * 16;
+            const double* bs = reinterpret_cast<const double*>(base + stage * STAGE_BYTES + A_BYTES) + (warp_n * TN + pg) * 16;
+            double a[MI], b[NI];
+#pragma unroll
+            for (int ks0 = 0; ks0 < 4; ks0 += KS) {
+              const int ks = ks0 + kg;
+              const int e = ks * 4 + t4;
+              const int off = (((e >> 1) ^ pg) << 1) | (e & 1);
+#pragma unroll
+              for (int mi = 0; mi < MI; ++mi) a[mi] = as[mi * 128 + off];
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni)
+                if (!GUARD || ((act >> ni) & 1u)) b[ni] = bs[ni * 128 + off];
+#pragma unroll
+              for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni)
+                  if (!GUARD || ((act >> ni) & 1u)) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+            }
+          }
+          held = (int)stage;
+          if (++stage == (unsigned)ST) { stage = 0; sph ^= 1u; }
+        }
+      };
+      if (!SKIP || act == (1u << NI) - 1u) k_loop(std::false_type{});
+      else k_loop(std::true_type{});
       if (KS > 1) {
         // partial accumulators of groups 1 .. KS-1 meet in `red`; group 0 adds them in group order
         named_barrier(1, NCW * 32);  // the previous item's readers of `red` are done
