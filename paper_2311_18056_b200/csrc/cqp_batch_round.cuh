@@ -93,7 +93,7 @@ template <int BM, int BN, int WM, int WN, int ST, int KS>
 constexpr int round_smem_bytes() {
   constexpr int MI = BM / WM / 8, NI = BN / WN / 8;
   return 1024 /* alignment slack: the 128-byte swizzle wants 1024-byte aligned tiles */ + ST * (BM + BN) * 128 +
-         (KS > 1 ? (KS - 1) * WM * WN * 32 * MI * NI * 2 * 8 : 0) + 8 * (2 * ST + 2 * kRoundQ) + 4 * kRoundQ + 16;
+         (KS > 1 ? (KS - 1) * WM * WN * 32 * MI * NI * 2 * 8 : 0) + 8 * (2 * ST + 2 * kRoundQ) + 12 * kRoundQ + 16;
 }
 
 template <int BM, int BN, int WM, int WN, int ST, int KS, int MINB>
@@ -155,9 +155,15 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       const int item = atomicAdd(p.work, 1);
       // the consumers learn about the item only once its inputs are complete: they read S too (the
       // diagonal terms of the lambda rows)
+      TileDesc td;
+      td.slot0 = 0; td.a_index = 0;
+      // (the tile descriptor rides along: the consumers' first loads, slot map -> bias, then do not wait
+      // for a third dependent round trip to L2)
       auto hand_over = [&](int value) {
         mbar_wait(&sempty[q], qph ^ 1, p.dbg, 20, item);
-        item_s[q] = value;
+        item_s[q * 3] = value;
+        item_s[q * 3 + 1] = td.slot0;
+        item_s[q * 3 + 2] = td.a_index;
         mbar_arrive(&sfull[q]);
         if (++q == kRoundQ) { q = 0; qph ^= 1; }
       };
@@ -165,7 +171,6 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       const int it = item / per_iter, r = item - it * per_iter;
       const int ns = r / per_tile_col, r2 = r - ns * per_tile_col;
       const int mt = r2 / KX, kx = r2 - mt * KX;
-      TileDesc td;
       td.slot0 = __ldcg(&p.tiles[ns].slot0);
       td.a_index = __ldcg(&p.tiles[ns].a_index);
       const int slot0 = td.slot0;
@@ -215,7 +220,10 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   const int pc0 = (((2 * t4) & 3) << 1) | ((2 * t4) >> 2), pc1 = (((2 * t4 + 1) & 3) << 1) | ((2 * t4 + 1) >> 2);
   for (;;) {
     mbar_wait(&sfull[q], qph, p.dbg, 23, 0);
-    const int item = item_s[q];
+    const int item = item_s[q * 3];
+    TileDesc td;
+    td.slot0 = item_s[q * 3 + 1];
+    td.a_index = item_s[q * 3 + 2];
     __syncwarp();
     if (item < 0) break;  // (the branch needs the loaded value: the slot is released only after the read returned)
     __syncwarp();
@@ -224,9 +232,6 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
     const int it = item / per_iter, r = item - it * per_iter;
     const int ns = r / per_tile_col, r2 = r - ns * per_tile_col;
     const int mt = r2 / KX, kx = r2 - mt * KX;
-    TileDesc td;
-    td.slot0 = __ldcg(&p.tiles[ns].slot0);
-    td.a_index = __ldcg(&p.tiles[ns].a_index);
     const int slot0 = td.slot0;
     const int m0 = mt * BM;
     const bool blk3 = p.split > 0 && m0 >= p.split;
