@@ -88,12 +88,14 @@ __device__ __forceinline__ void named_barrier(int id, int threads) {
 }
 
 constexpr int kRoundQ = 4;  // depth of the producer -> consumer item ring
+// ring entry: {item, first slot, ladder index, -, slot map of the tile's BN slots}
+__host__ __device__ constexpr int round_ring_ints(int BN) { return 4 + BN; }
 
 template <int BM, int BN, int WM, int WN, int ST, int KS>
 constexpr int round_smem_bytes() {
   constexpr int MI = BM / WM / 8, NI = BN / WN / 8;
   return 1024 /* alignment slack: the 128-byte swizzle wants 1024-byte aligned tiles */ + ST * (BM + BN) * 128 +
-         (KS > 1 ? (KS - 1) * WM * WN * 32 * MI * NI * 2 * 8 : 0) + 8 * (2 * ST + 2 * kRoundQ) + 12 * kRoundQ + 16;
+         (KS > 1 ? (KS - 1) * WM * WN * 32 * MI * NI * 2 * 8 : 0) + 8 * (2 * ST + 2 * kRoundQ) + 4 * round_ring_ints(BN) * kRoundQ + 16;
 }
 
 template <int BM, int BN, int WM, int WN, int ST, int KS, int MINB>
@@ -115,6 +117,7 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   unsigned long long* sfull = empty + ST;
   unsigned long long* sempty = sfull + kRoundQ;
   int* item_s = reinterpret_cast<int*>(sempty + kRoundQ);
+  constexpr int RING = round_ring_ints(BN);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m_tiles = p.M_pad / BM;
@@ -157,14 +160,22 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       // diagonal terms of the lambda rows)
       TileDesc td;
       td.slot0 = 0; td.a_index = 0;
-      // (the tile descriptor rides along: the consumers' first loads, slot map -> bias, then do not wait
-      // for a third dependent round trip to L2)
+      // (the tile descriptor and the tile's slot map ride along: the consumers' bias loads then do not
+      // wait behind two more dependent round trips to L2; the producer fetches them while it waits for
+      // the item's inputs anyway)
+      bool have_slot = false;
+      auto take_slot = [&]() {
+        if (!have_slot) mbar_wait(&sempty[q], qph ^ 1, p.dbg, 20, item);
+        have_slot = true;
+      };
       auto hand_over = [&](int value) {
-        mbar_wait(&sempty[q], qph ^ 1, p.dbg, 20, item);
-        item_s[q * 3] = value;
-        item_s[q * 3 + 1] = td.slot0;
-        item_s[q * 3 + 2] = td.a_index;
+        take_slot();
+        int* ring = item_s + q * RING;
+        ring[0] = value;
+        ring[1] = td.slot0;
+        ring[2] = td.a_index;
         mbar_arrive(&sfull[q]);
+        have_slot = false;
         if (++q == kRoundQ) { q = 0; qph ^= 1; }
       };
       if (item >= total) { hand_over(-1); break; }
@@ -179,6 +190,13 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       const int row0 = blk3 ? m0 - p.split + p.nm : m0;
       const int row_end = (p.split > 0 && !blk3) ? p.nm : p.D;
       if (row0 >= row_end) { hand_over(item); continue; }  // row tile of padding only: the consumers skip it too
+      {
+        take_slot();
+        int4* ring_cols = reinterpret_cast<int4*>(item_s + q * RING + 4);
+        const int4* src = reinterpret_cast<const int4*>(p.cols + slot0);
+#pragma unroll
+        for (int i = 0; i < BN / 4; ++i) ring_cols[i] = __ldcg(src + i);
+      }
       if (it > 0) {
         const int need = it * m_real * NW;
         long long t0 = 0;
@@ -220,12 +238,20 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
   const int pc0 = (((2 * t4) & 3) << 1) | ((2 * t4) >> 2), pc1 = (((2 * t4 + 1) & 3) << 1) | ((2 * t4 + 1) >> 2);
   for (;;) {
     mbar_wait(&sfull[q], qph, p.dbg, 23, 0);
-    const int item = item_s[q * 3];
+    const int* ring = item_s + q * RING;
+    const int item = ring[0];
     TileDesc td;
-    td.slot0 = item_s[q * 3 + 1];
-    td.a_index = item_s[q * 3 + 2];
+    td.slot0 = ring[1];
+    td.a_index = ring[2];
+    int colv[NI][2];  // this thread's columns (slot map of the tile, from the ring)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      colv[ni][0] = ring[4 + warp_n * TN + ni * 8 + pc0];
+      colv[ni][1] = ring[4 + warp_n * TN + ni * 8 + pc1];
+    }
     __syncwarp();
-    if (item < 0) break;  // (the branch needs the loaded value: the slot is released only after the read returned)
+    if (item < 0) break;  // (the branch needs the loaded value: the slot is released only after the reads returned)
+    // (the values read above feed address arithmetic below, so the loads have returned before the release)
     __syncwarp();
     if (lane == 0) mbar_arrive(&sempty[q]);
     if (++q == kRoundQ) { q = 0; qph ^= 1; }
@@ -249,14 +275,12 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
       // -rho_i z_i + lambda_i (blocks (3,2), (3,3) of W, layers.cpp:159-161); the loads overlap the
       // first stages.  S is read with ld.cg: these addresses are rewritten every other iteration.
       double acc[MI][NI][2];
-      int colv[NI][2];
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int cs = slot0 + warp_n * TN + ni * 8 + (j ? pc1 : pc0);
-          const int col = __ldcg(p.cols + cs);
-          colv[ni][j] = col;
+          const int col = colv[ni][j];
 #pragma unroll
           for (int mi = 0; mi < MI; ++mi) {
             const int row = row0 + warp_m * TM + mi * 8 + pg;
