@@ -83,6 +83,11 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int atom_acq_rel_gpu_add(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void named_barrier(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -392,14 +397,15 @@ round_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ C
             __stcg(mine + ((mi * NI + ni) * 2) * 32, acc[mi][ni][0]);
             __stcg(mine + ((mi * NI + ni) * 2 + 1) * 32, acc[mi][ni][1]);
           }
-        __threadfence();
+        // the warp meets, lane 0 counts the arrival with an acq_rel atom (release: cumulative over every lane's
+        // partial stores; acquire: the last arriver's re-reads below, behind the second meeting, see all splits)
         __syncwarp();
         int old = 0;
-        if (lane == 0) old = atomicAdd(p.tile_cnt + tile * NW + warp_in, 1);
+        if (lane == 0) old = atom_acq_rel_gpu_add(p.tile_cnt + tile * NW + warp_in, 1);
         old = __shfl_sync(0xffffffffu, old, 0);
         finalize = ((old + 1) % KX) == 0;  // (KX arrivals per iteration; iterations of a column tile do not overlap)
         if (finalize) {
-          __threadfence();
+          __syncwarp();
           for (int q2 = 0; q2 < KX; ++q2) {
             const double* theirs = p.part + ((tile * KX + q2) * NW + warp_in) * (32 * PER) + lane;
 #pragma unroll
