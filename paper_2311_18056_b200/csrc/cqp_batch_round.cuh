@@ -26,6 +26,11 @@
 //     grid drains once, at the end of the round.  Items are handed out in index order, so the owner
 //     of the lowest unfinished item is always resident and never blocked: no deadlock whatever part
 //     of the grid the device keeps resident (two lanes can run their kernels concurrently).
+//   * The chain of one iteration is kept short (it is what a small round costs): the producer hands the
+//     tile descriptor and the tile's slot map to the consumers through the shared-memory item ring, a
+//     warp's completion is ONE release red behind a warp meeting (cumulative over every lane's stores;
+//     no __threadfence per thread), the K split's arrival counter one acq_rel atom, and groups of 8
+//     padding slots get no fragment loads and no DMMAs (32 x 32 tiles).
 //   * KS > 1 (last rounds, a handful of columns): KS warp groups split the k steps of every k-tile
 //     and meet in shared memory; a tile's K loop is a latency chain, KS groups walk it KS steps at a
 //     time.
