@@ -766,10 +766,12 @@ __global__ void batch_permute_kernel(BatchDev b, const double* __restrict__ src,
 
 // Debug (CQP_ROUND_VERIFY=1): first entry where the round kernel's iterate differs from the
 // legacy kernel's, over the slots of the current map.  out[0] = min linear index (slot * ld + row).
+// Padding slots are not compared: their columns belong to no QP (whatever a departed column left there is
+// multiplied along by the per-iteration kernel and zeroed group-wise by the round kernel).
 __global__ void batch_compare_kernel(const double* __restrict__ a, const double* __restrict__ b, const int* n_tiles,
-                                     int ld, int D, unsigned long long* out) {
+                                     const int* __restrict__ cols, int ld, int D, unsigned long long* out) {
   const int s = blockIdx.x;
-  if (s >= (*n_tiles) * SLOT_TILE) return;
+  if (s >= (*n_tiles) * SLOT_TILE || cols[s] < 0) return;
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
     const double x = a[(size_t)s * ld + i], y = b[(size_t)s * ld + i];
     if (__double_as_longlong(x) != __double_as_longlong(y)) {
@@ -1402,7 +1404,7 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
         cur ^= steps & 1;
         const unsigned long long init[2] = {~0ull, 0ull};
         CQP_CUDA(cudaMemcpyAsync(b->vres, init, sizeof(init), cudaMemcpyHostToDevice, st));
-        batch_compare_kernel<<<(unsigned)slots_used, 256, 0, st>>>(Sbuf[cur], b->T[tc], b->n_tiles, b->ld_s, b->D, b->vres);
+        batch_compare_kernel<<<(unsigned)slots_used, 256, 0, st>>>(Sbuf[cur], b->T[tc], b->n_tiles, b->cols, b->ld_s, b->D, b->vres);
         unsigned long long got[2] = {0, 0};
         int nt = 0;
         CQP_CUDA(cudaMemcpyAsync(got, b->vres, sizeof(got), cudaMemcpyDeviceToHost, st));
