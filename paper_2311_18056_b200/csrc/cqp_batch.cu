@@ -857,7 +857,10 @@ struct cqp_batch {
   double* kx_part = nullptr;  // partial tiles of the K split over CTAs (RoundParams::part)
   int kx_cnt_off = 0;         // offset of its arrival counters inside round_ctrs
   // rounds with at most kx_thr active columns split every tile's K loop over kx CTAs (CQP_BATCH_KX=kx,thr)
-  int kx = 3, kx_thr = 350;
+  int kx = 4, kx_thr = 350;
+  // ... and over kx_few CTAs once at most kx_few_thr columns are left (the last rounds are one latency chain per
+  // iteration: the shorter every CTA's share of the K loop, the shorter the chain)
+  int kx_few = 6, kx_few_thr = 64;
   CUtensorMap* gmaps = nullptr;   // device copies: [box a][3] ... see round_run
   int round_flags = 0;
   int round_ctr_count = 0;
@@ -901,6 +904,7 @@ struct GemmConfig {
 };
 constexpr int kNumConfigs = 10;
 constexpr int kKxMaxTiles = 16;  // column tiles a round may have for its K loops to be split over CTAs
+constexpr int kKxMaxSplit = 8;  // CTAs one tile's K loop may be split over
 static_assert(kNumConfigs <= 16, "grid_ctas / round_grid hold 16 configurations");
 const GemmConfig kConfigs[kNumConfigs] = {
     {dmma_gemm_kernel<128, 128, 2, 4, 1>, 256, gemm_smem_bytes<128, 128>()},
@@ -1127,8 +1131,13 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
     }
   }
   if (const char* e = std::getenv("CQP_BATCH_DYNAMIC")) b->dynamic = std::atoi(e) ? 1 : 0;
-  if (const char* e = std::getenv("CQP_BATCH_KX")) std::sscanf(e, "%d,%d", &b->kx, &b->kx_thr);
-  b->kx = std::max(1, std::min(4, b->kx));
+  if (const char* e = std::getenv("CQP_BATCH_KX")) {
+    b->kx_few = 0;  // (a two-value setting switches the second level off: "kx,thr" keeps its old meaning)
+    std::sscanf(e, "%d,%d,%d,%d", &b->kx, &b->kx_thr, &b->kx_few, &b->kx_few_thr);
+    if (b->kx_few <= 0) { b->kx_few = b->kx; b->kx_few_thr = 0; }
+  }
+  b->kx = std::max(1, std::min(kKxMaxSplit, b->kx));
+  b->kx_few = std::max(1, std::min(kKxMaxSplit, b->kx_few));
   if (const char* e = std::getenv("CQP_BATCH_SMALL_CFG")) b->small_cfg = std::atoi(e);
   if (const char* e = std::getenv("CQP_BATCH_TINY")) std::sscanf(e, "%d,%d", &b->tiny_cfg, &b->thr_tiny);
   int rc;
@@ -1151,7 +1160,7 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
   b->kx_cnt_off = b->round_ctr_count;                       // per-tile arrival counters of the K split
   b->round_ctr_count += kKxMaxTiles * (b->Dm_pad / 32) * 4;
   BA(round_ctrs, (size_t)b->round_ctr_count);
-  BA(kx_part, (size_t)kKxMaxTiles * b->Dm_pad * 4 * 32);    // [tiles][row tiles][<= 4 splits][32 x 32]
+  BA(kx_part, (size_t)kKxMaxTiles * b->Dm_pad * kKxMaxSplit * 32);    // [tiles][row tiles][<= kKxMaxSplit splits][32 x 32]
   BA(g, cap * n); BA(c, cap * m); BA(d, cap * m);
   BA(gs, cap * b->ld_n); BA(lo, cap * b->ld_m); BA(hi, cap * b->ld_m);
   BA(uy, cap * b->ld_n); BA(ul, cap * b->ld_m); BA(uz, cap * b->ld_m);
@@ -1383,7 +1392,10 @@ static int batch_solve_single(cqp_batch* b, int B, const double* g_cols, const d
     const int steps = (r < full_rounds) ? interval : rem;
     // the host knows the active count with a lag of two rounds; it only decreases
     const int cfg = pick_config(b, r >= 2 ? b->h_active[r - 2] : B);
-    kx_for_round = ((r >= 2 ? b->h_active[r - 2] : B) <= b->kx_thr) ? b->kx : 1;
+    {
+      const int seen = r >= 2 ? b->h_active[r - 2] : B;  // (the active count two rounds ago: what the host has seen)
+      kx_for_round = seen <= b->kx_few_thr ? b->kx_few : seen <= b->kx_thr ? b->kx : 1;
+    }
     CQP_CUDA(cudaEventRecord(b->it0[r], st));
     if (b->legacy) {
       for (int k = 0; k < steps; ++k) {
