@@ -315,10 +315,10 @@ def test_round_kernel_matches_per_iteration_kernel(G, P, monkeypatch, nu, B):
                 assert rel_err(out[key], ref[key]) <= 1e-9, (cfg, key)
             else:
                 assert np.array_equal(out[key], ref[key]), (cfg, key)
-    # K loops split over 2, 3, 4 CTAs in EVERY round (threshold above B): the last split to arrive adds the
+    # K loops split over 2 ... 8 CTAs in EVERY round (threshold above B; the default plan uses 4 and 6): the last split to arrive adds the
     # partial tiles up in split order, so the result does not depend on the arrival order: two runs agree bit
     # for bit, and with the unsplit kernel to rounding
-    for kx in ("2", "3", "4"):
+    for kx in ("2", "3", "4", "6", "8"):
         a = run({"CQP_BATCH_FORCE_CFG": "6", "CQP_BATCH_KX": kx + ",100000"})
         b = run({"CQP_BATCH_FORCE_CFG": "6", "CQP_BATCH_KX": kx + ",100000"})
         for key in ("iterations", "status", "final_index", "n_switches"):
