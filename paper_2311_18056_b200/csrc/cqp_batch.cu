@@ -1120,6 +1120,9 @@ static int batch_create_single(cqp_batch** out, cqp_handle* h, int capacity) {
     // plain 32 x 32 configuration serves all of them (one B200, ms per solve of 512 / 4096 columns: no split
     // 64.3 / 225.8; split below 96 columns 57.2 / 221.7, below 350: 52.8 / 219.9; and without the in-CTA
     // k-split groups below 250 columns: 49.9 / 218.6).
+    // Session 4 (shorter hand-over chain in the round kernel): 4 CTAs per tile below 350 columns and 6 below 64
+    // (kx, kx_few): 64 / 512 / 4096 columns 26.7 / 46.6 / 214.7 -> 22.5 / 44.9 / 214.4 ms; thresholds of 500
+    // columns or 3 / 5 / 8 splits are slower.
     b->plan = {{1, 3400}, {2, 1600}, {9, 800}, {6, 0}};
   }
   if (const char* e = std::getenv("CQP_BATCH_PLAN")) {
